@@ -1,0 +1,38 @@
+# Build every native artefact in-tree (the .so files travel to the GPU box with gpurun).
+#   librg.so          product: C-ABI recycled-GMRES library, fp64 CUDA kernels for sm_100a
+#   libsynth*.so      seeded input generators (host C + device CUDA, bit-identical)
+#   liboracle.so      CPU oracle (test infrastructure only)
+NVCC      ?= /usr/local/cuda/bin/nvcc
+CC        ?= gcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+             --expt-relaxed-constexpr -Iinclude
+CFLAGS    := -O2 -fPIC -std=c99 -ffp-contract=off -Wall -Wno-unused-function
+
+PKG       := paper_1807_09467_b200
+RG_SRC    := $(wildcard $(PKG)/csrc/*.cu)
+RG_HDR    := $(wildcard $(PKG)/csrc/*.cuh) include/rg.h
+
+all: oracle synth rg
+
+rg: $(PKG)/lib/librg.so
+synth: synth/libsynth.so synth/libsynth_cuda.so
+oracle: oracle/liboracle.so
+
+$(PKG)/lib/librg.so: $(RG_SRC) $(RG_HDR)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(RG_SRC) -lcuda
+
+synth/libsynth.so: synth/synth.c synth/synth_common.h
+	$(CC) $(CFLAGS) -shared -o $@ synth/synth.c -lm
+
+synth/libsynth_cuda.so: synth/synth_cuda.cu synth/synth_common.h
+	$(NVCC) $(ARCH) -O3 -lineinfo -fmad=false -Xcompiler -fPIC -shared -o $@ synth/synth_cuda.cu
+
+oracle/liboracle.so: oracle/oracle.c
+	$(CC) $(CFLAGS) -shared -o $@ oracle/oracle.c -lm
+
+clean:
+	rm -f $(PKG)/lib/librg.so synth/*.so oracle/*.so
+
+.PHONY: all rg synth oracle clean

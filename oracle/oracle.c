@@ -1,0 +1,323 @@
+/* oracle.c — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation (C99, IEEE binary64, single thread,
+ * built with -O2 -ffp-contract=off, no -ffast-math) of what the recycled-GMRES hot path
+ * computes, written from PAPER.md (arXiv:1807.09467).  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.  It shares no code, header,
+ * table or helper with the CUDA library (paper_1807_09467_b200/csrc); neither includes the other.
+ *
+ * Definitions followed (SURVEY.md §8c gives the readings; DESIGN.md lists them):
+ *   - or_spmv:  y = A x, CSR or BSR, each row summed in stored order ("the cost of a
+ *               matrix-vector multiplication reduces to O(mb)").
+ *   - or_solve: the minimal-residual iterate ("minimal residual:
+ *               min_{z in S_k} ||r_k||") over the search space of each restart cycle c
+ *                 plain   : x_c + K_j(A, r_c)                        (GMRES)
+ *                 augment : x_c + span(W) + K_j(A, r_c)              (eq. def_aug_S_space)
+ *                 deflate : x_c + span(W) + K_j(P A, P r_c),         (Table 1 row "deflated LS",
+ *                           P = I - AW((AW)^T AW)^{-1}(AW)^T          PAPER.md:310, 348; eq. def_S_k_projected)
+ *               with the start x_0 <- x0 + W (C^T C)^{-1} C^T r(x0), C = AW (the j = 0 case of the
+ *               same minimisation; min-residual analogue of eq. projection_t_s).
+ *               The minimisation is solved EXPLICITLY: an orthonormal basis U_Z of the image
+ *               A*[W, v_0..v_j] is grown by modified Gram-Schmidt applied twice (MGS2), the residual
+ *               is r - U_Z U_Z^T r and the coefficients are R_Z^{-1} U_Z^T r.  This is the plain
+ *               definition, not the GPU's Hessenberg/Givens/GCRO algebra.
+ *   - or_svd:   thin SVD by one-sided (Hestenes) Jacobi directly on X, long-double dot products;
+ *               sorted non-increasing; rank = #{sigma > 1e-12 sigma_1} (PAPER.md:524-537, 552-553,
+ *               Algorithm 1; Schmidt-Eckart-Young eq. opt_svd).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int fmt;          /* 0 = CSR, 1 = BSR (b x b blocks, column-major inside a block) */
+  int64_t n;        /* scalar rows = columns */
+  int32_t b;        /* block size (1 for CSR) */
+  const int32_t* rp;/* row pointer (block rows for BSR), length n/b + 1 */
+  const int32_t* ci;/* column (block-column) indices */
+  const double* v;  /* values */
+} or_mat;
+
+typedef struct {
+  int iterations;   /* Arnoldi steps summed over cycles */
+  int cycles;       /* restart cycles started */
+  int converged;
+  int status;       /* 0 ok, 1 singular AW, 2 allocation failure */
+  int hist_len;
+  int k_used;
+  double rel_residual; /* final TRUE ||b - A x|| / ||b|| */
+} or_report;
+
+/* ------------------------------------------------------------------------------------------ */
+void or_spmv(const or_mat* A, const double* x, double* y) {
+  if (A->fmt == 0) {
+    for (int64_t i = 0; i < A->n; ++i) {
+      double s = 0.0;
+      for (int32_t p = A->rp[i]; p < A->rp[i + 1]; ++p) s += A->v[p] * x[A->ci[p]];
+      y[i] = s;
+    }
+    return;
+  }
+  const int64_t b = A->b, nb = A->n / b;
+  for (int64_t I = 0; I < nb; ++I)
+    for (int64_t r = 0; r < b; ++r) {
+      double s = 0.0;
+      for (int32_t p = A->rp[I]; p < A->rp[I + 1]; ++p)
+        for (int64_t c = 0; c < b; ++c) s += A->v[(int64_t)p * b * b + c * b + r] * x[(int64_t)A->ci[p] * b + c];
+      y[I * b + r] = s;
+    }
+}
+
+/* a single row of A x (used by tests to check sampled rows of huge products) */
+double or_spmv_row(const or_mat* A, int64_t row, const double* x) {
+  double s = 0.0;
+  if (A->fmt == 0) {
+    for (int32_t p = A->rp[row]; p < A->rp[row + 1]; ++p) s += A->v[p] * x[A->ci[p]];
+    return s;
+  }
+  const int64_t b = A->b, I = row / b, r = row % b;
+  for (int32_t p = A->rp[I]; p < A->rp[I + 1]; ++p)
+    for (int64_t c = 0; c < b; ++c) s += A->v[(int64_t)p * b * b + c * b + r] * x[(int64_t)A->ci[p] * b + c];
+  return s;
+}
+
+static double dot(int64_t n, const double* a, const double* b) {
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  return s;
+}
+static double nrm2(int64_t n, const double* a) { return sqrt(dot(n, a, a)); }
+static void axpy(int64_t n, double al, const double* x, double* y) {
+  for (int64_t i = 0; i < n; ++i) y[i] += al * x[i];
+}
+
+/* Modified Gram-Schmidt applied twice: z <- (I - U U^T) z against the q orthonormal columns
+ * of U (n x q, column-major, leading dimension n).  coef[i] accumulates u_i^T z over both
+ * passes (so that z_in = U coef + z_out).  Returns ||z_out||. */
+static double mgs2(int64_t n, int q, const double* U, double* z, double* coef) {
+  for (int i = 0; i < q; ++i) coef[i] = 0.0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int i = 0; i < q; ++i) {
+      double t = dot(n, U + (int64_t)i * n, z);
+      coef[i] += t;
+      axpy(n, -t, U + (int64_t)i * n, z);
+    }
+  return nrm2(n, z);
+}
+
+/* back substitution R c = e, R upper triangular q x q stored column-major with leading dim ld */
+static void backsolve(int q, const double* R, int ld, const double* e, double* c) {
+  for (int i = q - 1; i >= 0; --i) {
+    double s = e[i];
+    for (int l = i + 1; l < q; ++l) s -= R[(int64_t)l * ld + i] * c[l];
+    c[i] = s / R[(int64_t)i * ld + i];
+  }
+}
+
+static void residual(const or_mat* A, const double* b, const double* x, double* r) {
+  or_spmv(A, x, r);
+  for (int64_t i = 0; i < A->n; ++i) r[i] = b[i] - r[i];
+}
+
+int or_solve(const or_mat* A, const double* b, const double* x0, int m, int variant,
+             const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+             double* hist, int hist_cap) {
+  const int64_t n = A->n;
+  memset(rep, 0, sizeof(*rep));
+  const int kk = (variant != 0 && W != NULL) ? k : 0;
+  rep->k_used = kk;
+  double bnorm = nrm2(n, b);
+  if (bnorm == 0.0) {                       /* b = 0 -> x = 0 */
+    memset(x, 0, sizeof(double) * n);
+    rep->converged = 1;
+    return 0;
+  }
+  if (x0) memcpy(x, x0, sizeof(double) * n); else memset(x, 0, sizeof(double) * n);
+
+  const int qmax = kk + m;
+  double* V = malloc(sizeof(double) * n * (m + 1));       /* Krylov basis */
+  double* UZ = malloc(sizeof(double) * n * (qmax + 1));   /* orthonormal image basis */
+  double* RZ = calloc((size_t)(qmax + 1) * (qmax + 1), sizeof(double));
+  double* e = malloc(sizeof(double) * (qmax + 1));
+  double* c = malloc(sizeof(double) * (qmax + 1));
+  double* coef = malloc(sizeof(double) * (qmax + m + 2));
+  double* r = malloc(sizeof(double) * n);
+  double* rho = malloc(sizeof(double) * n);
+  double* w = malloc(sizeof(double) * n);
+  double* z = malloc(sizeof(double) * n);
+  if (!V || !UZ || !RZ || !e || !c || !coef || !r || !rho || !w || !z) { rep->status = 2; goto out; }
+
+  /* U_C, R_C: thin QR of C = A W by MGS2, column by column (columns 0..kk-1 of U_Z / R_Z). */
+  for (int l = 0; l < kk; ++l) {
+    or_spmv(A, W + (int64_t)l * n, z);
+    double cn = nrm2(n, z);
+    double zn = mgs2(n, l, UZ, z, coef);
+    if (!(zn > 1e-12 * cn)) { rep->status = 1; goto out; }
+    for (int i = 0; i < l; ++i) RZ[(int64_t)l * (qmax + 1) + i] = coef[i];
+    RZ[(int64_t)l * (qmax + 1) + l] = zn;
+    for (int64_t i = 0; i < n; ++i) UZ[(int64_t)l * n + i] = z[i] / zn;
+  }
+  /* start: x <- x + W R_C^{-1} U_C^T r(x)  (min over x + span W) */
+  if (kk > 0) {
+    residual(A, b, x, r);
+    for (int l = 0; l < kk; ++l) {          /* MGS projection coefficients of r on U_C */
+      e[l] = dot(n, UZ + (int64_t)l * n, r);
+      axpy(n, -e[l], UZ + (int64_t)l * n, r);
+    }
+    backsolve(kk, RZ, qmax + 1, e, c);
+    for (int l = 0; l < kk; ++l) axpy(n, c[l], W + (int64_t)l * n, x);
+  }
+
+  for (;;) {
+    residual(A, b, x, r);
+    double beta = nrm2(n, r);
+    rep->rel_residual = beta / bnorm;
+    if (beta / bnorm <= tol) { rep->converged = 1; break; }
+    if (rep->iterations >= max_iters) break;
+    rep->cycles++;
+    /* rho = r - U_C U_C^T r (MGS) and e[0..kk) */
+    memcpy(rho, r, sizeof(double) * n);
+    for (int l = 0; l < kk; ++l) {
+      e[l] = dot(n, UZ + (int64_t)l * n, rho);
+      axpy(n, -e[l], UZ + (int64_t)l * n, rho);
+    }
+    /* Krylov start vector: r_c (plain, augment) or P r_c (deflate, Table 1 row 6) */
+    if (variant == 2 && kk > 0) {
+      memcpy(w, r, sizeof(double) * n);
+      mgs2(n, kk, UZ, w, coef);
+    } else {
+      memcpy(w, r, sizeof(double) * n);
+    }
+    double v0n = nrm2(n, w);
+    if (!(v0n > 0.0)) break;
+    for (int64_t i = 0; i < n; ++i) V[i] = w[i] / v0n;
+
+    int q = kk;   /* current image-basis size */
+    for (int j = 0; j < m; ++j) {
+      double* vj = V + (int64_t)j * n;
+      or_spmv(A, vj, w);                    /* w = A v_j */
+      /* image column A v_j -> U_Z by MGS2 */
+      memcpy(z, w, sizeof(double) * n);
+      double wn = nrm2(n, w);
+      double zn = mgs2(n, q, UZ, z, coef);
+      int image_breakdown = !(zn > 1e-14 * wn);
+      if (!image_breakdown) {
+        for (int i = 0; i < q; ++i) RZ[(int64_t)q * (qmax + 1) + i] = coef[i];
+        RZ[(int64_t)q * (qmax + 1) + q] = zn;
+        for (int64_t i = 0; i < n; ++i) UZ[(int64_t)q * n + i] = z[i] / zn;
+        e[q] = dot(n, UZ + (int64_t)q * n, rho);
+        axpy(n, -e[q], UZ + (int64_t)q * n, rho);
+        ++q;
+      }
+      double res = nrm2(n, rho);
+      /* next Krylov vector: Arnoldi (MGS2) on A (plain/augment) or on P A (deflate) */
+      if (variant == 2 && kk > 0) mgs2(n, kk, UZ, w, coef);
+      double hn = mgs2(n, j + 1, V, w, coef);
+      rep->iterations++;
+      if (hist && rep->hist_len < hist_cap) hist[rep->hist_len++] = res / bnorm;
+      int stop = (res / bnorm <= tol) || image_breakdown || !(hn > 1e-14 * beta) || j == m - 1 ||
+                 rep->iterations >= max_iters;
+      if (!stop) {
+        for (int64_t i = 0; i < n; ++i) V[(int64_t)(j + 1) * n + i] = w[i] / hn;
+        continue;
+      }
+      /* coefficients over the search basis [W, v_0, ..., v_{q-kk-1}] */
+      backsolve(q, RZ, qmax + 1, e, c);
+      for (int l = 0; l < kk; ++l) axpy(n, c[l], W + (int64_t)l * n, x);
+      for (int i = kk; i < q; ++i) axpy(n, c[i], V + (int64_t)(i - kk) * n, x);
+      break;
+    }
+  }
+out:
+  free(V); free(UZ); free(RZ); free(e); free(c); free(coef); free(r); free(rho); free(w); free(z);
+  return rep->status;
+}
+
+/* Apply the north-star deflation projector P = I - AW((AW)^T AW)^{-1}(AW)^T (the
+ * "orthogonal projector onto A V_s" applied as I - P_{AV,AV}) to the `nz` vectors Z (n x nz,
+ * column-major) in place, via the MGS2 QR of AW exactly as or_solve uses it.  Returns 1 if AW is
+ * rank deficient.  Exposed so tests can check idempotence and P A W = 0. */
+int or_lsproj(const or_mat* A, const double* W, int k, double* Z, int nz) {
+  const int64_t n = A->n;
+  double* UC = malloc(sizeof(double) * n * (k + 1));
+  double* coef = malloc(sizeof(double) * (k + 1));
+  int st = 0;
+  for (int l = 0; l < k && !st; ++l) {
+    double* z = UC + (int64_t)l * n;
+    or_spmv(A, W + (int64_t)l * n, z);
+    double cn = nrm2(n, z);
+    double zn = mgs2(n, l, UC, z, coef);
+    if (!(zn > 1e-12 * cn)) { st = 1; break; }
+    for (int64_t i = 0; i < n; ++i) z[i] /= zn;
+  }
+  if (!st)
+    for (int c = 0; c < nz; ++c) mgs2(n, k, UC, Z + (int64_t)c * n, coef);
+  free(UC); free(coef);
+  return st;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Thin SVD of X (n x s, column-major, leading dimension ldx) by one-sided Jacobi.
+ * U (n x s) receives the left singular vectors (columns with sigma = 0 are left as computed,
+ * i.e. zero), sigma[0..s) the singular values non-increasing.  *rank = #{sigma > 1e-12 sigma_1}.
+ * Returns the number of sweeps used. */
+int or_svd(int64_t n, int s, const double* X, int64_t ldx, double* U, double* sigma, int* rank) {
+  for (int j = 0; j < s; ++j) memcpy(U + (int64_t)j * n, X + (int64_t)j * ldx, sizeof(double) * n);
+  int sweep;
+  for (sweep = 0; sweep < 60; ++sweep) {
+    int rotated = 0;
+    for (int p = 0; p < s - 1; ++p)
+      for (int q = p + 1; q < s; ++q) {
+        double* up = U + (int64_t)p * n;
+        double* uq = U + (int64_t)q * n;
+        long double a = 0.0L, bb = 0.0L, g = 0.0L;
+        for (int64_t i = 0; i < n; ++i) {
+          a += (long double)up[i] * up[i];
+          bb += (long double)uq[i] * uq[i];
+          g += (long double)up[i] * uq[i];
+        }
+        if (g == 0.0L) continue;
+        if (fabsl(g) <= 1e-15L * sqrtl(a * bb)) continue;
+        long double zeta = (bb - a) / (2.0L * g);
+        long double t = (zeta >= 0 ? 1.0L : -1.0L) / (fabsl(zeta) + sqrtl(1.0L + zeta * zeta));
+        long double cs = 1.0L / sqrtl(1.0L + t * t), sn = cs * t;
+        for (int64_t i = 0; i < n; ++i) {
+          long double xp = up[i], xq = uq[i];
+          up[i] = (double)(cs * xp - sn * xq);
+          uq[i] = (double)(sn * xp + cs * xq);
+        }
+        rotated = 1;
+      }
+    if (!rotated) break;
+  }
+  /* column norms, sort non-increasing (selection sort; s is small) */
+  int* perm = malloc(sizeof(int) * s);
+  double* nr = malloc(sizeof(double) * s);
+  for (int j = 0; j < s; ++j) {
+    long double t = 0.0L;
+    for (int64_t i = 0; i < n; ++i) t += (long double)U[(int64_t)j * n + i] * U[(int64_t)j * n + i];
+    nr[j] = (double)sqrtl(t);
+    perm[j] = j;
+  }
+  for (int a = 0; a < s; ++a) {
+    int best = a;
+    for (int c2 = a + 1; c2 < s; ++c2)
+      if (nr[perm[c2]] > nr[perm[best]]) best = c2;
+    int tmp = perm[a]; perm[a] = perm[best]; perm[best] = tmp;
+  }
+  double* tmpU = malloc(sizeof(double) * n * s);
+  memcpy(tmpU, U, sizeof(double) * n * s);
+  for (int a = 0; a < s; ++a) {
+    double sg = nr[perm[a]];
+    sigma[a] = sg;
+    for (int64_t i = 0; i < n; ++i)
+      U[(int64_t)a * n + i] = sg > 0.0 ? tmpU[(int64_t)perm[a] * n + i] / sg : 0.0;
+  }
+  int rk = 0;
+  for (int a = 0; a < s; ++a)
+    if (sigma[0] > 0.0 && sigma[a] > 1e-12 * sigma[0]) ++rk;
+  *rank = rk;
+  free(perm); free(nr); free(tmpU);
+  return sweep;
+}

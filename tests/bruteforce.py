@@ -1,0 +1,64 @@
+"""Brute-force numpy references used to PIN the oracle on tiny inputs.
+
+Independent of ``oracle/`` (no shared code): dense matrices, explicit spaces, LAPACK least squares
+(``numpy.linalg.lstsq``), Householder QR (``numpy.linalg.qr``) and the literal projector formula of
+PAPER.md Table 1 row 6 (``I - AV(V^T A^T A V)^{-1} V^T A^T``).  Small n only.
+"""
+import numpy as np
+
+
+def ls_projector(A, W):
+    """P = I - AW((AW)^T AW)^{-1}(AW)^T, written literally."""
+    C = A @ W
+    return np.eye(A.shape[0]) - C @ np.linalg.inv(C.T @ C) @ C.T
+
+
+def _orth_append(K, v):
+    """Return an orthonormal basis of span(K, v) (Householder QR of the stacked matrix)."""
+    M = np.column_stack(K + [v])
+    Q, _ = np.linalg.qr(M)
+    return [Q[:, i] for i in range(Q.shape[1])]
+
+
+def restarted_minres(A, b, m, variant="plain", W=None, tol=1e-8, max_iters=2000, x0=None):
+    """x_{c,j} = argmin over x_c (+ span W) + K_j(op, v) of ||b - A x||, cycle by cycle.
+
+    op/v: plain, augment -> (A, r_c); deflate -> (P A, P r_c).  Start for recycled variants:
+    x_0 <- x0 + W lstsq(AW, r(x0)).  Returns (x, iterations, history)."""
+    n = A.shape[0]
+    bn = np.linalg.norm(b)
+    x = np.zeros(n) if x0 is None else np.array(x0, dtype=float)
+    rec = variant != "plain" and W is not None and W.shape[1] > 0
+    if rec:
+        C = A @ W
+        x = x + W @ np.linalg.lstsq(C, b - A @ x, rcond=None)[0]
+        P = ls_projector(A, W)
+    hist, iters = [], 0
+    while True:
+        r = b - A @ x
+        if np.linalg.norm(r) / bn <= tol or iters >= max_iters:
+            break
+        if variant == "deflate" and rec:
+            op, v = P @ A, P @ r
+        else:
+            op, v = A, r
+        K = [v / np.linalg.norm(v)]
+        for j in range(m):
+            S = np.column_stack(([W[:, i] for i in range(W.shape[1])] if rec else []) + K)
+            y = np.linalg.lstsq(A @ S, r, rcond=None)[0]
+            res = np.linalg.norm(r - A @ S @ y)
+            hist.append(res / bn)
+            iters += 1
+            if res / bn <= tol or j == m - 1 or iters >= max_iters:
+                x = x + S @ y
+                break
+            K = _orth_append(K, op @ K[-1])
+    return x, iters, np.array(hist)
+
+
+def random_nonsym(n, rng, shift=2.5, density=1.0):
+    """Dense non-symmetric test matrix shift*I + G/sqrt(n) (eigenvalues in a disc around shift)."""
+    G = rng.standard_normal((n, n)) / np.sqrt(n)
+    if density < 1.0:
+        G *= rng.random((n, n)) < density
+    return shift * np.eye(n) + G
