@@ -1,0 +1,180 @@
+/* rg.h — C ABI of the B200-native recycled GMRES(m) library (librg.so).
+ *
+ * Solves a SEQUENCE of sparse non-symmetric systems A_t x_t = b_t whose matrices and right-hand
+ * sides arrive one at a time and may depend on earlier solutions (eqs.
+ * algebra_pde / sequence_linear_systems: "they are not entirely available until the very last
+ * element of the sequence").  Each solve is restarted GMRES(m),
+ * optionally accelerated by a recycle space W built from the dominant left singular vectors of a
+ * window of previous solutions (Algorithm 1), used through
+ *   augmentation: search space x_c + span(W) + K_j(A, r_c)
+ *   deflation   : x_c + span(W) + K_j(P A, P r_c), P = I - AW((AW)^T AW)^{-1}(AW)^T
+ *                 (Table 1 row "deflated LS" :348; = GCRO inner iteration :332).
+ * Every step runs in hand-written fp64 CUDA kernels for sm_100a; there is no CPU fallback.
+ *
+ * Conventions shared by all entry points
+ *   - Every function returns rg_status; nothing aborts, throws or exits.  On failure the
+ *     thread-local message rg_last_error() says why.
+ *   - Pointers tagged by an rg_mem argument are HOST (pageable or pinned) or DEVICE (same CUDA
+ *     device as the context, e.g. a torch tensor's data_ptr()) memory.  The caller owns every
+ *     buffer it passes; the library deep-copies what it keeps into device memory it owns.
+ *   - All work is issued on the caller's CUDA stream (rg_options.cuda_stream, NULL = legacy
+ *     default stream) and every call returns only when its results are complete
+ *     (host-synchronous).
+ *   - Dense vectors are fp64, length n, contiguous.  Indices are int32 (n, nnz < 2^31).
+ *   - A context is single-owner and not thread-safe; distinct contexts are independent.
+ */
+#ifndef RG_H
+#define RG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define RG_API __attribute__((visibility("default")))
+#else
+#define RG_API
+#endif
+
+typedef struct rg_ctx rg_ctx; /* opaque; created by rg_create, owned by the library */
+
+typedef enum {
+  RG_OK = 0,
+  RG_E_INVAL = 1,    /* invalid argument; no side effects                                      */
+  RG_E_NOMEM = 2,    /* device or host allocation failed                                       */
+  RG_E_CUDA = 3,     /* CUDA runtime error (message has the CUDA error string)                 */
+  RG_E_STATE = 4,    /* call not valid in the current state (e.g. build with no snapshots)      */
+  RG_E_SINGULAR = 5, /* A W rank deficient: min|r_ii| <= 1e-12 max|r_ii| of R_C (PAPER.md:562-564
+                        "E_s may be singular"); the recycle space is cleared                   */
+  RG_E_NUMERIC = 6   /* NaN/Inf met during the solve                                           */
+} rg_status;
+
+typedef enum { RG_CSR = 0, RG_BSR = 1 } rg_format;
+typedef enum { RG_PLAIN = 0, RG_AUGMENT = 1, RG_DEFLATE = 2 } rg_variant;
+typedef enum { RG_HOST = 0, RG_DEVICE = 1 } rg_mem;
+
+/* A sparse matrix handed to rg_create / rg_update_matrix.
+ *   CSR : n_rows scalar rows; row_ptr[n_rows+1] (row_ptr[0] = 0, non-decreasing,
+ *         row_ptr[n_rows] = nnz); col_idx[nnz] strictly increasing within each row, in [0,n);
+ *         val[nnz].  block must be 1.
+ *   BSR : block = b (b divides n_rows); nb = n_rows/b block rows; row_ptr[nb+1] over blocks;
+ *         col_idx[nnz] block-column indices (strictly increasing per block row); nnz = number of
+ *         stored blocks; val[nnz*b*b], each b x b block stored COLUMN-MAJOR
+ *         (val[p*b*b + c*b + r] = block_p(r, c)).
+ *   In rg_update_matrix, row_ptr == col_idx == NULL keeps the current pattern and replaces the
+ *   values only (the fast path for sequences with a fixed sparsity pattern).
+ *   sell_C = 32 packs a CSR matrix into SELL-32-sigma internally (sell_sigma = 1: no row
+ *   sorting; other sigma values are rejected in this version); sell_C = 0 keeps CSR. */
+typedef struct {
+  rg_format fmt;
+  int64_t n_rows;
+  int64_t nnz;
+  int32_t block;
+  const int32_t* row_ptr;
+  const int32_t* col_idx;
+  const double* val;
+  rg_mem mem;
+  int32_t sell_C;
+  int32_t sell_sigma;
+} rg_matrix;
+
+/* Capacity limits fixed at creation (they size the device buffers):
+ *   max_m         largest restart length m accepted by rg_solve      (1..128)
+ *   max_snapshots snapshot-window capacity s (Algorithm 1's window)   (1..64)
+ *   max_k         largest recycle dimension k                         (0..64, <= max_snapshots)
+ *   cuda_stream   cudaStream_t to issue all work on (NULL = default stream)
+ *   flags         RG_FLAG_* bits below */
+typedef struct {
+  int32_t max_m, max_snapshots, max_k;
+  void* cuda_stream;
+  int32_t flags;
+} rg_options;
+
+#define RG_FLAG_NO_GRAPH 1 /* launch kernels one by one instead of replaying CUDA graphs      */
+#define RG_FLAG_PROFILE 2  /* record per-kernel device time (%globaltimer) for rg_kernel_stats */
+
+/* Solve report (fields follow SPEC.md's SolveReport).
+ *   iterations   Arnoldi steps summed over restart cycles (residual and C = AW products are
+ *                not counted; they are in spmv_count)
+ *   restarts     restart cycles after the first
+ *   converged    1 iff the TRUE relative residual ||b - A x||/||b|| <= tol
+ *   k_eff        recycle dimension actually used (0 for plain or empty recycle space)
+ *   spmv_count   sparse products issued by this solve
+ *   history_len  entries written to history (one per Arnoldi step, least-squares estimate of
+ *                the relative residual)
+ *   rel_residual final true relative residual
+ *   ms_total     device time of the solve (CUDA events), milliseconds */
+typedef struct {
+  int32_t iterations, restarts, converged, k_eff, spmv_count, history_len;
+  double rel_residual, ms_total;
+} rg_report;
+
+/* Create a context for systems of dimension n with initial matrix A (validated and copied). */
+RG_API rg_status rg_create(rg_ctx** ctx, int64_t n, const rg_matrix* A, const rg_options* opt);
+
+/* Replace A (same n and format).  Keeps the snapshot window and W; invalidates C = A W, its QR
+ * factor Q and R_C, which are rebuilt by the next recycled solve. */
+RG_API rg_status rg_update_matrix(rg_ctx* ctx, const rg_matrix* A);
+
+/* Append solution x (length n) to the snapshot window X (Algorithm 1 line "store the solution
+ * x_i in the matrix X_m"), evicting the oldest column when the window is full. */
+RG_API rg_status rg_push_snapshot(rg_ctx* ctx, const double* x, rg_mem mem);
+
+/* Forget all snapshots and the recycle space. */
+RG_API rg_status rg_clear_snapshots(rg_ctx* ctx);
+
+/* Recycle space from the window: thin SVD X = Psi Sigma Phi^T, W = the first
+ * k_eff = min(k, #snapshots, #{sigma_i > 1e-12 sigma_1}) left singular vectors.
+ *   k       requested dimension, 1..max_k
+ *   k_eff   (out, nullable) dimension kept
+ *   sigma   (out, nullable, host) the #snapshots singular values, non-increasing
+ * RG_E_STATE if the window is empty. */
+RG_API rg_status rg_build_recycle(rg_ctx* ctx, int32_t k, int32_t* k_eff, double* sigma);
+
+/* Solve A x = b with restarted GMRES(m), variant plain / augment / deflate.
+ *   b, x0      length n in `mem`; x0 == NULL means x0 = 0
+ *   m          restart length, 1..max_m
+ *   tol        > 0; convergence is ||b - A x||_2 / ||b||_2 <= tol on the true residual
+ *   max_iters  cap on Arnoldi steps (>= 1)
+ *   x_out      length n in `mem`
+ *   history    nullable HOST array receiving up to history_cap relative-residual estimates
+ *   rep        nullable report
+ * A recycled variant with an empty recycle space runs plain GMRES (k_eff = 0).  b = 0 gives
+ * x = 0, converged, 0 iterations.  Non-convergence is RG_OK with rep->converged = 0. */
+RG_API rg_status rg_solve(rg_ctx* ctx, const double* b, const double* x0, int32_t m, rg_variant v,
+                          double tol, int32_t max_iters, double* x_out, rg_mem mem, double* history,
+                          int32_t history_cap, rg_report* rep);
+
+/* y = A x with the context's current matrix (x, y length n in `mem`). */
+RG_API rg_status rg_apply(rg_ctx* ctx, const double* x, double* y, rg_mem mem);
+
+/* Copy out internal recycle quantities (for inspection and tests):
+ *   RG_EXPORT_W   W   (n x k_eff, column-major, leading dimension n)
+ *   RG_EXPORT_Q   Q   (n x k_eff) orthonormal basis of A W       (after a recycled solve)
+ *   RG_EXPORT_RC  R_C (k_eff x k_eff, column-major, upper triangular, A W = Q R_C)
+ * `out` must hold the stated number of doubles; returns RG_E_STATE if the item is unavailable. */
+#define RG_EXPORT_W 0
+#define RG_EXPORT_Q 1
+#define RG_EXPORT_RC 2
+RG_API rg_status rg_export(rg_ctx* ctx, int32_t which, double* out, rg_mem mem, int32_t* k_eff);
+
+/* Per-kernel device-time statistics recorded while RG_FLAG_PROFILE is set. */
+typedef struct {
+  char name[24];
+  int64_t launches;     /* launches that did work           */
+  int64_t noop_launches;/* launches that returned early      */
+  double total_ms;      /* summed device time of working launches (%globaltimer, first CTA start to
+                           last CTA end) */
+  double bytes;         /* summed algorithmic bytes (DESIGN.md byte model) */
+} rg_kstat;
+RG_API rg_status rg_kernel_stats(rg_ctx* ctx, rg_kstat* out, int32_t cap, int32_t* count);
+RG_API rg_status rg_reset_kernel_stats(rg_ctx* ctx);
+
+RG_API void rg_destroy(rg_ctx* ctx);
+RG_API const char* rg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RG_H */

@@ -1,0 +1,72 @@
+"""B200-native recycled GMRES(m) for sequences of convection-diffusion systems (arXiv:1807.09467).
+
+The product is ``lib/librg.so`` (C ABI in ``include/rg.h``; fp64 CUDA kernels for sm_100a in
+``csrc/``).  ``rg`` is its thin ctypes binding (same function names); ``Context`` is a small
+convenience wrapper over it that keeps the argument arrays alive.  Importing this package fails
+loudly when the CUDA library has not been built: there is no CPU fallback.
+"""
+from __future__ import annotations
+
+from . import rg
+from .rg import RgError  # noqa: F401
+
+__all__ = ["rg", "Context", "RgError"]
+
+
+class Context:
+    """One rg_ctx: a sequence solver for systems of dimension n (marshalling only)."""
+
+    def __init__(self, n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, max_m=64,
+                 max_snapshots=32, max_k=32, stream=None, flags=0):
+        keep = []
+        self.n, self.fmt, self.block, self.sell_C = int(n), fmt, int(block), int(sell_C)
+        A = rg.make_matrix(n, row_ptr, col_idx, val, fmt, block, sell_C, keep)
+        self.max_snapshots = max_snapshots
+        self.ctx = rg.rg_create(n, A, max_m, max_snapshots, max_k, stream, flags)
+
+    def update_matrix(self, val, row_ptr=None, col_idx=None):
+        keep = []
+        A = rg.make_matrix(self.n, row_ptr, col_idx, val, self.fmt, self.block, self.sell_C, keep)
+        rg.rg_update_matrix(self.ctx, A)
+
+    def push_snapshot(self, x):
+        rg.rg_push_snapshot(self.ctx, x)
+
+    def clear_snapshots(self):
+        rg.rg_clear_snapshots(self.ctx)
+
+    def build_recycle(self, k):
+        k_eff, sig = rg.rg_build_recycle(self.ctx, k, self.max_snapshots)
+        return k_eff, sig
+
+    def solve(self, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=20000, history_cap=0):
+        return rg.rg_solve(self.ctx, b, x_out, x0, m, variant, tol, max_iters, history_cap)
+
+    def apply(self, x, y):
+        rg.rg_apply(self.ctx, x, y)
+
+    def export(self, which, out):
+        return rg.rg_export(self.ctx, which, out)
+
+    def kernel_stats(self):
+        return rg.rg_kernel_stats(self.ctx)
+
+    def reset_kernel_stats(self):
+        rg.rg_reset_kernel_stats(self.ctx)
+
+    def close(self):
+        if self.ctx is not None:
+            rg.rg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()

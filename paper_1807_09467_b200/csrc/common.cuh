@@ -1,0 +1,191 @@
+// common.cuh — internal definitions of librg (B200 / sm_100a, fp64).
+//
+// Device-resident solver state, the basis layout in HBM, and the deterministic grid-reduction
+// machinery shared by every reducing kernel.  See DESIGN.md §"Data layout" and §"Kernels".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rg.h"
+
+namespace rg {
+
+// ---------------------------------------------------------------- capacity limits
+constexpr int MAXM = 128;                  // restart length
+constexpr int MAXK = 64;                   // recycle dimension
+constexpr int MAXS = 64;                   // snapshot window
+constexpr int MAXCOL = 2 * MAXK + MAXM + 2;// columns of the basis buffer Z = [W | Q | V]
+constexpr int MAXRED = MAXCOL + 2;         // values one grid reduction can return
+
+// ---------------------------------------------------------------- launch geometry
+constexpr int OT = 512;                    // threads per CTA of the vector kernels
+constexpr int NWARP = OT / 32;
+constexpr int NSM = 148;                   // B200 SMs
+constexpr int VEC_CTAS_PER_SM = 2;         // -> 296 CTAs: 32 resident warps / SM
+
+// ---------------------------------------------------------------- kernel ids (statistics)
+enum KernelId {
+  K_SPMV_STEP = 0, K_SPMV_RES, K_SPMV_PLAIN, K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN,
+  K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_COUNT
+};
+
+struct KStatDev {
+  unsigned long long launches, noop, ns, start;
+  double bytes;
+};
+
+// ---------------------------------------------------------------- device-resident solver state
+// Written by the host once per solve (header) and then driven entirely by kernel epilogues:
+// the host never needs to read it until the solve (or a restart cycle) ends.
+struct DevState {
+  // per-solve header (host -> device before the solve)
+  int variant, m, k_eff, max_iters, hist_cap, profile;
+  double tol;
+  // dynamic scalars
+  int j;          // current Arnoldi step within the cycle
+  int active;     // Arnoldi steps of this cycle still running
+  int done;       // solve finished
+  int converged;
+  int iters;      // Arnoldi steps summed over cycles
+  int cycles;
+  int status;     // 0 ok, RG_E_NUMERIC
+  int have_xupd;  // cycle-end x update pending
+  int jfinal;     // last step index of the finished cycle
+  int hist_len;
+  int spmv_count;
+  int bzero;
+  double bnorm, beta, relres;
+  // least-squares state
+  double cs[MAXM], sn[MAXM], g[MAXM + 2], y[MAXM + 2];
+  double R[MAXM][MAXM + 2];        // rotated columns, R[j][0..j]
+  double Hraw[MAXM][MAXM + 2];     // unrotated Hessenberg columns (augment)
+  double Bm[MAXM][MAXK];           // deflate: B[:, j] = Q^T A v_j   (GCRO: A V = Q B + V H)
+  double Gm[MAXM + 2][MAXK];       // augment: G[i, :] = Q^T v_i
+  double T[MAXM + 2][MAXM + 2];    // augment: Cholesky factor of I - G^T G, T[col][row]
+  double RCinv[MAXK][MAXK];        // R_C^{-1}, column-major [col][row]
+  double RC[MAXK][MAXK];           // R_C, column-major [col][row]
+  double coef[MAXCOL];             // coefficients of the current CGS pass (absolute column)
+  double hcol[MAXCOL];             // accumulated coefficients of the current column
+  double coefx[MAXCOL];            // cycle-end x-update coefficients
+  double sc[MAXCOL];               // column scales (V stored un-normalised: v_i = sc_i * raw_i)
+  KStatDev kstat[K_COUNT];
+};
+
+// Basis layout (constant per context).  Z is n_pad x MAXCOL... column-major with leading
+// dimension ld; columns [0, maxk) hold W, [VB - k_eff, VB) hold Q, [VB, VB + m + 1) hold V.
+struct Layout {
+  double* Z;
+  int64_t ld;      // = n_pad (multiple of 64)
+  int64_t n;       // true dimension
+  int maxk;        // W / Q region width
+  int VB;          // first V column = 2 * maxk
+  double* x;       // iterate (n_pad)
+  const double* b; // right-hand side (n_pad)
+  double* hist;    // history buffer (hist_cap)
+  double* partial; // grid-reduction partials [grid][MAXRED]
+  unsigned* counter;
+};
+
+// ---------------------------------------------------------------- small device helpers
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;  // valid in lane 0
+}
+
+// Deterministic block sum (fixed tree), result broadcast to all threads.  `sh` >= 33 doubles.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < nw; ++i) s += sh[i];
+    sh[32] = s;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+// Kernel-entry profiling hook (block 0 stamps the start time).
+__device__ __forceinline__ void prof_begin(DevState* st, int kid) {
+  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) st->kstat[kid].start = gtimer();
+}
+__device__ __forceinline__ void prof_noop(DevState* st, int kid) {
+  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) st->kstat[kid].noop++;
+}
+// Called by ONE thread of the last CTA.
+__device__ __forceinline__ void prof_end(DevState* st, int kid, double bytes) {
+  if (st->profile) {
+    KStatDev& k = st->kstat[kid];
+    k.ns += gtimer() - k.start;
+    k.launches++;
+    k.bytes += bytes;
+  }
+}
+
+// Deterministic two-stage grid reduction.  Every CTA passes nv values in shared memory `vals`
+// (nv <= MAXRED).  Returns true in exactly one CTA (the last to arrive), whose shared array `tot`
+// then holds the totals, summed over CTAs in index order.  `scr` needs max(blockDim, MAXRED)
+// doubles (max(blockDim, nv) if nv > MAXRED).  ldp = row stride of `partial`.
+// All threads of every CTA must call it.
+__device__ __forceinline__ bool grid_reduce(const double* vals, int nv, double* partial,
+                                            unsigned* counter, double* tot, double* scr,
+                                            int ldp = MAXRED) {
+  __shared__ unsigned s_ticket;
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) partial[(size_t)blockIdx.x * ldp + i] = vals[i];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (s_ticket != gridDim.x - 1) return false;
+  __threadfence();
+  const int G = gridDim.x;
+  int S = nv > 0 ? (int)blockDim.x / nv : 1;
+  if (S < 1) S = 1;
+  for (int idx = threadIdx.x; idx < S * nv; idx += blockDim.x) {
+    const int c = idx % nv, s = idx / nv;
+    double a = 0.0;
+    for (int b = s; b < G; b += S) a += __ldcg(&partial[(size_t)b * ldp + c]);
+    scr[idx] = a;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+    double a = 0.0;
+    for (int s = 0; s < S; ++s) a += scr[s * nv + c];
+    tot[c] = a;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  __syncthreads();
+  return true;
+}
+
+// Ticket only (no values): returns true in the last CTA.  Used for profiling of kernels that
+// have no reduction.
+__device__ __forceinline__ bool grid_last(unsigned* counter) {
+  __shared__ unsigned s_t;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_t = atomicAdd(counter, 1u);
+  __syncthreads();
+  if (s_t != gridDim.x - 1) return false;
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+inline int vec_grid(int64_t rows) {
+  int64_t g = (rows + OT - 1) / OT;
+  int64_t cap = (int64_t)NSM * VEC_CTAS_PER_SM;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+}  // namespace rg

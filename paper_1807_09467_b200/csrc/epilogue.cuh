@@ -1,0 +1,235 @@
+// epilogue.cuh — work done by the LAST CTA of a reducing kernel, on the device-resident state.
+//
+// These replace the host round trips of a textbook GMRES: the Givens least-squares update
+// (one warp / thread, "not computed naively ... but in more efficient ways"), the
+// restart decision, the GCRO (deflate) and G/T/M (augment) bookkeeping and the cycle-end
+// coefficient computation.  All threads of the last CTA call each function (they contain
+// __syncthreads); the serial chains run in thread 0 from shared memory.
+#pragma once
+#include "common.cuh"
+
+namespace rg {
+
+// ---------------------------------------------------------------- cycle start
+// beta2 = ||r_c||^2 of the (projected) residual r_c = b - A x_c stored in V column 0.
+__device__ __forceinline__ void epi_cycle_start(DevState* st, const Layout& L, double beta2) {
+  if (threadIdx.x == 0) {
+    const double beta = sqrt(beta2);
+    st->beta = beta;
+    st->relres = beta / st->bnorm;
+    st->have_xupd = 0;
+    if (!isfinite(beta)) {
+      st->status = RG_E_NUMERIC;
+      st->done = 1;
+      st->active = 0;
+    } else if (st->relres <= st->tol) {
+      st->done = 1;
+      st->converged = 1;
+      st->active = 0;
+    } else if (st->iters >= st->max_iters) {
+      st->done = 1;
+      st->active = 0;
+    } else {
+      st->active = 1;
+      st->j = 0;
+      st->cycles++;
+      st->sc[L.VB] = 1.0 / beta;
+      st->g[0] = beta;
+      if (st->variant == RG_AUGMENT) {
+        // v_0 = r_c/beta with Q^T r_c = 0 after the cycle-start projection: G[0,:] = 0, T00 = 1.
+        st->T[0][0] = 1.0;
+        for (int l = 0; l < st->k_eff; ++l) st->Gm[0][l] = 0.0;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- CGS2 passes
+// tot[0..nd) = raw dots with columns [d0, d0+nd); h_c = sc_c * dot.
+__device__ __forceinline__ void epi_pass(DevState* st, const double* tot, int d0, int nd, bool first) {
+  for (int c = threadIdx.x; c < nd; c += blockDim.x) {
+    const double v = st->sc[d0 + c] * tot[c];
+    st->coef[d0 + c] = v;
+    st->hcol[d0 + c] = first ? v : st->hcol[d0 + c] + v;
+  }
+  __syncthreads();
+}
+
+// R_C^{-1} u for the k-vector u in shared memory -> out (shared); parallel over rows.
+__device__ __forceinline__ void rcinv_apply(const DevState* st, int k, const double* u, double* out) {
+  for (int l = threadIdx.x; l < k; l += blockDim.x) {
+    double s = 0.0;
+    for (int c = l; c < k; ++c) s += st->RCinv[c][l] * u[c];
+    out[l] = s;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- least-squares step
+// After the last CGS2 pass of Arnoldi step j: tot[0..nd) = Q^T w (augment, nd = k_eff),
+// tot[nd] = ||w||^2 of the new (un-normalised) basis vector w = raw v_{j+1}.
+__device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const double* tot, int nd) {
+  __shared__ double h[MAXM + 2], mc[MAXM + 2], tv[MAXM + 2], csS[MAXM], snS[MAXM];
+  __shared__ double ys[MAXM + 2], gs[MAXM + 2], us[MAXK], zs[MAXK];
+  __shared__ int s_stop, s_jf, s_tb;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int j = st->j, VB = L.VB, k = st->k_eff, var = st->variant;
+  const int QB = VB - k;
+  const double nrm = sqrt(tot[nd]);
+  for (int i = tid; i <= j; i += bd) h[i] = st->hcol[VB + i];
+  for (int i = tid; i < j; i += bd) { csS[i] = st->cs[i]; snS[i] = st->sn[i]; }
+  if (tid == 0) { h[j + 1] = nrm; s_tb = 0; s_stop = 0; }
+  __syncthreads();
+  for (int i = tid; i <= j + 1; i += bd) st->Hraw[j][i] = h[i];
+  if (var == RG_DEFLATE)
+    for (int l = tid; l < k; l += bd) st->Bm[j][l] = st->hcol[QB + l];
+  if (var == RG_AUGMENT)
+    for (int l = tid; l < k; l += bd) st->Gm[j + 1][l] = nrm > 0.0 ? tot[l] / nrm : 0.0;
+  __syncthreads();
+  if (var == RG_AUGMENT && k > 0) {
+    // M = I - G^T G restricted to v_0..v_{j+1}; new column of its Cholesky factor T.
+    for (int i = tid; i <= j + 1; i += bd) {
+      double s = (i == j + 1) ? 1.0 : 0.0;
+      for (int l = 0; l < k; ++l) s -= st->Gm[i][l] * st->Gm[j + 1][l];
+      mc[i] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double t2 = 0.0;
+      for (int i = 0; i <= j; ++i) {  // T_old^T t = M[0..j, j+1]
+        double s = mc[i];
+        for (int l = 0; l < i; ++l) s -= st->T[i][l] * tv[l];
+        tv[i] = s / st->T[i][i];
+        t2 += tv[i] * tv[i];
+      }
+      const double tau2 = mc[j + 1] - t2;
+      if (!(tau2 > 1e-14)) {
+        s_tb = 1;  // v_{j+1} (numerically) in span(Q) + span(V_{j+1}): end the cycle
+      } else {
+        for (int i = 0; i <= j; ++i) st->T[j + 1][i] = tv[i];
+        st->T[j + 1][j + 1] = sqrt(tau2);
+      }
+    }
+    __syncthreads();
+    if (!s_tb) {  // column j of M = T H: mc_i = sum_{l>=i} T(i,l) h_l
+      for (int i = tid; i <= j + 1; i += bd) {
+        double s = 0.0;
+        for (int l = i; l <= j + 1; ++l) s += st->T[l][i] * h[l];
+        mc[i] = s;
+      }
+      __syncthreads();
+      for (int i = tid; i <= j + 1; i += bd) h[i] = mc[i];
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    st->sc[VB + j + 1] = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    int stop = 0, jf = j;
+    if (s_tb) {
+      stop = 1;
+      jf = j - 1;
+      st->iters++;
+    } else {
+      for (int i = 0; i < j; ++i) {  // apply the previous rotations
+        const double a = h[i], b = h[i + 1];
+        h[i] = csS[i] * a + snS[i] * b;
+        h[i + 1] = -snS[i] * a + csS[i] * b;
+      }
+      const double a = h[j], b = h[j + 1];
+      const double den = hypot(a, b);
+      if (!(den > 0.0)) {  // A v_j = 0 within span: no progress possible in this cycle
+        s_tb = 1;
+        st->iters++;
+        jf = j - 1;
+        stop = 1;
+      }
+    }
+    if (!s_tb) {
+      const double a = h[j], b = h[j + 1];
+      const double den = hypot(a, b);
+      const double c = a / den, s = b / den;
+      st->cs[j] = c;
+      st->sn[j] = s;
+      h[j] = den;
+      for (int i = 0; i <= j; ++i) st->R[j][i] = h[i];
+      const double gj = st->g[j];
+      st->g[j] = c * gj;
+      st->g[j + 1] = -s * gj;
+      const double res = fabs(st->g[j + 1]) / st->bnorm;
+      if (st->hist_len < st->hist_cap) L.hist[st->hist_len++] = res;
+      st->iters++;
+      if (!isfinite(res)) {
+        st->status = RG_E_NUMERIC;
+        st->done = 1;
+        stop = 1;
+        jf = -1;
+      } else {
+        stop = (res <= st->tol) || (nrm <= 1e-14 * st->beta) || (j + 1 >= st->m) ||
+               (st->iters >= st->max_iters);
+      }
+    }
+    if (!stop) st->j = j + 1;
+    s_stop = stop;
+    s_jf = jf;
+    if (stop) {
+      st->active = 0;
+      st->jfinal = jf;
+      st->have_xupd = jf >= 0;
+    }
+    for (int i = 0; i <= jf; ++i) gs[i] = st->g[i];
+  }
+  __syncthreads();
+  if (!s_stop || s_jf < 0) return;
+  const int jf = s_jf;
+  // y = R^{-1} g[0..jf]  (column-oriented back substitution, parallel updates)
+  for (int i = jf; i >= 0; --i) {
+    if (tid == 0) ys[i] = gs[i] / st->R[i][i];
+    __syncthreads();
+    for (int l = tid; l < i; l += bd) gs[l] -= st->R[i][l] * ys[i];
+    __syncthreads();
+  }
+  for (int i = tid; i <= jf; i += bd) st->coefx[VB + i] = -ys[i];  // x += V y
+  if (k > 0 && var != RG_PLAIN) {
+    if (var == RG_DEFLATE) {  // x -= W R_C^{-1} B y
+      for (int l = tid; l < k; l += bd) {
+        double s = 0.0;
+        for (int i = 0; i <= jf; ++i) s += st->Bm[i][l] * ys[i];
+        us[l] = s;
+      }
+    } else {  // augment: x -= W R_C^{-1} G Hbar y
+      for (int i = tid; i <= jf + 1; i += bd) {
+        double s = 0.0;
+        for (int c = (i > 0 ? i - 1 : 0); c <= jf; ++c) s += st->Hraw[c][i] * ys[c];  // Hessenberg
+        mc[i] = s;
+      }
+      __syncthreads();
+      for (int l = tid; l < k; l += bd) {
+        double s = 0.0;
+        for (int i = 0; i <= jf + 1; ++i) s += st->Gm[i][l] * mc[i];
+        us[l] = s;
+      }
+    }
+    __syncthreads();
+    rcinv_apply(st, k, us, zs);
+    for (int l = tid; l < k; l += bd) st->coefx[l] = zs[l];  // x -= coefx_l W_l
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- cycle-start projection
+// tot[0..k) = Q^T r_c.  Sets the r update (r -= Q a) and the x update (x += W R_C^{-1} a).
+__device__ __forceinline__ void epi_cs_dq(DevState* st, const Layout& L, const double* tot) {
+  __shared__ double us[MAXK], zs[MAXK];
+  const int k = st->k_eff, QB = L.VB - k;
+  for (int l = threadIdx.x; l < k; l += blockDim.x) {
+    us[l] = tot[l];
+    st->coef[QB + l] = tot[l];
+  }
+  __syncthreads();
+  rcinv_apply(st, k, us, zs);
+  for (int l = threadIdx.x; l < k; l += blockDim.x) st->coefx[l] = -zs[l];
+  __syncthreads();
+}
+
+}  // namespace rg

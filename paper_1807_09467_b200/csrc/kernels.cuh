@@ -1,0 +1,62 @@
+// kernels.cuh — host-side launch interface of librg's device kernels.
+#pragma once
+#include "common.cuh"
+
+namespace rg {
+
+// Sparse matrix as stored on the device.
+struct MatDev {
+  int fmt = 0;                  // 0 CSR, 1 SELL-32, 2 BSR
+  int64_t n = 0;
+  const int32_t* rp = nullptr;  // CSR row pointer / BSR block-row pointer
+  const int32_t* ci = nullptr;  // CSR columns / BSR block columns
+  const double* v = nullptr;    // CSR values / BSR blocks (column-major b x b)
+  int lpr = 4;                  // CSR lanes per row
+  int b = 1;                    // BSR block size
+  int64_t nb = 0;               // BSR block rows
+  const int64_t* sp = nullptr;  // SELL slice pointer (entry offset of slice s)
+  const int32_t* sw = nullptr;  // SELL slice widths
+  const int32_t* sci = nullptr; // SELL columns (column-major inside a slice)
+  const double* sv = nullptr;   // SELL values
+  int64_t nslices = 0;
+  double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
+};
+
+enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2 };
+
+// w = A v_j (STEP), r = b - A x (RES; epi != 0 runs the cycle-start epilogue on ||r||^2),
+// y = A x (PLAIN).
+cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode, const double* x,
+                        double* y, int res_epi, cudaStream_t s);
+
+enum OrthOp { OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB };
+cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s);
+
+// ---- dense / recycle-build kernels (dense.cu)
+// G = Y^T Y (s x s, column-major) for Y (n x s, leading dimension ld).
+cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G, double* partial,
+                        unsigned* counter, DevState* st, cudaStream_t strm);
+// Symmetric eigen-decomposition of G (s x s) by parallel cyclic Jacobi in one CTA:
+// lam (s, non-increasing), V (s x s column-major eigenvectors).  sigma_out (nullable) = sqrt(max(lam,0)).
+cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double* sigma_out,
+                          DevState* st, cudaStream_t strm);
+// Y[:, c] = colscale[c] * sum_a X[:, a] M[a, c]  (M s x q column-major, leading dim ldm; colscale nullable).
+cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const double* M, int ldm, int q,
+                      const double* colscale, double* Y, int64_t ldy, DevState* st, cudaStream_t strm);
+// 1 / sigma for c < q
+cudaError_t launch_inv(const double* sigma, int q, double* out, cudaStream_t strm);
+// Cholesky G = R^T R (k x k) and R^{-1}; fail[0] = 1 if not positive definite.
+cudaError_t launch_chol(const double* G, int k, double* R, double* Rinv, int* fail, cudaStream_t strm);
+// R_C = R2 R1, R_C^{-1} = R1^{-1} R2^{-1} into the state; fail if min|diag| <= 1e-12 max|diag|.
+cudaError_t launch_rc_finish(const double* R1, const double* R1i, const double* R2, const double* R2i,
+                             int k, DevState* st, int* fail, cudaStream_t strm);
+// SELL packing of a CSR matrix (values, and columns when pattern != 0)
+cudaError_t launch_sell_pack(const int32_t* rp, const int32_t* ci, const double* v, int64_t n,
+                             const int64_t* sp, const int32_t* sw, int32_t* sci, double* sv,
+                             int pattern, cudaStream_t strm);
+cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaStream_t strm);
+// CSR / BSR pattern validation on the device; bad[0] != 0 on failure.
+cudaError_t launch_validate(const int32_t* rp, const int32_t* ci, int64_t nrows, int64_t ncols,
+                            int64_t nnz, int* bad, cudaStream_t strm);
+
+}  // namespace rg

@@ -1,0 +1,166 @@
+// orth.cu — fused block-vector kernels of the Arnoldi step and the cycle boundaries (K5/K6/K8/K13).
+//
+// One kernel family covers every tall-skinny operation of the hot path:
+//   target w (an n-vector) is optionally UPDATED  w -= sum_{c in U} cf_c Z_c      (Z_c one read each)
+//   then optionally DOTTED                           d_c = Z_c . w,  c in D       (same sweep)
+//   and/or NORMED                                    ||w||^2
+// with a deterministic grid reduction whose last CTA runs the epilogue (epilogue.cuh).  The
+// CGS2 step of PAPER.md's GMRES (classical Gram-Schmidt with one re-orthogonalisation, the
+// "Arnoldi orthogonalization" of PAPER.md:705-711) is then three launches:
+//   OP_D1   h1 = [Q|V]^T w                         (deflate orthogonalises against Q too)
+//   OP_UD2  w -= [Q|V] h1 ; h2 = [Q|V]^T w         (update fused with the second pass' dots)
+//   OP_UN   w -= [Q|V] h2 ; ||w||  (+ Q^T w for augment) -> least-squares epilogue
+// Cycle start (recycled variants): OP_CS_DQ a = Q^T r ; OP_XW x += W R_C^{-1} a ;
+// OP_CS_UN r -= Q a, ||r|| -> cycle-start epilogue.  Cycle end: OP_XUPD x += V y + W z.
+// OP_NORMB: ||b||.
+#include "epilogue.cuh"
+#include "kernels.cuh"
+
+namespace rg {
+namespace {
+
+struct OrthArgs {
+  Layout L;
+  DevState* st;
+  int op;
+};
+
+__global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
+  __shared__ double cf[MAXCOL];
+  __shared__ double ws[OT];
+  __shared__ double dpart[MAXRED];
+  __shared__ double tot[MAXRED];
+  __shared__ double scr[OT > MAXRED ? OT : MAXRED];
+  __shared__ double bsh[33];
+  DevState* st = a.st;
+  const Layout& L = a.L;
+  const int op = a.op;
+  static constexpr int kids[8] = {K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN, K_XW, K_XUPD, K_NORMB};
+  const int kid = kids[op];
+  bool go;
+  switch (op) {
+    case OP_D1: case OP_UD2: case OP_UN: go = st->active != 0; break;
+    case OP_CS_DQ: case OP_CS_UN: case OP_XW: go = st->done == 0; break;
+    case OP_XUPD: go = st->have_xupd != 0; break;
+    default: go = true;
+  }
+  if (!go) { prof_noop(st, kid); return; }
+  prof_begin(st, kid);
+
+  const int j = st->j, k = st->k_eff, var = st->variant;
+  const int VB = L.VB, QB = VB - k;
+  const int64_t ld = L.ld;
+  double* w = nullptr;
+  const double* csrc = st->coef;
+  int u0 = 0, u1 = 0, u2 = 0, u3 = 0, d0 = 0, d1 = 0;
+  bool nrmflag = false;
+  const int lo = (var == RG_DEFLATE) ? QB : VB;
+  switch (op) {
+    case OP_D1:
+      w = L.Z + (int64_t)(VB + j + 1) * ld; d0 = lo; d1 = VB + j + 1; break;
+    case OP_UD2:
+      w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = lo; u1 = VB + j + 1; d0 = lo; d1 = VB + j + 1; break;
+    case OP_UN:
+      w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = lo; u1 = VB + j + 1; nrmflag = true;
+      if (var == RG_AUGMENT) { d0 = QB; d1 = VB; }
+      break;
+    case OP_CS_DQ: w = L.Z + (int64_t)VB * ld; d0 = QB; d1 = VB; break;
+    case OP_CS_UN: w = L.Z + (int64_t)VB * ld; u0 = QB; u1 = VB; nrmflag = true; break;
+    case OP_XW: w = L.x; csrc = st->coefx; u0 = 0; u1 = k; break;
+    case OP_XUPD:
+      w = L.x; csrc = st->coefx; u0 = VB; u1 = VB + st->jfinal + 1;
+      if (var != RG_PLAIN) { u2 = 0; u3 = k; }
+      break;
+    default: w = const_cast<double*>(L.b); nrmflag = true; break;  // OP_NORMB (read only)
+  }
+  const bool upd = (u1 > u0) || (u3 > u2);
+  const bool dots = d1 > d0;
+  const int nd = d1 - d0;
+  for (int c = threadIdx.x; c < MAXCOL; c += OT) {
+    const bool in = (c >= u0 && c < u1) || (c >= u2 && c < u3);
+    cf[c] = in ? csrc[c] * st->sc[c] : 0.0;
+  }
+  for (int c = threadIdx.x; c < MAXRED; c += OT) dpart[c] = 0.0;
+  __syncthreads();
+
+  // even split of the n_pad rows over the CTAs, in 32-row granules
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  const double* __restrict__ Z = L.Z;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double nrm = 0.0;
+  for (int64_t base = r0; base < r1; base += OT) {
+    const int64_t r = base + threadIdx.x;
+    const bool in = r < r1;
+    double acc = 0.0;
+    if (in) {
+      acc = w[r];
+      if (upd) {
+#pragma unroll 8
+        for (int c = u0; c < u1; ++c) acc -= cf[c] * __ldcs(Z + (int64_t)c * ld + r);
+        for (int c = u2; c < u3; ++c) acc -= cf[c] * __ldcs(Z + (int64_t)c * ld + r);
+        w[r] = acc;
+      }
+      nrm += acc * acc;
+    }
+    if (dots) {
+      ws[threadIdx.x] = acc;
+      __syncthreads();
+      const int cnt = (int)((r1 - base) < OT ? (r1 - base) : OT);
+      for (int c = d0 + wid; c < d1; c += NWARP) {
+        const double* __restrict__ zc = Z + (int64_t)c * ld + base;
+        double s = 0.0;
+#pragma unroll 4
+        for (int q = lane; q < cnt; q += 32) s += zc[q] * ws[q];
+        s = warp_sum(s);
+        if (lane == 0) dpart[c - d0] += s;
+      }
+      __syncthreads();
+    }
+  }
+  if (!dots && !nrmflag) {
+    if (st->profile && grid_last(L.counter) && threadIdx.x == 0)
+      prof_end(st, kid, 8.0 * (double)L.n * ((u1 - u0) + (u3 - u2) + 2));
+    return;
+  }
+  if (nrmflag) {
+    const double t = block_sum(nrm, bsh);
+    if (threadIdx.x == 0) dpart[nd] = t;
+  }
+  __syncthreads();
+  const int nv = nd + (nrmflag ? 1 : 0);
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, scr)) return;
+
+  switch (op) {
+    case OP_D1: epi_pass(st, tot, d0, nd, true); break;
+    case OP_UD2: epi_pass(st, tot, d0, nd, false); break;
+    case OP_UN: epi_ls(st, L, tot, nd); break;
+    case OP_CS_DQ: epi_cs_dq(st, L, tot); break;
+    case OP_CS_UN: epi_cycle_start(st, L, tot[0]); break;
+    default:
+      if (threadIdx.x == 0) {  // OP_NORMB
+        st->bnorm = sqrt(tot[0]);
+        if (!(st->bnorm > 0.0)) {
+          st->bzero = st->bnorm == 0.0;
+          st->done = 1;
+          st->converged = st->bzero;
+          if (!st->bzero) st->status = RG_E_NUMERIC;
+        }
+      }
+  }
+  if (threadIdx.x == 0) {
+    const double upd_cols = (u1 - u0) + (u3 - u2);
+    const double wio = upd ? 2.0 : 1.0;
+    prof_end(st, kid, 8.0 * (double)L.n * (upd_cols + nd + wio));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s) {
+  k_orth<<<vec_grid(L.ld), OT, 0, s>>>(OrthArgs{L, st, op});
+  return cudaGetLastError();
+}
+
+}  // namespace rg

@@ -1,0 +1,678 @@
+// rg.cu — host engine and C-ABI entry points of librg (include/rg.h).
+//
+// The host validates arguments, owns the device buffers, and orchestrates the kernels; every
+// arithmetic step of the method runs on the device.  A restart cycle (m Arnoldi steps, the
+// cycle-end update and the next cycle start) is captured once as a CUDA graph and replayed;
+// the host reads one 4-byte-class header per cycle to learn whether the solve has finished.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace rg;
+
+namespace {
+
+thread_local std::string g_err;
+
+rg_status fail(rg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      return fail(RG_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));      \
+    }                                                                                  \
+  } while (0)
+
+constexpr int HIST_CAP = 1 << 16;
+constexpr int SMALL = MAXS * MAXS;  // doubles per small-matrix slot
+
+struct GraphKey {
+  int variant, m;
+  bool operator<(const GraphKey& o) const { return variant != o.variant ? variant < o.variant : m < o.m; }
+};
+
+}  // namespace
+
+struct rg_ctx {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int flags = 0;
+  int64_t n = 0, npad = 0;
+  int max_m = 0, max_s = 0, max_k = 0;
+  int ncol = 0;
+  // matrix
+  int fmt = 0;          // 0 CSR, 1 SELL, 2 BSR
+  int block = 1;
+  int64_t nnz = 0;      // CSR entries / BSR blocks
+  int32_t* rp = nullptr;
+  int32_t* ci = nullptr;
+  double* v = nullptr;
+  int64_t v_len = 0;
+  int64_t nslices = 0, sell_len = 0;
+  int64_t* sp = nullptr;
+  int32_t* sw = nullptr;
+  int32_t* sci = nullptr;
+  double* sv = nullptr;
+  MatDev A;
+  // vectors and bases
+  double* Z = nullptr;
+  double* x = nullptr;
+  double* b = nullptr;
+  double* X = nullptr;   // snapshot ring, npad x max_s
+  double* Y = nullptr;   // scratch, npad x max_s
+  double* t1 = nullptr;  // scratch vectors
+  double* t2 = nullptr;
+  double* hist = nullptr;
+  double* partial = nullptr;
+  unsigned* counter = nullptr;
+  double* small = nullptr;
+  int* dflag = nullptr;
+  DevState* st = nullptr;
+  DevState* hst = nullptr;  // pinned host mirror
+  Layout L;
+  // snapshots / recycle space
+  int s_count = 0, s_head = 0;
+  int k_eff = 0;
+  bool have_W = false;
+  bool c_valid = false;
+  // graphs
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+};
+
+namespace {
+
+size_t header_bytes() { return offsetof(DevState, cs); }
+
+void clear_graphs(rg_ctx* c) {
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  c->graphs.clear();
+}
+
+void free_matrix(rg_ctx* c) {
+  cudaFree(c->rp); cudaFree(c->ci); cudaFree(c->v);
+  cudaFree(c->sp); cudaFree(c->sw); cudaFree(c->sci); cudaFree(c->sv);
+  c->rp = c->ci = nullptr; c->v = nullptr; c->sp = nullptr; c->sw = c->sci = nullptr; c->sv = nullptr;
+}
+
+bool is_dev_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+rg_status copy_in(void* dst, const void* src, size_t bytes, rg_mem mem, cudaStream_t s) {
+  if (bytes == 0) return RG_OK;
+  CK(cudaMemcpyAsync(dst, src, bytes, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  return RG_OK;
+}
+
+rg_status validate_host_pattern(const int32_t* rp, const int32_t* ci, int64_t nrows, int64_t ncols, int64_t nnz) {
+  if (rp[0] != 0) return fail(RG_E_INVAL, "row_ptr[0] != 0");
+  if (rp[nrows] != nnz) return fail(RG_E_INVAL, "row_ptr[n] != nnz");
+  for (int64_t r = 0; r < nrows; ++r) {
+    if (rp[r + 1] < rp[r]) return fail(RG_E_INVAL, "row_ptr not monotone at row " + std::to_string(r));
+    int64_t prev = -1;
+    for (int32_t p = rp[r]; p < rp[r + 1]; ++p) {
+      if (ci[p] < 0 || ci[p] >= ncols) return fail(RG_E_INVAL, "column index out of range in row " + std::to_string(r));
+      if (ci[p] <= prev) return fail(RG_E_INVAL, "columns not strictly increasing in row " + std::to_string(r));
+      prev = ci[p];
+    }
+  }
+  return RG_OK;
+}
+
+// Validate the rg_matrix descriptor against the context dimension (no data access).
+rg_status check_desc(const rg_matrix* A, int64_t n, bool pattern_required) {
+  if (!A) return fail(RG_E_INVAL, "matrix descriptor is NULL");
+  if (A->fmt != RG_CSR && A->fmt != RG_BSR) return fail(RG_E_INVAL, "unknown matrix format");
+  if (A->mem != RG_HOST && A->mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  if (A->n_rows != n) return fail(RG_E_INVAL, "n_rows does not match n");
+  if (A->nnz < 0 || A->nnz >= (int64_t)INT32_MAX) return fail(RG_E_INVAL, "nnz out of range");
+  if (A->fmt == RG_CSR && A->block != 1) return fail(RG_E_INVAL, "CSR requires block = 1");
+  if (A->fmt == RG_BSR) {
+    if (A->block < 1 || A->block > 64 || n % A->block) return fail(RG_E_INVAL, "BSR block must divide n and be <= 64");
+    if (A->sell_C) return fail(RG_E_INVAL, "SELL packing applies to CSR only");
+  }
+  if (A->sell_C != 0 && A->sell_C != 32) return fail(RG_E_INVAL, "sell_C must be 0 or 32");
+  if (A->sell_C == 32 && A->sell_sigma > 1) return fail(RG_E_INVAL, "sell_sigma > 1 is not supported");
+  const bool has_rp = A->row_ptr != nullptr, has_ci = A->col_idx != nullptr;
+  if (has_rp != has_ci) return fail(RG_E_INVAL, "row_ptr and col_idx must both be given or both be NULL");
+  if (pattern_required && !has_rp) return fail(RG_E_INVAL, "row_ptr/col_idx required");
+  if (A->nnz > 0 && !A->val) return fail(RG_E_INVAL, "val is NULL");
+  return RG_OK;
+}
+
+rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
+  const bool pattern = A->row_ptr != nullptr;
+  const int newfmt = A->fmt == RG_BSR ? 2 : (A->sell_C == 32 ? 1 : 0);
+  if (!first && !pattern) {
+    if (A->nnz != c->nnz) return fail(RG_E_INVAL, "values-only update with a different nnz");
+    if (newfmt != c->fmt || A->block != c->block) return fail(RG_E_INVAL, "values-only update must keep the format");
+  }
+  const int b = A->fmt == RG_BSR ? A->block : 1;
+  const int64_t nrows = c->n / b;
+  const int64_t vlen = A->nnz * (int64_t)b * b;
+  if (pattern) {
+    // validate the pattern before touching any state
+    if (A->mem == RG_HOST) {
+      rg_status s = validate_host_pattern(A->row_ptr, A->col_idx, nrows, nrows, A->nnz);
+      if (s != RG_OK) return s;
+    } else {
+      if (!is_dev_ptr(A->row_ptr) || !is_dev_ptr(A->col_idx)) return fail(RG_E_INVAL, "mem = RG_DEVICE but pointers are not device memory");
+      CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), c->stream));
+      CK(launch_validate(A->row_ptr, A->col_idx, nrows, nrows, A->nnz, c->dflag, c->stream));
+      int bad = 0;
+      CK(cudaMemcpyAsync(&bad, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (bad) return fail(RG_E_INVAL, "invalid sparsity pattern (device check code " + std::to_string(bad) + ")");
+    }
+    const bool realloc = first || A->nnz != c->nnz || newfmt != c->fmt || b != c->block;
+    if (realloc) {
+      clear_graphs(c);
+      free_matrix(c);
+      if (cudaMalloc(&c->rp, sizeof(int32_t) * (nrows + 1)) != cudaSuccess ||
+          cudaMalloc(&c->ci, sizeof(int32_t) * std::max<int64_t>(A->nnz, 1)) != cudaSuccess ||
+          cudaMalloc(&c->v, sizeof(double) * std::max<int64_t>(vlen, 1)) != cudaSuccess) {
+        cudaGetLastError();
+        free_matrix(c);
+        return fail(RG_E_NOMEM, "device allocation of the matrix failed");
+      }
+    }
+    c->nnz = A->nnz;
+    c->fmt = newfmt;
+    c->block = b;
+    c->v_len = vlen;
+    rg_status s;
+    if ((s = copy_in(c->rp, A->row_ptr, sizeof(int32_t) * (nrows + 1), A->mem, c->stream)) != RG_OK) return s;
+    if ((s = copy_in(c->ci, A->col_idx, sizeof(int32_t) * A->nnz, A->mem, c->stream)) != RG_OK) return s;
+    if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
+    if (newfmt == 1) {  // SELL-32 packing
+      c->nslices = (c->n + 31) / 32;
+      cudaFree(c->sp); cudaFree(c->sw); cudaFree(c->sci); cudaFree(c->sv);
+      c->sp = nullptr; c->sw = nullptr; c->sci = nullptr; c->sv = nullptr;
+      CK(cudaMalloc(&c->sw, sizeof(int32_t) * c->nslices));
+      CK(cudaMalloc(&c->sp, sizeof(int64_t) * (c->nslices + 1)));
+      CK(launch_sell_widths(c->rp, c->n, c->sw, c->stream));
+      std::vector<int32_t> w(c->nslices);
+      std::vector<int64_t> sp(c->nslices + 1);
+      CK(cudaMemcpyAsync(w.data(), c->sw, sizeof(int32_t) * c->nslices, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      sp[0] = 0;
+      for (int64_t i = 0; i < c->nslices; ++i) sp[i + 1] = sp[i] + 32 * (int64_t)w[i];
+      c->sell_len = sp[c->nslices];
+      CK(cudaMemcpyAsync(c->sp, sp.data(), sizeof(int64_t) * (c->nslices + 1), cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMalloc(&c->sci, sizeof(int32_t) * std::max<int64_t>(c->sell_len, 1)));
+      CK(cudaMalloc(&c->sv, sizeof(double) * std::max<int64_t>(c->sell_len, 1)));
+      CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 1, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      clear_graphs(c);
+    }
+  } else {
+    rg_status s;
+    if (A->mem == RG_DEVICE && !is_dev_ptr(A->val)) return fail(RG_E_INVAL, "mem = RG_DEVICE but val is not device memory");
+    if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
+    if (c->fmt == 1) CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 0, c->stream));
+  }
+  // device descriptor and byte model
+  MatDev& M = c->A;
+  M = MatDev();
+  M.fmt = c->fmt;
+  M.n = c->n;
+  M.rp = c->rp; M.ci = c->ci; M.v = c->v;
+  if (c->fmt == 0) {
+    const double avg = c->n > 0 ? (double)c->nnz / (double)c->n : 0.0;
+    M.lpr = avg <= 3.0 ? 2 : avg <= 6.0 ? 4 : avg <= 12.0 ? 8 : avg <= 24.0 ? 16 : 32;
+    M.bytes = 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n;
+  } else if (c->fmt == 1) {
+    M.sp = c->sp; M.sw = c->sw; M.sci = c->sci; M.sv = c->sv; M.nslices = c->nslices;
+    M.bytes = 12.0 * c->sell_len + 12.0 * c->nslices + 16.0 * c->n;
+  } else {
+    M.b = c->block;
+    M.nb = c->n / c->block;
+    M.bytes = 8.0 * c->v_len + 4.0 * c->nnz + 4.0 * (M.nb + 1) + 16.0 * c->n;
+  }
+  c->c_valid = false;
+  return RG_OK;
+}
+
+// C = A W into the Q region, then CholQR2 -> Q (orthonormal), R_C, R_C^{-1} (state).
+rg_status build_c(rg_ctx* c) {
+  const int k = c->k_eff;
+  const int QB = c->L.VB - k;
+  const int64_t ld = c->npad;
+  cudaStream_t s = c->stream;
+  for (int l = 0; l < k; ++l)
+    CK(launch_spmv(c->A, c->L, c->st, SM_PLAIN, c->Z + (int64_t)l * ld, c->Z + (int64_t)(QB + l) * ld, 0, s));
+  double* G = c->small;
+  double* R1 = c->small + 1 * SMALL;
+  double* R1i = c->small + 2 * SMALL;
+  double* R2 = c->small + 3 * SMALL;
+  double* R2i = c->small + 4 * SMALL;
+  double* Q = c->Z + (int64_t)QB * ld;
+  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
+  CK(launch_gram(Q, ld, c->n, k, G, c->partial, c->counter, c->st, s));
+  CK(launch_chol(G, k, R1, R1i, c->dflag, s));
+  CK(launch_xm(Q, ld, c->n, k, R1i, k, k, nullptr, c->Y, ld, c->st, s));
+  CK(launch_gram(c->Y, ld, c->n, k, G, c->partial, c->counter, c->st, s));
+  CK(launch_chol(G, k, R2, R2i, c->dflag, s));
+  CK(launch_xm(c->Y, ld, c->n, k, R2i, k, k, nullptr, Q, ld, c->st, s));
+  CK(launch_rc_finish(R1, R1i, R2, R2i, k, c->st, c->dflag, s));
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (getenv("RG_DEBUG")) {
+    std::vector<double> hb(5 * SMALL);
+    cudaMemcpy(hb.data(), c->small, sizeof(double) * 5 * SMALL, cudaMemcpyDeviceToHost);
+    for (int slot = 0; slot < 5; ++slot) {
+      fprintf(stderr, "slot %d:", slot);
+      for (int i = 0; i < k * k; ++i) fprintf(stderr, " %.4g", hb[slot * SMALL + i]);
+      fprintf(stderr, "\n");
+    }
+    fprintf(stderr, "bad=%d k=%d QB=%d\n", bad, k, QB);
+  }
+  if (bad) {
+    c->have_W = false;
+    c->k_eff = 0;
+    c->c_valid = false;
+    return fail(RG_E_SINGULAR, "A W is numerically rank deficient (R_C singular); recycle space cleared");
+  }
+  c->c_valid = true;
+  return RG_OK;
+}
+
+// ---- the kernel sequences of one solve
+cudaError_t cycle_start(rg_ctx* c, int variant) {
+  cudaError_t e = launch_spmv(c->A, c->L, c->st, SM_RES, nullptr, nullptr, variant == RG_PLAIN ? 1 : 0, c->stream);
+  if (e != cudaSuccess || variant == RG_PLAIN) return e;
+  if ((e = launch_orth(c->L, c->st, OP_CS_DQ, c->stream)) != cudaSuccess) return e;
+  if ((e = launch_orth(c->L, c->st, OP_XW, c->stream)) != cudaSuccess) return e;
+  return launch_orth(c->L, c->st, OP_CS_UN, c->stream);
+}
+
+cudaError_t cycle_body(rg_ctx* c, int variant, int m) {
+  cudaError_t e;
+  for (int j = 0; j < m; ++j) {
+    if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_orth(c->L, c->st, OP_D1, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_orth(c->L, c->st, OP_UD2, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_orth(c->L, c->st, OP_UN, c->stream)) != cudaSuccess) return e;
+  }
+  if ((e = launch_orth(c->L, c->st, OP_XUPD, c->stream)) != cudaSuccess) return e;
+  return cycle_start(c, variant);
+}
+
+rg_status run_cycle(rg_ctx* c, int variant, int m) {
+  if (c->flags & RG_FLAG_NO_GRAPH) {
+    CK(cycle_body(c, variant, m));
+    return RG_OK;
+  }
+  GraphKey key{variant, m};
+  auto it = c->graphs.find(key);
+  if (it == c->graphs.end()) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = cycle_body(c, variant, m);
+    cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
+    if (e != cudaSuccess) return fail(RG_E_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+    if (e2 != cudaSuccess) return fail(RG_E_CUDA, std::string("end capture: ") + cudaGetErrorString(e2));
+    cudaGraphExec_t ge;
+    cudaError_t e3 = cudaGraphInstantiate(&ge, g, 0);
+    cudaGraphDestroy(g);
+    if (e3 != cudaSuccess) return fail(RG_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e3));
+    it = c->graphs.emplace(key, ge).first;
+  }
+  CK(cudaGraphLaunch(it->second, c->stream));
+  return RG_OK;
+}
+
+rg_status read_header(rg_ctx* c) {
+  CK(cudaMemcpyAsync(c->hst, c->st, header_bytes(), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return RG_OK;
+}
+
+template <class T>
+rg_status dalloc(T** p, size_t count, const char* what) {
+  if (cudaMalloc(p, sizeof(T) * std::max<size_t>(count, 1)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(RG_E_NOMEM, std::string("device allocation failed: ") + what);
+  }
+  return RG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+RG_API const char* rg_last_error(void) { return g_err.c_str(); }
+
+RG_API void rg_destroy(rg_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  clear_graphs(c);
+  free_matrix(c);
+  cudaFree(c->Z); cudaFree(c->x); cudaFree(c->b); cudaFree(c->X); cudaFree(c->Y);
+  cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
+  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st);
+  if (c->hst) cudaFreeHost(c->hst);
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg_options* opt) {
+  if (!out) return fail(RG_E_INVAL, "ctx is NULL");
+  *out = nullptr;
+  if (n < 1 || n >= (int64_t)INT32_MAX) return fail(RG_E_INVAL, "n out of range");
+  if (!opt) return fail(RG_E_INVAL, "options are NULL");
+  if (opt->max_m < 1 || opt->max_m > MAXM) return fail(RG_E_INVAL, "max_m must be in 1..128");
+  if (opt->max_snapshots < 1 || opt->max_snapshots > MAXS) return fail(RG_E_INVAL, "max_snapshots must be in 1..64");
+  if (opt->max_k < 0 || opt->max_k > MAXK || opt->max_k > opt->max_snapshots)
+    return fail(RG_E_INVAL, "max_k must be in 0..min(64, max_snapshots)");
+  rg_status s = check_desc(A, n, true);
+  if (s != RG_OK) return s;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(RG_E_CUDA, "no CUDA device available");
+  }
+  rg_ctx* c = new rg_ctx();
+  CK(cudaGetDevice(&c->dev));
+  c->flags = opt->flags;
+  if (opt->cuda_stream) {
+    c->stream = (cudaStream_t)opt->cuda_stream;
+  } else {
+    if (cudaStreamCreate(&c->stream) != cudaSuccess) { delete c; return fail(RG_E_CUDA, "stream creation failed"); }
+    c->own_stream = true;
+  }
+  c->n = n;
+  c->npad = (n + 63) / 64 * 64;
+  c->max_m = opt->max_m;
+  c->max_s = opt->max_snapshots;
+  c->max_k = opt->max_k;
+  const int VB = 2 * c->max_k;
+  c->ncol = VB + c->max_m + 1;
+  const size_t np = (size_t)c->npad;
+  const size_t part = std::max<size_t>((size_t)NSM * 8 * MAXRED, (size_t)NSM * 2080);
+  if ((s = dalloc(&c->Z, np * c->ncol, "Z")) != RG_OK || (s = dalloc(&c->x, np, "x")) != RG_OK ||
+      (s = dalloc(&c->b, np, "b")) != RG_OK || (s = dalloc(&c->X, np * c->max_s, "X")) != RG_OK ||
+      (s = dalloc(&c->Y, np * c->max_s, "Y")) != RG_OK || (s = dalloc(&c->t1, np, "t1")) != RG_OK ||
+      (s = dalloc(&c->t2, np, "t2")) != RG_OK || (s = dalloc(&c->hist, (size_t)HIST_CAP, "hist")) != RG_OK ||
+      (s = dalloc(&c->partial, part, "partial")) != RG_OK || (s = dalloc(&c->counter, 4, "counter")) != RG_OK ||
+      (s = dalloc(&c->small, (size_t)SMALL * 16, "small")) != RG_OK || (s = dalloc(&c->dflag, 4, "flag")) != RG_OK ||
+      (s = dalloc(&c->st, 1, "state")) != RG_OK) {
+    rg_destroy(c);
+    return s;
+  }
+  if (cudaMallocHost(&c->hst, sizeof(DevState)) != cudaSuccess) {
+    cudaGetLastError();
+    rg_destroy(c);
+    return fail(RG_E_NOMEM, "pinned host allocation failed");
+  }
+  memset(c->hst, 0, sizeof(DevState));
+  cudaError_t e = cudaSuccess;
+  auto ok = [&](cudaError_t x) { if (e == cudaSuccess) e = x; };
+  ok(cudaMemsetAsync(c->Z, 0, sizeof(double) * np * c->ncol, c->stream));
+  ok(cudaMemsetAsync(c->x, 0, sizeof(double) * np, c->stream));
+  ok(cudaMemsetAsync(c->b, 0, sizeof(double) * np, c->stream));
+  ok(cudaMemsetAsync(c->X, 0, sizeof(double) * np * c->max_s, c->stream));
+  ok(cudaMemsetAsync(c->Y, 0, sizeof(double) * np * c->max_s, c->stream));
+  ok(cudaMemsetAsync(c->t1, 0, sizeof(double) * np, c->stream));
+  ok(cudaMemsetAsync(c->t2, 0, sizeof(double) * np, c->stream));
+  ok(cudaMemsetAsync(c->counter, 0, sizeof(unsigned) * 4, c->stream));
+  ok(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
+  for (int i = 0; i < MAXCOL; ++i) c->hst->sc[i] = i < VB ? 1.0 : 0.0;
+  ok(cudaMemcpyAsync(&c->st->sc[0], &c->hst->sc[0], sizeof(double) * MAXCOL, cudaMemcpyHostToDevice, c->stream));
+  ok(cudaEventCreate(&c->e0));
+  ok(cudaEventCreate(&c->e1));
+  ok(cudaStreamSynchronize(c->stream));
+  if (e != cudaSuccess) {
+    rg_destroy(c);
+    return fail(RG_E_CUDA, std::string("initialisation: ") + cudaGetErrorString(e));
+  }
+  c->L.Z = c->Z;
+  c->L.ld = c->npad;
+  c->L.n = n;
+  c->L.maxk = c->max_k;
+  c->L.VB = VB;
+  c->L.x = c->x;
+  c->L.b = c->b;
+  c->L.hist = c->hist;
+  c->L.partial = c->partial;
+  c->L.counter = c->counter;
+  if ((s = set_matrix(c, A, true)) != RG_OK) {
+    std::string msg = g_err;
+    rg_destroy(c);
+    return fail(s, msg);
+  }
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    rg_destroy(c);
+    return fail(RG_E_CUDA, "matrix upload failed");
+  }
+  *out = c;
+  g_err.clear();
+  return RG_OK;
+}
+
+RG_API rg_status rg_update_matrix(rg_ctx* c, const rg_matrix* A) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  rg_status s = check_desc(A, c->n, false);
+  if (s != RG_OK) return s;
+  if ((A->fmt == RG_BSR) != (c->fmt == 2)) return fail(RG_E_INVAL, "matrix format differs from the context's");
+  if ((s = set_matrix(c, A, false)) != RG_OK) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  return RG_OK;
+}
+
+RG_API rg_status rg_push_snapshot(rg_ctx* c, const double* x, rg_mem mem) {
+  if (!c || !x) return fail(RG_E_INVAL, "NULL argument");
+  if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  rg_status s = copy_in(c->X + (int64_t)c->s_head * c->npad, x, sizeof(double) * c->n, mem, c->stream);
+  if (s != RG_OK) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  c->s_head = (c->s_head + 1) % c->max_s;
+  c->s_count = std::min(c->s_count + 1, c->max_s);
+  return RG_OK;
+}
+
+RG_API rg_status rg_clear_snapshots(rg_ctx* c) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  c->s_count = c->s_head = 0;
+  c->have_W = false;
+  c->k_eff = 0;
+  c->c_valid = false;
+  return RG_OK;
+}
+
+RG_API rg_status rg_build_recycle(rg_ctx* c, int32_t k, int32_t* k_eff, double* sigma) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  if (k < 1 || k > c->max_k) return fail(RG_E_INVAL, "k must be in 1..max_k");
+  if (c->s_count == 0) return fail(RG_E_STATE, "no snapshots");
+  const int s = c->s_count;
+  const int64_t ld = c->npad;
+  cudaStream_t st = c->stream;
+  double* G = c->small;
+  double* V1 = c->small + 1 * SMALL;
+  double* lam = c->small + 2 * SMALL;
+  double* V2 = c->small + 3 * SMALL;
+  double* sig = c->small + 4 * SMALL;
+  double* inv = c->small + 5 * SMALL;
+  // pass 1: G = X^T X, Jacobi -> V1 ; Y = X V1
+  CK(launch_gram(c->X, ld, c->n, s, G, c->partial, c->counter, c->st, st));
+  CK(launch_jacobi(G, s, lam, V1, nullptr, c->st, st));
+  CK(launch_xm(c->X, ld, c->n, s, V1, s, s, nullptr, c->Y, ld, c->st, st));
+  // pass 2: Y^T Y (nearly diagonal, column-scaled) -> V2, sigma
+  CK(launch_gram(c->Y, ld, c->n, s, G, c->partial, c->counter, c->st, st));
+  CK(launch_jacobi(G, s, lam, V2, sig, c->st, st));
+  std::vector<double> hs(s);
+  CK(cudaMemcpyAsync(hs.data(), sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  int rank = 0;
+  for (int i = 0; i < s; ++i)
+    if (hs[0] > 0.0 && hs[i] > 1e-12 * hs[0]) ++rank;
+  const int ke = std::min(std::min(k, s), rank);
+  if (sigma) memcpy(sigma, hs.data(), sizeof(double) * s);
+  if (k_eff) *k_eff = ke;
+  c->k_eff = ke;
+  c->have_W = ke > 0;
+  c->c_valid = false;
+  if (ke > 0) {
+    // W = Y V2[:, :k] Sigma^{-1} into Z[:, 0:k]
+    CK(launch_inv(sig, ke, inv, st));
+    CK(launch_xm(c->Y, ld, c->n, s, V2, s, ke, inv, c->Z, ld, c->st, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return RG_OK;
+}
+
+RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t m, rg_variant v, double tol,
+                          int32_t max_iters, double* x_out, rg_mem mem, double* history, int32_t history_cap,
+                          rg_report* rep) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  if (!b || !x_out) return fail(RG_E_INVAL, "b and x_out are required");
+  if (m < 1 || m > c->max_m) return fail(RG_E_INVAL, "m must be in 1..max_m");
+  if (!(tol > 0.0)) return fail(RG_E_INVAL, "tol must be > 0");
+  if (max_iters < 1) return fail(RG_E_INVAL, "max_iters must be >= 1");
+  if (v != RG_PLAIN && v != RG_AUGMENT && v != RG_DEFLATE) return fail(RG_E_INVAL, "unknown variant");
+  if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  if (history_cap < 0) return fail(RG_E_INVAL, "history_cap < 0");
+  cudaStream_t s = c->stream;
+  rg_status rs;
+  const int eff = (v != RG_PLAIN && c->have_W && c->k_eff > 0) ? (int)v : (int)RG_PLAIN;
+  const int k = eff == RG_PLAIN ? 0 : c->k_eff;
+  int c_spmv = 0;
+  if (eff != RG_PLAIN && !c->c_valid) {
+    if ((rs = build_c(c)) != RG_OK) return rs;
+    c_spmv = k;
+  }
+  if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+  if (x0) {
+    if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+  } else {
+    CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->npad, s));
+  }
+  DevState* h = c->hst;
+  memset(h, 0, header_bytes());
+  h->variant = eff;
+  h->m = m;
+  h->k_eff = k;
+  h->max_iters = max_iters;
+  h->hist_cap = std::min(HIST_CAP, std::max(history_cap, 0));
+  h->profile = (c->flags & RG_FLAG_PROFILE) ? 1 : 0;
+  h->tol = tol;
+  h->jfinal = -1;
+  CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
+  CK(cudaEventRecord(c->e0, s));
+  CK(launch_orth(c->L, c->st, OP_NORMB, s));
+  CK(cycle_start(c, eff));
+  for (;;) {
+    if ((rs = read_header(c)) != RG_OK) return rs;
+    if (h->done) break;
+    if ((rs = run_cycle(c, eff, m)) != RG_OK) return rs;
+  }
+  CK(cudaEventRecord(c->e1, s));
+  if (h->bzero) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n, s));
+  CK(cudaMemcpyAsync(x_out, c->x, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  const int hl = std::min(h->hist_len, history_cap);
+  if (history && hl > 0) CK(cudaMemcpyAsync(history, c->hist, sizeof(double) * hl, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, c->e0, c->e1);
+  if (rep) {
+    rep->iterations = h->iters;
+    rep->restarts = h->cycles > 0 ? h->cycles - 1 : 0;
+    rep->converged = h->converged;
+    rep->k_eff = k;
+    rep->spmv_count = h->bzero ? 0 : h->iters + h->cycles + 1 + c_spmv;
+    rep->history_len = hl;
+    rep->rel_residual = h->bzero ? 0.0 : h->relres;
+    rep->ms_total = ms;
+  }
+  if (h->status == RG_E_NUMERIC) return fail(RG_E_NUMERIC, "NaN/Inf met during the solve");
+  return RG_OK;
+}
+
+RG_API rg_status rg_apply(rg_ctx* c, const double* x, double* y, rg_mem mem) {
+  if (!c || !x || !y) return fail(RG_E_INVAL, "NULL argument");
+  if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  rg_status s = copy_in(c->t1, x, sizeof(double) * c->n, mem, c->stream);
+  if (s != RG_OK) return s;
+  CK(launch_spmv(c->A, c->L, nullptr, SM_PLAIN, c->t1, c->t2, 0, c->stream));
+  CK(cudaMemcpyAsync(y, c->t2, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return RG_OK;
+}
+
+RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, int32_t* k_eff) {
+  if (!c || !out) return fail(RG_E_INVAL, "NULL argument");
+  if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  const int k = c->have_W ? c->k_eff : 0;
+  if (k_eff) *k_eff = k;
+  if (k == 0) return fail(RG_E_STATE, "no recycle space");
+  const cudaMemcpyKind kind = mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (which == RG_EXPORT_W || which == RG_EXPORT_Q) {
+    if (which == RG_EXPORT_Q && !c->c_valid) return fail(RG_E_STATE, "Q is not built (run a recycled solve)");
+    const int c0 = which == RG_EXPORT_W ? 0 : c->L.VB - k;
+    CK(cudaMemcpy2DAsync(out, sizeof(double) * c->n, c->Z + (int64_t)c0 * c->npad, sizeof(double) * c->npad,
+                         sizeof(double) * c->n, k, kind, c->stream));
+  } else if (which == RG_EXPORT_RC) {
+    if (!c->c_valid) return fail(RG_E_STATE, "R_C is not built (run a recycled solve)");
+    CK(cudaMemcpy2DAsync(out, sizeof(double) * k, &c->st->RC[0][0], sizeof(double) * MAXK, sizeof(double) * k, k,
+                         kind, c->stream));
+  } else {
+    return fail(RG_E_INVAL, "unknown export item");
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  return RG_OK;
+}
+
+RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t* count) {
+  static const char* names[K_COUNT] = {"spmv_step", "spmv_res", "spmv_plain", "orth_dots1", "orth_upd_dots2",
+                                       "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
+                                       "norm_b", "gram", "jacobi", "xm", "chol", "misc"};
+  if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
+  KStatDev ks[K_COUNT];
+  CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int n = 0;
+  for (int i = 0; i < K_COUNT && n < cap; ++i) {
+    if (!out) break;
+    rg_kstat& o = out[n++];
+    memset(&o, 0, sizeof(o));
+    strncpy(o.name, names[i], sizeof(o.name) - 1);
+    o.launches = (int64_t)ks[i].launches;
+    o.noop_launches = (int64_t)ks[i].noop;
+    o.total_ms = ks[i].ns * 1e-6;
+    o.bytes = ks[i].bytes;
+  }
+  *count = out ? n : K_COUNT;
+  return RG_OK;
+}
+
+RG_API rg_status rg_reset_kernel_stats(rg_ctx* c) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  CK(cudaMemsetAsync(&c->st->kstat[0], 0, sizeof(KStatDev) * K_COUNT, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return RG_OK;
+}
+
+}  // extern "C"

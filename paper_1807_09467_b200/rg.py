@@ -1,0 +1,208 @@
+"""Thin ctypes binding of librg (include/rg.h): argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does nothing but convert
+numpy arrays / torch tensors to pointers, call the library and raise on a non-OK status.  All
+arithmetic runs in the CUDA kernels of ``csrc/``; there is no CPU fallback: if ``lib/librg.so`` is
+missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librg.so")
+
+RG_OK, RG_E_INVAL, RG_E_NOMEM, RG_E_CUDA, RG_E_STATE, RG_E_SINGULAR, RG_E_NUMERIC = range(7)
+RG_CSR, RG_BSR = 0, 1
+RG_PLAIN, RG_AUGMENT, RG_DEFLATE = 0, 1, 2
+RG_HOST, RG_DEVICE = 0, 1
+RG_FLAG_NO_GRAPH, RG_FLAG_PROFILE = 1, 2
+RG_EXPORT_W, RG_EXPORT_Q, RG_EXPORT_RC = 0, 1, 2
+VARIANTS = {"plain": RG_PLAIN, "augment": RG_AUGMENT, "deflate": RG_DEFLATE}
+STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E_STATE",
+          5: "RG_E_SINGULAR", 6: "RG_E_NUMERIC"}
+
+# Symbols declared in include/rg.h (tests check the .so exports exactly these).
+SYMBOLS = ("rg_create", "rg_update_matrix", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle",
+           "rg_solve", "rg_apply", "rg_export", "rg_kernel_stats", "rg_reset_kernel_stats", "rg_destroy",
+           "rg_last_error")
+
+
+class RgError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class rg_matrix(ctypes.Structure):
+    _fields_ = [("fmt", ctypes.c_int), ("n_rows", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("block", ctypes.c_int32), ("row_ptr", ctypes.c_void_p), ("col_idx", ctypes.c_void_p),
+                ("val", ctypes.c_void_p), ("mem", ctypes.c_int), ("sell_C", ctypes.c_int32),
+                ("sell_sigma", ctypes.c_int32)]
+
+
+class rg_options(ctypes.Structure):
+    _fields_ = [("max_m", ctypes.c_int32), ("max_snapshots", ctypes.c_int32), ("max_k", ctypes.c_int32),
+                ("cuda_stream", ctypes.c_void_p), ("flags", ctypes.c_int32)]
+
+
+class rg_report(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("restarts", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("k_eff", ctypes.c_int32), ("spmv_count", ctypes.c_int32), ("history_len", ctypes.c_int32),
+                ("rel_residual", ctypes.c_double), ("ms_total", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class rg_kstat(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 24), ("launches", ctypes.c_int64), ("noop_launches", ctypes.c_int64),
+                ("total_ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+
+
+def load(path: str = LIB_PATH):
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with __graft_entry__.build() (no CPU fallback exists)")
+    L = ctypes.CDLL(path)
+    vp, i32, i64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    L.rg_create.argtypes = [ctypes.POINTER(vp), i64, ctypes.POINTER(rg_matrix), ctypes.POINTER(rg_options)]
+    L.rg_update_matrix.argtypes = [vp, ctypes.POINTER(rg_matrix)]
+    L.rg_push_snapshot.argtypes = [vp, vp, ctypes.c_int]
+    L.rg_clear_snapshots.argtypes = [vp]
+    L.rg_build_recycle.argtypes = [vp, i32, ctypes.POINTER(i32), vp]
+    L.rg_solve.argtypes = [vp, vp, vp, i32, ctypes.c_int, d, i32, vp, ctypes.c_int, vp, i32,
+                           ctypes.POINTER(rg_report)]
+    L.rg_apply.argtypes = [vp, vp, vp, ctypes.c_int]
+    L.rg_export.argtypes = [vp, i32, vp, ctypes.c_int, ctypes.POINTER(i32)]
+    L.rg_kernel_stats.argtypes = [vp, ctypes.POINTER(rg_kstat), i32, ctypes.POINTER(i32)]
+    L.rg_reset_kernel_stats.argtypes = [vp]
+    L.rg_destroy.argtypes = [vp]
+    L.rg_destroy.restype = None
+    L.rg_last_error.restype = ctypes.c_char_p
+    for f in SYMBOLS:
+        if f not in ("rg_destroy", "rg_last_error"):
+            getattr(L, f).restype = ctypes.c_int
+    return L
+
+
+_lib = load()
+
+
+def _check(st):
+    if st != RG_OK:
+        raise RgError(st, _lib.rg_last_error().decode())
+
+
+def _ptr(a):
+    """(pointer, mem) of a numpy array or torch tensor (None -> (None, None))."""
+    if a is None:
+        return None, None
+    if isinstance(a, np.ndarray):
+        if not a.flags.c_contiguous:
+            raise ValueError("arrays must be contiguous")
+        return a.ctypes.data, RG_HOST
+    # torch tensor
+    if not a.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return a.data_ptr(), (RG_DEVICE if a.is_cuda else RG_HOST)
+
+
+def _mem_of(*arrays):
+    mems = {m for _, m in (_ptr(a) for a in arrays if a is not None)}
+    if len(mems) > 1:
+        raise ValueError("all arrays of one call must live in the same memory (host or device)")
+    return mems.pop() if mems else RG_HOST
+
+
+def make_matrix(n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, keep=None):
+    """Build an rg_matrix descriptor.  row_ptr/col_idx None -> values-only update.  Arrays must
+    stay alive during the call (`keep` collects references)."""
+    arrs = [a for a in (row_ptr, col_idx, val) if a is not None]
+    mem = _mem_of(*arrs)
+    if keep is not None:
+        keep.extend(arrs)
+    if fmt == "bsr":
+        nnz = int(col_idx.shape[0]) if col_idx is not None else int(val.shape[0]) // (block * block)
+    else:
+        nnz = int(val.shape[0])
+    rp, _ = _ptr(row_ptr)
+    ci, _ = _ptr(col_idx)
+    v, _ = _ptr(val)
+    return rg_matrix(RG_BSR if fmt == "bsr" else RG_CSR, int(n), nnz, int(block), rp, ci, v, mem, int(sell_C), 1)
+
+
+def rg_create(n, A: rg_matrix, max_m=64, max_snapshots=32, max_k=32, stream=None, flags=0):
+    ctx = ctypes.c_void_p()
+    opt = rg_options(int(max_m), int(max_snapshots), int(max_k), stream, int(flags))
+    _check(_lib.rg_create(ctypes.byref(ctx), int(n), ctypes.byref(A), ctypes.byref(opt)))
+    return ctx
+
+
+def rg_update_matrix(ctx, A: rg_matrix):
+    _check(_lib.rg_update_matrix(ctx, ctypes.byref(A)))
+
+
+def rg_push_snapshot(ctx, x):
+    p, mem = _ptr(x)
+    _check(_lib.rg_push_snapshot(ctx, p, mem))
+
+
+def rg_clear_snapshots(ctx):
+    _check(_lib.rg_clear_snapshots(ctx))
+
+
+def rg_build_recycle(ctx, k, n_snapshots=64):
+    ke = ctypes.c_int32(0)
+    sig = np.zeros(n_snapshots)
+    _check(_lib.rg_build_recycle(ctx, int(k), ctypes.byref(ke), sig.ctypes.data))
+    return ke.value, sig
+
+
+def rg_solve(ctx, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=20000, history_cap=0):
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    mem = _mem_of(b, x_out, x0)
+    pb, _ = _ptr(b)
+    px, _ = _ptr(x_out)
+    p0, _ = _ptr(x0)
+    hist = np.zeros(max(history_cap, 1))
+    rep = rg_report()
+    _check(_lib.rg_solve(ctx, pb, p0, int(m), v, float(tol), int(max_iters), px, mem,
+                         hist.ctypes.data if history_cap > 0 else None, int(history_cap), ctypes.byref(rep)))
+    out = rep.as_dict()
+    out["history"] = hist[: rep.history_len].copy()
+    return out
+
+
+def rg_apply(ctx, x, y):
+    mem = _mem_of(x, y)
+    _check(_lib.rg_apply(ctx, _ptr(x)[0], _ptr(y)[0], mem))
+
+
+def rg_export(ctx, which, out):
+    ke = ctypes.c_int32(0)
+    p, mem = _ptr(out)
+    _check(_lib.rg_export(ctx, int(which), p, mem, ctypes.byref(ke)))
+    return ke.value
+
+
+def rg_kernel_stats(ctx):
+    buf = (rg_kstat * 32)()
+    cnt = ctypes.c_int32(0)
+    _check(_lib.rg_kernel_stats(ctx, buf, 32, ctypes.byref(cnt)))
+    return {buf[i].name.decode(): dict(launches=buf[i].launches, noop=buf[i].noop_launches,
+                                       ms=buf[i].total_ms, bytes=buf[i].bytes) for i in range(cnt.value)}
+
+
+def rg_reset_kernel_stats(ctx):
+    _check(_lib.rg_reset_kernel_stats(ctx))
+
+
+def rg_destroy(ctx):
+    _lib.rg_destroy(ctx)
+
+
+def rg_last_error():
+    return _lib.rg_last_error().decode()

@@ -1,0 +1,212 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  pattern / indices        bit-exact
+  SpMV                     ||y_g - y_o|| <= 1e-13 ||y_o||  and componentwise <= 1e-13 (|A||x|)
+  singular values          |d sigma_i| <= max(1e-10 sigma_i, 1e-15 sigma_1)
+  solutions at tol 1e-8    ||x_g - x_o|| <= 1e-7 ||x_o||
+  iteration counts         within +-2
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def make_ctx(hm, cfg=None, sell=False, max_m=64, s=16, k=8, flags=0):
+    from paper_1807_09467_b200 import Context
+    return Context(hm.n, t(hm.row_ptr), t(hm.col_idx), t(hm.val), fmt=hm.fmt, block=hm.block,
+                   sell_C=32 if sell else 0, max_m=max_m, max_snapshots=s, max_k=k, flags=flags)
+
+
+def random_csr(n, rng, per_row=(0, 9), diag=4.0):
+    rp = [0]
+    ci, v = [], []
+    for i in range(n):
+        nr = rng.integers(per_row[0], per_row[1] + 1)
+        cols = set(rng.choice(n, size=min(nr, n), replace=False).tolist()) | {i}
+        for c in sorted(cols):
+            ci.append(c)
+            v.append(diag if c == i else rng.standard_normal() / np.sqrt(max(nr, 1)))
+        rp.append(len(ci))
+    return synth.HostMatrix("csr", n, np.array(rp, np.int32), np.array(ci, np.int32), np.array(v))
+
+
+def spmv_check(hm, x, y):
+    yo = oracle.spmv(oracle.Matrix.from_host(hm), x)
+    S = hm.to_scipy()
+    ax = abs(S) @ np.abs(x)
+    assert np.linalg.norm(y - yo) <= 1e-13 * np.linalg.norm(yo)
+    assert np.all(np.abs(y - yo) <= 1e-13 * ax + 1e-300)
+
+
+# ------------------------------------------------------------------------------------- SpMV
+@pytest.mark.parametrize("n", [1, 31, 1000, 4097])
+@pytest.mark.parametrize("sell", [False, True])
+def test_spmv_random_ragged(n, sell, rng):
+    hm = random_csr(n, rng, per_row=(0, 40) if n > 100 else (0, 5))
+    ctx = make_ctx(hm, sell=sell)
+    x = rng.standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device=DEV)
+    ctx.apply(t(x), y)
+    spmv_check(hm, x, y.cpu().numpy())
+    yh = np.zeros(n)
+    ctx.apply(x, yh)                   # host-pointer path
+    assert np.array_equal(yh, y.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,N", [("C1", 32), ("C2", 512), ("C3", 256), ("C4", 40), ("C5", 3)])
+def test_spmv_configs(name, N, rng):
+    cfg = synth.CONFIGS[name].reduced(N)
+    seq = synth.HostSequence(cfg)
+    hm = seq.matrix(2, seq.initial())
+    ctx = make_ctx(hm, sell=cfg.fmt == "sell")
+    x = rng.standard_normal(cfg.n)
+    y = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+    ctx.apply(t(x), y)
+    spmv_check(hm, x, y.cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_spmv_full_size_sampled_rows(name, rng):
+    """Full BASELINE size, in the launch configuration the bench uses: sampled rows against the
+    oracle's single-row product."""
+    cfg = synth.CONFIGS[name]
+    seq = synth.HostSequence(cfg)
+    hm = seq.matrix(1, seq.initial())
+    ctx = make_ctx(hm, sell=cfg.fmt == "sell")
+    x = rng.standard_normal(cfg.n)
+    y = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+    ctx.apply(t(x), y)
+    y = y.cpu().numpy()
+    M = oracle.Matrix.from_host(hm)
+    rows = np.concatenate([[0, 1, cfg.n - 1], rng.integers(0, cfg.n, 2000)])
+    for r in rows:
+        yo = oracle.spmv_row(M, int(r), x)
+        assert abs(y[r] - yo) <= 1e-13 * (np.abs(hm.val[hm.row_ptr[r]:hm.row_ptr[r + 1]]) @
+                                         np.abs(x[hm.col_idx[hm.row_ptr[r]:hm.row_ptr[r + 1]]]))
+
+
+# ------------------------------------------------------------------------------------- solves
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate"])
+@pytest.mark.parametrize("n,m,k", [(200, 10, 4), (1023, 25, 8), (64, 64, 3)])
+def test_solve_random_vs_oracle(variant, n, m, k, rng):
+    hm = random_csr(n, rng, per_row=(2, 8), diag=2.2)
+    W = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    b = rng.standard_normal(n)
+    ctx = make_ctx(hm, max_m=max(m, 8), s=k, k=k)
+    for i in range(k):
+        ctx.push_snapshot(t(W[:, i] * (k - i)))
+    ke, sig = ctx.build_recycle(k)
+    assert ke == k
+    Wg = np.zeros((k, n))
+    ctx.export(0, Wg)
+    Wg = Wg.T
+    x = torch.zeros(n, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), x, m=m, variant=variant, tol=1e-8, history_cap=5000)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=m, variant=variant, W=W, tol=1e-8)
+    xg = x.cpu().numpy()
+    assert rep["converged"] and ref["converged"]
+    assert np.linalg.norm(xg - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+    assert abs(rep["iterations"] - ref["iterations"]) <= 2
+    # true residual from the oracle's SpMV
+    r = b - oracle.spmv(oracle.Matrix.from_host(hm), xg)
+    assert np.linalg.norm(r) / np.linalg.norm(b) <= 1e-8
+    assert abs(rep["rel_residual"] - np.linalg.norm(r) / np.linalg.norm(b)) <= 1e-12
+    # span(W_gpu) == span(W)
+    assert np.linalg.norm(Wg @ Wg.T - W @ W.T, 2) <= 1e-10
+    h = rep["history"]
+    assert len(h) == rep["iterations"]
+
+
+def test_b_zero_and_converged_x0(rng):
+    hm = random_csr(100, rng)
+    ctx = make_ctx(hm)
+    x = torch.ones(100, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(torch.zeros(100, dtype=torch.float64, device=DEV), x, x0=x.clone(), m=10)
+    assert rep["converged"] and rep["iterations"] == 0 and float(x.abs().max()) == 0.0
+    xs = rng.standard_normal(100)
+    b = hm.to_scipy() @ xs
+    x2 = torch.zeros(100, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), x2, x0=t(xs), m=10)
+    assert rep["converged"] and rep["iterations"] == 0
+
+
+def test_max_iters_cap_reports_not_converged(rng):
+    hm = random_csr(500, rng, diag=1.0)
+    ctx = make_ctx(hm)
+    x = torch.zeros(500, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(rng.standard_normal(500)), x, m=5, tol=1e-14, max_iters=7)
+    assert rep["iterations"] == 7 and not rep["converged"]
+
+
+def test_rhs_in_image_of_recycle_space(rng):
+    n, k = 300, 4
+    hm = random_csr(n, rng)
+    W = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    ctx = make_ctx(hm, s=k, k=k)
+    for i in range(k):
+        ctx.push_snapshot(t(W[:, i] * (i + 1)))
+    ctx.build_recycle(k)
+    c = rng.standard_normal(k)
+    b = hm.to_scipy() @ (W @ c)
+    for v in ("augment", "deflate"):
+        x = torch.zeros(n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=10, variant=v)
+        assert rep["iterations"] == 0 and rep["converged"]
+        assert np.linalg.norm(x.cpu().numpy() - W @ c) <= 1e-10 * np.linalg.norm(c)
+
+
+def test_bitwise_deterministic(rng):
+    cfg = synth.CONFIGS["C2"].reduced(128)
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    hm = seq.matrix(1, u)
+    b = seq.rhs(1, u)
+    outs = []
+    for _ in range(2):
+        ctx = make_ctx(hm, max_m=cfg.m)
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        ctx.solve(t(b), x, m=cfg.m)
+        outs.append(x.cpu().numpy())
+        ctx.close()
+    assert np.array_equal(outs[0], outs[1])
+
+
+# ------------------------------------------------------------------------------------- SVD
+def test_singular_values_vs_oracle(rng):
+    n, s = 5000, 12
+    P = np.linalg.qr(rng.standard_normal((n, s)))[0]
+    Q = np.linalg.qr(rng.standard_normal((s, s)))[0]
+    true = np.logspace(0, -6, s)
+    X = P @ np.diag(true) @ Q.T
+    hm = random_csr(n, rng)
+    ctx = make_ctx(hm, s=s, k=s)
+    for i in range(s):
+        ctx.push_snapshot(t(X[:, i]))
+    ke, sig = ctx.build_recycle(5)
+    _, so, rank, _ = oracle.svd(X)
+    sg = sig[:s]
+    assert ke == 5
+    assert np.all(np.abs(sg - so) <= np.maximum(1e-10 * so, 1e-15 * so[0]))
+
+
+def test_rank_deficient_window(rng):
+    n = 777
+    hm = random_csr(n, rng)
+    ctx = make_ctx(hm, s=6, k=6)
+    a, b2 = rng.standard_normal(n), rng.standard_normal(n)
+    for v in (a, b2, a + b2, 2 * a):
+        ctx.push_snapshot(t(v))
+    ke, sig = ctx.build_recycle(4)
+    assert ke == 2

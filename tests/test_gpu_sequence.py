@@ -1,0 +1,79 @@
+"""Teacher-forced sequence parity: for each system the oracle's x_{t-1}
+builds A_t, b_t and is the snapshot pushed to BOTH sides; the GPU builds its own recycle space
+(two-pass Gram-Jacobi SVD) and solves; the oracle builds its own (one-sided Jacobi) and solves.
+Compared per system: singular values, solution, iteration count."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def run(cfg, variant, T, k=None):
+    from paper_1807_09467_b200 import Context
+    k = k or cfg.k
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    A1 = seq.matrix(1, u)
+    ctx = Context(cfg.n, t(A1.row_ptr), t(A1.col_idx), t(A1.val), fmt=A1.fmt, block=A1.block,
+                  sell_C=32 if cfg.fmt == "sell" else 0, max_m=cfg.m, max_snapshots=cfg.s, max_k=k)
+    X = []
+    rows = []
+    for step in range(1, T + 1):
+        A = seq.matrix(step, u)
+        b = seq.rhs(step, u)
+        ctx.update_matrix(t(A.val))
+        W = None
+        sg = so = None
+        if variant != "plain" and X:
+            ke, sg = ctx.build_recycle(k)
+            W, so, ko = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), k)
+            assert ke == ko
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=cfg.m, variant=variant, tol=cfg.tol)
+        ref = oracle.solve(oracle.Matrix.from_host(A), b, m=cfg.m, variant=variant, W=W, tol=cfg.tol)
+        xg = x.cpu().numpy()
+        rows.append((step, rep["iterations"], ref["iterations"],
+                     np.linalg.norm(xg - ref["x"]) / np.linalg.norm(ref["x"])))
+        assert rep["converged"] and ref["converged"], rows[-1]
+        assert abs(rep["iterations"] - ref["iterations"]) <= 2, rows
+        assert rows[-1][3] <= 1e-7, rows
+        if sg is not None:
+            s = len(so)
+            assert np.all(np.abs(sg[:s] - so) <= np.maximum(1e-10 * so, 1e-15 * so[0])), (sg[:s], so)
+        u = ref["x"]
+        X.append(u)
+        ctx.push_snapshot(t(u))
+    ctx.close()
+    return rows
+
+
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate"])
+def test_c1_full_sequence(variant):
+    run(synth.CONFIGS["C1"], variant, 10)
+
+
+@pytest.mark.parametrize("variant", ["augment", "deflate"])
+def test_c2_reduced(variant):
+    run(synth.CONFIGS["C2"].reduced(96), variant, 6)
+
+
+def test_c3_reduced_sell_deflate():
+    run(synth.CONFIGS["C3"].reduced(96), "deflate", 5)
+
+
+@pytest.mark.parametrize("variant", ["augment", "deflate"])
+def test_c4_reduced(variant):
+    run(synth.CONFIGS["C4"].reduced(20), variant, 5, k=8)
+
+
+def test_c5_reduced_bsr():
+    run(synth.CONFIGS["C5"].reduced(3), "deflate", 5)
