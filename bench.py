@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the recycled GMRES(m) hot path on B200 (one JSON line on rank 0).
+
+A STEP is one system of the sequence (every row of SURVEY.md §8a): the next A_t, b_t are generated
+in HBM from x_{t-1} (a1), the values are handed to the library (rg_update_matrix), the recycle
+space is rebuilt from the snapshot window (a3; C = A W and its QR are rebuilt inside the solve, a4),
+the system is solved with the recycled variant (a5-a10), and x_t is pushed as a snapshot (a2).
+
+Default workload: BASELINE.json configs[1] (C2, n = 262,144, GMRES(50), k = 10 from 20
+snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|augment|deflate.
+
+  value      seconds per system (device time, CUDA events on the library's stream), whole job:
+             max-over-ranks time / (systems solved by all ranks)
+  e2e        the same metric through the public API with HOST buffers (host generator, H2D of
+             A_t values / b_t / snapshot, D2H of x_t inside the timed region)
+  roofline   the dominant kernel's algorithmic bytes / its measured device time (%globaltimer
+             stamps inside the kernels: launches live inside CUDA graphs, where host-side events
+             cannot bracket single kernels), against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the oracle (plain C, 1 thread) on a bounded sample of the same workload
+
+--impl reference runs the oracle (the reference arm for this tier) on the same config.
+Multi-GPU (torchrun): independent replicas, one sequence per rank, no collective on the data
+path ("replicas only"); barrier + max-over-ranks timing.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "recycled GMRES(m) sec per system & sequence; SpMV/Arnoldi HBM GB/s vs peak"
+UNIT = "s/system"
+
+
+# ---------------------------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def reduce_max(value: float, dist_on: bool, device=None) -> float:
+    """Max over ranks (the contract's timing rule)."""
+    if not dist_on:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rg_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------- our arm
+class GpuRun:
+    """One replica: the library context plus the device-side sequence generator."""
+
+    def __init__(self, cfg, variant, k, device, stream, profile, sell):
+        import torch
+
+        import synth
+        from paper_1807_09467_b200 import Context, rg
+        self.torch, self.cfg, self.variant, self.k = torch, cfg, variant, k
+        self.dev = device
+        self.stream = stream
+        self.gen = synth.DeviceSequence(cfg, device)
+        u0 = torch.from_numpy(self.gen.host.initial()).to(device)
+        self.x = torch.zeros(cfg.n, dtype=torch.float64, device=device)
+        self.x.copy_(u0)
+        self.gen.fill(1, self.x)
+        flags = rg.RG_FLAG_PROFILE if profile else 0
+        self.ctx = Context(cfg.n, self.gen.row_ptr, self.gen.col_idx, self.gen.val,
+                           fmt="bsr" if cfg.kind == "bsr" else "csr", block=cfg.B if cfg.kind == "bsr" else 1,
+                           sell_C=32 if sell else 0, max_m=cfg.m, max_snapshots=cfg.s,
+                           max_k=max(k, 1), stream=stream.cuda_stream, flags=flags)
+        self.t = 0
+        self.iters = []
+        self.nsnap = 0
+
+    def step(self):
+        """One system t of the sequence, entirely on the device (inputs resident in HBM)."""
+        cfg = self.cfg
+        self.t += 1
+        self.gen.fill(self.t, self.x)                   # A_t, b_t from x_{t-1}
+        self.ctx.update_matrix(self.gen.val)           # values-only fast path (a1)
+        if self.variant != "plain" and self.nsnap > 0:
+            self.ctx.build_recycle(self.k)             # a3 (a4 happens inside the solve)
+        rep = self.ctx.solve(self.gen.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol)
+        if not rep["converged"]:
+            raise RuntimeError(f"system {self.t} did not converge: {rep}")
+        self.ctx.push_snapshot(self.x)                 # a2
+        self.nsnap += 1
+        self.iters.append(rep["iterations"])
+        return rep
+
+
+class HostE2ERun:
+    """The same sequence through the public API with HOST buffers (pinned), host generator."""
+
+    def __init__(self, cfg, variant, k, device, stream, sell):
+        import torch
+
+        import synth
+        from paper_1807_09467_b200 import Context
+        self.torch, self.cfg, self.variant, self.k = torch, cfg, variant, k
+        self.seq = synth.HostSequence(cfg)
+        u0 = self.seq.initial()
+        A1 = self.seq.matrix(1, u0)
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        self.x = torch.zeros(cfg.n, dtype=torch.float64).pin_memory()
+        self.x.copy_(torch.from_numpy(u0))
+        self.val = pin(A1.val)
+        self.b = torch.zeros(cfg.n, dtype=torch.float64).pin_memory()
+        self.ctx = Context(cfg.n, pin(A1.row_ptr), pin(A1.col_idx), self.val,
+                           fmt="bsr" if cfg.kind == "bsr" else "csr", block=cfg.B if cfg.kind == "bsr" else 1,
+                           sell_C=32 if sell else 0, max_m=cfg.m, max_snapshots=cfg.s,
+                           max_k=max(k, 1), stream=stream.cuda_stream)
+        self.t = 0
+        self.nsnap = 0
+        self.h2d = 0
+        self.d2h = 0
+
+    def step(self):
+        cfg = self.cfg
+        self.t += 1
+        xn = self.x.numpy()
+        hm = self.seq.matrix(self.t, xn)
+        self.val.numpy()[:] = hm.val
+        self.b.numpy()[:] = self.seq.rhs(self.t, xn)
+        self.ctx.update_matrix(self.val)
+        if self.variant != "plain" and self.nsnap > 0:
+            self.ctx.build_recycle(self.k)
+        rep = self.ctx.solve(self.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol)
+        self.ctx.push_snapshot(self.x)
+        self.nsnap += 1
+        self.h2d = 8 * (self.val.numel() + 2 * cfg.n)   # values, b, snapshot
+        self.d2h = 8 * cfg.n                            # x_t
+        return rep
+
+
+def flush_l2(buf):
+    buf.add_(1.0)   # 256 MiB write > 126 MB L2
+
+
+def oracle_time(cfg, variant, k, systems, budget_s=30.0):
+    """The oracle (plain C, 1 thread) on the first `systems` systems of its own sequence."""
+    import oracle
+    import synth
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    X = []
+    times = []
+    its = []
+    for t in range(1, systems + 1):
+        A = oracle.Matrix.from_host(seq.matrix(t, u))
+        b = seq.rhs(t, u)
+        t0 = time.perf_counter()
+        W = None
+        if variant != "plain" and X:
+            W, _, _ = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), k)
+        r = oracle.solve(A, b, m=cfg.m, variant=variant, W=W, tol=cfg.tol)
+        times.append(time.perf_counter() - t0)
+        its.append(r["iterations"])
+        u = r["x"]
+        X.append(u)
+        if sum(times) > budget_s:
+            break
+    return times, its
+
+
+def run_ours(args, cfg):
+    import torch
+    ws, rank, local = dist_env()
+    dist_on = ws > 1
+    if dist_on:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    stream = torch.cuda.Stream(device)
+    k = args.k or cfg.k
+    flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=device)
+    with torch.cuda.stream(stream):
+        sell = (cfg.fmt == "sell") if args.sell < 0 else bool(args.sell)
+        run = GpuRun(cfg, args.variant, k, device, stream, profile=not args.no_profile, sell=sell)
+        for _ in range(args.warmup):
+            run.step()
+        torch.cuda.synchronize()
+        run.ctx.reset_kernel_stats()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if dist_on:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush_l2(flush)                         # outside the timed events
+                evs[i][0].record(stream)
+                run.step()
+                evs[i][1].record(stream)
+            torch.cuda.synchronize()
+        if dist_on:
+            torch.distributed.barrier()
+        per = [a.elapsed_time(b) / 1e3 for a, b in evs]
+        kstats = run.ctx.kernel_stats()
+        t_local = sum(per)
+        t_max = reduce_max(t_local, dist_on, device)
+        value = t_max / (args.steps * ws)
+        timed_iters = run.iters[args.warmup:]
+
+        # e2e through the public API with host buffers
+        e2e = None
+        if not args.no_e2e:
+            hrun = HostE2ERun(cfg, args.variant, k, device, stream, sell)
+            for _ in range(min(args.warmup, 2)):
+                hrun.step()
+            torch.cuda.synchronize()
+            if dist_on:
+                torch.distributed.barrier()
+            t0 = time.perf_counter()
+            ke = max(1, min(args.steps, args.e2e_steps))
+            for _ in range(ke):
+                hrun.step()
+            torch.cuda.synchronize()
+            te = reduce_max(time.perf_counter() - t0, dist_on, device)
+            e2e = {"value": te / (ke * ws), "unit": UNIT, "h2d_bytes_per_step": hrun.h2d,
+                   "d2h_bytes_per_step": hrun.d2h, "steps": ke}
+
+    if rank != 0:
+        if dist_on:
+            torch.distributed.destroy_process_group()
+        return
+    # roofline of the dominant kernel (largest summed device time in the timed region)
+    peak, peak_kind = measured_peaks()
+    work = {kname: s for kname, s in kstats.items() if s["launches"] > 0 and s["ms"] > 0}
+    dom = max(work, key=lambda kname: work[kname]["ms"]) if work else None
+    roof = None
+    if dom:
+        s = work[dom]
+        bytes_per = s["bytes"] / s["launches"]
+        ms_per = s["ms"] / s["launches"]
+        achieved = bytes_per / (ms_per * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", f"traffic_{cfg.name}_{args.variant}.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(dom)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": bytes_per, "avg_launch_us": ms_per * 1e3,
+                "share_of_step": round(s["ms"] / 1e3 / t_local, 4)}
+    launches = sum(s["launches"] + s["noop"] for s in kstats.values())
+    cpu = None
+    if not args.no_cpu_baseline and ws == 1:
+        times, its = oracle_time(cfg, args.variant, k, args.cpu_systems, budget_s=args.cpu_budget)
+        cpu = {"value": sum(times) / len(times), "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{cfg.name} systems 1..{len(times)} of the oracle's own sequence ({args.variant}, "
+                         f"iterations {its}), plain C fp64 single thread"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, synth/)",
+        "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.cid - 1}]", "variant": args.variant,
+                   "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "fmt": cfg.fmt,
+                   "device_format": "SELL-32" if sell else ("BSR-64" if cfg.kind == "bsr" else "CSR"),
+                   "tol": cfg.tol,
+                   "systems_timed": f"t={args.warmup + 1}..{args.warmup + args.steps}",
+                   "iterations_timed": timed_iters,
+                   "l2": "flushed (256 MiB write) between steps, outside the timed events",
+                   "parallelism": f"replicas x{ws}"},
+        "per_step_s": [round(p, 6) for p in per],
+        "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "kernels": {kname: {"launches": s["launches"], "noop": s["noop"], "ms": round(s["ms"], 4),
+                            "GBps": round(s["bytes"] / (s["ms"] * 1e-3) / 1e9, 1) if s["ms"] > 0 else None}
+                    for kname, s in kstats.items() if s["launches"] + s["noop"] > 0},
+    }
+    print(json.dumps(line))
+    if dist_on:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args, cfg):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    k = args.k or cfg.k
+    n_sys = args.warmup + args.steps
+    times, its = oracle_time(cfg, args.variant, k, n_sys, budget_s=1e9)
+    timed = times[args.warmup:]
+    v = sum(timed) / len(timed)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, synth/)",
+            "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.cid - 1}]", "variant": args.variant,
+                       "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "iterations": its},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{cfg.name} systems {args.warmup + 1}..{n_sys} of the oracle's sequence"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate"])
+    ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--sell", type=int, default=-1, help="1: pack CSR to SELL-32 inside the library, "
+                    "0: keep CSR, -1: config default")
+    ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-systems", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+    import synth
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -148,21 +148,44 @@ __device__ __forceinline__ bool grid_reduce(const double* vals, int nv, double* 
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return false;
   __threadfence();
+  // warp w reduces columns c = w, w + nwarps, ...: lane l sums partials of CTAs l, l+32, ...
+  // (8 independent loads in flight), then a fixed shuffle tree: deterministic order.
   const int G = gridDim.x;
-  int S = nv > 0 ? (int)blockDim.x / nv : 1;
-  if (S < 1) S = 1;
-  for (int idx = threadIdx.x; idx < S * nv; idx += blockDim.x) {
-    const int c = idx % nv, s = idx / nv;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  (void)scr;
+  if (nv > 2 * nw) {  // many columns (Gram): thread per column, CTAs summed in index order
+    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+      double a = 0.0;
+      for (int b = 0; b < G; b += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = b + u < G ? __ldcg(&partial[(size_t)(b + u) * ldp + c]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a += v[u];
+      }
+      tot[c] = a;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *counter = 0u;
+    __syncthreads();
+    return true;
+  }
+  for (int c = threadIdx.x >> 5; c < nv; c += nw) {
     double a = 0.0;
-    for (int b = s; b < G; b += S) a += __ldcg(&partial[(size_t)b * ldp + c]);
-    scr[idx] = a;
+    for (int b = lane; b < G; b += 8 * 32) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int bb = b + u * 32;
+        v[u] = bb < G ? __ldcg(&partial[(size_t)bb * ldp + c]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
+    }
+    a = warp_sum(a);
+    if (lane == 0) tot[c] = a;
   }
   __syncthreads();
-  for (int c = threadIdx.x; c < nv; c += blockDim.x) {
-    double a = 0.0;
-    for (int s = 0; s < S; ++s) a += scr[s * nv + c];
-    tot[c] = a;
-  }
   if (threadIdx.x == 0) *counter = 0u;
   __syncthreads();
   return true;

@@ -30,7 +30,10 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
                         double* y, int res_epi, cudaStream_t s);
 
 enum OrthOp { OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB };
-cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s);
+// cond != 0: cudaGraphConditionalHandle set to st->active by OP_UN's epilogue (graph WHILE node)
+cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond = 0);
+// WHILE-node condition from the state: which 0 -> active, 1 -> !done
+cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s);
 
 // ---- dense / recycle-build kernels (dense.cu)
 // G = Y^T Y (s x s, column-major) for Y (n x s, leading dimension ld).

@@ -23,14 +23,21 @@ struct OrthArgs {
   Layout L;
   DevState* st;
   int op;
+  unsigned long long cond;  // cudaGraphConditionalHandle of the Arnoldi-step WHILE node (OP_UN)
+  int use_cond;
 };
 
-__global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
+// Sets a WHILE-node condition from the device state: which = 0 -> st->active (Arnoldi loop),
+// which = 1 -> !st->done (restart-cycle loop).
+__global__ void k_cond(const DevState* st, cudaGraphConditionalHandle h, int which) {
+  if (threadIdx.x == 0) cudaGraphSetConditional(h, which == 0 ? (st->active ? 1u : 0u) : (st->done ? 0u : 1u));
+}
+
+__global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
   __shared__ double cf[MAXCOL];
   __shared__ double ws[OT];
   __shared__ double dpart[MAXRED];
   __shared__ double tot[MAXRED];
-  __shared__ double scr[OT > MAXRED ? OT : MAXRED];
   __shared__ double bsh[33];
   DevState* st = a.st;
   const Layout& L = a.L;
@@ -76,11 +83,9 @@ __global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
   const bool upd = (u1 > u0) || (u3 > u2);
   const bool dots = d1 > d0;
   const int nd = d1 - d0;
-  for (int c = threadIdx.x; c < MAXCOL; c += OT) {
-    const bool in = (c >= u0 && c < u1) || (c >= u2 && c < u3);
-    cf[c] = in ? csrc[c] * st->sc[c] : 0.0;
-  }
-  for (int c = threadIdx.x; c < MAXRED; c += OT) dpart[c] = 0.0;
+  for (int c = u0 + threadIdx.x; c < u1; c += OT) cf[c] = csrc[c] * st->sc[c];
+  for (int c = u2 + threadIdx.x; c < u3; c += OT) cf[c] = csrc[c] * st->sc[c];
+  for (int c = threadIdx.x; c <= nd; c += OT) dpart[c] = 0.0;
   __syncthreads();
 
   // even split of the n_pad rows over the CTAs, in 32-row granules
@@ -97,8 +102,15 @@ __global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
     if (in) {
       acc = w[r];
       if (upd) {
-#pragma unroll 8
-        for (int c = u0; c < u1; ++c) acc -= cf[c] * __ldcs(Z + (int64_t)c * ld + r);
+        int c = u0;
+        for (; c + 8 <= u1; c += 8) {   // 8 independent loads in flight, applied in order
+          double z[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) z[u] = __ldcs(Z + (int64_t)(c + u) * ld + r);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc -= cf[c + u] * z[u];
+        }
+        for (; c < u1; ++c) acc -= cf[c] * __ldcs(Z + (int64_t)c * ld + r);
         for (int c = u2; c < u3; ++c) acc -= cf[c] * __ldcs(Z + (int64_t)c * ld + r);
         w[r] = acc;
       }
@@ -108,13 +120,19 @@ __global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
       ws[threadIdx.x] = acc;
       __syncthreads();
       const int cnt = (int)((r1 - base) < OT ? (r1 - base) : OT);
+      // each warp owns columns c = d0 + wid (mod NWARP): 16 independent 8-byte loads in flight
+      // per lane (OT/32 rows per lane), then a fixed shuffle tree
+      constexpr int RPL = OT / 32;
       for (int c = d0 + wid; c < d1; c += NWARP) {
-        const double* __restrict__ zc = Z + (int64_t)c * ld + base;
-        double s = 0.0;
-#pragma unroll 4
-        for (int q = lane; q < cnt; q += 32) s += zc[q] * ws[q];
-        s = warp_sum(s);
-        if (lane == 0) dpart[c - d0] += s;
+        const double* __restrict__ za = Z + (int64_t)c * ld + base + lane;
+        double va[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) va[q] = (lane + 32 * q < cnt) ? __ldcs(za + 32 * q) : 0.0;
+        double sa = 0.0;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) sa += va[q] * ws[lane + 32 * q];
+        sa = warp_sum(sa);
+        if (lane == 0) dpart[c - d0] += sa;
       }
       __syncthreads();
     }
@@ -130,12 +148,15 @@ __global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
   }
   __syncthreads();
   const int nv = nd + (nrmflag ? 1 : 0);
-  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, scr)) return;
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot)) return;
 
   switch (op) {
     case OP_D1: epi_pass(st, tot, d0, nd, true); break;
     case OP_UD2: epi_pass(st, tot, d0, nd, false); break;
-    case OP_UN: epi_ls(st, L, tot, nd); break;
+    case OP_UN:
+      epi_ls(st, L, tot, nd);
+      if (a.use_cond && threadIdx.x == 0) cudaGraphSetConditional(a.cond, st->active ? 1u : 0u);
+      break;
     case OP_CS_DQ: epi_cs_dq(st, L, tot); break;
     case OP_CS_UN: epi_cycle_start(st, L, tot[0]); break;
     default:
@@ -150,16 +171,30 @@ __global__ void __launch_bounds__(OT) k_orth(OrthArgs a) {
       }
   }
   if (threadIdx.x == 0) {
-    const double upd_cols = (u1 - u0) + (u3 - u2);
-    const double wio = upd ? 2.0 : 1.0;
-    prof_end(st, kid, 8.0 * (double)L.n * (upd_cols + nd + wio));
+    // algorithmic bytes = every DISTINCT column touched once + w read (+ write if updated)
+    int distinct = (u1 - u0) + (u3 - u2);
+    if (dots) {
+      const int lo_o = d0 > u0 ? d0 : u0, hi_o = d1 < u1 ? d1 : u1;
+      distinct += nd - (hi_o > lo_o ? hi_o - lo_o : 0);
+    }
+    prof_end(st, kid, 8.0 * (double)L.n * (distinct + (upd ? 2.0 : 1.0)));
   }
 }
 
 }  // namespace
 
-cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s) {
-  k_orth<<<vec_grid(L.ld), OT, 0, s>>>(OrthArgs{L, st, op});
+cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s) {
+  k_cond<<<1, 32, 0, s>>>(st, (cudaGraphConditionalHandle)h, which);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond) {
+  static bool init = false;
+  if (!init) {  // two 512-thread CTAs per SM need more than the default shared-memory carveout
+    cudaFuncSetAttribute(k_orth, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    init = true;
+  }
+  k_orth<<<vec_grid(L.ld), OT, 0, s>>>(OrthArgs{L, st, op, cond, cond != 0ull});
   return cudaGetLastError();
 }
 

@@ -239,7 +239,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
   M.rp = c->rp; M.ci = c->ci; M.v = c->v;
   if (c->fmt == 0) {
     const double avg = c->n > 0 ? (double)c->nnz / (double)c->n : 0.0;
-    M.lpr = avg <= 3.0 ? 2 : avg <= 6.0 ? 4 : avg <= 12.0 ? 8 : avg <= 24.0 ? 16 : 32;
+    M.lpr = avg <= 12.0 ? 1 : avg <= 24.0 ? 8 : avg <= 48.0 ? 16 : 32;
     M.bytes = 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n;
   } else if (c->fmt == 1) {
     M.sp = c->sp; M.sw = c->sw; M.sci = c->sci; M.sv = c->sv; M.nslices = c->nslices;
@@ -307,36 +307,99 @@ cudaError_t cycle_start(rg_ctx* c, int variant) {
   return launch_orth(c->L, c->st, OP_CS_UN, c->stream);
 }
 
+cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
+  cudaError_t e;
+  if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
+  if ((e = launch_orth(c->L, c->st, OP_D1, c->stream)) != cudaSuccess) return e;
+  if ((e = launch_orth(c->L, c->st, OP_UD2, c->stream)) != cudaSuccess) return e;
+  return launch_orth(c->L, c->st, OP_UN, c->stream, cond);
+}
+
 cudaError_t cycle_body(rg_ctx* c, int variant, int m) {
   cudaError_t e;
-  for (int j = 0; j < m; ++j) {
-    if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
-    if ((e = launch_orth(c->L, c->st, OP_D1, c->stream)) != cudaSuccess) return e;
-    if ((e = launch_orth(c->L, c->st, OP_UD2, c->stream)) != cudaSuccess) return e;
-    if ((e = launch_orth(c->L, c->st, OP_UN, c->stream)) != cudaSuccess) return e;
-  }
+  for (int j = 0; j < m; ++j)
+    if ((e = arnoldi_step(c, 0)) != cudaSuccess) return e;
   if ((e = launch_orth(c->L, c->st, OP_XUPD, c->stream)) != cudaSuccess) return e;
   return cycle_start(c, variant);
 }
 
-rg_status run_cycle(rg_ctx* c, int variant, int m) {
-  if (c->flags & RG_FLAG_NO_GRAPH) {
-    CK(cycle_body(c, variant, m));
-    return RG_OK;
+#define CKG(call)                                                                      \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      cudaGraphDestroy(G);                                                             \
+      return fail(RG_E_CUDA, std::string("graph build: ") + #call + ": " + cudaGetErrorString(e_)); \
+    }                                                                                  \
+  } while (0)
+
+// The whole remainder of a solve as ONE graph with two nested WHILE nodes:
+//   WHILE (!done) { set(inner = active); WHILE (active) { Arnoldi step }; x update; cycle start;
+//                   set(outer = !done) }
+// The Arnoldi-step condition is set by the least-squares epilogue itself, so no launch is wasted
+// after convergence and the host never synchronises inside a solve.
+rg_status build_solve_graph(rg_ctx* c, int variant, cudaGraphExec_t* out) {
+  cudaGraph_t G = nullptr;
+  CK(cudaGraphCreate(&G, 0));
+  cudaGraphConditionalHandle hout, hin;
+  CKG(cudaGraphConditionalHandleCreate(&hout, G, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams op{};
+  op.type = cudaGraphNodeTypeConditional;
+  op.conditional.handle = hout;
+  op.conditional.type = cudaGraphCondTypeWhile;
+  op.conditional.size = 1;
+  cudaGraphNode_t outer;
+  CKG(cudaGraphAddNode(&outer, G, nullptr, 0, &op));
+  cudaGraph_t bodyO = op.conditional.phGraph_out[0];
+  CKG(cudaGraphConditionalHandleCreate(&hin, bodyO, 0, 0));
+  cudaGraph_t tmp;
+  CKG(cudaStreamBeginCaptureToGraph(c->stream, bodyO, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e1 = launch_cond(c->st, hin, 0, c->stream);
+  CKG(cudaStreamEndCapture(c->stream, &tmp));
+  CKG(e1);
+  cudaGraphNode_t pre;
+  size_t nn = 1;
+  CKG(cudaGraphGetNodes(bodyO, &pre, &nn));
+  cudaGraphNodeParams ip{};
+  ip.type = cudaGraphNodeTypeConditional;
+  ip.conditional.handle = hin;
+  ip.conditional.type = cudaGraphCondTypeWhile;
+  ip.conditional.size = 1;
+  cudaGraphNode_t inner;
+  CKG(cudaGraphAddNode(&inner, bodyO, &pre, 1, &ip));
+  cudaGraph_t bodyI = ip.conditional.phGraph_out[0];
+  CKG(cudaStreamBeginCaptureToGraph(c->stream, bodyI, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  e1 = arnoldi_step(c, (unsigned long long)hin);
+  CKG(cudaStreamEndCapture(c->stream, &tmp));
+  CKG(e1);
+  CKG(cudaStreamBeginCaptureToGraph(c->stream, bodyO, &inner, nullptr, 1, cudaStreamCaptureModeThreadLocal));
+  e1 = launch_orth(c->L, c->st, OP_XUPD, c->stream);
+  if (e1 == cudaSuccess) e1 = cycle_start(c, variant);
+  if (e1 == cudaSuccess) e1 = launch_cond(c->st, hout, 1, c->stream);
+  CKG(cudaStreamEndCapture(c->stream, &tmp));
+  CKG(e1);
+  cudaGraphExec_t ge;
+  CKG(cudaGraphInstantiate(&ge, G, 0));
+  cudaGraphDestroy(G);
+  *out = ge;
+  return RG_OK;
+}
+
+// Runs the rest of the solve after the first cycle start.
+rg_status run_solve(rg_ctx* c, int variant, int m) {
+  if (c->flags & RG_FLAG_NO_GRAPH) {  // host-driven loop (debugging): one sync per cycle
+    for (;;) {
+      CK(cudaMemcpyAsync(c->hst, c->st, offsetof(DevState, cs), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (c->hst->done) return RG_OK;
+      CK(cycle_body(c, variant, m));
+    }
   }
-  GraphKey key{variant, m};
+  GraphKey key{variant, 0};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
-    cudaGraph_t g;
-    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t e = cycle_body(c, variant, m);
-    cudaError_t e2 = cudaStreamEndCapture(c->stream, &g);
-    if (e != cudaSuccess) return fail(RG_E_CUDA, std::string("capture: ") + cudaGetErrorString(e));
-    if (e2 != cudaSuccess) return fail(RG_E_CUDA, std::string("end capture: ") + cudaGetErrorString(e2));
     cudaGraphExec_t ge;
-    cudaError_t e3 = cudaGraphInstantiate(&ge, g, 0);
-    cudaGraphDestroy(g);
-    if (e3 != cudaSuccess) return fail(RG_E_CUDA, std::string("instantiate: ") + cudaGetErrorString(e3));
+    rg_status s = build_solve_graph(c, variant, &ge);
+    if (s != RG_OK) return s;
     it = c->graphs.emplace(key, ge).first;
   }
   CK(cudaGraphLaunch(it->second, c->stream));
@@ -398,6 +461,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   rg_ctx* c = new rg_ctx();
   CK(cudaGetDevice(&c->dev));
   c->flags = opt->flags;
+  if (getenv("RG_NO_GRAPH")) c->flags |= RG_FLAG_NO_GRAPH;  // ncu cannot profile kernels inside conditional graphs
   if (opt->cuda_stream) {
     c->stream = (cudaStream_t)opt->cuda_stream;
   } else {
@@ -584,12 +648,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   CK(cudaEventRecord(c->e0, s));
   CK(launch_orth(c->L, c->st, OP_NORMB, s));
   CK(cycle_start(c, eff));
-  for (;;) {
-    if ((rs = read_header(c)) != RG_OK) return rs;
-    if (h->done) break;
-    if ((rs = run_cycle(c, eff, m)) != RG_OK) return rs;
-  }
+  if ((rs = run_solve(c, eff, m)) != RG_OK) return rs;
   CK(cudaEventRecord(c->e1, s));
+  if ((rs = read_header(c)) != RG_OK) return rs;
   if (h->bzero) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n, s));
   CK(cudaMemcpyAsync(x_out, c->x, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   const int hl = std::min(h->hist_len, history_cap);

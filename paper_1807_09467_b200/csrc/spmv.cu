@@ -62,13 +62,13 @@ __device__ __forceinline__ bool setup(const SpmvArgs& a, Io& io, int& kid) {
 
 // Tail shared by every format: residual reduction + epilogue, profiling.
 __device__ __forceinline__ void finish(const SpmvArgs& a, const Io& io, int kid, double nrm) {
-  __shared__ double bsh[33], vals[1], tot[1], scr[OT];
+  __shared__ double bsh[33], vals[1], tot[1];
   DevState* st = a.st;
   if (io.res) {
     const double t = block_sum(nrm, bsh);
     if (threadIdx.x == 0) vals[0] = t;
     __syncthreads();
-    if (!grid_reduce(vals, 1, a.L.partial, a.L.counter, tot, scr)) return;
+    if (!grid_reduce(vals, 1, a.L.partial, a.L.counter, tot, tot)) return;
     if (a.res_epi) epi_cycle_start(st, a.L, tot[0]);
     if (threadIdx.x == 0) prof_end(st, kid, a.A.bytes + 8.0 * a.L.n);
     return;
@@ -91,7 +91,7 @@ __device__ __forceinline__ double emit(const Io& io, int64_t r, double s) {
 
 // ---------------------------------------------------------------- CSR, LPR lanes per row
 template <int LPR>
-__global__ void __launch_bounds__(OT) k_spmv_csr(SpmvArgs a) {
+__global__ void __launch_bounds__(OT, 2) k_spmv_csr(SpmvArgs a) {
   Io io;
   int kid;
   if (!setup(a, io, kid)) return;
@@ -111,17 +111,36 @@ __global__ void __launch_bounds__(OT) k_spmv_csr(SpmvArgs a) {
     double s = 0.0;
     if (row < A.n) {
       const int32_t p0 = __ldg(rp + row), p1 = __ldg(rp + row + 1);
-      for (int32_t p = p0 + lane; p < p1; p += LPR) s += __ldcs(v + p) * __ldg(x + __ldcs(ci + p));
-    }
+      if constexpr (LPR == 1) {
+        // thread per row: up to 8 (column, value) pairs in flight, then 8 gathers of x
+        for (int32_t p = p0; p < p1; p += 8) {
+          int32_t cc[8];
+          double vv[8];
 #pragma unroll
-    for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, LPR);
+          for (int u = 0; u < 8; ++u) {
+            const bool ok = p + u < p1;
+            cc[u] = ok ? __ldcs(ci + p + u) : 0;
+            vv[u] = ok ? __ldcs(v + p + u) : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (p + u < p1) s += vv[u] * __ldg(x + cc[u]);
+        }
+      } else {
+        for (int32_t p = p0 + lane; p < p1; p += LPR) s += __ldcs(v + p) * __ldg(x + __ldcs(ci + p));
+      }
+    }
+    if constexpr (LPR > 1) {
+#pragma unroll
+      for (int o = LPR / 2; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o, LPR);
+    }
     if (lane == 0 && row < A.n) nrm += emit(io, row, s);
   }
   finish(a, io, kid, nrm);
 }
 
 // ---------------------------------------------------------------- SELL-32 (sigma = 1)
-__global__ void __launch_bounds__(OT) k_spmv_sell(SpmvArgs a) {
+__global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
   Io io;
   int kid;
   if (!setup(a, io, kid)) return;
@@ -134,10 +153,19 @@ __global__ void __launch_bounds__(OT) k_spmv_sell(SpmvArgs a) {
     const int w = __ldg(A.sw + sl);
     const int64_t base = __ldg(A.sp + sl) + (row & 31);
     double s = 0.0;
-#pragma unroll 4
-    for (int c = 0; c < w; ++c) {
-      const int64_t e = base + (int64_t)c * 32;
-      s += __ldcs(A.sv + e) * __ldg(x + __ldcs(A.sci + e));
+    for (int c = 0; c < w; c += 8) {  // 8 coalesced (column, value) pairs in flight, then gathers
+      int32_t cc[8];
+      double vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = c + u < w;
+        const int64_t e = base + (int64_t)(c + u) * 32;
+        cc[u] = ok ? __ldcs(A.sci + e) : 0;
+        vv[u] = ok ? __ldcs(A.sv + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c + u < w) s += vv[u] * __ldg(x + cc[u]);
     }
     if (row < A.n) nrm += emit(io, row, s);
   }
@@ -192,6 +220,7 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
     if (g > cap) g = cap;
     const int gi = (int)(g < 1 ? 1 : g);
     switch (A.lpr) {
+      case 1: k_spmv_csr<1><<<gi, OT, 0, s>>>(a); break;
       case 2: k_spmv_csr<2><<<gi, OT, 0, s>>>(a); break;
       case 4: k_spmv_csr<4><<<gi, OT, 0, s>>>(a); break;
       case 8: k_spmv_csr<8><<<gi, OT, 0, s>>>(a); break;
