@@ -84,6 +84,8 @@ struct Layout {
   double* hist;    // history buffer (hist_cap)
   double* partial; // grid-reduction partials [grid][MAXRED]
   unsigned* counter;
+  int cgs_ok;      // [Q|V] (max_k + max_m + 1 columns) fits k_cgs (16 chunks of 8 columns)
+  int augment;     // variant of the graph being built / launched is augment
 };
 
 // ---------------------------------------------------------------- small device helpers

@@ -11,66 +11,96 @@
 namespace rg {
 namespace {
 
-constexpr int GT = 256;         // threads of the Gram kernel
-constexpr int GTR = 32;         // rows per Gram tile
-constexpr int MAXP = MAXS * (MAXS + 1) / 2;
-constexpr int PPT = (MAXP + GT - 1) / GT;
+constexpr int GT = 256;         // threads of the Gram kernel (8 warps)
+constexpr int GTR = 64;         // rows per Gram tile
+constexpr int S8MAX = 64;       // s rounded up to a multiple of 8
+constexpr int GTS = S8MAX + 1;  // tile row stride (odd: spreads banks)
+constexpr int GRAM_CTAS = NSM * 2;
+constexpr int GPL = S8MAX * S8MAX;  // partial stride per CTA
 
-// G = Y^T Y.  Each thread owns fixed (a,b) pairs (deterministic), tiles of GTR rows staged in
-// shared memory (row-major, padded), per-CTA partials grid-reduced in index order.
-__global__ void __launch_bounds__(GT) k_gram(const double* __restrict__ Y, int64_t ld, int64_t n, int s,
-                                             double* G, double* partial, unsigned* counter, DevState* st) {
-  extern __shared__ double sm[];
-  double* tile = sm;                        // GTR x (s+1)
-  double* pv = tile + GTR * (MAXS + 1);     // MAXP
-  double* tot = pv + MAXP;                  // MAXP
-  double* scr = tot + MAXP;                 // MAXP (>= GT)
-  __shared__ unsigned char pa[MAXP], pb[MAXP];
-  const int P = s * (s + 1) / 2;
-  if (st) prof_begin(st, K_GRAM);
-  if (threadIdx.x == 0) {
-    int p = 0;
-    for (int a2 = 0; a2 < s; ++a2)
-      for (int b2 = a2; b2 < s; ++b2) { pa[p] = (unsigned char)a2; pb[p] = (unsigned char)b2; ++p; }
+// FP64 tensor-core MMA (DMMA.8x8x4): C[8x8] += A[8x4] B[4x8].  Fragments (PTX ISA, m8n8k4 .f64):
+// a: A(lane/4, lane%4), b: B(lane%4, lane/4), c{0,1}: C(lane/4, 2*(lane%4) + {0,1}).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// Stage GTR rows x s8 columns of the column-major Y into a row-major shared tile (zero padded).
+__device__ __forceinline__ void stage_tile(double* tile, const double* __restrict__ Y, int64_t ld, int64_t n,
+                                           int s, int s8, int64_t r0) {
+  for (int e = threadIdx.x; e < GTR * s8; e += blockDim.x) {
+    const int c = e / GTR, r = e % GTR;  // consecutive threads: consecutive rows (coalesced)
+    tile[r * GTS + c] = (c < s && r0 + r < n) ? __ldcs(Y + (int64_t)c * ld + r0 + r) : 0.0;
   }
-  __syncthreads();
-  double acc[PPT];
+}
+
+// Pass 1 of G = Y^T Y: every CTA accumulates the upper block pairs (I <= J) of its rows with
+// DMMA; warp w owns pairs w, w+8, ... and keeps their 8x8 accumulators in registers across tiles.
+__global__ void __launch_bounds__(GT) k_gram_mma(const double* __restrict__ Y, int64_t ld, int64_t n, int s,
+                                                 double* __restrict__ partial, DevState* st) {
+  __shared__ double tile[GTR * GTS];
+  if (st) prof_begin(st, K_GRAM);
+  const int s8 = (s + 7) & ~7, nb = s8 / 8, np = nb * (nb + 1) / 2;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int MAXQ = (S8MAX / 8) * (S8MAX / 8 + 1) / 2 / 8 + 1;  // pairs per warp (<= 5)
+  double acc[MAXQ][2];
+  int pi[MAXQ], pj[MAXQ];
 #pragma unroll
-  for (int q = 0; q < PPT; ++q) acc[q] = 0.0;
+  for (int q = 0; q < MAXQ; ++q) {
+    acc[q][0] = acc[q][1] = 0.0;
+    int p = wid + 8 * q, I = 0;
+    while (p >= nb - I && I < nb) { p -= nb - I; ++I; }  // p-th upper pair in row-major order
+    pi[q] = I;
+    pj[q] = I + p;
+  }
+  const int nq = (np - wid + 7) / 8;
   const int64_t ntiles = (n + GTR - 1) / GTR;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t r0 = t * GTR;
-    for (int e = threadIdx.x; e < GTR * s; e += GT) {
-      const int c = e / GTR, r = e % GTR;      // coalesced: consecutive threads, consecutive rows
-      tile[r * (s + 1) + c] = (r0 + r < n) ? Y[(int64_t)c * ld + r0 + r] : 0.0;
-    }
+    __syncthreads();
+    stage_tile(tile, Y, ld, n, s, s8, t * GTR);
     __syncthreads();
 #pragma unroll
-    for (int q = 0; q < PPT; ++q) {
-      const int p = threadIdx.x + q * GT;
-      if (p < P) {
-        const int a2 = pa[p], b2 = pb[p];
-        double sacc = 0.0;
-#pragma unroll 8
-        for (int r = 0; r < GTR; ++r) sacc += tile[r * (s + 1) + a2] * tile[r * (s + 1) + b2];
-        acc[q] += sacc;
+    for (int q = 0; q < MAXQ; ++q) {
+      if (q < nq) {
+        const double* ta = tile + (lane & 3) * GTS + pi[q] * 8 + (lane >> 2);
+        const double* tb = tile + (lane & 3) * GTS + pj[q] * 8 + (lane >> 2);
+#pragma unroll
+        for (int kk = 0; kk < GTR / 4; ++kk) dmma(acc[q][0], acc[q][1], ta[kk * 4 * GTS], tb[kk * 4 * GTS]);
       }
     }
-    __syncthreads();
   }
+  double* P = partial + (size_t)blockIdx.x * GPL;
 #pragma unroll
-  for (int q = 0; q < PPT; ++q) {
-    const int p = threadIdx.x + q * GT;
-    if (p < P) pv[p] = acc[q];
+  for (int q = 0; q < MAXQ; ++q) {
+    if (q < nq) {
+      const int row = pi[q] * 8 + (lane >> 2), col = pj[q] * 8 + (lane & 3) * 2;
+      P[row * S8MAX + col] = acc[q][0];
+      P[row * S8MAX + col + 1] = acc[q][1];
+    }
   }
-  __syncthreads();
-  if (!grid_reduce(pv, P, partial, counter, tot, scr, MAXP)) return;
-  for (int p = threadIdx.x; p < P; p += GT) {
-    const int a2 = pa[p], b2 = pb[p];
-    G[a2 * s + b2] = tot[p];
-    G[b2 * s + a2] = tot[p];
+}
+
+// Pass 2: G(a,b) = sum over CTAs (index order) of the partials, a <= b; mirrored.
+__global__ void __launch_bounds__(256) k_gram_reduce(const double* __restrict__ partial, int nparts, int s,
+                                                     double* G, unsigned* counter, DevState* st, double bytes) {
+  const int P = s * (s + 1) / 2;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    int a = 0, q = p;
+    while (q >= s - a) { q -= s - a; ++a; }
+    const int b = a + q;
+    const int off = a * S8MAX + b;
+    double acc = 0.0;
+    for (int c = 0; c < nparts; c += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = c + u < nparts ? __ldcg(partial + (size_t)(c + u) * GPL + off) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
+    }
+    G[a * s + b] = acc;
+    G[b * s + a] = acc;
   }
-  if (st && threadIdx.x == 0) prof_end(st, K_GRAM, 8.0 * (double)n * s);
+  if (st && st->profile && grid_last(counter) && threadIdx.x == 0) prof_end(st, K_GRAM, bytes);
 }
 
 // Parallel cyclic (round-robin) Jacobi on a symmetric s x s matrix, one CTA.
@@ -177,36 +207,55 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* G, int s, double* 
   if (st && tid == 0) prof_end(st, K_JACOBI, 0.0);
 }
 
-// Y[:, c] = colscale[c] * X[:, 0:s] M[:, c]; tiles of 64 rows staged in shared memory.
+// Y[:, c] = colscale[c] * X[:, 0:s] M[:, c] with DMMA: tiles of 64 rows of X staged in shared
+// memory; warp w computes rows 8w..8w+7 of the tile for all column blocks; the output tile is staged
+// in shared memory and written column-coalesced.
 constexpr int XT = 256, XTR = 64;
+constexpr int XMS = S8MAX + 1;  // stride of the M (a-major) and output tiles
 __global__ void __launch_bounds__(XT) k_xm(const double* __restrict__ X, int64_t ldx, int64_t n, int s,
                                            const double* __restrict__ M, int ldm, int q,
                                            const double* __restrict__ colscale, double* Y, int64_t ldy,
                                            DevState* st) {
   extern __shared__ double sm[];
-  double* Ms = sm;                       // s x q, [c * s + a]
-  double* tile = Ms + MAXS * MAXS;       // XTR x (s+1)
+  double* Ms = sm;                     // S8MAX x XMS : Ms[a * XMS + c]
+  double* tile = Ms + S8MAX * XMS;     // XTR x GTS   : tile[r * GTS + a]
+  double* out = tile + XTR * GTS;      // XTR x XMS   : out[r * XMS + c]
   (void)st;
-  for (int e = threadIdx.x; e < s * q; e += XT) {
-    const int c = e / s, a2 = e % s;
-    Ms[e] = M[(int64_t)c * ldm + a2] * (colscale ? colscale[c] : 1.0);
+  const int s8 = (s + 7) & ~7, q8 = (q + 7) & ~7, ncb = q8 / 8;
+  for (int e = threadIdx.x; e < s8 * q8; e += XT) {
+    const int c = e / s8, a2 = e % s8;
+    Ms[a2 * XMS + c] = (a2 < s && c < q) ? M[(int64_t)c * ldm + a2] * (colscale ? colscale[c] : 1.0) : 0.0;
   }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t ntiles = (n + XTR - 1) / XTR;
-  const int row = threadIdx.x % XTR, cg = threadIdx.x / XTR;  // 4 column groups
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t r0 = t * XTR;
     __syncthreads();
-    for (int e = threadIdx.x; e < XTR * s; e += XT) {
-      const int c = e / XTR, r = e % XTR;
-      tile[r * (s + 1) + c] = (r0 + r < n) ? X[(int64_t)c * ldx + r0 + r] : 0.0;
+    stage_tile(tile, X, ldx, n, s, s8, r0);
+    __syncthreads();
+    double acc[S8MAX / 8][2];
+#pragma unroll
+    for (int cb = 0; cb < S8MAX / 8; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+    const double* ta = tile + (wid * 8 + (lane >> 2)) * GTS + (lane & 3);
+    for (int k4 = 0; k4 < s8; k4 += 4) {
+      const double a = ta[k4];
+      const double* mb = Ms + (k4 + (lane & 3)) * XMS + (lane >> 2);
+#pragma unroll
+      for (int cb = 0; cb < S8MAX / 8; ++cb)
+        if (cb < ncb) dmma(acc[cb][0], acc[cb][1], a, mb[cb * 8]);
+    }
+#pragma unroll
+    for (int cb = 0; cb < S8MAX / 8; ++cb) {
+      if (cb < ncb) {
+        const int r = wid * 8 + (lane >> 2), c = cb * 8 + (lane & 3) * 2;
+        out[r * XMS + c] = acc[cb][0];
+        out[r * XMS + c + 1] = acc[cb][1];
+      }
     }
     __syncthreads();
-    if (r0 + row < n) {
-      for (int c = cg; c < q; c += XT / XTR) {
-        double acc = 0.0;
-        for (int a2 = 0; a2 < s; ++a2) acc += tile[row * (s + 1) + a2] * Ms[c * s + a2];
-        Y[(int64_t)c * ldy + r0 + row] = acc;
-      }
+    for (int e = threadIdx.x; e < XTR * q; e += XT) {
+      const int c = e / XTR, r = e % XTR;
+      if (r0 + r < n) Y[(int64_t)c * ldy + r0 + r] = out[r * XMS + c];
     }
   }
 }
@@ -336,15 +385,12 @@ __global__ void k_validate(const int32_t* rp, const int32_t* ci, int64_t nrows, 
 
 cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G, double* partial,
                         unsigned* counter, DevState* st, cudaStream_t strm) {
-  const size_t smem = sizeof(double) * (GTR * (MAXS + 1) + 3 * MAXP);
-  static bool init = false;
-  if (!init) {
-    cudaFuncSetAttribute(k_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    init = true;
-  }
   int64_t g = (n + GTR - 1) / GTR;
-  if (g > NSM) g = NSM;
-  k_gram<<<(int)(g < 1 ? 1 : g), GT, smem, strm>>>(Y, ld, n, s, G, partial, counter, st);
+  if (g > GRAM_CTAS) g = GRAM_CTAS;
+  const int gi = (int)(g < 1 ? 1 : g);
+  k_gram_mma<<<gi, GT, 0, strm>>>(Y, ld, n, s, partial, st);
+  const int P = s * (s + 1) / 2;
+  k_gram_reduce<<<(P + 255) / 256, 256, 0, strm>>>(partial, gi, s, G, counter, st, 8.0 * (double)n * s);
   return cudaGetLastError();
 }
 
@@ -362,14 +408,14 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
 
 cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const double* M, int ldm, int q,
                       const double* colscale, double* Y, int64_t ldy, DevState* st, cudaStream_t strm) {
-  const size_t smem = sizeof(double) * (MAXS * MAXS + XTR * (MAXS + 1));
+  const size_t smem = sizeof(double) * (S8MAX * XMS + XTR * GTS + XTR * XMS);
   static bool init = false;
   if (!init) {
     cudaFuncSetAttribute(k_xm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     init = true;
   }
   int64_t g = (n + XTR - 1) / XTR;
-  if (g > NSM * 4) g = NSM * 4;
+  if (g > NSM * 2) g = NSM * 2;
   k_xm<<<(int)(g < 1 ? 1 : g), XT, smem, strm>>>(X, ldx, n, s, M, ldm, q, colscale, Y, ldy, st);
   return cudaGetLastError();
 }

@@ -181,6 +181,129 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Register-resident CGS kernel for the Arnoldi step (OP_D1 / OP_UD2 / OP_UN non-augment).
+//
+// The p columns of [Q|V] are split into G <= 16 chunks of <= 8 columns; thread t owns row
+// t % TR (TR = 512/G rows per tile) and chunk t / TR.  Per tile a thread loads its <= 8 basis
+// values and the target entry (all loads independent), keeps them in registers for BOTH the
+// update w_r -= sum_c cf_c Z_rc (chunk partials combined in a fixed order through shared memory)
+// and the dots d_c += Z_rc w_r (accumulated per thread across all tiles; one deterministic
+// shuffle/shared-memory tree at the end).  Every column is read from HBM once per launch; there
+// is no per-tile reduction and at most two barriers per tile (none when G == 1).
+constexpr int CT = 512;
+constexpr int CPG = 8;  // columns per thread chunk
+
+template <int OPK>  // 0 = D1 (dots), 1 = UD2 (update + dots), 2 = UN (update + norm -> LS step)
+__global__ void __launch_bounds__(CT, 2) k_cgs(Layout L, DevState* st, unsigned long long cond) {
+  __shared__ double cf[MAXCOL];
+  __shared__ double part[CT];
+  __shared__ double ws[CT];
+  __shared__ double wred[CT / 32][CPG];
+  __shared__ double dpart[MAXRED];
+  __shared__ double tot[MAXRED];
+  __shared__ double bsh[33];
+  constexpr int kid = OPK == 0 ? K_ORTH_D1 : OPK == 1 ? K_ORTH_UD2 : K_ORTH_UN;
+  constexpr bool UPD = OPK != 0, DOTS = OPK != 2, NRM = OPK == 2;
+  if (!st->active) { prof_noop(st, kid); return; }
+  prof_begin(st, kid);
+  const int j = st->j, k = st->k_eff, var = st->variant;
+  const int VB = L.VB, QB = VB - k;
+  const int64_t ld = L.ld;
+  const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j + 1, p = hi - lo;
+  double* __restrict__ w = L.Z + (int64_t)hi * ld;
+  const double* __restrict__ Z = L.Z;
+  int G = 1;
+  while (G * CPG < p) G <<= 1;
+  const int TR = CT / G;
+  const int r = threadIdx.x % TR, g = threadIdx.x / TR;
+  const int ca = g * CPG, nc = max(0, min(CPG, p - ca));   // my columns: lo + ca .. lo + ca + nc
+  if (UPD)
+    for (int c = threadIdx.x; c < p; c += CT) cf[c] = st->coef[lo + c] * st->sc[lo + c];
+  __syncthreads();
+  double cfr[CPG];
+#pragma unroll
+  for (int i = 0; i < CPG; ++i) cfr[i] = (UPD && i < nc) ? cf[ca + i] : 0.0;
+  const double* __restrict__ zb = Z + (int64_t)(lo + ca) * ld;
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  double dacc[CPG];
+#pragma unroll
+  for (int i = 0; i < CPG; ++i) dacc[i] = 0.0;
+  double nrm = 0.0;
+  for (int64_t base = r0; base < r1; base += TR) {
+    const int64_t row = base + r;
+    const bool in = row < r1;
+    double z[CPG];
+#pragma unroll
+    for (int i = 0; i < CPG; ++i) z[i] = (in && i < nc) ? __ldcs(zb + (int64_t)i * ld + row) : 0.0;
+    const double wr = (in && (OPK == 0 || g == 0)) ? w[row] : 0.0;
+    double wn = wr;
+    if (UPD) {
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < CPG; i += 2) {
+        a0 += cfr[i] * z[i];
+        a1 += cfr[i + 1] * z[i + 1];
+      }
+      const double pa = a0 + a1;
+      if (G == 1) {
+        wn = wr - pa;
+      } else {
+        part[threadIdx.x] = pa;
+        __syncthreads();
+        if (g == 0) {
+          double sum = pa;
+          for (int gg = 1; gg < G; ++gg) sum += part[gg * TR + r];
+          wn = wr - sum;
+          ws[r] = wn;
+        }
+        __syncthreads();
+        if (g != 0) wn = ws[r];
+      }
+      if (g == 0 && in) {
+        w[row] = wn;
+        if (NRM) nrm += wn * wn;
+      }
+    }
+    if (DOTS) {
+#pragma unroll
+      for (int i = 0; i < CPG; ++i) dacc[i] += z[i] * wn;
+    }
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (DOTS) {
+#pragma unroll
+    for (int i = 0; i < CPG; ++i) {
+      const double v = warp_sum(dacc[i]);
+      if (lane == 0) wred[wid][i] = v;
+    }
+    __syncthreads();
+    const int wpg = TR / 32;  // warps per chunk group
+    for (int c = threadIdx.x; c < p; c += CT) {
+      const int gg = c / CPG, i = c % CPG;
+      double sum = 0.0;
+      for (int ww = 0; ww < wpg; ++ww) sum += wred[gg * wpg + ww][i];
+      dpart[c] = sum;
+    }
+  }
+  if (NRM) {
+    const double tn = block_sum(nrm, bsh);
+    if (threadIdx.x == 0) dpart[0] = tn;
+  }
+  __syncthreads();
+  const int nv = DOTS ? p : 1;
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot)) return;
+  if (OPK == 0) epi_pass(st, tot, lo, p, true);
+  else if (OPK == 1) epi_pass(st, tot, lo, p, false);
+  else {
+    epi_ls(st, L, tot, 0);
+    if (cond && threadIdx.x == 0) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
+  }
+  if (threadIdx.x == 0) prof_end(st, kid, 8.0 * (double)L.n * (p + (UPD ? 2.0 : 1.0)));
+}
+
 }  // namespace
 
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s) {
@@ -192,7 +315,16 @@ cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, u
   static bool init = false;
   if (!init) {  // two 512-thread CTAs per SM need more than the default shared-memory carveout
     cudaFuncSetAttribute(k_orth, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_cgs<0>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_cgs<1>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_cgs<2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     init = true;
+  }
+  if (L.cgs_ok) {  // register-resident CGS kernels (augment's OP_UN also needs Q^T w: generic path)
+    const int g = vec_grid(L.ld);
+    // measured on B200 (C2, C4): k_cgs wins for the fused update+dots pass; the row-parallel
+    // generic kernel is faster for the dots-only and update+norm passes
+    if (op == OP_UD2) { k_cgs<1><<<g, CT, 0, s>>>(L, st, 0ull); return cudaGetLastError(); }
   }
   k_orth<<<vec_grid(L.ld), OT, 0, s>>>(OrthArgs{L, st, op, cond, cond != 0ull});
   return cudaGetLastError();

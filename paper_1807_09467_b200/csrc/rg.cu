@@ -476,7 +476,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   const int VB = 2 * c->max_k;
   c->ncol = VB + c->max_m + 1;
   const size_t np = (size_t)c->npad;
-  const size_t part = std::max<size_t>((size_t)NSM * 8 * MAXRED, (size_t)NSM * 2080);
+  const size_t part = std::max<size_t>((size_t)NSM * 8 * MAXRED, (size_t)NSM * 2 * 64 * 64);  // Gram: 296 CTAs x 64^2
   if ((s = dalloc(&c->Z, np * c->ncol, "Z")) != RG_OK || (s = dalloc(&c->x, np, "x")) != RG_OK ||
       (s = dalloc(&c->b, np, "b")) != RG_OK || (s = dalloc(&c->X, np * c->max_s, "X")) != RG_OK ||
       (s = dalloc(&c->Y, np * c->max_s, "Y")) != RG_OK || (s = dalloc(&c->t1, np, "t1")) != RG_OK ||
@@ -523,6 +523,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   c->L.hist = c->hist;
   c->L.partial = c->partial;
   c->L.counter = c->counter;
+  c->L.cgs_ok = (c->max_k + c->max_m + 1) <= 128 && !getenv("RG_NO_CGS");
   if ((s = set_matrix(c, A, true)) != RG_OK) {
     std::string msg = g_err;
     rg_destroy(c);
@@ -645,6 +646,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   h->tol = tol;
   h->jfinal = -1;
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
+  c->L.augment = eff == RG_AUGMENT;
   CK(cudaEventRecord(c->e0, s));
   CK(launch_orth(c->L, c->st, OP_NORMB, s));
   CK(cycle_start(c, eff));
