@@ -134,6 +134,13 @@ __device__ __forceinline__ void prof_end(DevState* st, int kid, double bytes) {
   }
 }
 
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p) {
+  unsigned t;
+  asm volatile("atom.add.release.gpu.u32 %0, [%1], 1;" : "=r"(t) : "l"(p) : "memory");
+  return t;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
 // Deterministic two-stage grid reduction.  Every CTA passes nv values in shared memory `vals`
 // (nv <= MAXRED).  Returns true in exactly one CTA (the last to arrive), whose shared array `tot`
 // then holds the totals, summed over CTAs in index order.  `scr` needs max(blockDim, MAXRED)
@@ -144,12 +151,14 @@ __device__ __forceinline__ bool grid_reduce(const double* vals, int nv, double* 
                                             int ldp = MAXRED) {
   __shared__ unsigned s_ticket;
   for (int i = threadIdx.x; i < nv; i += blockDim.x) partial[(size_t)blockIdx.x * ldp + i] = vals[i];
-  __threadfence();
+  // One release by thread 0 after the CTA barrier publishes every thread's partials (PTX memory
+  // model: bar.sync orders them before the gpu-scope release); no per-thread membar.gl.
   __syncthreads();
-  if (threadIdx.x == 0) s_ticket = atomicAdd(counter, 1u);
+  if (threadIdx.x == 0) s_ticket = atom_add_release(counter);
   __syncthreads();
   if (s_ticket != gridDim.x - 1) return false;
-  __threadfence();
+  if (threadIdx.x == 0) fence_acq_rel();
+  __syncthreads();
   // warp w reduces columns c = w, w + nwarps, ...: lane l sums partials of CTAs l, l+32, ...
   // (8 independent loads in flight), then a fixed shuffle tree: deterministic order.
   const int G = gridDim.x;
@@ -197,9 +206,8 @@ __device__ __forceinline__ bool grid_reduce(const double* vals, int nv, double* 
 // have no reduction.
 __device__ __forceinline__ bool grid_last(unsigned* counter) {
   __shared__ unsigned s_t;
-  __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_t = atomicAdd(counter, 1u);
+  if (threadIdx.x == 0) s_t = atom_add_release(counter);
   __syncthreads();
   if (s_t != gridDim.x - 1) return false;
   if (threadIdx.x == 0) *counter = 0u;

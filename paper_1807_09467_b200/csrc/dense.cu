@@ -80,25 +80,30 @@ __global__ void __launch_bounds__(GT) k_gram_mma(const double* __restrict__ Y, i
   }
 }
 
-// Pass 2: G(a,b) = sum over CTAs (index order) of the partials, a <= b; mirrored.
+// Pass 2: G(a,b) = sum over CTAs (index order within each lane, fixed shuffle tree) of the
+// partials, a <= b; mirrored.  One warp per entry.
 __global__ void __launch_bounds__(256) k_gram_reduce(const double* __restrict__ partial, int nparts, int s,
                                                      double* G, unsigned* counter, DevState* st, double bytes) {
   const int P = s * (s + 1) / 2;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P; p += (gridDim.x * blockDim.x) >> 5) {
     int a = 0, q = p;
     while (q >= s - a) { q -= s - a; ++a; }
     const int b = a + q;
     const int off = a * S8MAX + b;
     double acc = 0.0;
-    for (int c = 0; c < nparts; c += 8) {
+    for (int c = lane; c < nparts; c += 8 * 32) {
       double v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = c + u < nparts ? __ldcg(partial + (size_t)(c + u) * GPL + off) : 0.0;
+      for (int u = 0; u < 8; ++u) v[u] = c + 32 * u < nparts ? __ldcg(partial + (size_t)(c + 32 * u) * GPL + off) : 0.0;
 #pragma unroll
       for (int u = 0; u < 8; ++u) acc += v[u];
     }
-    G[a * s + b] = acc;
-    G[b * s + a] = acc;
+    acc = warp_sum(acc);
+    if (lane == 0) {
+      G[a * s + b] = acc;
+      G[b * s + a] = acc;
+    }
   }
   if (st && st->profile && grid_last(counter) && threadIdx.x == 0) prof_end(st, K_GRAM, bytes);
 }
@@ -390,7 +395,7 @@ cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G
   const int gi = (int)(g < 1 ? 1 : g);
   k_gram_mma<<<gi, GT, 0, strm>>>(Y, ld, n, s, partial, st);
   const int P = s * (s + 1) / 2;
-  k_gram_reduce<<<(P + 255) / 256, 256, 0, strm>>>(partial, gi, s, G, counter, st, 8.0 * (double)n * s);
+  k_gram_reduce<<<(P + 7) / 8, 256, 0, strm>>>(partial, gi, s, G, counter, st, 8.0 * (double)n * s);
   return cudaGetLastError();
 }
 
