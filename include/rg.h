@@ -93,6 +93,8 @@ typedef struct {
 
 #define RG_FLAG_NO_GRAPH 1 /* launch kernels one by one instead of replaying CUDA graphs      */
 #define RG_FLAG_PROFILE 2  /* record per-kernel device time (%globaltimer) for rg_kernel_stats */
+#define RG_FLAG_CGS2 4     /* classical CGS2 (3 reductions per Arnoldi step) instead of the default
+                              delayed CGS2 (1 reduction per step); same iterates in exact arithmetic */
 
 /* Solve report (fields follow SPEC.md's SolveReport).
  *   iterations   Arnoldi steps summed over restart cycles (residual and C = AW products are

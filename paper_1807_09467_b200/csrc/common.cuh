@@ -26,7 +26,7 @@ constexpr int VEC_CTAS_PER_SM = 2;         // -> 296 CTAs: 32 resident warps / S
 // ---------------------------------------------------------------- kernel ids (statistics)
 enum KernelId {
   K_SPMV_STEP = 0, K_SPMV_RES, K_SPMV_PLAIN, K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN,
-  K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_COUNT
+  K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_DK1, K_DK2, K_COUNT
 };
 
 struct KStatDev {
@@ -54,7 +54,9 @@ struct DevState {
   int hist_len;
   int spmv_count;
   int bzero;
+  int dcgs;       // 1: delayed CGS2 (one reduction per Arnoldi step), 0: classical CGS2
   double bnorm, beta, relres;
+  double k2_inv_nu, k2_u_next, k2_y;  // DCGS2 update-pass scalars (v_j = u/nu + ..., u_next = ...)
   // least-squares state
   double cs[MAXM], sn[MAXM], g[MAXM + 2], y[MAXM + 2];
   double R[MAXM][MAXM + 2];        // rotated columns, R[j][0..j]
@@ -62,12 +64,14 @@ struct DevState {
   double Bm[MAXM][MAXK];           // deflate: B[:, j] = Q^T A v_j   (GCRO: A V = Q B + V H)
   double Gm[MAXM + 2][MAXK];       // augment: G[i, :] = Q^T v_i
   double T[MAXM + 2][MAXM + 2];    // augment: Cholesky factor of I - G^T G, T[col][row]
+  double Si[MAXM + 2][MAXM + 2];   // augment: S = T^{-1} (upper triangular), Si[col][row]
   double RCinv[MAXK][MAXK];        // R_C^{-1}, column-major [col][row]
   double RC[MAXK][MAXK];           // R_C, column-major [col][row]
   double coef[MAXCOL];             // coefficients of the current CGS pass (absolute column)
   double hcol[MAXCOL];             // accumulated coefficients of the current column
   double coefx[MAXCOL];            // cycle-end x-update coefficients
   double sc[MAXCOL];               // column scales (V stored un-normalised: v_i = sc_i * raw_i)
+  double coefv[MAXCOL];            // DCGS2: v_j = u/nu + sum_c coefv_c P_c
   KStatDev kstat[K_COUNT];
 };
 

@@ -1,0 +1,263 @@
+// dcgs.cu — delayed classical Gram-Schmidt with re-orthogonalisation (DCGS2) for the Arnoldi
+// step: one grid reduction and two passes over the basis per step (the classical CGS2 path in
+// orth.cu needs three of each).
+//
+// Iteration j of a restart cycle holds u = the step-(j-1) vector after ONE CGS pass against
+// P_j = [Q | v_0 .. v_{j-1}] (deflate) or [v_0 .. v_{j-1}] (plain, augment), stored raw in V
+// column j, and y = A u (SpMV, V column j+1).
+//   DK1 (this file): one sweep computing a = P_j^T u, b = P_j^T y, s = u.u, g = u.y (+ Q^T u for
+//       augment).  Its last CTA finishes column j-1 of the Hessenberg matrix: the delayed second
+//       pass gives h_{j-1} += a and nu = sqrt(s - a.a) = H[j][j-1] (Pythagoras: a is O(eps |u|),
+//       no cancellation), runs the least-squares step on it (epi_ls), and, from the Arnoldi
+//       relation A V_j = Q B_j + V_{j+1} H_j, derives without another pass
+//         A v_j = (y - A P_j a)/nu,  w = [P] A v_j,  first-pass coefficients h1 = P_{j+1}^T w.
+//   DK2 (this file): one sweep writing v_j = (u - P_j a)/nu and the next u = w - P_{j+1} h1 as two
+//       linear combinations of the same rows of [u, y, P_j]; no reduction.
+// (Swirydowicz, Langou, Ananthan, Yang, Thomas, "Low synchronization Gram-Schmidt and GMRES
+// algorithms", 2020, and Bielich et al. 2022 describe the delayed re-orthogonalisation idea; the
+// recycled (Q) bookkeeping here follows the GCRO relation of PAPER.md:332.)  The A Q a_Q term is
+// dropped: a_Q = Q^T u is at rounding level because u was projected against Q.
+#include "epilogue.cuh"
+#include "kernels.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int DT = 512;
+
+// ---------------------------------------------------------------- DK1 epilogue
+// tot = [a (p) | b (p) | s | g | q (k, augment)],  P = columns [lo, VB + j).
+__device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p) {
+  __shared__ double lst[MAXK + 2];
+  __shared__ double Ha[MAXM + 2], Ba[MAXK];
+  __shared__ double s_nu, s_d, s_aj;
+  __shared__ int s_go;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
+  const int lo = (var == RG_DEFLATE) ? QB : VB;
+  const int nq = VB - lo;  // Q columns inside P (deflate)
+  const double* a = tot;
+  const double* b = tot + p;
+  const double ss = tot[2 * p], gg = tot[2 * p + 1];
+  if (tid == 0) {
+    double aa = 0.0;
+    for (int c = 0; c < p; ++c) aa += a[c] * a[c];
+    const double nu2 = ss - aa;
+    s_nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+  }
+  __syncthreads();
+  const double nu = s_nu;
+  if (j >= 1) {
+    // finish column j-1: second-pass coefficients a (V part -> H, Q part -> B via hcol)
+    for (int c = tid; c < p; c += bd) st->hcol[lo + c] += a[c];
+    if (var == RG_AUGMENT && k > 0) {  // Q^T v_j = (Q^T u - G_j^T a_V) / nu, handed to epi_ls as (.)*nu
+      for (int l = tid; l < k; l += bd) {
+        double q = tot[2 * p + 2 + l];
+        for (int i = 0; i < j; ++i) q -= st->Gm[i][l] * a[nq + i];
+        lst[l] = q;
+      }
+    }
+    if (tid == 0) {
+      lst[(var == RG_AUGMENT) ? k : 0] = nu * nu;
+      st->j = j - 1;
+    }
+    __syncthreads();
+    epi_ls(st, L, lst, (var == RG_AUGMENT) ? k : 0);
+    if (tid == 0) {
+      st->sc[VB + j] = 1.0;  // DK2 writes v_j normalised
+      s_go = st->active;
+    }
+    __syncthreads();
+    if (!s_go) return;
+  } else {
+    if (tid == 0) s_go = 1;
+    __syncthreads();
+  }
+  // ---- coefficients of DK2 and the first-pass coefficients of column j
+  const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
+  // (H a_V)_c over the final columns 0..j-1 (Hessenberg) and (B a_V)_l: one warp per output,
+  // lanes over the summation index (all loads of a warp in flight), fixed shuffle tree.
+  {
+    const int lane = tid & 31, nw = bd >> 5;
+    for (int o = tid >> 5; o < j + (var == RG_DEFLATE ? nq : 0); o += nw) {
+      double s = 0.0;
+      if (o < j) {
+        for (int i = (o > 0 ? o - 1 : 0) + lane; i < j; i += 32) s += st->Hraw[i][o] * a[nq + i];
+      } else {
+        const int l = o - j;
+        for (int i = lane; i < j; i += 32) s += st->Bm[i][l] * a[nq + i];
+      }
+      s = warp_sum(s);
+      if (lane == 0) {
+        if (o < j) Ha[o] = s;
+        else Ba[o - j] = s;
+      }
+    }
+  }
+  if (tid == 0) {
+    double ab = 0.0;
+    for (int c = 0; c < p; ++c) ab += a[c] * b[c];
+    const double aj = j >= 1 ? a[nq + j - 1] : 0.0;
+    s_aj = aj;
+    s_d = ((gg - ab) * inv - nu * aj) * inv;  // v_j^T w
+    st->k2_inv_nu = inv;
+    st->k2_y = inv;
+    st->k2_u_next = -(aj + s_d) * inv;
+    st->hcol[VB + j] = s_d;
+  }
+  __syncthreads();
+  const double f = (s_aj + s_d) * inv;
+  for (int c = tid; c < j; c += bd) {  // V columns
+    const double cv = (b[nq + c] - Ha[c]) * inv;
+    st->hcol[VB + c] = cv;
+    st->coef[VB + c] = -Ha[c] * inv - cv + f * a[nq + c];
+    st->coefv[VB + c] = -a[nq + c] * inv;
+  }
+  for (int l = tid; l < nq; l += bd) {  // Q columns (deflate): w = (I - QQ^T) A v_j
+    st->hcol[QB + l] = (b[l] - Ba[l]) * inv;
+    st->coef[QB + l] = -b[l] * inv + f * a[l];
+    st->coefv[QB + l] = -a[l] * inv;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- DK1: dots of u and y with P
+// Rows are split evenly over the CTAs; per 512-row sub-tile u and y are staged in shared memory,
+// warp w owns columns w, w+16, ...: 16 independent loads per lane, two products, fixed shuffle
+// tree, warp-owned shared-memory accumulators (deterministic).
+__global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned long long cond) {
+  __shared__ double us[DT], ys[DT];
+  __shared__ double dpart[MAXRED];
+  __shared__ double tot[MAXRED];
+  __shared__ double bsh[33];
+  if (!st->active) { prof_noop(st, K_DK1); return; }
+  prof_begin(st, K_DK1);
+  const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
+  const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
+  const int nqd = (var == RG_AUGMENT) ? k : 0;  // extra Q^T u dots
+  const bool have_y = j < st->m;                // no SpMV was run at j == m
+  const int64_t ld = L.ld;
+  const double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;
+  const double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;
+  const double* __restrict__ Z = L.Z;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nv = 2 * p + 2 + nqd;
+  for (int c = threadIdx.x; c < nv; c += DT) dpart[c] = 0.0;
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  double s_uu = 0.0, s_uy = 0.0;
+  constexpr int RPL = DT / 32;
+  for (int64_t base = r0; base < r1; base += DT) {
+    const int64_t r = base + threadIdx.x;
+    const bool in = r < r1;
+    const double ur = in ? u[r] : 0.0;
+    const double yr = (in && have_y) ? y[r] : 0.0;
+    __syncthreads();  // previous sub-tile's readers are done with us/ys (and dpart zeroed)
+    us[threadIdx.x] = ur;
+    ys[threadIdx.x] = yr;
+    s_uu += ur * ur;
+    s_uy += ur * yr;
+    __syncthreads();
+    const int cnt = (int)((r1 - base) < DT ? (r1 - base) : DT);
+    for (int c = wid; c < p + nqd; c += 16) {
+      const int col = c < p ? lo + c : QB + (c - p);
+      const double* __restrict__ zc = Z + (int64_t)col * ld + base + lane;
+      double zv[RPL];
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) zv[q] = (lane + 32 * q < cnt) ? __ldcs(zc + 32 * q) : 0.0;
+      double su = 0.0, sy = 0.0;
+#pragma unroll
+      for (int q = 0; q < RPL; ++q) {
+        su += zv[q] * us[lane + 32 * q];
+        sy += zv[q] * ys[lane + 32 * q];
+      }
+      su = warp_sum(su);
+      if (c < p) {
+        sy = warp_sum(sy);
+        if (lane == 0) {
+          dpart[c] += su;
+          dpart[p + c] += sy;
+        }
+      } else if (lane == 0) {
+        dpart[2 * p + 2 + (c - p)] += su;
+      }
+    }
+  }
+  // layout of the reduced vector: [a (p) | b (p) | s | g | q (nqd)]
+  const double t1 = block_sum(s_uu, bsh);
+  const double t2 = block_sum(s_uy, bsh);
+  if (threadIdx.x == 0) {
+    dpart[2 * p] = t1;
+    dpart[2 * p + 1] = t2;
+  }
+  __syncthreads();
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot)) return;
+  epi_dcgs(st, L, tot, p);
+  if (threadIdx.x == 0) {
+    if (st->active) st->j = j + 1;  // next iteration (DK2 of this one uses st->j - 1)
+    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
+    prof_end(st, K_DK1, 8.0 * (double)L.n * (p + nqd + (have_y ? 2 : 1)));
+  }
+}
+
+// ---------------------------------------------------------------- DK2: v_j and the next u
+__global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
+  __shared__ double cv[MAXCOL], cn[MAXCOL];
+  if (!st->active) { prof_noop(st, K_DK2); return; }
+  prof_begin(st, K_DK2);
+  const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
+  const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
+  const int64_t ld = L.ld;
+  double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;      // in: u, out: v_j
+  double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;  // in: y, out: next u
+  const double* __restrict__ Z = L.Z;
+  for (int c = threadIdx.x; c < p; c += DT) {
+    cv[c] = st->coefv[lo + c];
+    cn[c] = st->coef[lo + c];
+  }
+  const double inv = st->k2_inv_nu, fy = st->k2_y, fu = st->k2_u_next;
+  __syncthreads();
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += DT) {
+    const double ur = u[r], yr = y[r];
+    double sv = 0.0, sn = 0.0;
+    int c = 0;
+    for (; c + 8 <= p; c += 8) {
+      double z[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) z[t] = __ldcs(Z + (int64_t)(lo + c + t) * ld + r);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        sv += cv[c + t] * z[t];
+        sn += cn[c + t] * z[t];
+      }
+    }
+    for (; c < p; ++c) {
+      const double z = __ldcs(Z + (int64_t)(lo + c) * ld + r);
+      sv += cv[c] * z;
+      sn += cn[c] * z;
+    }
+    u[r] = ur * inv + sv;
+    y[r] = yr * fy + ur * fu + sn;
+  }
+  if (st->profile && grid_last(L.counter) && threadIdx.x == 0) prof_end(st, K_DK2, 8.0 * (double)L.n * (p + 4));
+}
+
+}  // namespace
+
+cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_dk1, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    cudaFuncSetAttribute(k_dk2, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    init = true;
+  }
+  if (phase == 1) k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
+  else k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
+  return cudaGetLastError();
+}
+
+}  // namespace rg

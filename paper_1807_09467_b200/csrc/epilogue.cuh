@@ -33,11 +33,12 @@ __device__ __forceinline__ void epi_cycle_start(DevState* st, const Layout& L, d
       st->active = 1;
       st->j = 0;
       st->cycles++;
-      st->sc[L.VB] = 1.0 / beta;
+      st->sc[L.VB] = st->dcgs ? 1.0 : 1.0 / beta;  // DCGS2 stores every v_i normalised
       st->g[0] = beta;
       if (st->variant == RG_AUGMENT) {
         // v_0 = r_c/beta with Q^T r_c = 0 after the cycle-start projection: G[0,:] = 0, T00 = 1.
         st->T[0][0] = 1.0;
+        st->Si[0][0] = 1.0;
         for (int l = 0; l < st->k_eff; ++l) st->Gm[0][l] = 0.0;
       }
     }
@@ -67,19 +68,37 @@ __device__ __forceinline__ void rcinv_apply(const DevState* st, int k, const dou
 }
 
 // ---------------------------------------------------------------- least-squares step
-// After the last CGS2 pass of Arnoldi step j: tot[0..nd) = Q^T w (augment, nd = k_eff),
-// tot[nd] = ||w||^2 of the new (un-normalised) basis vector w = raw v_{j+1}.
+// After the last orthogonalisation pass of Arnoldi step j: tot[0..nd) = Q^T w (augment,
+// nd = k_eff), tot[nd] = ||w||^2 of the new (un-normalised) basis vector w = raw v_{j+1}.
+// Every global access is issued as a parallel batch (no serial chains of dependent loads);
+// the serial Givens recurrence runs in thread 0 from shared memory.
 __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const double* tot, int nd) {
   __shared__ double h[MAXM + 2], mc[MAXM + 2], tv[MAXM + 2], csS[MAXM], snS[MAXM];
-  __shared__ double ys[MAXM + 2], gs[MAXM + 2], us[MAXK], zs[MAXK];
+  __shared__ double ys[MAXM + 2], gs[MAXM + 2], us[MAXK], zs[MAXK], rd[MAXM + 2];
   __shared__ int s_stop, s_jf, s_tb;
-  const int tid = threadIdx.x, bd = blockDim.x;
+  __shared__ double s_sc[8];
+  __shared__ int s_ic[8];
+  const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, nw = bd >> 5;
   const int j = st->j, VB = L.VB, k = st->k_eff, var = st->variant;
   const int QB = VB - k;
   const double nrm = sqrt(tot[nd]);
+  // ---- one parallel batch of loads: h column, rotations, scalars
   for (int i = tid; i <= j; i += bd) h[i] = st->hcol[VB + i];
   for (int i = tid; i < j; i += bd) { csS[i] = st->cs[i]; snS[i] = st->sn[i]; }
-  if (tid == 0) { h[j + 1] = nrm; s_tb = 0; s_stop = 0; }
+  if (tid == 0) {
+    h[j + 1] = nrm;
+    s_tb = 0;
+    s_stop = 0;
+    s_sc[0] = st->g[j];
+    s_sc[1] = st->bnorm;
+    s_sc[2] = st->tol;
+    s_sc[3] = st->beta;
+    s_ic[0] = st->m;
+    s_ic[1] = st->iters;
+    s_ic[2] = st->max_iters;
+    s_ic[3] = st->hist_len;
+    s_ic[4] = st->hist_cap;
+  }
   __syncthreads();
   for (int i = tid; i <= j + 1; i += bd) st->Hraw[j][i] = h[i];
   if (var == RG_DEFLATE)
@@ -88,35 +107,50 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
     for (int l = tid; l < k; l += bd) st->Gm[j + 1][l] = nrm > 0.0 ? tot[l] / nrm : 0.0;
   __syncthreads();
   if (var == RG_AUGMENT && k > 0) {
-    // M = I - G^T G restricted to v_0..v_{j+1}; new column of its Cholesky factor T.
-    for (int i = tid; i <= j + 1; i += bd) {
-      double s = (i == j + 1) ? 1.0 : 0.0;
-      for (int l = 0; l < k; ++l) s -= st->Gm[i][l] * st->Gm[j + 1][l];
-      mc[i] = s;
+    // M = I - G^T G on v_0..v_{j+1}; new column (t, tau) of its Cholesky factor T = S^{-1}:
+    //   t = T_old^{-T} M[0..j, j+1] = S_old^T M[0..j, j+1],  tau^2 = M[j+1,j+1] - t.t,
+    //   new column of S: -S_old t / tau, S[j+1][j+1] = 1/tau.  Warp per output, lanes over the sum.
+    for (int i = tid >> 5; i <= j + 1; i += nw) {
+      double sacc = 0.0;
+      for (int l = lane; l < k; l += 32) sacc += st->Gm[i][l] * st->Gm[j + 1][l];
+      sacc = warp_sum(sacc);
+      if (lane == 0) mc[i] = ((i == j + 1) ? 1.0 : 0.0) - sacc;
+    }
+    __syncthreads();
+    for (int i = tid >> 5; i <= j; i += nw) {  // t_i = sum_{l<=i} S(l,i) mc_l
+      double sacc = 0.0;
+      for (int l = lane; l <= i; l += 32) sacc += st->Si[i][l] * mc[l];
+      sacc = warp_sum(sacc);
+      if (lane == 0) tv[i] = sacc;
     }
     __syncthreads();
     if (tid == 0) {
       double t2 = 0.0;
-      for (int i = 0; i <= j; ++i) {  // T_old^T t = M[0..j, j+1]
-        double s = mc[i];
-        for (int l = 0; l < i; ++l) s -= st->T[i][l] * tv[l];
-        tv[i] = s / st->T[i][i];
-        t2 += tv[i] * tv[i];
-      }
+      for (int i = 0; i <= j; ++i) t2 += tv[i] * tv[i];
       const double tau2 = mc[j + 1] - t2;
-      if (!(tau2 > 1e-14)) {
-        s_tb = 1;  // v_{j+1} (numerically) in span(Q) + span(V_{j+1}): end the cycle
-      } else {
-        for (int i = 0; i <= j; ++i) st->T[j + 1][i] = tv[i];
-        st->T[j + 1][j + 1] = sqrt(tau2);
-      }
+      if (!(tau2 > 1e-14)) s_tb = 1;  // v_{j+1} (numerically) in span(Q) + span(V_{j+1}): end the cycle
+      else s_sc[4] = sqrt(tau2);
     }
     __syncthreads();
-    if (!s_tb) {  // column j of M = T H: mc_i = sum_{l>=i} T(i,l) h_l
-      for (int i = tid; i <= j + 1; i += bd) {
-        double s = 0.0;
-        for (int l = i; l <= j + 1; ++l) s += st->T[l][i] * h[l];
-        mc[i] = s;
+    if (!s_tb) {
+      const double tau = s_sc[4];
+      for (int l = tid >> 5; l <= j; l += nw) {  // S(l, j+1) = -(sum_{i>=l} S(l,i) t_i)/tau
+        double sacc = 0.0;
+        for (int i = l + lane; i <= j; i += 32) sacc += st->Si[i][l] * tv[i];
+        sacc = warp_sum(sacc);
+        if (lane == 0) st->Si[j + 1][l] = -sacc / tau;
+      }
+      for (int i = tid; i <= j; i += bd) st->T[j + 1][i] = tv[i];
+      if (tid == 0) {
+        st->T[j + 1][j + 1] = tau;
+        st->Si[j + 1][j + 1] = 1.0 / tau;
+      }
+      __syncthreads();
+      for (int i = tid >> 5; i <= j + 1; i += nw) {  // column j of M = T H: sum_{l>=i} T(i,l) h_l
+        double sacc = 0.0;
+        for (int l = i + lane; l <= j + 1; l += 32) sacc += st->T[l][i] * h[l];
+        sacc = warp_sum(sacc);
+        if (lane == 0) mc[i] = sacc;
       }
       __syncthreads();
       for (int i = tid; i <= j + 1; i += bd) h[i] = mc[i];
@@ -125,50 +159,44 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
   }
   if (tid == 0) {
     st->sc[VB + j + 1] = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    const double bnorm = s_sc[1], tol = s_sc[2], beta = s_sc[3];
+    int iters = s_ic[1];
     int stop = 0, jf = j;
-    if (s_tb) {
-      stop = 1;
-      jf = j - 1;
-      st->iters++;
-    } else {
+    if (!s_tb) {
       for (int i = 0; i < j; ++i) {  // apply the previous rotations
         const double a = h[i], b = h[i + 1];
         h[i] = csS[i] * a + snS[i] * b;
         h[i + 1] = -snS[i] * a + csS[i] * b;
       }
-      const double a = h[j], b = h[j + 1];
-      const double den = hypot(a, b);
-      if (!(den > 0.0)) {  // A v_j = 0 within span: no progress possible in this cycle
-        s_tb = 1;
-        st->iters++;
-        jf = j - 1;
-        stop = 1;
-      }
+      if (!(hypot(h[j], h[j + 1]) > 0.0)) s_tb = 1;  // A v_j = 0 within span: no progress possible
     }
-    if (!s_tb) {
+    if (s_tb) {
+      stop = 1;
+      jf = j - 1;
+      ++iters;
+    } else {
       const double a = h[j], b = h[j + 1];
       const double den = hypot(a, b);
       const double c = a / den, s = b / den;
       st->cs[j] = c;
       st->sn[j] = s;
       h[j] = den;
-      for (int i = 0; i <= j; ++i) st->R[j][i] = h[i];
-      const double gj = st->g[j];
+      const double gj = s_sc[0];
       st->g[j] = c * gj;
       st->g[j + 1] = -s * gj;
-      const double res = fabs(st->g[j + 1]) / st->bnorm;
-      if (st->hist_len < st->hist_cap) L.hist[st->hist_len++] = res;
-      st->iters++;
+      const double res = fabs(s * gj) / bnorm;
+      if (s_ic[3] < s_ic[4]) { L.hist[s_ic[3]] = res; st->hist_len = s_ic[3] + 1; }
+      ++iters;
       if (!isfinite(res)) {
         st->status = RG_E_NUMERIC;
         st->done = 1;
         stop = 1;
         jf = -1;
       } else {
-        stop = (res <= st->tol) || (nrm <= 1e-14 * st->beta) || (j + 1 >= st->m) ||
-               (st->iters >= st->max_iters);
+        stop = (res <= tol) || (nrm <= 1e-14 * beta) || (j + 1 >= s_ic[0]) || (iters >= s_ic[2]);
       }
     }
+    st->iters = iters;
     if (!stop) st->j = j + 1;
     s_stop = stop;
     s_jf = jf;
@@ -177,37 +205,45 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
       st->jfinal = jf;
       st->have_xupd = jf >= 0;
     }
-    for (int i = 0; i <= jf; ++i) gs[i] = st->g[i];
   }
   __syncthreads();
+  if (!s_tb) for (int i = tid; i <= j; i += bd) st->R[j][i] = h[i];  // rotated column (parallel stores)
   if (!s_stop || s_jf < 0) return;
+  // ---- cycle end: y = R^{-1} g[0..jf] (R columns 0..jf-1 from global, column jf possibly fresh)
   const int jf = s_jf;
-  // y = R^{-1} g[0..jf]  (column-oriented back substitution, parallel updates)
+  for (int i = tid; i <= jf; i += bd) {
+    gs[i] = (i == j && !s_tb) ? st->g[j] : st->g[i];
+    rd[i] = (i == j && !s_tb) ? h[j] : st->R[i][i];
+  }
+  __syncthreads();
   for (int i = jf; i >= 0; --i) {
-    if (tid == 0) ys[i] = gs[i] / st->R[i][i];
+    if (tid == 0) ys[i] = gs[i] / rd[i];
     __syncthreads();
-    for (int l = tid; l < i; l += bd) gs[l] -= st->R[i][l] * ys[i];
+    for (int l = tid; l < i; l += bd) gs[l] -= ((i == j && !s_tb) ? h[l] : st->R[i][l]) * ys[i];
     __syncthreads();
   }
   for (int i = tid; i <= jf; i += bd) st->coefx[VB + i] = -ys[i];  // x += V y
   if (k > 0 && var != RG_PLAIN) {
     if (var == RG_DEFLATE) {  // x -= W R_C^{-1} B y
-      for (int l = tid; l < k; l += bd) {
-        double s = 0.0;
-        for (int i = 0; i <= jf; ++i) s += st->Bm[i][l] * ys[i];
-        us[l] = s;
+      for (int l = tid >> 5; l < k; l += nw) {
+        double sacc = 0.0;
+        for (int i = lane; i <= jf; i += 32) sacc += st->Bm[i][l] * ys[i];
+        sacc = warp_sum(sacc);
+        if (lane == 0) us[l] = sacc;
       }
     } else {  // augment: x -= W R_C^{-1} G Hbar y
-      for (int i = tid; i <= jf + 1; i += bd) {
-        double s = 0.0;
-        for (int c = (i > 0 ? i - 1 : 0); c <= jf; ++c) s += st->Hraw[c][i] * ys[c];  // Hessenberg
-        mc[i] = s;
+      for (int i = tid >> 5; i <= jf + 1; i += nw) {
+        double sacc = 0.0;
+        for (int c = (i > 0 ? i - 1 : 0) + lane; c <= jf; c += 32) sacc += st->Hraw[c][i] * ys[c];  // Hessenberg
+        sacc = warp_sum(sacc);
+        if (lane == 0) mc[i] = sacc;
       }
       __syncthreads();
-      for (int l = tid; l < k; l += bd) {
-        double s = 0.0;
-        for (int i = 0; i <= jf + 1; ++i) s += st->Gm[i][l] * mc[i];
-        us[l] = s;
+      for (int l = tid >> 5; l < k; l += nw) {
+        double sacc = 0.0;
+        for (int i = lane; i <= jf + 1; i += 32) sacc += st->Gm[i][l] * mc[i];
+        sacc = warp_sum(sacc);
+        if (lane == 0) us[l] = sacc;
       }
     }
     __syncthreads();

@@ -32,6 +32,8 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
 enum OrthOp { OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB };
 // cond != 0: cudaGraphConditionalHandle set to st->active by OP_UN's epilogue (graph WHILE node)
 cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond = 0);
+// DCGS2 Arnoldi step (dcgs.cu): phase 1 = dots + epilogue (sets the WHILE condition), 2 = update
+cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond = 0);
 // WHILE-node condition from the state: which 0 -> active, 1 -> !done
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s);
 

@@ -92,6 +92,7 @@ struct rg_ctx {
   int k_eff = 0;
   bool have_W = false;
   bool c_valid = false;
+  bool use_dcgs = true;
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -310,6 +311,10 @@ cudaError_t cycle_start(rg_ctx* c, int variant) {
 cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
   cudaError_t e;
   if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
+  if (c->use_dcgs) {  // delayed CGS2: one reduction + one update pass
+    if ((e = launch_dcgs(c->L, c->st, 1, c->stream, cond)) != cudaSuccess) return e;
+    return launch_dcgs(c->L, c->st, 2, c->stream);
+  }
   if ((e = launch_orth(c->L, c->st, OP_D1, c->stream)) != cudaSuccess) return e;
   if ((e = launch_orth(c->L, c->st, OP_UD2, c->stream)) != cudaSuccess) return e;
   return launch_orth(c->L, c->st, OP_UN, c->stream, cond);
@@ -317,7 +322,8 @@ cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
 
 cudaError_t cycle_body(rg_ctx* c, int variant, int m) {
   cudaError_t e;
-  for (int j = 0; j < m; ++j)
+  const int steps = m + (c->use_dcgs ? 1 : 0);  // DCGS2 finishes column j-1 in step j
+  for (int j = 0; j < steps; ++j)
     if ((e = arnoldi_step(c, 0)) != cudaSuccess) return e;
   if ((e = launch_orth(c->L, c->st, OP_XUPD, c->stream)) != cudaSuccess) return e;
   return cycle_start(c, variant);
@@ -462,6 +468,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   CK(cudaGetDevice(&c->dev));
   c->flags = opt->flags;
   if (getenv("RG_NO_GRAPH")) c->flags |= RG_FLAG_NO_GRAPH;  // ncu cannot profile kernels inside conditional graphs
+  if (getenv("RG_CGS2") || (opt->flags & RG_FLAG_CGS2)) c->use_dcgs = false;
   if (opt->cuda_stream) {
     c->stream = (cudaStream_t)opt->cuda_stream;
   } else {
@@ -645,6 +652,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   h->profile = (c->flags & RG_FLAG_PROFILE) ? 1 : 0;
   h->tol = tol;
   h->jfinal = -1;
+  h->dcgs = c->use_dcgs ? 1 : 0;
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
   c->L.augment = eff == RG_AUGMENT;
   CK(cudaEventRecord(c->e0, s));
@@ -711,7 +719,8 @@ RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, in
 RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t* count) {
   static const char* names[K_COUNT] = {"spmv_step", "spmv_res", "spmv_plain", "orth_dots1", "orth_upd_dots2",
                                        "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
-                                       "norm_b", "gram", "jacobi", "xm", "chol", "misc"};
+                                       "norm_b", "gram", "jacobi", "xm", "chol", "misc", "dcgs_dots_ls",
+                                       "dcgs_update"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));

@@ -39,11 +39,11 @@ __device__ __forceinline__ bool setup(const SpmvArgs& a, Io& io, int& kid) {
   io.xs = 1.0;
   if (a.mode == SM_STEP) {
     kid = K_SPMV_STEP;
-    if (!st->active) { prof_noop(st, kid); return false; }
     const int j = st->j;
+    if (!st->active || (st->dcgs && j >= st->m)) { prof_noop(st, kid); return false; }
     io.x = L.Z + (int64_t)(L.VB + j) * L.ld;
     io.y = L.Z + (int64_t)(L.VB + j + 1) * L.ld;
-    io.xs = st->sc[L.VB + j];
+    io.xs = st->dcgs ? 1.0 : st->sc[L.VB + j];  // DCGS2: y = A u on the raw vector
   } else if (a.mode == SM_RES) {
     kid = K_SPMV_RES;
     if (st->done) { prof_noop(st, kid); return false; }
