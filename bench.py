@@ -341,6 +341,7 @@ def run_ours(args, cfg):
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
         "clocks": clk.summary(),
         "kernels": {kname: {"launches": s["launches"], "noop": s["noop"], "ms": round(s["ms"], 4),
+                            "tail_ms": round(s["tail_ms"], 4),
                             "GBps": round(s["bytes"] / (s["ms"] * 1e-3) / 1e9, 1) if s["ms"] > 0 else None}
                     for kname, s in kstats.items() if s["launches"] + s["noop"] > 0},
     }

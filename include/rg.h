@@ -17,9 +17,12 @@
  *   - Pointers tagged by an rg_mem argument are HOST (pageable or pinned) or DEVICE (same CUDA
  *     device as the context, e.g. a torch tensor's data_ptr()) memory.  The caller owns every
  *     buffer it passes; the library deep-copies what it keeps into device memory it owns.
- *   - All work is issued on the caller's CUDA stream (rg_options.cuda_stream, NULL = legacy
- *     default stream) and every call returns only when its results are complete
- *     (host-synchronous).
+ *   - All work is issued on the caller's CUDA stream (rg_options.cuda_stream, NULL = a stream the
+ *     library creates, ordered with the legacy default stream).  Calls that return results to
+ *     the host (rg_build_recycle, rg_solve, rg_apply, rg_export, rg_kernel_stats) return when
+ *     they are complete.  rg_update_matrix and rg_push_snapshot return when HOST inputs have been
+ *     copied; with DEVICE inputs they return once the copy is enqueued on the stream (the caller
+ *     must not overwrite the source buffer except by work ordered after it on that stream).
  *   - Dense vectors are fp64, length n, contiguous.  Indices are int32 (n, nnz < 2^31).
  *   - A context is single-owner and not thread-safe; distinct contexts are independent.
  */
@@ -168,6 +171,7 @@ typedef struct {
   int64_t noop_launches;/* launches that returned early      */
   double total_ms;      /* summed device time of working launches (%globaltimer, first CTA start to
                            last CTA end) */
+  double tail_ms;       /* part of total_ms spent in the last CTA's epilogue (reducing kernels) */
   double bytes;         /* summed algorithmic bytes (DESIGN.md byte model) */
 } rg_kstat;
 RG_API rg_status rg_kernel_stats(rg_ctx* ctx, rg_kstat* out, int32_t cap, int32_t* count);

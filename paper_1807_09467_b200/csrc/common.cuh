@@ -30,7 +30,7 @@ enum KernelId {
 };
 
 struct KStatDev {
-  unsigned long long launches, noop, ns, start;
+  unsigned long long launches, noop, ns, start, tail_start, tail_ns;
   double bytes;
 };
 
@@ -90,6 +90,7 @@ struct Layout {
   unsigned* counter;
   int cgs_ok;      // [Q|V] (max_k + max_m + 1 columns) fits k_cgs (16 chunks of 8 columns)
   int augment;     // variant of the graph being built / launched is augment
+  int keep_l2;     // the whole basis [W|Q|V] is L2-sized: DCGS2 passes use cached (not streaming) loads
 };
 
 // ---------------------------------------------------------------- small device helpers
@@ -128,11 +129,18 @@ __device__ __forceinline__ void prof_begin(DevState* st, int kid) {
 __device__ __forceinline__ void prof_noop(DevState* st, int kid) {
   if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) st->kstat[kid].noop++;
 }
+// Called by thread 0 of the last CTA when it has won the grid-reduction ticket.
+__device__ __forceinline__ void prof_tail(DevState* st, int kid) {
+  if (st->profile && threadIdx.x == 0) st->kstat[kid].tail_start = gtimer();
+}
 // Called by ONE thread of the last CTA.
 __device__ __forceinline__ void prof_end(DevState* st, int kid, double bytes) {
   if (st->profile) {
     KStatDev& k = st->kstat[kid];
-    k.ns += gtimer() - k.start;
+    const unsigned long long t = gtimer();
+    if (k.tail_start > k.start) k.tail_ns += t - k.tail_start;
+    k.tail_start = 0;
+    k.ns += t - k.start;
     k.launches++;
     k.bytes += bytes;
   }

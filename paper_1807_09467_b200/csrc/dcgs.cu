@@ -39,13 +39,24 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   const double* a = tot;
   const double* b = tot + p;
   const double ss = tot[2 * p], gg = tot[2 * p + 1];
-  if (tid == 0) {
-    double aa = 0.0;
-    for (int c = 0; c < p; ++c) aa += a[c] * a[c];
-    const double nu2 = ss - aa;
-    s_nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+  {  // a.a and a.b: deterministic block reductions (warp 0 and warp 1)
+    const int lane = tid & 31, w = tid >> 5;
+    if (w < 2) {
+      double acc = 0.0;
+      for (int c = lane; c < p; c += 32) acc += a[c] * (w == 0 ? a[c] : b[c]);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        if (w == 0) {
+          const double nu2 = ss - acc;
+          s_nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+        } else {
+          s_d = acc;  // a.b, consumed below
+        }
+      }
+    }
   }
   __syncthreads();
+  const double ab = s_d;
   const double nu = s_nu;
   if (j >= 1) {
     // finish column j-1: second-pass coefficients a (V part -> H, Q part -> B via hcol)
@@ -94,9 +105,8 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
       }
     }
   }
+  __syncthreads();
   if (tid == 0) {
-    double ab = 0.0;
-    for (int c = 0; c < p; ++c) ab += a[c] * b[c];
     const double aj = j >= 1 ? a[nq + j - 1] : 0.0;
     s_aj = aj;
     s_d = ((gg - ab) * inv - nu * aj) * inv;  // v_j^T w
@@ -136,6 +146,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
   const int nqd = (var == RG_AUGMENT) ? k : 0;  // extra Q^T u dots
   const bool have_y = j < st->m;                // no SpMV was run at j == m
+  const bool keep = L.keep_l2 != 0;  // basis fits L2: let DK2 re-hit what DK1 streamed
   const int64_t ld = L.ld;
   const double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;
   const double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;
@@ -165,7 +176,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
       const double* __restrict__ zc = Z + (int64_t)col * ld + base + lane;
       double zv[RPL];
 #pragma unroll
-      for (int q = 0; q < RPL; ++q) zv[q] = (lane + 32 * q < cnt) ? __ldcs(zc + 32 * q) : 0.0;
+      for (int q = 0; q < RPL; ++q) zv[q] = (lane + 32 * q < cnt) ? (keep ? zc[32 * q] : __ldcs(zc + 32 * q)) : 0.0;
       double su = 0.0, sy = 0.0;
 #pragma unroll
       for (int q = 0; q < RPL; ++q) {
@@ -193,6 +204,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
   }
   __syncthreads();
   if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot)) return;
+  prof_tail(st, K_DK1);
   epi_dcgs(st, L, tot, p);
   if (threadIdx.x == 0) {
     if (st->active) st->j = j + 1;  // next iteration (DK2 of this one uses st->j - 1)
@@ -209,6 +221,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
   const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
   const int64_t ld = L.ld;
+  const bool keep = L.keep_l2 != 0;
   double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;      // in: u, out: v_j
   double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;  // in: y, out: next u
   const double* __restrict__ Z = L.Z;
@@ -228,7 +241,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
     for (; c + 8 <= p; c += 8) {
       double z[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) z[t] = __ldcs(Z + (int64_t)(lo + c + t) * ld + r);
+      for (int t = 0; t < 8; ++t) z[t] = keep ? Z[(int64_t)(lo + c + t) * ld + r] : __ldcs(Z + (int64_t)(lo + c + t) * ld + r);
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
         sv += cv[c + t] * z[t];
@@ -236,7 +249,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
       }
     }
     for (; c < p; ++c) {
-      const double z = __ldcs(Z + (int64_t)(lo + c) * ld + r);
+      const double z = keep ? Z[(int64_t)(lo + c) * ld + r] : __ldcs(Z + (int64_t)(lo + c) * ld + r);
       sv += cv[c] * z;
       sn += cn[c] * z;
     }
@@ -255,8 +268,11 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
     cudaFuncSetAttribute(k_dk2, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     init = true;
   }
-  if (phase == 1) k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
-  else k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
+  if (phase == 1) {
+    k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
+    return cudaGetLastError();
+  }
+  k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
   return cudaGetLastError();
 }
 

@@ -86,6 +86,8 @@ struct rg_ctx {
   int* dflag = nullptr;
   DevState* st = nullptr;
   DevState* hst = nullptr;  // pinned host mirror
+  double* hhist = nullptr;  // pinned history staging
+  int* hflag = nullptr;     // pinned flag staging
   Layout L;
   // snapshots / recycle space
   int s_count = 0, s_head = 0;
@@ -255,7 +257,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
 }
 
 // C = A W into the Q region, then CholQR2 -> Q (orthonormal), R_C, R_C^{-1} (state).
-rg_status build_c(rg_ctx* c) {
+rg_status build_c(rg_ctx* c, bool sync) {
   const int k = c->k_eff;
   const int QB = c->L.VB - k;
   const int64_t ld = c->npad;
@@ -276,6 +278,10 @@ rg_status build_c(rg_ctx* c) {
   CK(launch_chol(G, k, R2, R2i, c->dflag, s));
   CK(launch_xm(c->Y, ld, c->n, k, R2i, k, k, nullptr, Q, ld, c->st, s));
   CK(launch_rc_finish(R1, R1i, R2, R2i, k, c->st, c->dflag, s));
+  if (!sync) {  // the caller reads dflag together with the solve header (one sync per solve)
+    c->c_valid = true;
+    return RG_OK;
+  }
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -412,12 +418,6 @@ rg_status run_solve(rg_ctx* c, int variant, int m) {
   return RG_OK;
 }
 
-rg_status read_header(rg_ctx* c) {
-  CK(cudaMemcpyAsync(c->hst, c->st, header_bytes(), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  return RG_OK;
-}
-
 template <class T>
 rg_status dalloc(T** p, size_t count, const char* what) {
   if (cudaMalloc(p, sizeof(T) * std::max<size_t>(count, 1)) != cudaSuccess) {
@@ -442,6 +442,8 @@ RG_API void rg_destroy(rg_ctx* c) {
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
   cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st);
   if (c->hst) cudaFreeHost(c->hst);
+  if (c->hhist) cudaFreeHost(c->hhist);
+  if (c->hflag) cudaFreeHost(c->hflag);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -494,7 +496,9 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
     rg_destroy(c);
     return s;
   }
-  if (cudaMallocHost(&c->hst, sizeof(DevState)) != cudaSuccess) {
+  if (cudaMallocHost(&c->hst, sizeof(DevState)) != cudaSuccess ||
+      cudaMallocHost(&c->hhist, sizeof(double) * HIST_CAP) != cudaSuccess ||
+      cudaMallocHost(&c->hflag, sizeof(int) * 4) != cudaSuccess) {
     cudaGetLastError();
     rg_destroy(c);
     return fail(RG_E_NOMEM, "pinned host allocation failed");
@@ -531,6 +535,8 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   c->L.partial = c->partial;
   c->L.counter = c->counter;
   c->L.cgs_ok = (c->max_k + c->max_m + 1) <= 128 && !getenv("RG_NO_CGS");
+  c->L.keep_l2 = (double)c->npad * 8.0 * (2 * c->max_k + c->max_m + 1) <= 160e6;  // ~L2-sized (126 MB)
+
   if ((s = set_matrix(c, A, true)) != RG_OK) {
     std::string msg = g_err;
     rg_destroy(c);
@@ -551,7 +557,7 @@ RG_API rg_status rg_update_matrix(rg_ctx* c, const rg_matrix* A) {
   if (s != RG_OK) return s;
   if ((A->fmt == RG_BSR) != (c->fmt == 2)) return fail(RG_E_INVAL, "matrix format differs from the context's");
   if ((s = set_matrix(c, A, false)) != RG_OK) return s;
-  CK(cudaStreamSynchronize(c->stream));
+  if (A->mem == RG_HOST) CK(cudaStreamSynchronize(c->stream));  // device inputs: stream-ordered
   return RG_OK;
 }
 
@@ -560,7 +566,7 @@ RG_API rg_status rg_push_snapshot(rg_ctx* c, const double* x, rg_mem mem) {
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
   rg_status s = copy_in(c->X + (int64_t)c->s_head * c->npad, x, sizeof(double) * c->n, mem, c->stream);
   if (s != RG_OK) return s;
-  CK(cudaStreamSynchronize(c->stream));
+  if (mem == RG_HOST) CK(cudaStreamSynchronize(c->stream));  // device inputs: stream-ordered
   c->s_head = (c->s_head + 1) % c->max_s;
   c->s_count = std::min(c->s_count + 1, c->max_s);
   return RG_OK;
@@ -632,9 +638,11 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   const int eff = (v != RG_PLAIN && c->have_W && c->k_eff > 0) ? (int)v : (int)RG_PLAIN;
   const int k = eff == RG_PLAIN ? 0 : c->k_eff;
   int c_spmv = 0;
+  bool check_c = false;
   if (eff != RG_PLAIN && !c->c_valid) {
-    if ((rs = build_c(c)) != RG_OK) return rs;
+    if ((rs = build_c(c, false)) != RG_OK) return rs;
     c_spmv = k;
+    check_c = true;
   }
   if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
   if (x0) {
@@ -660,12 +668,31 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   CK(cycle_start(c, eff));
   if ((rs = run_solve(c, eff, m)) != RG_OK) return rs;
   CK(cudaEventRecord(c->e1, s));
-  if ((rs = read_header(c)) != RG_OK) return rs;
-  if (h->bzero) CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->n, s));
+  // one synchronisation per solve: header, C=AW singularity flag, x and the history together
+  int bad = 0;
+  CK(cudaMemcpyAsync(h, c->st, header_bytes(), cudaMemcpyDeviceToHost, s));
+  if (check_c) CK(cudaMemcpyAsync(c->hflag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(x_out, c->x, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
-  const int hl = std::min(h->hist_len, history_cap);
-  if (history && hl > 0) CK(cudaMemcpyAsync(history, c->hist, sizeof(double) * hl, cudaMemcpyDeviceToHost, s));
+  const int hcap = std::min(history_cap, HIST_CAP);
+  if (history && hcap > 0) CK(cudaMemcpyAsync(c->hhist, c->hist, sizeof(double) * hcap, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  if (check_c) bad = c->hflag[0];
+  if (bad) {
+    c->have_W = false;
+    c->k_eff = 0;
+    c->c_valid = false;
+    return fail(RG_E_SINGULAR, "A W is numerically rank deficient (R_C singular); recycle space cleared");
+  }
+  if (h->bzero) {
+    if (mem == RG_DEVICE) {
+      CK(cudaMemsetAsync(x_out, 0, sizeof(double) * c->n, s));
+      CK(cudaStreamSynchronize(s));
+    } else {
+      memset(x_out, 0, sizeof(double) * c->n);
+    }
+  }
+  const int hl = std::min(h->hist_len, history_cap);
+  if (history && hl > 0) memcpy(history, c->hhist, sizeof(double) * hl);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, c->e0, c->e1);
   if (rep) {
@@ -734,6 +761,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
     o.launches = (int64_t)ks[i].launches;
     o.noop_launches = (int64_t)ks[i].noop;
     o.total_ms = ks[i].ns * 1e-6;
+    o.tail_ms = ks[i].tail_ns * 1e-6;
     o.bytes = ks[i].bytes;
   }
   *count = out ? n : K_COUNT;

@@ -60,7 +60,7 @@ class rg_report(ctypes.Structure):
 
 class rg_kstat(ctypes.Structure):
     _fields_ = [("name", ctypes.c_char * 24), ("launches", ctypes.c_int64), ("noop_launches", ctypes.c_int64),
-                ("total_ms", ctypes.c_double), ("bytes", ctypes.c_double)]
+                ("total_ms", ctypes.c_double), ("tail_ms", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
 def load(path: str = LIB_PATH):
@@ -193,7 +193,8 @@ def rg_kernel_stats(ctx):
     cnt = ctypes.c_int32(0)
     _check(_lib.rg_kernel_stats(ctx, buf, 32, ctypes.byref(cnt)))
     return {buf[i].name.decode(): dict(launches=buf[i].launches, noop=buf[i].noop_launches,
-                                       ms=buf[i].total_ms, bytes=buf[i].bytes) for i in range(cnt.value)}
+                                       ms=buf[i].total_ms, tail_ms=buf[i].tail_ms, bytes=buf[i].bytes)
+            for i in range(cnt.value)}
 
 
 def rg_reset_kernel_stats(ctx):
