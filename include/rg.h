@@ -122,6 +122,13 @@ RG_API rg_status rg_create(rg_ctx** ctx, int64_t n, const rg_matrix* A, const rg
  * factor Q and R_C, which are rebuilt by the next recycled solve. */
 RG_API rg_status rg_update_matrix(rg_ctx* ctx, const rg_matrix* A);
 
+/* Device pointer and length (doubles) of the library-owned matrix values (CSR order, or BSR blocks
+ * column-major), for callers that generate A_t on the device: write the new values there on the
+ * context's stream, then call rg_update_matrix with val == *values (row_ptr = col_idx = NULL), which
+ * then skips the copy (SELL packing and the C = AW invalidation still happen).  The pointer stays
+ * valid until the pattern changes or the context is destroyed. */
+RG_API rg_status rg_matrix_values(rg_ctx* ctx, double** values, int64_t* len);
+
 /* Append solution x (length n) to the snapshot window X (Algorithm 1 line "store the solution
  * x_i in the matrix X_m"), evicting the oldest column when the window is full. */
 RG_API rg_status rg_push_snapshot(rg_ctx* ctx, const double* x, rg_mem mem);

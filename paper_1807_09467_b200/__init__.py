@@ -29,6 +29,14 @@ class Context:
         A = rg.make_matrix(self.n, row_ptr, col_idx, val, self.fmt, self.block, self.sell_C, keep)
         rg.rg_update_matrix(self.ctx, A)
 
+    def values_ptr(self):
+        """Device pointer / length of the library-owned matrix values (rg_matrix_values)."""
+        return rg.rg_matrix_values(self.ctx)
+
+    def update_values_inplace(self, nnz):
+        """The values behind values_ptr() were rewritten on the context's stream."""
+        rg.rg_update_values_inplace(self.ctx, self.n, nnz, self.fmt, self.block, self.sell_C)
+
     def push_snapshot(self, x):
         rg.rg_push_snapshot(self.ctx, x)
 

@@ -19,6 +19,7 @@ struct MatDev {
   const int32_t* sci = nullptr; // SELL columns (column-major inside a slice)
   const double* sv = nullptr;   // SELL values
   int64_t nslices = 0;
+  int tma = 1;                  // BSR-64: stream blocks with TMA bulk copies
   double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
 };
 
@@ -28,6 +29,11 @@ enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2 };
 // y = A x (PLAIN).
 cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode, const double* x,
                         double* y, int res_epi, cudaStream_t s);
+
+// Y[:, 0:k] = A W[:, 0:k] (columns with leading dimension ld) with ONE read of A (a4: C = A W).
+// Returns cudaErrorNotSupported when no SpMM kernel covers the format (caller loops SpMVs).
+cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld, int k, DevState* st, unsigned* counter,
+                        cudaStream_t s);
 
 enum OrthOp { OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB };
 // cond != 0: cudaGraphConditionalHandle set to st->active by OP_UN's epilogue (graph WHILE node)

@@ -230,8 +230,10 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
     }
   } else {
     rg_status s;
-    if (A->mem == RG_DEVICE && !is_dev_ptr(A->val)) return fail(RG_E_INVAL, "mem = RG_DEVICE but val is not device memory");
-    if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
+    if (A->val != c->v) {  // val == rg_matrix_values(): updated in place, nothing to copy
+      if (A->mem == RG_DEVICE && !is_dev_ptr(A->val)) return fail(RG_E_INVAL, "mem = RG_DEVICE but val is not device memory");
+      if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
+    }
     if (c->fmt == 1) CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 0, c->stream));
   }
   // device descriptor and byte model
@@ -250,6 +252,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
   } else {
     M.b = c->block;
     M.nb = c->n / c->block;
+    M.tma = getenv("RG_NO_BSR_TMA") ? 0 : 1;
     M.bytes = 8.0 * c->v_len + 4.0 * c->nnz + 4.0 * (M.nb + 1) + 16.0 * c->n;
   }
   c->c_valid = false;
@@ -262,8 +265,14 @@ rg_status build_c(rg_ctx* c, bool sync) {
   const int QB = c->L.VB - k;
   const int64_t ld = c->npad;
   cudaStream_t s = c->stream;
-  for (int l = 0; l < k; ++l)
-    CK(launch_spmv(c->A, c->L, c->st, SM_PLAIN, c->Z + (int64_t)l * ld, c->Z + (int64_t)(QB + l) * ld, 0, s));
+  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported : launch_spmm(c->A, c->Z, c->Z + (int64_t)QB * ld, ld, k, c->st, c->counter, s);
+  if (es == cudaErrorNotSupported) {
+    cudaGetLastError();
+    for (int l = 0; l < k; ++l)
+      CK(launch_spmv(c->A, c->L, c->st, SM_PLAIN, c->Z + (int64_t)l * ld, c->Z + (int64_t)(QB + l) * ld, 0, s));
+  } else {
+    CK(es);
+  }
   double* G = c->small;
   double* R1 = c->small + 1 * SMALL;
   double* R1i = c->small + 2 * SMALL;
@@ -558,6 +567,13 @@ RG_API rg_status rg_update_matrix(rg_ctx* c, const rg_matrix* A) {
   if ((A->fmt == RG_BSR) != (c->fmt == 2)) return fail(RG_E_INVAL, "matrix format differs from the context's");
   if ((s = set_matrix(c, A, false)) != RG_OK) return s;
   if (A->mem == RG_HOST) CK(cudaStreamSynchronize(c->stream));  // device inputs: stream-ordered
+  return RG_OK;
+}
+
+RG_API rg_status rg_matrix_values(rg_ctx* c, double** values, int64_t* len) {
+  if (!c || !values) return fail(RG_E_INVAL, "NULL argument");
+  *values = c->v;
+  if (len) *len = c->v_len;
   return RG_OK;
 }
 

@@ -184,18 +184,314 @@ __global__ void __launch_bounds__(256) k_spmv_bsr(SpmvArgs a) {
   const double* __restrict__ x = io.x;
   for (int64_t I = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 6); I < A.nb; I += (int64_t)gridDim.x * 4) {
     if (r < b) {
-      double s = 0.0;
+      double s0 = 0.0, s1 = 0.0;
       const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
       for (int32_t p = p0; p < p1; ++p) {
         const double* __restrict__ blk = A.v + (int64_t)p * b * b + r;
         const double* __restrict__ xb = x + (int64_t)__ldg(A.ci + p) * b;
-#pragma unroll 16
-        for (int c = 0; c < b; ++c) s += __ldcs(blk + (int64_t)c * b) * __ldg(xb + c);
+        int c = 0;
+        for (; c + 16 <= b; c += 16) {  // 16 block values + 16 x entries in flight, then FMAs
+          double av[16], xv[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            av[u] = __ldcs(blk + (int64_t)(c + u) * b);
+            xv[u] = __ldg(xb + c + u);
+          }
+          asm volatile("" ::: "memory");  // keep ptxas from sinking the loads into the FMA chain
+#pragma unroll
+          for (int u = 0; u < 16; u += 2) {
+            s0 += av[u] * xv[u];
+            s1 += av[u + 1] * xv[u + 1];
+          }
+        }
+        for (; c < b; ++c) s0 += __ldcs(blk + (int64_t)c * b) * __ldg(xb + c);
       }
-      nrm += emit(io, I * b + r, s);
+      nrm += emit(io, I * b + r, s0 + s1);
     }
   }
   finish(a, io, kid, nrm);
+}
+
+// ---------------------------------------------------------------- BSR-64 via TMA bulk copies
+// Each 64x64 fp64 block is 32 KB contiguous: a producer warp streams the CTA's blocks (block rows
+// blockIdx.x, +gridDim.x, ...) into a 4-stage shared-memory ring with cp.async.bulk (TMA),
+// completing on per-stage mbarriers; 8 consumer warps compute from shared memory: thread t owns
+// row t % 64 and column quarter t / 64; the quarters are combined in a fixed order per block row.
+constexpr int BT_CONS = 256;            // consumer threads
+constexpr int BT = BT_CONS + 32;        // + producer warp
+constexpr int BNS = 4;                  // stages
+constexpr int BSTAGE = 64 * 64 * 8;     // bytes per stage (one block)
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(su32(bar)), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(BT, 1) k_spmv_bsr_tma(SpmvArgs a) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
+  __shared__ double qpart[4][64];
+  Io io;
+  int kid;
+  if (!setup(a, io, kid)) return;
+  const MatDev& A = a.A;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < BNS; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[i])), "r"(BT_CONS / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  double nrm = 0.0;
+  if (wid == BT_CONS / 32) {
+    // ---- producer: lane 0 walks the same block sequence as the consumers
+    if (lane == 0) {
+      int t = 0;
+      for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
+        const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
+        for (int32_t p = p0; p < p1; ++p, ++t) {
+          const int s = t % BNS;
+          if (t >= BNS) bar_wait(&empty[s], (uint32_t)((t / BNS - 1) & 1));
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su32(ring + (size_t)s * (BSTAGE / 8))), "l"(A.v + (int64_t)p * 4096), "r"(BSTAGE),
+                       "r"(su32(&full[s])) : "memory");
+        }
+      }
+    }
+  } else {
+    // ---- consumers
+    const int r = tid & 63, q = tid >> 6;
+    int t = 0;
+    for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
+      const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
+      double s0 = 0.0, s1 = 0.0;
+      for (int32_t p = p0; p < p1; ++p, ++t) {
+        const int st = t % BNS;
+        const double* __restrict__ xb = io.x + (int64_t)__ldg(A.ci + p) * 64 + q * 16;
+        double xv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) xv[u] = __ldg(xb + u);
+        bar_wait(&full[st], (uint32_t)((t / BNS) & 1));
+        const double* blk = ring + (size_t)st * (BSTAGE / 8) + (q * 16) * 64 + r;
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          s0 += blk[u * 64] * xv[u];
+          s1 += blk[(u + 1) * 64] * xv[u + 1];
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
+      }
+      qpart[q][r] = s0 + s1;
+      asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
+      if (q == 0) nrm += emit(io, I * 64 + r, ((qpart[0][r] + qpart[1][r]) + qpart[2][r]) + qpart[3][r]);
+      asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
+    }
+  }
+  finish(a, io, kid, nrm);
+}
+
+// ---------------------------------------------------------------- SpMM  Y = A W  (C = A W, a4)
+// BSR-64: one TMA-streamed read of A for all k columns; the 64x64 block (shared memory) times the
+// 64 x k panel of W runs on the FP64 tensor cores (DMMA m8n8k4): warp w owns output rows
+// 8w..8w+7 of the block row and every 8-column group.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
+
+// acc[g] += A_block(rows 8w.., :) * W_panel(:, 8g..8g+7), g < NG (WSP = panel stride)
+template <int NG>
+__device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int rrow, int lane) {
+  // CH independent accumulator chains per column group hide the DMMA latency when NG is small
+  constexpr int CH = NG >= 4 ? 1 : (NG >= 2 ? 2 : 4);
+  double ch[NG][CH][2];
+#pragma unroll
+  for (int g = 0; g < NG; ++g)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) ch[g][c][0] = ch[g][c][1] = 0.0;
+#pragma unroll
+  for (int c0 = 0; c0 < 64; c0 += 4 * CH) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      const int cc = c0 + 4 * c;
+      const double av = blk[(cc + (lane & 3)) * 64 + rrow];    // A(rrow, cc + lane%4)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) dmma884(ch[g][c][0], ch[g][c][1], av, wp[g * 8 * 68 + cc]);  // W(cc + lane%4, 8g + lane/4)
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < NG; ++g)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      acc[g][0] += ch[g][c][0];
+      acc[g][1] += ch[g][c][1];
+    }
+}
+
+__global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* __restrict__ W, double* Y,
+                                                        int64_t ld, int k, DevState* pst, unsigned* counter) {
+  if (pst) prof_begin(pst, K_SPMV_PLAIN);
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < BNS; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[i])), "r"(BT_CONS / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int ng = (k + 7) / 8;
+  if (wid == BT_CONS / 32) {
+    if (lane == 0) {
+      int t = 0;
+      for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
+        const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
+        for (int32_t p = p0; p < p1; ++p, ++t) {
+          const int s = t % BNS;
+          if (t >= BNS) bar_wait(&empty[s], (uint32_t)((t / BNS - 1) & 1));
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                       ::"r"(su32(ring + (size_t)s * (BSTAGE / 8))), "l"(A.v + (int64_t)p * 4096), "r"(BSTAGE),
+                       "r"(su32(&full[s])) : "memory");
+        }
+      }
+    }
+    return;
+  }
+  // consumers: W panel of block t in shared memory (double-buffered, stride WSP), the next panel
+  // is prefetched into registers while block t's DMMAs run.
+  constexpr int WSP = 68;
+  double* wpan = ring + (size_t)BNS * (BSTAGE / 8);          // 2 x 64 cols x WSP
+  const int rrow = wid * 8 + (lane >> 2);                    // A fragment row inside the block
+  const int nval = 64 * k;                                   // panel values
+  constexpr int PPT = (64 * 64 + BT_CONS - 1) / BT_CONS;     // panel values per thread (<= 16)
+  // first block of this CTA
+  int64_t I = blockIdx.x;
+  int32_t p = I < A.nb ? __ldg(A.rp + I) : 0, pend = I < A.nb ? __ldg(A.rp + I + 1) : 0;
+  double pre[PPT];
+  auto load_panel = [&](int32_t pp) {
+    const int64_t wr = (int64_t)__ldg(A.ci + pp) * 64;
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const int e = tid + u * BT_CONS;
+      pre[u] = e < nval ? __ldg(W + (int64_t)(e >> 6) * ld + wr + (e & 63)) : 0.0;
+    }
+  };
+  auto store_panel = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const int e = tid + u * BT_CONS;
+      if (e < nval) wpan[(size_t)buf * 64 * WSP + (e >> 6) * WSP + (e & 63)] = pre[u];
+    }
+  };
+  if (I < A.nb && p < pend) {
+    load_panel(p);
+    store_panel(0);
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
+  int t = 0;
+  for (; I < A.nb; I += gridDim.x) {
+    double acc[8][2];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
+    for (; p < pend; ++p, ++t) {
+      // next block in this CTA's sequence (same block row, or the first block of the next one)
+      int32_t pn = p + 1;
+      int64_t In = I;
+      int32_t pendn = pend;
+      if (pn >= pend) {
+        In = I + gridDim.x;
+        pn = In < A.nb ? __ldg(A.rp + In) : 0;
+        pendn = In < A.nb ? __ldg(A.rp + In + 1) : 0;
+      }
+      const bool has_next = In < A.nb && pn < pendn;
+      if (has_next) load_panel(pn);
+      const int st = t % BNS;
+      bar_wait(&full[st], (uint32_t)((t / BNS) & 1));
+      const double* blk = ring + (size_t)st * (BSTAGE / 8);
+      const double* wp = wpan + (size_t)(t & 1) * 64 * WSP + (lane >> 2) * WSP + (lane & 3);
+      switch (ng) {  // exact trip count: predicated-off DMMAs still occupy the tensor pipe
+        case 1: block_mma<1>(acc, blk, wp, rrow, lane); break;
+        case 2: block_mma<2>(acc, blk, wp, rrow, lane); break;
+        case 3: block_mma<3>(acc, blk, wp, rrow, lane); break;
+        case 4: block_mma<4>(acc, blk, wp, rrow, lane); break;
+        case 5: block_mma<5>(acc, blk, wp, rrow, lane); break;
+        case 6: block_mma<6>(acc, blk, wp, rrow, lane); break;
+        case 7: block_mma<7>(acc, blk, wp, rrow, lane); break;
+        default: block_mma<8>(acc, blk, wp, rrow, lane); break;
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
+      if (has_next) store_panel((t + 1) & 1);
+      asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      if (g < ng) {
+        const int col = g * 8 + (lane & 3) * 2;
+        const int64_t row = I * 64 + rrow;
+        if (col < k) Y[(int64_t)col * ld + row] = acc[g][0];
+        if (col + 1 < k) Y[(int64_t)(col + 1) * ld + row] = acc[g][1];
+      }
+    }
+    const int64_t In = I + gridDim.x;
+    p = In < A.nb ? __ldg(A.rp + In) : 0;
+    pend = In < A.nb ? __ldg(A.rp + In + 1) : 0;
+  }
+  if (pst && pst->profile) {
+    asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
+    if (tid == 0) {
+      const unsigned tk = atom_add_release(counter);
+      if (tk == gridDim.x - 1) {
+        *counter = 0u;
+        prof_end(pst, K_SPMV_PLAIN, A.bytes + 16.0 * (double)A.n * k);
+      }
+    }
+  }
+}
+
+// CSR / SELL: thread per row, 16 columns of W per pass (k <= 64 -> at most 4 reads of A).
+template <int KC>
+__global__ void __launch_bounds__(256) k_spmm_rows(MatDev A, const double* __restrict__ W, double* Y, int64_t ld,
+                                                   int k0, int kc) {
+  for (int64_t row = blockIdx.x * 256ll + threadIdx.x; row < A.n; row += (int64_t)gridDim.x * 256) {
+    double acc[KC];
+#pragma unroll
+    for (int l = 0; l < KC; ++l) acc[l] = 0.0;
+    if (A.fmt == 1) {
+      const int64_t sl = row >> 5;
+      const int w = __ldg(A.sw + sl);
+      const int64_t base = __ldg(A.sp + sl) + (row & 31);
+      for (int c = 0; c < w; ++c) {
+        const int64_t e = base + (int64_t)c * 32;
+        const double v = __ldcs(A.sv + e);
+        const int32_t col = __ldcs(A.sci + e);
+#pragma unroll
+        for (int l = 0; l < KC; ++l)
+          if (l < kc) acc[l] += v * __ldg(W + (int64_t)(k0 + l) * ld + col);
+      }
+    } else {
+      const int32_t p0 = __ldg(A.rp + row), p1 = __ldg(A.rp + row + 1);
+      for (int32_t p = p0; p < p1; ++p) {
+        const double v = __ldcs(A.v + p);
+        const int32_t col = __ldcs(A.ci + p);
+#pragma unroll
+        for (int l = 0; l < KC; ++l)
+          if (l < kc) acc[l] += v * __ldg(W + (int64_t)(k0 + l) * ld + col);
+      }
+    }
+#pragma unroll
+    for (int l = 0; l < KC; ++l)
+      if (l < kc) Y[(int64_t)(k0 + l) * ld + row] = acc[l];
+  }
 }
 
 }  // namespace
@@ -204,9 +500,19 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
                         double* y, int res_epi, cudaStream_t s) {
   SpmvArgs a{A, L, st, mode, x, y, res_epi};
   const int cap_red = NSM * VEC_CTAS_PER_SM;  // reducing launches: bounded partials
+  if (A.fmt == 2 && A.b == 64 && A.tma) {
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_spmv_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, BNS * BSTAGE);
+      init = true;
+    }
+    int64_t g = A.nb < NSM ? A.nb : NSM;
+    k_spmv_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, BNS * BSTAGE, s>>>(a);
+    return cudaGetLastError();
+  }
   if (A.fmt == 2) {
     int64_t g = (A.nb + 3) / 4;
-    const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * 8;
+    const int64_t cap = (int64_t)NSM * 8;  // partials buffer holds NSM*8 rows: RES may use them all
     if (g > cap) g = cap;
     k_spmv_bsr<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(a);
   } else if (A.fmt == 1) {
@@ -227,6 +533,28 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
       case 16: k_spmv_csr<16><<<gi, OT, 0, s>>>(a); break;
       default: k_spmv_csr<32><<<gi, OT, 0, s>>>(a); break;
     }
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld, int k, DevState* st, unsigned* counter,
+                        cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  if (A.fmt == 2 && A.b == 64 && A.tma && k <= 64) {
+    static bool init = false;
+    if (!init) {
+      cudaFuncSetAttribute(k_spmm_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, BNS * BSTAGE + 2 * 64 * 68 * 8);
+      init = true;
+    }
+    int64_t g = A.nb < NSM ? A.nb : NSM;
+    k_spmm_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, BNS * BSTAGE + 2 * 64 * 68 * 8, s>>>(A, W, Y, ld, k, st, counter);
+    return cudaGetLastError();
+  }
+  if (A.fmt == 2) return cudaErrorNotSupported;  // caller falls back to per-column SpMV
+  int64_t g = (A.n + 255) / 256;
+  if (g > NSM * 8) g = NSM * 8;
+  for (int k0 = 0; k0 < k; k0 += 16) {
+    k_spmm_rows<16><<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(A, W, Y, ld, k0, k - k0 < 16 ? k - k0 : 16);
   }
   return cudaGetLastError();
 }

@@ -26,7 +26,7 @@ STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E
           5: "RG_E_SINGULAR", 6: "RG_E_NUMERIC"}
 
 # Symbols declared in include/rg.h (tests check the .so exports exactly these).
-SYMBOLS = ("rg_create", "rg_update_matrix", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle",
+SYMBOLS = ("rg_create", "rg_update_matrix", "rg_matrix_values", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle",
            "rg_solve", "rg_apply", "rg_export", "rg_kernel_stats", "rg_reset_kernel_stats", "rg_destroy",
            "rg_last_error")
 
@@ -70,6 +70,7 @@ def load(path: str = LIB_PATH):
     vp, i32, i64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     L.rg_create.argtypes = [ctypes.POINTER(vp), i64, ctypes.POINTER(rg_matrix), ctypes.POINTER(rg_options)]
     L.rg_update_matrix.argtypes = [vp, ctypes.POINTER(rg_matrix)]
+    L.rg_matrix_values.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(i64)]
     L.rg_push_snapshot.argtypes = [vp, vp, ctypes.c_int]
     L.rg_clear_snapshots.argtypes = [vp]
     L.rg_build_recycle.argtypes = [vp, i32, ctypes.POINTER(i32), vp]
@@ -142,6 +143,22 @@ def rg_create(n, A: rg_matrix, max_m=64, max_snapshots=32, max_k=32, stream=None
 
 
 def rg_update_matrix(ctx, A: rg_matrix):
+    _check(_lib.rg_update_matrix(ctx, ctypes.byref(A)))
+
+
+def rg_matrix_values(ctx):
+    """(device pointer, length) of the library-owned matrix values."""
+    p = ctypes.c_void_p()
+    n = ctypes.c_int64(0)
+    _check(_lib.rg_matrix_values(ctx, ctypes.byref(p), ctypes.byref(n)))
+    return p.value, n.value
+
+
+def rg_update_values_inplace(ctx, n, nnz, fmt="csr", block=1, sell_C=0):
+    """rg_update_matrix with val == rg_matrix_values() (values already written in place)."""
+    ptr, _ = rg_matrix_values(ctx)
+    A = rg_matrix(RG_BSR if fmt == "bsr" else RG_CSR, int(n), int(nnz), int(block), None, None, ptr, RG_DEVICE,
+                  int(sell_C), 1)
     _check(_lib.rg_update_matrix(ctx, ctypes.byref(A)))
 
 

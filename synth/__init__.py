@@ -334,31 +334,34 @@ class DeviceSequence:
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
 
-    def fill(self, t: int, u_prev_dev):
-        """Write A_t into self.val and b_t into self.b (device), from device x_{t-1}."""
+    def fill(self, t: int, u_prev_dev, val_ptr=None):
+        """Write A_t and b_t (into self.b) on the device, from device x_{t-1}.  The values go to
+        self.val, or to the raw device pointer val_ptr (e.g. the solver's own buffer from
+        rg_matrix_values, which then must hold A_{t-1} for the C5 multiplicative update)."""
         cfg, C, st = self.cfg, culib(), self._stream()
         vp = ctypes.c_void_p
+        dst = vp(val_ptr if val_ptr is not None else self.val.data_ptr())
         if cfg.kind == "bsr":
             if self._t == 0 or t < self._t:
                 C.syd_c5_values(self.host.col_idx.shape[0], cfg.B, cfg.seed, vp(self.kind.data_ptr()),
-                                0.1 * 1.5, 0.1 * 0.5, vp(self.val.data_ptr()), st)
+                                0.1 * 1.5, 0.1 * 0.5, dst, st)
                 self._t = 1
                 C.syd_normal_vec(self.n, cfg.seed, 0xB, vp(self.b.data_ptr()), st)
             while self._t < t:
                 self._t += 1
-                C.syd_c5_perturb(self.val.numel(), cfg.seed, self._t, vp(self.val.data_ptr()), st)
+                C.syd_c5_perturb(self.val.numel(), cfg.seed, self._t, dst, st)
             return
         sc = self.host.scalars()
         if cfg.kind == "5pt":
             if cfg.cid == 2:
                 C.syd_fill5_values(cfg.N, sc["cd"], sc["ih"], sc["idt"], 0.0, 0.0, vp(u_prev_dev.data_ptr()),
-                                   vp(self.row_ptr.data_ptr()), vp(self.val.data_ptr()), st)
+                                   vp(self.row_ptr.data_ptr()), dst, st)
             else:
                 bx, by = velocity(cfg, t)
                 C.syd_fill5_values(cfg.N, sc["cd"], sc["ih"], sc["idt"], bx, by, None,
-                                   vp(self.row_ptr.data_ptr()), vp(self.val.data_ptr()), st)
+                                   vp(self.row_ptr.data_ptr()), dst, st)
         elif cfg.kind == "7pt":
             bx, by, bz = velocity(cfg, t)
             C.syd_fill7_values(cfg.N, sc["cd"], sc["ih"], sc["idt"], bx, by, bz,
-                               vp(self.row_ptr.data_ptr()), vp(self.val.data_ptr()), st)
+                               vp(self.row_ptr.data_ptr()), dst, st)
         C.syd_rhs(self.n, vp(u_prev_dev.data_ptr()), cfg.dt, cfg.forcing, vp(self.b.data_ptr()), st)

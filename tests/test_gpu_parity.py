@@ -210,3 +210,27 @@ def test_rank_deficient_window(rng):
         ctx.push_snapshot(t(v))
     ke, sig = ctx.build_recycle(4)
     assert ke == 2
+
+
+@pytest.mark.parametrize("name,N,sell", [("C4", 14, False), ("C3", 40, True), ("C5", 3, False)])
+def test_recycle_operator_thin_qr(name, N, sell, rng):
+    """a4: C = A W (single-read SpMM) and its CholQR2 factors: A W = Q R_C, Q^T Q = I,
+    checked with the oracle's SpMV on the exported W."""
+    cfg = synth.CONFIGS[name].reduced(N)
+    seq = synth.HostSequence(cfg)
+    hm = seq.matrix(1, seq.initial())
+    k = 12
+    ctx = make_ctx(hm, sell=sell, s=k, k=k, max_m=cfg.m)
+    for i in range(k):
+        ctx.push_snapshot(t(rng.standard_normal(cfg.n)))
+    ke, _ = ctx.build_recycle(k)
+    x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+    ctx.solve(t(rng.standard_normal(cfg.n)), x, m=cfg.m, variant="deflate", max_iters=3)
+    W = np.zeros((ke, cfg.n)); ctx.export(0, W); W = W.T
+    Q = np.zeros((ke, cfg.n)); ctx.export(1, Q); Q = Q.T
+    R = np.zeros((ke, ke)); ctx.export(2, R); R = R.T      # exported column-major
+    M = oracle.Matrix.from_host(hm)
+    AW = np.column_stack([oracle.spmv(M, W[:, i]) for i in range(ke)])
+    assert np.linalg.norm(AW - Q @ R) <= 1e-12 * np.linalg.norm(AW)
+    assert np.linalg.norm(Q.T @ Q - np.eye(ke)) <= 1e-12
+    assert np.allclose(np.tril(R, -1), 0.0)
