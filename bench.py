@@ -60,6 +60,46 @@ def reduce_max(value: float, dist_on: bool, device=None) -> float:
     return float(t.item())
 
 
+def timed_replicas(step, steps, warmup, dist_on, device=None, timer="cuda", between=None, stream=None):
+    """The contract's timing skeleton, shared by every rank: `warmup` untimed steps, barrier,
+    exactly `steps` timed steps (per-step device events on `stream`, or host clock for
+    timer="cpu"), barrier, max over ranks.  `between` runs before each timed step, outside the
+    timed window (the L2 flush).  Returns (per_step_seconds, local_total, max_total)."""
+    for _ in range(warmup):
+        step()
+    if timer == "cuda":
+        import torch
+        torch.cuda.synchronize()
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+    per = []
+    if timer == "cuda":
+        import torch
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        for i in range(steps):
+            if between:
+                between()
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        per = [a.elapsed_time(b) / 1e3 for a, b in evs]
+    else:
+        for i in range(steps):
+            if between:
+                between()
+            t0 = time.perf_counter()
+            step()
+            per.append(time.perf_counter() - t0)
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+    t_local = sum(per)
+    return per, t_local, reduce_max(t_local, dist_on, device)
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -262,23 +302,10 @@ def run_ours(args, cfg):
             run.step()
         torch.cuda.synchronize()
         run.ctx.reset_kernel_stats()
-        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        if dist_on:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
         with ClockSampler(local) as clk:
-            for i in range(args.steps):
-                flush_l2(flush)                         # outside the timed events
-                evs[i][0].record(stream)
-                run.step()
-                evs[i][1].record(stream)
-            torch.cuda.synchronize()
-        if dist_on:
-            torch.distributed.barrier()
-        per = [a.elapsed_time(b) / 1e3 for a, b in evs]
+            per, t_local, t_max = timed_replicas(run.step, args.steps, 0, dist_on, device, "cuda",
+                                                 between=lambda: flush_l2(flush), stream=stream)
         kstats = run.ctx.kernel_stats()
-        t_local = sum(per)
-        t_max = reduce_max(t_local, dist_on, device)
         value = t_max / (args.steps * ws)
         timed_iters = run.iters[args.warmup:]
 
