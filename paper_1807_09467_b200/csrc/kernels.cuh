@@ -43,6 +43,11 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
 // WHILE-node condition from the state: which 0 -> active, 1 -> !done
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s);
 
+// Whole solve in one cooperative kernel (persistent.cu): plain / deflate, CSR / SELL, m <= 64,
+// k <= 64.  cudaErrorNotSupported when outside that scope (caller uses the graph path).
+cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar, int m,
+                              int k, int variant, cudaStream_t s);
+
 // ---- dense / recycle-build kernels (dense.cu)
 // G = Y^T Y (s x s, column-major) for Y (n x s, leading dimension ld).
 cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G, double* partial,

@@ -1,0 +1,529 @@
+// persistent.cu — the whole restarted solve in ONE cooperative kernel (plain / deflate, CSR / SELL).
+//
+// Why: at the sizes of configs C1-C2 every kernel boundary of the graph path costs a launch ramp
+// plus a single-CTA epilogue tail (~10 us per Arnoldi step).  Here every CTA of a co-resident grid
+// keeps an IDENTICAL copy of the least-squares state (unrotated Hessenberg H, rotated R, GCRO B,
+// Givens rotations, right-hand side g) in shared memory and recomputes the deterministic epilogue
+// from the reduced totals itself; kernel boundaries become grid barriers.  Per Arnoldi step (DCGS2,
+// see dcgs.cu): barrier, SpMV y = A u + local dots [P^T u, P^T y, u.u, u.y], two-barrier
+// deterministic reduction, replicated epilogue, row update of v_j and the next u.
+// CTA 0 alone writes the solve report (iterations, history, status) to the device state.
+#include "epilogue.cuh"
+#include "kernels.cuh"
+
+namespace rg {
+namespace {
+
+constexpr int PT = 512;       // threads per CTA
+constexpr int PM = 64;        // max restart length on this path
+constexpr int PK = 64;        // max recycle dimension on this path
+constexpr int PCOL = PK + PM + 2;
+
+struct PArgs {
+  Layout L;
+  MatDev A;
+  DevState* st;
+  double* tot_g;        // reduced totals (MAXRED)
+  unsigned* bar;        // [0] arrival count, [1] generation
+  int m, k;             // m <= PM, k <= PK (k = 0: plain)
+};
+
+// ---- grid barrier (all CTAs co-resident: cooperative launch).  Spins with a timeout so that a
+// bug cannot hang the GPU: after ~2 s every CTA gives up and the solve reports RG_E_CUDA.
+__device__ __forceinline__ bool gbar(unsigned* bar, int* s_fail) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      const long long t0 = clock64();
+      unsigned ns = 32;
+      while (*gen == g) {  // exponential back-off keeps ~300 pollers off the barrier's L2 line
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+        if (clock64() - t0 > 4000000000LL) { *s_fail = 1; break; }
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return *s_fail == 0;
+}
+
+// ---- deterministic grid reduction: every CTA writes its nv partials; CTA c sums columns
+// c, c+G, ... over CTAs in index order; every CTA then reads the nv totals into `tot`.
+// (Measured: a single "last CTA reduces" wave is slower here — the reducing CTA competes with ~300
+// pollers — so the work is spread over all CTAs between two barriers.)
+__device__ __forceinline__ bool greduce(const double* vals, int nv, double* partial, double* tot_g, double* tot,
+                                        unsigned* bar, int* s_fail) {
+  for (int i = threadIdx.x; i < nv; i += PT) partial[(size_t)blockIdx.x * MAXRED + i] = vals[i];
+  if (!gbar(bar, s_fail)) return false;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, G = gridDim.x;
+  for (int col = blockIdx.x + G * wid; col < nv; col += G * (PT / 32)) {
+    double a = 0.0;
+    for (int b = lane; b < G; b += 32) a += __ldcg(partial + (size_t)b * MAXRED + col);
+    a = warp_sum(a);
+    if (lane == 0) tot_g[col] = a;
+  }
+  if (!gbar(bar, s_fail)) return false;
+  for (int i = threadIdx.x; i < nv; i += PT) tot[i] = __ldcg(tot_g + i);
+  __syncthreads();
+  return true;
+}
+
+// y_r = (A x)_r for one row (CSR thread-per-row / SELL)
+__device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const double* __restrict__ x) {
+  double s = 0.0;
+  if (A.fmt == 1) {
+    const int64_t sl = row >> 5;
+    const int w = __ldg(A.sw + sl);
+    const int64_t base = __ldg(A.sp + sl) + (row & 31);
+    for (int c = 0; c < w; c += 8) {
+      int32_t cc[8];
+      double vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = c + u < w;
+        const int64_t e = base + (int64_t)(c + u) * 32;
+        cc[u] = ok ? __ldcs(A.sci + e) : 0;
+        vv[u] = ok ? __ldcs(A.sv + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (c + u < w) s += vv[u] * __ldg(x + cc[u]);
+    }
+  } else {
+    const int32_t p0 = __ldg(A.rp + row), p1 = __ldg(A.rp + row + 1);
+    for (int32_t p = p0; p < p1; p += 8) {
+      int32_t cc[8];
+      double vv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const bool ok = p + u < p1;
+        cc[u] = ok ? __ldcs(A.ci + p + u) : 0;
+        vv[u] = ok ? __ldcs(A.v + p + u) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (p + u < p1) s += vv[u] * __ldg(x + cc[u]);
+    }
+  }
+  return s;
+}
+
+// phase timer (CTA 0, thread 0, profiling only): adds now - *t0 to the phase slot and resets t0
+__device__ __forceinline__ void ptick(DevState* st, int kid, unsigned long long& t0) {
+  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    st->kstat[kid].ns += t - t0;
+    st->kstat[kid].launches++;
+    t0 = t;
+  }
+}
+
+__global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
+  extern __shared__ double sm[];
+  const Layout& L = pa.L;
+  const MatDev& A = pa.A;
+  DevState* st = pa.st;
+  const int m = pa.m, k = pa.k, VB = L.VB, QB = VB - k, lo = QB, nq = k;
+  const int64_t ld = L.ld;
+  double* Z = L.Z;
+  // ---- shared-memory layout (replicated least-squares state + staging)
+  double* Hs = sm;                           // [m][m+2]  H(r, i) = Hs[i*(m+2) + r]
+  double* Rs = Hs + m * (m + 2);             // [m][m+1]
+  double* Bs = Rs + m * (m + 1);             // [m][k]    B(l, i) = Bs[i*k + l]
+  double* cs = Bs + m * (k > 0 ? k : 1);
+  double* sn = cs + PM;
+  double* gg = sn + PM;                      // PM + 2
+  double* h1 = gg + PM + 2;                  // PCOL: first-pass coefficients of the pending column
+  double* cv = h1 + PCOL;                    // PCOL: v_j coefficients
+  double* cn = cv + PCOL;                    // PCOL: next-u coefficients
+  double* us = cn + PCOL;                    // PT
+  double* ysm = us + PT;                     // PT
+  double* dpart = ysm + PT;                  // MAXRED
+  double* tot = dpart + MAXRED;              // MAXRED
+  double* ys = tot + MAXRED;                 // PM + 2: cycle-end y
+  double* zk = ys + PM + 2;                  // PK
+  double* wk = zk + PK;                      // PK (+ PM+2 behind it: (H a)_c at wk[PK + c])
+  __shared__ double bsh[33];
+  __shared__ int s_fail, s_stop;
+  __shared__ double s_sc[8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) { s_fail = 0; s_stop = 0; }
+  __syncthreads();
+  const bool cta0 = blockIdx.x == 0;
+  if (cta0) prof_begin(st, K_MISC);
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  const double tol = st->tol;
+  const int max_iters = st->max_iters, hist_cap = st->hist_cap;
+  double* __restrict__ x = L.x;
+  const double* __restrict__ b = L.b;
+  double bytes = 0.0;  // algorithmic bytes (CTA 0 accounts them)
+  const bool keep = L.keep_l2 != 0;  // basis L2-sized: cached loads (the update pass re-hits them)
+
+  // ---- ||b||
+  {
+    double s = 0.0;
+    for (int64_t r = r0 + tid; r < r1; r += PT) s += b[r] * b[r];
+    s = block_sum(s, bsh);
+    if (tid == 0) dpart[0] = s;
+    __syncthreads();
+    if (!greduce(dpart, 1, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+  }
+  {
+  const double bnorm = sqrt(tot[0]);
+  if (!(bnorm > 0.0)) {
+    if (cta0 && tid == 0) {
+      st->bnorm = bnorm;
+      st->bzero = bnorm == 0.0;
+      st->done = 1;
+      st->converged = st->bzero;
+      if (!st->bzero) st->status = RG_E_NUMERIC;
+    }
+    goto out;
+  }
+  int iters = 0, cycles = 0, hist_len = 0, converged = 0, status = 0;
+  double beta = 0.0, relres = 0.0;
+  for (;;) {
+    // ================= cycle start: r = b - A x into V column 0 (+ Q^T r, ||r||^2)
+    if (!gbar(pa.bar, &s_fail)) goto fail;  // x complete
+    double* __restrict__ u0 = Z + (int64_t)VB * ld;
+    {
+      double s = 0.0;
+      for (int64_t r = r0 + tid; r < r1; r += PT) {
+        const double rr = r < L.n ? b[r] - row_dot(A, r, x) : 0.0;
+        u0[r] = rr;
+        s += rr * rr;
+      }
+      s = block_sum(s, bsh);
+      if (tid == 0) dpart[0] = s;
+      __syncthreads();
+      if (!greduce(dpart, 1, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      beta = sqrt(tot[0]);
+      if (cta0) bytes += A.bytes + 8.0 * L.n;
+    }
+    if (k > 0) {  // LS projection onto span(W): a = Q^T r, x += W R_C^{-1} a, r -= Q a
+      for (int c = tid; c < k; c += PT) dpart[c] = 0.0;
+      __syncthreads();
+      for (int64_t base = r0; base < r1; base += PT) {
+        const int64_t r = base + tid;
+        us[tid] = r < r1 ? u0[r] : 0.0;
+        __syncthreads();
+        const int cnt = (int)min((int64_t)PT, r1 - base);
+        for (int c = wid; c < k; c += PT / 32) {
+          const double* zc = Z + (int64_t)(QB + c) * ld + base;
+          double s = 0.0;
+          for (int q = lane; q < cnt; q += 32) s += zc[q] * us[q];
+          s = warp_sum(s);
+          if (lane == 0) dpart[c] += s;
+        }
+        __syncthreads();
+      }
+      if (!greduce(dpart, k, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      for (int l = tid; l < k; l += PT) {  // z = R_C^{-1} a
+        double s = 0.0;
+        for (int c = l; c < k; ++c) s += st->RCinv[c][l] * tot[c];
+        zk[l] = s;
+      }
+      __syncthreads();
+      double s2 = 0.0;
+      for (int64_t r = r0 + tid; r < r1; r += PT) {
+        double xr = x[r], rr = u0[r];
+        for (int l = 0; l < k; ++l) {
+          xr += zk[l] * Z[(int64_t)l * ld + r];
+          rr -= tot[l] * Z[(int64_t)(QB + l) * ld + r];
+        }
+        x[r] = xr;
+        u0[r] = rr;
+        s2 += rr * rr;
+      }
+      s2 = block_sum(s2, bsh);
+      if (tid == 0) dpart[0] = s2;
+      __syncthreads();
+      if (!greduce(dpart, 1, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      beta = sqrt(tot[0]);
+      if (cta0) bytes += 8.0 * L.n * (4 * k + 4);
+    }
+    relres = beta / bnorm;
+    if (!isfinite(beta)) { status = RG_E_NUMERIC; break; }
+    if (relres <= tol) { converged = 1; break; }
+    if (iters >= max_iters) break;
+    ++cycles;
+    if (tid == 0) gg[0] = beta;
+    for (int i = tid; i < PCOL; i += PT) h1[i] = 0.0;
+    __syncthreads();
+    // ================= Arnoldi steps (DCGS2), u = V column j (raw), y -> V column j+1
+    int jf = -1;
+    for (int j = 0; j <= m; ++j) {
+      const int p = nq + j;
+      double* __restrict__ u = Z + (int64_t)(VB + j) * ld;
+      double* __restrict__ y = Z + (int64_t)(VB + j + 1) * ld;
+      const bool have_y = j < m;
+      unsigned long long tph = (st->profile && cta0 && tid == 0) ? gtimer() : 0ull;
+      if (j > 0 && !gbar(pa.bar, &s_fail)) goto fail;  // u complete
+      ptick(st, K_PB1, tph);
+      const int nv = 2 * p + 2;
+      for (int c = tid; c < nv; c += PT) dpart[c] = 0.0;
+      double s_uu = 0.0, s_uy = 0.0;
+      if (have_y)  // SpMV over this CTA's rows first (many rows in flight), then the dot pass
+        for (int64_t r = r0 + tid; r < r1; r += PT) y[r] = r < L.n ? row_dot(A, r, u) : 0.0;
+      for (int64_t base = r0; base < r1; base += PT) {
+        const int64_t r = base + tid;
+        double ur = 0.0, yr = 0.0;
+        if (r < r1) {
+          ur = u[r];
+          if (have_y) yr = y[r];  // written by this thread above
+        }
+        __syncthreads();
+        us[tid] = ur;
+        ysm[tid] = yr;
+        s_uu += ur * ur;
+        s_uy += ur * yr;
+        __syncthreads();
+        const int cnt = (int)min((int64_t)PT, r1 - base);
+        constexpr int RPL = PT / 32;
+        for (int c = wid; c < p; c += PT / 32) {
+          const double* zc = Z + (int64_t)(lo + c) * ld + base + lane;
+          double zv[RPL];
+#pragma unroll
+          for (int q = 0; q < RPL; ++q)  // 16 independent loads in flight per lane
+            zv[q] = (lane + 32 * q < cnt) ? (keep ? zc[32 * q] : __ldcs(zc + 32 * q)) : 0.0;
+          double su = 0.0, sy = 0.0;
+#pragma unroll
+          for (int q = 0; q < RPL; ++q) {
+            su += zv[q] * us[lane + 32 * q];
+            sy += zv[q] * ysm[lane + 32 * q];
+          }
+          su = warp_sum(su);
+          sy = warp_sum(sy);
+          if (lane == 0) {
+            dpart[c] += su;
+            dpart[p + c] += sy;
+          }
+        }
+      }
+      {
+        const double t1 = block_sum(s_uu, bsh);
+        const double t2 = block_sum(s_uy, bsh);
+        if (tid == 0) { dpart[2 * p] = t1; dpart[2 * p + 1] = t2; }
+        __syncthreads();
+      }
+      ptick(st, K_PB2, tph);
+      if (!greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      ptick(st, K_PB3, tph);
+      if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + 2);
+      // ---- replicated epilogue: delayed second pass, column j-1, least squares
+      const double* a = tot;
+      const double* bb = tot + p;
+      const double ss = tot[2 * p], gm = tot[2 * p + 1];
+      if (wid < 2) {
+        double acc = 0.0;
+        for (int c = lane; c < p; c += 32) acc += a[c] * (wid == 0 ? a[c] : bb[c]);
+        acc = warp_sum(acc);
+        if (lane == 0) s_sc[wid] = acc;
+      }
+      __syncthreads();
+      const double nu2 = ss - s_sc[0], ab = s_sc[1];
+      const double nu = nu2 > 0.0 ? sqrt(nu2) : 0.0;
+      if (j >= 1) {
+        const int col = j - 1;
+        for (int i = tid; i < j; i += PT) Hs[col * (m + 2) + i] = h1[nq + i] + a[nq + i];
+        for (int l = tid; l < nq; l += PT) Bs[col * k + l] = h1[l] + a[l];
+        if (tid == 0) Hs[col * (m + 2) + j] = nu;
+        __syncthreads();
+        if (tid == 0) {  // Givens on column col (same arithmetic in every CTA)
+          double hv[PM + 2];
+          for (int i = 0; i <= j; ++i) hv[i] = Hs[col * (m + 2) + i];
+          for (int i = 0; i < col; ++i) {
+            const double x0 = hv[i], x1 = hv[i + 1];
+            hv[i] = cs[i] * x0 + sn[i] * x1;
+            hv[i + 1] = -sn[i] * x0 + cs[i] * x1;
+          }
+          const double den = hypot(hv[col], hv[col + 1]);
+          int stop = 0;
+          if (!(den > 0.0)) {
+            stop = 2;  // no progress possible: end the cycle at the previous column
+          } else {
+            const double c = hv[col] / den, s = hv[col + 1] / den;
+            cs[col] = c;
+            sn[col] = s;
+            hv[col] = den;
+            for (int i = 0; i <= col; ++i) Rs[col * (m + 1) + i] = hv[i];
+            const double gj = gg[col];
+            gg[col] = c * gj;
+            gg[col + 1] = -s * gj;
+            const double res = fabs(s * gj) / bnorm;
+            if (cta0 && hist_len < hist_cap) L.hist[hist_len] = res;
+            if (!isfinite(res)) stop = 3;
+            else if (res <= tol || nu <= 1e-14 * beta || col + 1 >= m || iters + 1 >= max_iters) stop = 1;
+          }
+          s_stop = stop;
+        }
+        __syncthreads();
+        ++iters;
+        if (hist_len < hist_cap && s_stop != 2) ++hist_len;
+        if (s_stop) {
+          jf = s_stop == 2 ? col - 1 : (s_stop == 3 ? -1 : col);
+          if (s_stop == 3) status = RG_E_NUMERIC;
+          break;
+        }
+      }
+      // ---- coefficients of the update pass and first-pass coefficients of column j
+      const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
+      const double aj = j >= 1 ? a[nq + j - 1] : 0.0;
+      const double d = ((gm - ab) * inv - nu * aj) * inv;
+      const double f = (aj + d) * inv;
+      for (int o = wid; o < j + nq; o += PT / 32) {  // (H a_V)_c and (B a_V)_l
+        double s = 0.0;
+        if (o < j) {
+          for (int i = (o > 0 ? o - 1 : 0) + lane; i < j; i += 32) s += Hs[i * (m + 2) + o] * a[nq + i];
+        } else {
+          for (int i = lane; i < j; i += 32) s += Bs[i * k + (o - j)] * a[nq + i];
+        }
+        s = warp_sum(s);
+        if (lane == 0) wk[o < j ? PK + o : o - j] = s;  // reuse: [0,k) Ba, [PK, PK+j) Ha
+      }
+      __syncthreads();
+      for (int c = tid; c < j; c += PT) {
+        const double Ha = wk[PK + c];
+        const double cvv = (bb[nq + c] - Ha) * inv;
+        cn[nq + c] = -Ha * inv - cvv + f * a[nq + c];
+        cv[nq + c] = -a[nq + c] * inv;
+        h1[nq + c] = cvv;
+      }
+      for (int l = tid; l < nq; l += PT) {
+        cn[l] = -bb[l] * inv + f * a[l];
+        cv[l] = -a[l] * inv;
+        h1[l] = (bb[l] - wk[l]) * inv;
+      }
+      if (tid == 0) h1[nq + j] = d;
+      __syncthreads();
+      ptick(st, K_PB4, tph);
+      // ---- update pass: v_j = u/nu + P cv, u_next = y/nu - f u + P cn  (own rows)
+      const double fu = -(aj + d) * inv;
+      for (int64_t r = r0 + tid; r < r1; r += PT) {
+        const double ur = u[r], yr = y[r];
+        double sv = 0.0, sn2 = 0.0;
+        int c = 0;
+        for (; c + 8 <= p; c += 8) {  // 8 independent loads in flight
+          double z[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const double* zp = Z + (int64_t)(lo + c + t) * ld + r;
+            z[t] = keep ? *zp : __ldcs(zp);
+          }
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            sv += cv[c + t] * z[t];
+            sn2 += cn[c + t] * z[t];
+          }
+        }
+        for (; c < p; ++c) {
+          const double z = Z[(int64_t)(lo + c) * ld + r];
+          sv += cv[c] * z;
+          sn2 += cn[c] * z;
+        }
+        u[r] = ur * inv + sv;
+        y[r] = yr * inv + ur * fu + sn2;
+      }
+      if (cta0) bytes += 8.0 * L.n * (p + 4);
+      __syncthreads();
+      ptick(st, K_PB5, tph);
+    }
+    // ================= cycle end: y = R^{-1} g, x += V y - W R_C^{-1} B y (own rows)
+    if (jf >= 0) {
+      if (tid == 0) {
+        for (int i = jf; i >= 0; --i) {
+          double s = gg[i];
+          for (int l = i + 1; l <= jf; ++l) s -= Rs[l * (m + 1) + i] * ys[l];
+          ys[i] = s / Rs[i * (m + 1) + i];
+        }
+      }
+      __syncthreads();
+      if (k > 0) {
+        for (int l = tid; l < k; l += PT) {
+          double s = 0.0;
+          for (int i = 0; i <= jf; ++i) s += Bs[i * k + l] * ys[i];
+          wk[l] = s;
+        }
+        __syncthreads();
+        for (int l = tid; l < k; l += PT) {
+          double s = 0.0;
+          for (int c = l; c < k; ++c) s += st->RCinv[c][l] * wk[c];
+          zk[l] = s;
+        }
+        __syncthreads();
+      }
+      for (int64_t r = r0 + tid; r < r1; r += PT) {
+        double xr = x[r];
+        for (int i = 0; i <= jf; ++i) xr += ys[i] * Z[(int64_t)(VB + i) * ld + r];
+        for (int l = 0; l < k; ++l) xr -= zk[l] * Z[(int64_t)l * ld + r];
+        x[r] = xr;
+      }
+      if (cta0) bytes += 8.0 * L.n * (jf + 1 + k + 2);
+    }
+    if (status) break;
+  }
+  if (cta0 && tid == 0) {
+    st->bnorm = bnorm;
+    st->beta = beta;
+    st->relres = relres;
+    st->iters = iters;
+    st->cycles = cycles;
+    st->hist_len = hist_len;
+    st->converged = converged;
+    st->status = status;
+    st->done = 1;
+    prof_end(st, K_MISC, bytes);
+  }
+  }
+out:
+  return;
+fail:
+  if (cta0 && tid == 0) {
+    st->status = RG_E_CUDA;
+    st->done = 1;
+  }
+}
+
+}  // namespace
+
+size_t persistent_smem(int m, int k) {
+  return sizeof(double) * ((size_t)m * (m + 2) + (size_t)m * (m + 1) + (size_t)m * (k > 0 ? k : 1) + 2 * PM +
+                           (PM + 2) + 3 * PCOL + 2 * PT + 2 * MAXRED + (PM + 2) + 2 * PK + PM + 2);
+}
+
+// Returns cudaErrorNotSupported when the configuration is outside this path.
+cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar, int m,
+                              int k, int variant, cudaStream_t s) {
+  if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE) || A.fmt == 2)
+    return cudaErrorNotSupported;
+  const size_t smem = persistent_smem(m, k);
+  static int max_smem = -1;
+  if (max_smem < 0) {
+    cudaFuncSetAttribute(k_solve_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_solve_persistent, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         cudaSharedmemCarveoutMaxShared);
+    max_smem = 200 * 1024;
+  }
+  if (smem > (size_t)max_smem) return cudaErrorNotSupported;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_persistent, PT, smem);
+  if (occ < 1) return cudaErrorNotSupported;
+  int64_t want = (L.ld + PT - 1) / PT;
+  int64_t cap = (int64_t)NSM * (occ >= 2 ? 2 : 1);
+  const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_DEFLATE ? k : 0};
+  void* args[] = {&pa};
+  return cudaLaunchCooperativeKernel((const void*)k_solve_persistent, dim3(G), dim3(PT), args, smem, s);
+}
+
+}  // namespace rg

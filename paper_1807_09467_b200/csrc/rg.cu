@@ -84,6 +84,8 @@ struct rg_ctx {
   unsigned* counter = nullptr;
   double* small = nullptr;
   int* dflag = nullptr;
+  double* tot_g = nullptr;   // persistent solve: reduced totals
+  unsigned* gbar = nullptr;  // persistent solve: grid-barrier words
   DevState* st = nullptr;
   DevState* hst = nullptr;  // pinned host mirror
   double* hhist = nullptr;  // pinned history staging
@@ -95,6 +97,7 @@ struct rg_ctx {
   bool have_W = false;
   bool c_valid = false;
   bool use_dcgs = true;
+  bool use_persist = true;  // one cooperative kernel per solve where supported (persistent.cu)
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -449,7 +452,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   free_matrix(c);
   cudaFree(c->Z); cudaFree(c->x); cudaFree(c->b); cudaFree(c->X); cudaFree(c->Y);
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
-  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st);
+  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->hhist) cudaFreeHost(c->hhist);
   if (c->hflag) cudaFreeHost(c->hflag);
@@ -480,6 +483,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   c->flags = opt->flags;
   if (getenv("RG_NO_GRAPH")) c->flags |= RG_FLAG_NO_GRAPH;  // ncu cannot profile kernels inside conditional graphs
   if (getenv("RG_CGS2") || (opt->flags & RG_FLAG_CGS2)) c->use_dcgs = false;
+  if (getenv("RG_NO_PERSIST") || (opt->flags & RG_FLAG_NO_PERSIST)) c->use_persist = false;
   if (opt->cuda_stream) {
     c->stream = (cudaStream_t)opt->cuda_stream;
   } else {
@@ -501,6 +505,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
       (s = dalloc(&c->t2, np, "t2")) != RG_OK || (s = dalloc(&c->hist, (size_t)HIST_CAP, "hist")) != RG_OK ||
       (s = dalloc(&c->partial, part, "partial")) != RG_OK || (s = dalloc(&c->counter, 4, "counter")) != RG_OK ||
       (s = dalloc(&c->small, (size_t)SMALL * 16, "small")) != RG_OK || (s = dalloc(&c->dflag, 4, "flag")) != RG_OK ||
+      (s = dalloc(&c->tot_g, (size_t)MAXRED, "totals")) != RG_OK || (s = dalloc(&c->gbar, 4, "barrier")) != RG_OK ||
       (s = dalloc(&c->st, 1, "state")) != RG_OK) {
     rg_destroy(c);
     return s;
@@ -680,9 +685,23 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
   c->L.augment = eff == RG_AUGMENT;
   CK(cudaEventRecord(c->e0, s));
-  CK(launch_orth(c->L, c->st, OP_NORMB, s));
-  CK(cycle_start(c, eff));
-  if ((rs = run_solve(c, eff, m)) != RG_OK) return rs;
+  bool done_persist = false;
+  // Measured on B200: the single cooperative kernel wins while kernel-boundary
+  // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
+  // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
+  const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
+  if (c->use_persist && persist_size && c->use_dcgs && !(c->flags & RG_FLAG_NO_GRAPH)) {
+    CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * 4, s));
+    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, m, k, eff, s);
+    if (ep == cudaSuccess) done_persist = true;
+    else if (ep == cudaErrorNotSupported || ep == cudaErrorCooperativeLaunchTooLarge) cudaGetLastError();
+    else CK(ep);
+  }
+  if (!done_persist) {
+    CK(launch_orth(c->L, c->st, OP_NORMB, s));
+    CK(cycle_start(c, eff));
+    if ((rs = run_solve(c, eff, m)) != RG_OK) return rs;
+  }
   CK(cudaEventRecord(c->e1, s));
   // one synchronisation per solve: header, C=AW singularity flag, x and the history together
   int bad = 0;
@@ -722,6 +741,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     rep->ms_total = ms;
   }
   if (h->status == RG_E_NUMERIC) return fail(RG_E_NUMERIC, "NaN/Inf met during the solve");
+  if (h->status == RG_E_CUDA) return fail(RG_E_CUDA, "persistent solve: grid barrier timed out");
   return RG_OK;
 }
 
@@ -762,8 +782,9 @@ RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, in
 RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t* count) {
   static const char* names[K_COUNT] = {"spmv_step", "spmv_res", "spmv_plain", "orth_dots1", "orth_upd_dots2",
                                        "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
-                                       "norm_b", "gram", "jacobi", "xm", "chol", "misc", "dcgs_dots_ls",
-                                       "dcgs_update"};
+                                       "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
+                                       "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
+                                       "p_update"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));

@@ -234,3 +234,31 @@ def test_recycle_operator_thin_qr(name, N, sell, rng):
     assert np.linalg.norm(AW - Q @ R) <= 1e-12 * np.linalg.norm(AW)
     assert np.linalg.norm(Q.T @ Q - np.eye(ke)) <= 1e-12
     assert np.allclose(np.tril(R, -1), 0.0)
+
+
+@pytest.mark.parametrize("variant", ["plain", "deflate"])
+def test_persistent_and_graph_paths_agree(variant, rng):
+    """The single cooperative-kernel solve and the CUDA-graph solve compute the same iterates
+    (same DCGS2 arithmetic, different reduction trees): same iteration counts, x within 1e-10."""
+    from paper_1807_09467_b200 import rg as rgb
+    cfg = synth.CONFIGS["C2"].reduced(160)
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    hm = seq.matrix(1, u)
+    b = seq.rhs(1, u)
+    snaps = [rng.standard_normal(cfg.n) for _ in range(4)]
+    out = []
+    for flags in (0, rgb.RG_FLAG_NO_PERSIST):
+        ctx = make_ctx(hm, max_m=cfg.m, s=8, k=4, flags=flags)
+        for v in snaps:
+            ctx.push_snapshot(t(v))
+        ctx.build_recycle(4)
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=cfg.m, variant=variant, history_cap=1000)
+        out.append((rep, x.cpu().numpy()))
+        ctx.close()
+    (r0, x0), (r1, x1) = out
+    assert r0["converged"] and r1["converged"]
+    assert r0["iterations"] == r1["iterations"]
+    assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x1)
+    assert np.allclose(r0["history"], r1["history"], rtol=1e-8, atol=1e-14)
