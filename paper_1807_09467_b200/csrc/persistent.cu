@@ -10,6 +10,7 @@
 // CTA 0 alone writes the solve report (iterations, history, status) to the device state.
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include <cstdlib>
 
 namespace rg {
 namespace {
@@ -519,7 +520,8 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_persistent, PT, smem);
   if (occ < 1) return cudaErrorNotSupported;
   int64_t want = (L.ld + PT - 1) / PT;
-  int64_t cap = (int64_t)NSM * (occ >= 2 ? 2 : 1);
+  static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : 2;
+  int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   PArgs pa{L, A, st, tot_g, bar, m, variant == RG_DEFLATE ? k : 0};
   void* args[] = {&pa};

@@ -262,3 +262,85 @@ def test_persistent_and_graph_paths_agree(variant, rng):
     assert r0["iterations"] == r1["iterations"]
     assert np.linalg.norm(x0 - x1) <= 1e-10 * np.linalg.norm(x1)
     assert np.allclose(r0["history"], r1["history"], rtol=1e-8, atol=1e-14)
+
+
+def test_bsr_generic_block_size(rng):
+    """BSR with 16x16 blocks (generic kernel, not the TMA 64x64 path): SpMV and a solve."""
+    nb, B = 40, 16
+    rp, ci = [0], []
+    for I in range(nb):
+        cols = sorted(set([I, (I + 1) % nb, (I + 7) % nb]))
+        ci += cols
+        rp.append(len(ci))
+    vals = rng.standard_normal(len(ci) * B * B) * 0.1
+    for p in range(len(ci)):
+        I = next(i for i in range(nb) if rp[i] <= p < rp[i + 1])
+        if ci[p] == I:
+            blk = vals[p * B * B:(p + 1) * B * B]
+            blk[::B + 1] += 3.0                      # diagonal of a column-major block
+    hm = synth.HostMatrix("bsr", nb * B, np.array(rp, np.int32), np.array(ci, np.int32), vals, B)
+    ctx = make_ctx(hm)
+    x = rng.standard_normal(nb * B)
+    y = torch.zeros(nb * B, dtype=torch.float64, device=DEV)
+    ctx.apply(t(x), y)
+    spmv_check(hm, x, y.cpu().numpy())
+    b = rng.standard_normal(nb * B)
+    xs = torch.zeros(nb * B, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), xs, m=20)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=20)
+    assert rep["converged"] and abs(rep["iterations"] - ref["iterations"]) <= 2
+    assert np.linalg.norm(xs.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+
+
+def test_update_matrix_new_pattern_and_validation(rng):
+    """rg_update_matrix with a different pattern (re-validated, re-allocated, graphs rebuilt) and
+    rejection of invalid patterns from host and device memory with no side effects."""
+    from paper_1807_09467_b200 import rg as rgb
+    h1 = random_csr(300, rng, per_row=(1, 4))
+    h2 = random_csr(300, rng, per_row=(5, 12))
+    ctx = make_ctx(h1)
+    b = rng.standard_normal(300)
+    x = torch.zeros(300, dtype=torch.float64, device=DEV)
+    ctx.solve(t(b), x, m=10)
+    ctx.update_matrix(t(h2.val), t(h2.row_ptr), t(h2.col_idx))
+    rep = ctx.solve(t(b), x, m=10)
+    ref = oracle.solve(oracle.Matrix.from_host(h2), b, m=10)
+    assert abs(rep["iterations"] - ref["iterations"]) <= 2
+    assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+    bad = h2.col_idx.copy()
+    bad[5], bad[6] = bad[6], bad[5]                  # unsorted row
+    for mem in ("host", "device"):
+        arr = (lambda a: a) if mem == "host" else t
+        with pytest.raises(rgb.RgError) as e:
+            ctx.update_matrix(arr(h2.val), arr(h2.row_ptr), arr(bad))
+        assert e.value.status == rgb.RG_E_INVAL
+    y = torch.zeros(300, dtype=torch.float64, device=DEV)   # the context still holds h2
+    xx = rng.standard_normal(300)
+    ctx.apply(t(xx), y)
+    spmv_check(h2, xx, y.cpu().numpy())
+
+
+def test_singular_recycle_operator_reported(rng):
+    """A W rank deficient (A annihilates part of span W) -> RG_E_SINGULAR and the recycle space is
+    cleared (E_s may be singular)."""
+    from paper_1807_09467_b200 import rg as rgb
+    n = 200
+    D = np.ones(n) * 2.0
+    D[:50] = 0.0                                     # A e_i = 0 for i < 50
+    hm = synth.HostMatrix("csr", n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), D)
+    ctx = make_ctx(hm, s=4, k=4)
+    for i in range(3):
+        v = np.zeros(n)
+        v[i] = 1.0                                   # snapshots inside the null space of A
+        ctx.push_snapshot(t(v))
+    ctx.push_snapshot(t(rng.standard_normal(n)))
+    ke, _ = ctx.build_recycle(4)
+    assert ke == 4
+    x = torch.zeros(n, dtype=torch.float64, device=DEV)
+    with pytest.raises(rgb.RgError) as e:
+        ctx.solve(t(rng.standard_normal(n)), x, m=10, variant="deflate")
+    assert e.value.status == rgb.RG_E_SINGULAR
+    W = np.zeros((4, n))
+    with pytest.raises(rgb.RgError) as e:
+        ctx.export(0, W)                             # cleared
+    assert e.value.status == rgb.RG_E_STATE
