@@ -33,6 +33,7 @@ struct PArgs {
 // bug cannot hang the GPU: after ~2 s every CTA gives up and the solve reports RG_E_CUDA.
 __device__ __forceinline__ bool gbar(unsigned* bar, int* s_fail) {
   __syncthreads();
+  if (gridDim.x == 1) return true;  // single-CTA solve (tiny systems): a CTA barrier suffices
   if (threadIdx.x == 0) {
     volatile unsigned* gen = bar + 1;
     const unsigned g = *gen;
@@ -62,6 +63,12 @@ __device__ __forceinline__ bool gbar(unsigned* bar, int* s_fail) {
 // pollers — so the work is spread over all CTAs between two barriers.)
 __device__ __forceinline__ bool greduce(const double* vals, int nv, double* partial, double* tot_g, double* tot,
                                         unsigned* bar, int* s_fail) {
+  if (gridDim.x == 1) {  // single CTA: the CTA's values are the totals
+    __syncthreads();
+    for (int i = threadIdx.x; i < nv; i += PT) tot[i] = vals[i];
+    __syncthreads();
+    return true;
+  }
   for (int i = threadIdx.x; i < nv; i += PT) partial[(size_t)blockIdx.x * MAXRED + i] = vals[i];
   if (!gbar(bar, s_fail)) return false;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, G = gridDim.x;
@@ -77,7 +84,11 @@ __device__ __forceinline__ bool greduce(const double* vals, int nv, double* part
   return true;
 }
 
-// y_r = (A x)_r for one row (CSR thread-per-row / SELL)
+// y_r = (A x)_r for one row (CSR thread-per-row / SELL).  x is written INSIDE this kernel (V columns
+// are reused every cycle, x is updated at every cycle end), so it is gathered with ordinary coherent
+// loads — never through the non-coherent read-only path (__ldg / ld.global.nc).  Visibility of other
+// CTAs' rows follows from the grid barrier's release/acquire fences (the acquire fence also
+// invalidates the SM's L1), and within one CTA from __syncthreads.
 __device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const double* __restrict__ x) {
   double s = 0.0;
   if (A.fmt == 1) {
@@ -96,7 +107,7 @@ __device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const do
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (c + u < w) s += vv[u] * __ldg(x + cc[u]);
+        if (c + u < w) s += vv[u] * x[cc[u]];
     }
   } else {
     const int32_t p0 = __ldg(A.rp + row), p1 = __ldg(A.rp + row + 1);
@@ -111,7 +122,7 @@ __device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const do
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (p + u < p1) s += vv[u] * __ldg(x + cc[u]);
+        if (p + u < p1) s += vv[u] * x[cc[u]];
     }
   }
   return s;
@@ -519,7 +530,8 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_persistent, PT, smem);
   if (occ < 1) return cudaErrorNotSupported;
-  int64_t want = (L.ld + PT - 1) / PT;
+  // tiny systems (<= 8 rows per thread of one CTA) run on ONE CTA: no grid barriers at all
+  int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;
   static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : 2;
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
