@@ -146,6 +146,15 @@ RG_API rg_status rg_clear_snapshots(rg_ctx* ctx);
  * RG_E_STATE if the window is empty. */
 RG_API rg_status rg_build_recycle(rg_ctx* ctx, int32_t k, int32_t* k_eff, double* sigma);
 
+/* As rg_build_recycle, choosing which singular modes span W (PAPER.md:673-676 compares both):
+ *   RG_MODES_LARGEST   the k dominant left singular vectors (Algorithm 1, the default)
+ *   RG_MODES_SMALLEST  the k smallest NON-ZERO ones (sigma_i > 1e-12 sigma_1)
+ * The SVD interval l of Algorithm 1 ("if (i mod l) = 0") is the caller's schedule: W and
+ * the window persist across solves, and C = A W is rebuilt after every rg_update_matrix. */
+#define RG_MODES_LARGEST 0
+#define RG_MODES_SMALLEST 1
+RG_API rg_status rg_build_recycle_modes(rg_ctx* ctx, int32_t k, int32_t modes, int32_t* k_eff, double* sigma);
+
 /* Solve A x = b with restarted GMRES(m), variant plain / augment / deflate.
  *   b, x0      length n in `mem`; x0 == NULL means x0 = 0
  *   m          restart length, 1..max_m

@@ -173,9 +173,13 @@ def svd(X):
     return U, sig, rk.value, sweeps
 
 
-def recycle_basis(X, k):
-    """Algorithm 1: V_s = first k left singular vectors of the window X,
-    with k_eff = min(k, #columns, rank).  Returns (W, sigma, k_eff)."""
+def recycle_basis(X, k, modes="largest"):
+    """Algorithm 1: V_s = first k left singular vectors of the window X
+    ("largest"), or the k smallest NON-ZERO ones ("smallest", the alternative of PAPER.md:673-676:
+    "the SVD modes with smaller singular values"), with k_eff = min(k, #columns, rank) where
+    rank = #{sigma > 1e-12 sigma_1}.  Returns (W, sigma, k_eff)."""
     U, sig, rank, _ = svd(X)
     k_eff = min(int(k), U.shape[1], rank)
+    if modes == "smallest":
+        return np.ascontiguousarray(U[:, rank - k_eff:rank]), sig, k_eff
     return np.ascontiguousarray(U[:, :k_eff]), sig, k_eff

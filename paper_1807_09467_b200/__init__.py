@@ -43,9 +43,10 @@ class Context:
     def clear_snapshots(self):
         rg.rg_clear_snapshots(self.ctx)
 
-    def build_recycle(self, k):
-        k_eff, sig = rg.rg_build_recycle(self.ctx, k, self.max_snapshots)
-        return k_eff, sig
+    def build_recycle(self, k, modes="largest"):
+        if modes == "largest":
+            return rg.rg_build_recycle(self.ctx, k, self.max_snapshots)
+        return rg.rg_build_recycle_modes(self.ctx, k, modes, self.max_snapshots)
 
     def solve(self, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=20000, history_cap=0):
         return rg.rg_solve(self.ctx, b, x_out, x0, m, variant, tol, max_iters, history_cap)

@@ -603,7 +603,12 @@ RG_API rg_status rg_clear_snapshots(rg_ctx* c) {
 }
 
 RG_API rg_status rg_build_recycle(rg_ctx* c, int32_t k, int32_t* k_eff, double* sigma) {
+  return rg_build_recycle_modes(c, k, RG_MODES_LARGEST, k_eff, sigma);
+}
+
+RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int32_t* k_eff, double* sigma) {
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  if (modes != RG_MODES_LARGEST && modes != RG_MODES_SMALLEST) return fail(RG_E_INVAL, "unknown modes");
   if (k < 1 || k > c->max_k) return fail(RG_E_INVAL, "k must be in 1..max_k");
   if (c->s_count == 0) return fail(RG_E_STATE, "no snapshots");
   const int s = c->s_count;
@@ -635,9 +640,10 @@ RG_API rg_status rg_build_recycle(rg_ctx* c, int32_t k, int32_t* k_eff, double* 
   c->have_W = ke > 0;
   c->c_valid = false;
   if (ke > 0) {
-    // W = Y V2[:, :k] Sigma^{-1} into Z[:, 0:k]
-    CK(launch_inv(sig, ke, inv, st));
-    CK(launch_xm(c->Y, ld, c->n, s, V2, s, ke, inv, c->Z, ld, c->st, st));
+    // W = Y V2[:, off:off+k] Sigma^{-1}[off:off+k] into Z[:, 0:k]; off = 0 (largest) or rank-k (smallest)
+    const int off = modes == RG_MODES_SMALLEST ? rank - ke : 0;
+    CK(launch_inv(sig + off, ke, inv, st));
+    CK(launch_xm(c->Y, ld, c->n, s, V2 + (int64_t)off * s, s, ke, inv, c->Z, ld, c->st, st));
     CK(cudaStreamSynchronize(st));
   }
   return RG_OK;

@@ -21,12 +21,14 @@ RG_PLAIN, RG_AUGMENT, RG_DEFLATE = 0, 1, 2
 RG_HOST, RG_DEVICE = 0, 1
 RG_FLAG_NO_GRAPH, RG_FLAG_PROFILE, RG_FLAG_CGS2, RG_FLAG_NO_PERSIST = 1, 2, 4, 8
 RG_EXPORT_W, RG_EXPORT_Q, RG_EXPORT_RC = 0, 1, 2
+RG_MODES_LARGEST, RG_MODES_SMALLEST = 0, 1
+MODES = {"largest": RG_MODES_LARGEST, "smallest": RG_MODES_SMALLEST}
 VARIANTS = {"plain": RG_PLAIN, "augment": RG_AUGMENT, "deflate": RG_DEFLATE}
 STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E_STATE",
           5: "RG_E_SINGULAR", 6: "RG_E_NUMERIC"}
 
 # Symbols declared in include/rg.h (tests check the .so exports exactly these).
-SYMBOLS = ("rg_create", "rg_update_matrix", "rg_matrix_values", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle",
+SYMBOLS = ("rg_create", "rg_update_matrix", "rg_matrix_values", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle", "rg_build_recycle_modes",
            "rg_solve", "rg_apply", "rg_export", "rg_kernel_stats", "rg_reset_kernel_stats", "rg_destroy",
            "rg_last_error")
 
@@ -74,6 +76,7 @@ def load(path: str = LIB_PATH):
     L.rg_push_snapshot.argtypes = [vp, vp, ctypes.c_int]
     L.rg_clear_snapshots.argtypes = [vp]
     L.rg_build_recycle.argtypes = [vp, i32, ctypes.POINTER(i32), vp]
+    L.rg_build_recycle_modes.argtypes = [vp, i32, i32, ctypes.POINTER(i32), vp]
     L.rg_solve.argtypes = [vp, vp, vp, i32, ctypes.c_int, d, i32, vp, ctypes.c_int, vp, i32,
                            ctypes.POINTER(rg_report)]
     L.rg_apply.argtypes = [vp, vp, vp, ctypes.c_int]
@@ -175,6 +178,14 @@ def rg_build_recycle(ctx, k, n_snapshots=64):
     ke = ctypes.c_int32(0)
     sig = np.zeros(n_snapshots)
     _check(_lib.rg_build_recycle(ctx, int(k), ctypes.byref(ke), sig.ctypes.data))
+    return ke.value, sig
+
+
+def rg_build_recycle_modes(ctx, k, modes="largest", n_snapshots=64):
+    ke = ctypes.c_int32(0)
+    sig = np.zeros(n_snapshots)
+    md = MODES[modes] if isinstance(modes, str) else int(modes)
+    _check(_lib.rg_build_recycle_modes(ctx, int(k), md, ctypes.byref(ke), sig.ctypes.data))
     return ke.value, sig
 
 

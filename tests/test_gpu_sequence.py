@@ -77,3 +77,46 @@ def test_c4_reduced(variant):
 
 def test_c5_reduced_bsr():
     run(synth.CONFIGS["C5"].reduced(3), "deflate", 5)
+
+
+def run_schedule(cfg, variant, T, ell=1, modes="largest", k=None):
+    """Algorithm 1 with SVD interval ell (P:551 'if (i mod l) = 0') and mode selection: the recycle
+    space is rebuilt only before systems t with (t-1) mod ell == 0 and kept in between."""
+    from paper_1807_09467_b200 import Context
+    k = k or cfg.k
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    A1 = seq.matrix(1, u)
+    ctx = Context(cfg.n, t(A1.row_ptr), t(A1.col_idx), t(A1.val), max_m=cfg.m, max_snapshots=cfg.s, max_k=k)
+    X, W = [], None
+    its = []
+    for step in range(1, T + 1):
+        A = seq.matrix(step, u)
+        b = seq.rhs(step, u)
+        ctx.update_matrix(t(A.val))
+        if X and (step - 1) % ell == 0:
+            ke, sg = ctx.build_recycle(k, modes)
+            W, so, ko = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), k, modes)
+            assert ke == ko
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=cfg.m, variant=variant, tol=cfg.tol)
+        ref = oracle.solve(oracle.Matrix.from_host(A), b, m=cfg.m, variant=variant, W=W, tol=cfg.tol)
+        assert rep["converged"] and ref["converged"]
+        assert abs(rep["iterations"] - ref["iterations"]) <= 2, (step, rep["iterations"], ref["iterations"])
+        assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+        its.append(rep["iterations"])
+        u = ref["x"]
+        X.append(u)
+        ctx.push_snapshot(t(u))
+    ctx.close()
+    return its
+
+
+@pytest.mark.parametrize("ell", [3])
+def test_c1_svd_interval(ell):
+    run_schedule(synth.CONFIGS["C1"], "deflate", 10, ell=ell)
+
+
+@pytest.mark.parametrize("variant", ["deflate", "augment"])
+def test_c1_smallest_modes(variant):
+    run_schedule(synth.CONFIGS["C1"], variant, 8, modes="smallest", k=3)

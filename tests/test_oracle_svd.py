@@ -82,3 +82,21 @@ def test_rank_deficient_window_and_k_eff(rng):
 def test_zero_window():
     U, sig, rank, _ = oracle.svd(np.zeros((5, 3)))
     assert rank == 0 and np.all(sig == 0)
+
+
+def test_smallest_modes_selection(rng):
+    """PAPER.md:673-676 alternative: the k smallest NON-ZERO singular modes.  Known spectrum:
+    X = P diag(s) Q^T; the selected span equals span(P[:, rank-k:rank]) and skips zero modes."""
+    n, s = 120, 8
+    P = np.linalg.qr(rng.standard_normal((n, s)))[0]
+    Q = np.linalg.qr(rng.standard_normal((s, s)))[0]
+    true = np.array([5.0, 3.0, 2.0, 1.0, 0.5, 0.25, 0.0, 0.0])   # rank 6
+    X = P @ np.diag(true) @ Q.T
+    W, sig, k_eff = oracle.recycle_basis(X, 2, modes="smallest")
+    assert k_eff == 2
+    ref = P[:, 4:6]
+    assert np.linalg.norm(W @ W.T - ref @ ref.T, 2) <= 1e-10
+    Wl, _, _ = oracle.recycle_basis(X, 2)
+    assert np.linalg.norm(Wl @ Wl.T - P[:, :2] @ P[:, :2].T, 2) <= 1e-10
+    Wall, _, kall = oracle.recycle_basis(X, 10, modes="smallest")
+    assert kall == 6                                             # zero modes never selected
