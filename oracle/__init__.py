@@ -10,6 +10,10 @@ Parity status of each function:
   solve (plain)       pinned: I, 2I, dense LU, restart = n termination, Arnoldi/monotonicity
   solve (aug/defl)    pinned: brute-force dense least squares over the explicit space, b = A W c
                       special case, k = 0 reduces to plain, Table-1 row-6 projector properties
+  solve (oblique)     pinned: brute-force dense least squares over the explicit monomial Krylov
+                      space K_j(M_D A, M_D r_0), rows 2 = 5 (eq. equivalence_oblique), b = A W c
+                      special case, W^T r = 0 on return, dense LU solution; obproj pinned by the
+                      projector's defining properties (M_D A W = 0, W^T M_D = 0, M_D^2 = M_D, rank)
   svd / recycle_basis pinned: [3,4,0] closed form, orthonormal input, Eckart-Young tail,
                       numpy.linalg.svd brute force
 """
@@ -26,8 +30,10 @@ _LIB = None
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _f64p = ctypes.POINTER(ctypes.c_double)
 
-PLAIN, AUGMENT, DEFLATE = 0, 1, 2
-VARIANTS = {"plain": PLAIN, "augment": AUGMENT, "deflate": DEFLATE}
+PLAIN, AUGMENT, DEFLATE, OBLIQUE, OBLIQUE_AUG = 0, 1, 2, 3, 4
+# "oblique" = Table 1 row 5 (deflated oblique), "oblique_aug" = row 2 (augmented oblique)
+VARIANTS = {"plain": PLAIN, "augment": AUGMENT, "deflate": DEFLATE, "oblique": OBLIQUE,
+            "oblique_aug": OBLIQUE_AUG}
 
 
 class _Mat(ctypes.Structure):
@@ -58,6 +64,8 @@ def lib():
                                _f64p, ctypes.c_int]
         L.or_lsproj.restype = ctypes.c_int
         L.or_lsproj.argtypes = [ctypes.POINTER(_Mat), _f64p, ctypes.c_int, _f64p, ctypes.c_int]
+        L.or_obproj.restype = ctypes.c_int
+        L.or_obproj.argtypes = [ctypes.POINTER(_Mat), _f64p, ctypes.c_int, _f64p, ctypes.c_int]
         L.or_svd.restype = ctypes.c_int
         L.or_svd.argtypes = [ctypes.c_int64, ctypes.c_int, _f64p, ctypes.c_int64, _f64p, _f64p,
                              ctypes.POINTER(ctypes.c_int)]
@@ -139,7 +147,8 @@ def solve(A: Matrix, b, x0=None, m=30, variant="plain", W=None, tol=1e-8, max_it
                         Wf.ctypes.data_as(_f64p) if Wf is not None and k > 0 else None, k, float(tol),
                         int(max_iters), _f(x), ctypes.byref(rep), _f(hist), hist_cap)
     if st == 1:
-        raise np.linalg.LinAlgError("oracle: A W is (numerically) rank deficient")
+        raise np.linalg.LinAlgError("oracle: A W is (numerically) rank deficient" if v < OBLIQUE
+                                    else "oracle: E = W^T A W is (numerically) singular")
     if st != 0:
         raise MemoryError("oracle: allocation failed")
     return dict(x=x, iterations=rep.iterations, cycles=rep.cycles, converged=bool(rep.converged),
@@ -157,6 +166,20 @@ def lsproj(A: Matrix, W, Z):
                          Zf.shape[1])
     if st:
         raise np.linalg.LinAlgError("oracle: A W is (numerically) rank deficient")
+    return Zf[:, 0].copy() if one else Zf
+
+
+def obproj(A: Matrix, W, Z):
+    """M_D Z with M_D = I - A W E^{-1} W^T, E = W^T A W (eq. left_deflation),
+    computed as the oracle's oblique solver does (LU of E).  Z: n-vector or n x q array."""
+    W = np.asfortranarray(np.asarray(W, dtype=np.float64).reshape(A.n, -1))
+    Z = np.asarray(Z, dtype=np.float64)
+    one = Z.ndim == 1
+    Zf = np.asfortranarray(Z.reshape(A.n, -1)).copy(order="F")
+    st = lib().or_obproj(ctypes.byref(A._m), W.ctypes.data_as(_f64p), W.shape[1], Zf.ctypes.data_as(_f64p),
+                         Zf.shape[1])
+    if st:
+        raise np.linalg.LinAlgError("oracle: E = W^T A W is (numerically) singular")
     return Zf[:, 0].copy() if one else Zf
 
 

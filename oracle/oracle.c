@@ -17,6 +17,9 @@
  *                           P = I - AW((AW)^T AW)^{-1}(AW)^T          PAPER.md:310, 348; eq. def_S_k_projected)
  *               with the start x_0 <- x0 + W (C^T C)^{-1} C^T r(x0), C = AW (the j = 0 case of the
  *               same minimisation; min-residual analogue of eq. projection_t_s).
+ *                 oblique : Table 1 rows 5 / 2 (deflated / augmented oblique):
+ *                           GMRES(m) on M_D A, M_D = I - AW E^{-1} W^T, E = W^T A W,
+ *                           Galerkin start x_c += W E^{-1} W^T r(x_c) at every cycle (reading R15)
  *               The minimisation is solved EXPLICITLY: an orthonormal basis U_Z of the image
  *               A*[W, v_0..v_j] is grown by modified Gram-Schmidt applied twice (MGS2), the residual
  *               is r - U_Z U_Z^T r and the coefficients are R_Z^{-1} U_Z^T r.  This is the plain
@@ -120,9 +123,16 @@ static void residual(const or_mat* A, const double* b, const double* x, double* 
   for (int64_t i = 0; i < A->n; ++i) r[i] = b[i] - r[i];
 }
 
+static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2,
+                         const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+                         double* hist, int hist_cap);
+
 int or_solve(const or_mat* A, const double* b, const double* x0, int m, int variant,
              const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
              double* hist, int hist_cap) {
+  if ((variant == 3 || variant == 4) && W != NULL && k > 0)
+    return solve_oblique(A, b, x0, m, variant == 4, W, k, tol, max_iters, x, rep, hist, hist_cap);
+  if (variant == 3 || variant == 4) variant = 0;   /* no recycle space: plain GMRES */
   const int64_t n = A->n;
   memset(rep, 0, sizeof(*rep));
   const int kk = (variant != 0 && W != NULL) ? k : 0;
@@ -254,6 +264,190 @@ int or_lsproj(const or_mat* A, const double* W, int k, double* Z, int nz) {
   if (!st)
     for (int c = 0; c < nz; ++c) mgs2(n, k, UC, Z + (int64_t)c * n, coef);
   free(UC); free(coef);
+  return st;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* Galerkin restriction and oblique deflation projector (eq. left_deflation):
+ *   E = W^T A W  (k x k, "the restriction of A onto V_s"),  M_D = I - A W E^{-1} W^T.
+ * E is factored by Gaussian elimination with partial pivoting (plain textbook LU). */
+typedef struct {
+  int k;
+  int64_t n;
+  const double* W;
+  double* C;    /* A W, n x k column-major */
+  double* LU;   /* k x k, row-major, L (unit) and U packed */
+  int* piv;
+} oblique_ctx;
+
+static void ob_free(oblique_ctx* o) { free(o->C); free(o->LU); free(o->piv); }
+
+/* returns 0 ok, 1 E singular (the paper takes no preventive measure), 2 no memory */
+static int ob_setup(const or_mat* A, const double* W, int k, oblique_ctx* o) {
+  const int64_t n = A->n;
+  o->k = k; o->n = n; o->W = W;
+  o->C = malloc(sizeof(double) * n * k);
+  o->LU = malloc(sizeof(double) * k * k);
+  o->piv = malloc(sizeof(int) * k);
+  if (!o->C || !o->LU || !o->piv) return 2;
+  for (int l = 0; l < k; ++l) or_spmv(A, W + (int64_t)l * n, o->C + (int64_t)l * n);
+  double emax = 0.0;
+  for (int a = 0; a < k; ++a)                       /* E[a][c] = w_a^T (A w_c) */
+    for (int c = 0; c < k; ++c) {
+      o->LU[a * k + c] = dot(n, W + (int64_t)a * n, o->C + (int64_t)c * n);
+      if (fabs(o->LU[a * k + c]) > emax) emax = fabs(o->LU[a * k + c]);
+    }
+  for (int c = 0; c < k; ++c) {
+    int p = c;
+    for (int r = c + 1; r < k; ++r)
+      if (fabs(o->LU[r * k + c]) > fabs(o->LU[p * k + c])) p = r;
+    o->piv[c] = p;
+    if (!(fabs(o->LU[p * k + c]) > 1e-13 * emax)) return 1;
+    if (p != c)
+      for (int cc = 0; cc < k; ++cc) {
+        double t = o->LU[c * k + cc]; o->LU[c * k + cc] = o->LU[p * k + cc]; o->LU[p * k + cc] = t;
+      }
+    for (int r = c + 1; r < k; ++r) {
+      double f = o->LU[r * k + c] / o->LU[c * k + c];
+      o->LU[r * k + c] = f;
+      for (int cc = c + 1; cc < k; ++cc) o->LU[r * k + cc] -= f * o->LU[c * k + cc];
+    }
+  }
+  return 0;
+}
+
+/* t = E^{-1} W^T y */
+static void ob_coef(const oblique_ctx* o, const double* y, double* t) {
+  const int k = o->k;
+  for (int a = 0; a < k; ++a) t[a] = dot(o->n, o->W + (int64_t)a * o->n, y);
+  for (int c = 0; c < k; ++c) {                     /* apply the row swaps, then L, then U */
+    double s = t[c]; t[c] = t[o->piv[c]]; t[o->piv[c]] = s;
+  }
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c < r; ++c) t[r] -= o->LU[r * k + c] * t[c];
+  for (int r = k - 1; r >= 0; --r) {
+    for (int c = r + 1; c < k; ++c) t[r] -= o->LU[r * k + c] * t[c];
+    t[r] /= o->LU[r * k + r];
+  }
+}
+
+/* y <- M_D y = y - A W E^{-1} W^T y */
+static void ob_apply(const oblique_ctx* o, double* y, double* t) {
+  ob_coef(o, y, t);
+  for (int l = 0; l < o->k; ++l) axpy(o->n, -t[l], o->C + (int64_t)l * o->n, y);
+}
+
+/* x <- x + W E^{-1} W^T (b - A x): the Galerkin projection start (eq. projection_guess /
+ * projection_t_s) applied to the correction equation of x. */
+static void ob_galerkin(const or_mat* A, const oblique_ctx* o, const double* b, double* x, double* r,
+                        double* t) {
+  residual(A, b, x, r);
+  ob_coef(o, r, t);
+  for (int l = 0; l < o->k; ++l) axpy(o->n, t[l], o->W + (int64_t)l * o->n, x);
+}
+
+/* Table 1 rows 5 ("deflated oblique", row2 = 0) and 2 ("augmented oblique", row2 = 1):
+ * GMRES(m) on the Krylov operator M_D A, each restart cycle c being
+ *   x_c <- x_c + W E^{-1} W^T r(x_c)                  (Galerkin start of the cycle)
+ *   r_c = b - A x_c  (recomputed; equals M_D r of the un-projected iterate)
+ *   stop if ||r_c|| / ||b|| <= tol                    (TRUE residual)
+ *   Krylov initial vector  M_D r_c (row 5)  or  r_c (row 2)     (Table 1)
+ *   x_{c+1} = x_c + z,  z = argmin_{z in K_j(M_D A, .)} ||M_D r_c - M_D A z||
+ *                                                     (eq. left_deflation_iterate, PAPER.md:263,
+ *                                                      with C_k = M_D A S_k: minimal residual)
+ * The minimisation is explicit (MGS2 image basis of M_D A v_i, as in or_solve).  The last cycle
+ * start also serves as the final oblique correction, so on return V^T (b - A x) = 0.
+ * reading R15 (Galerkin start at every restart; makes rows 2 and 5 coincide at every cycle, the
+ * identity eq. equivalence_oblique). */
+static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2,
+                         const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+                         double* hist, int hist_cap) {
+  const int64_t n = A->n;
+  memset(rep, 0, sizeof(*rep));
+  rep->k_used = k;
+  double bnorm = nrm2(n, b);
+  if (bnorm == 0.0) {
+    memset(x, 0, sizeof(double) * n);
+    rep->converged = 1;
+    return 0;
+  }
+  if (x0) memcpy(x, x0, sizeof(double) * n); else memset(x, 0, sizeof(double) * n);
+  oblique_ctx o = {0};
+  double* V = malloc(sizeof(double) * n * (m + 1));
+  double* UZ = malloc(sizeof(double) * n * (m + 1));
+  double* RZ = calloc((size_t)(m + 1) * (m + 1), sizeof(double));
+  double* e = malloc(sizeof(double) * (m + 1));
+  double* c = malloc(sizeof(double) * (m + 1));
+  double* coef = malloc(sizeof(double) * (2 * m + 2));
+  double* t = malloc(sizeof(double) * (k + 1));
+  double* r = malloc(sizeof(double) * n);
+  double* rho = malloc(sizeof(double) * n);
+  double* w = malloc(sizeof(double) * n);
+  double* z = malloc(sizeof(double) * n);
+  if (!V || !UZ || !RZ || !e || !c || !coef || !t || !r || !rho || !w || !z) { rep->status = 2; goto out; }
+  int st = ob_setup(A, W, k, &o);
+  if (st) { rep->status = st; goto out; }
+  for (;;) {
+    ob_galerkin(A, &o, b, x, r, t);
+    residual(A, b, x, r);
+    double beta = nrm2(n, r);
+    rep->rel_residual = beta / bnorm;
+    if (beta / bnorm <= tol) { rep->converged = 1; break; }
+    if (rep->iterations >= max_iters) break;
+    rep->cycles++;
+    memcpy(rho, r, sizeof(double) * n);               /* target M_D r_c */
+    ob_apply(&o, rho, t);
+    memcpy(w, row2 ? r : rho, sizeof(double) * n);   /* Krylov initial vector */
+    double v0n = nrm2(n, w);
+    if (!(v0n > 0.0)) break;
+    for (int64_t i = 0; i < n; ++i) V[i] = w[i] / v0n;
+    int q = 0;
+    for (int j = 0; j < m; ++j) {
+      or_spmv(A, V + (int64_t)j * n, w);              /* w = M_D A v_j */
+      ob_apply(&o, w, t);
+      memcpy(z, w, sizeof(double) * n);
+      double wn = nrm2(n, w);
+      double zn = mgs2(n, q, UZ, z, coef);
+      int image_breakdown = !(zn > 1e-14 * wn);
+      if (!image_breakdown) {
+        for (int i = 0; i < q; ++i) RZ[(int64_t)q * (m + 1) + i] = coef[i];
+        RZ[(int64_t)q * (m + 1) + q] = zn;
+        for (int64_t i = 0; i < n; ++i) UZ[(int64_t)q * n + i] = z[i] / zn;
+        e[q] = dot(n, UZ + (int64_t)q * n, rho);
+        axpy(n, -e[q], UZ + (int64_t)q * n, rho);
+        ++q;
+      }
+      double res = nrm2(n, rho);
+      double hn = mgs2(n, j + 1, V, w, coef);         /* Arnoldi on M_D A */
+      rep->iterations++;
+      if (hist && rep->hist_len < hist_cap) hist[rep->hist_len++] = res / bnorm;
+      int stop = (res / bnorm <= tol) || image_breakdown || !(hn > 1e-14 * beta) || j == m - 1 ||
+                 rep->iterations >= max_iters;
+      if (!stop) {
+        for (int64_t i = 0; i < n; ++i) V[(int64_t)(j + 1) * n + i] = w[i] / hn;
+        continue;
+      }
+      backsolve(q, RZ, m + 1, e, c);
+      for (int i = 0; i < q; ++i) axpy(n, c[i], V + (int64_t)i * n, x);
+      break;
+    }
+  }
+out:
+  ob_free(&o);
+  free(V); free(UZ); free(RZ); free(e); free(c); free(coef); free(t); free(r); free(rho); free(w); free(z);
+  return rep->status;
+}
+
+/* M_D Z for the nz columns of Z (in place); returns 1 if E = W^T A W is singular.  Exposed so
+ * tests can check the projector's defining properties (M_D A W = 0, W^T M_D = 0, M_D^2 = M_D). */
+int or_obproj(const or_mat* A, const double* W, int k, double* Z, int nz) {
+  oblique_ctx o = {0};
+  double* t = malloc(sizeof(double) * (k + 1));
+  int st = t ? ob_setup(A, W, k, &o) : 2;
+  if (!st)
+    for (int c = 0; c < nz; ++c) ob_apply(&o, Z + (int64_t)c * A->n, t);
+  ob_free(&o);
+  free(t);
   return st;
 }
 

@@ -56,6 +56,43 @@ def restarted_minres(A, b, m, variant="plain", W=None, tol=1e-8, max_iters=2000,
     return x, iters, np.array(hist)
 
 
+def oblique_projector(A, W):
+    """M_D = I - A W E^{-1} W^T with E = W^T A W, written literally (Table 1 rows 2/5)."""
+    return np.eye(A.shape[0]) - A @ W @ np.linalg.inv(W.T @ A @ W) @ W.T
+
+
+def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False):
+    """Table 1 rows 5 (row2=False) / 2 (row2=True) with the Galerkin start at every cycle
+    (R15): x_c <- x_c + W E^{-1} W^T r(x_c); z = argmin over K_j(M_D A, v) of
+    ||M_D r_c - M_D A z|| with v = M_D r_c (row 5) or r_c (row 2).  Returns (x, iterations, history)."""
+    n = A.shape[0]
+    bn = np.linalg.norm(b)
+    x = np.zeros(n)
+    E = W.T @ A @ W
+    M = oblique_projector(A, W)
+    MA = M @ A
+    hist, iters = [], 0
+    while True:
+        x = x + W @ np.linalg.solve(E, W.T @ (b - A @ x))
+        r = b - A @ x
+        if np.linalg.norm(r) / bn <= tol or iters >= max_iters:
+            break
+        rh = M @ r
+        v = r if row2 else rh
+        K = [v / np.linalg.norm(v)]
+        for j in range(m):
+            S = np.column_stack(K)
+            y = np.linalg.lstsq(MA @ S, rh, rcond=None)[0]
+            res = np.linalg.norm(rh - MA @ S @ y)
+            hist.append(res / bn)
+            iters += 1
+            if res / bn <= tol or j == m - 1 or iters >= max_iters:
+                x = x + S @ y
+                break
+            K = _orth_append(K, MA @ K[-1])
+    return x, iters, np.array(hist)
+
+
 def random_nonsym(n, rng, shift=2.5, density=1.0):
     """Dense non-symmetric test matrix shift*I + G/sqrt(n) (eigenvalues in a disc around shift)."""
     G = rng.standard_normal((n, n)) / np.sqrt(n)
