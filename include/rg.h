@@ -48,13 +48,22 @@ typedef enum {
   RG_E_NOMEM = 2,    /* device or host allocation failed                                       */
   RG_E_CUDA = 3,     /* CUDA runtime error (message has the CUDA error string)                 */
   RG_E_STATE = 4,    /* call not valid in the current state (e.g. build with no snapshots)      */
-  RG_E_SINGULAR = 5, /* A W rank deficient: min|r_ii| <= 1e-12 max|r_ii| of R_C (PAPER.md:562-564
+  RG_E_SINGULAR = 5, /* A W rank deficient: min|r_ii| <= 1e-12 max|r_ii| of R_C, or (oblique)
+                        E = W^T A W singular: a pivot <= 1e-13 max|E_ab| (PAPER.md:562-564
                         "E_s may be singular"); the recycle space is cleared                   */
   RG_E_NUMERIC = 6   /* NaN/Inf met during the solve                                           */
 } rg_status;
 
 typedef enum { RG_CSR = 0, RG_BSR = 1 } rg_format;
-typedef enum { RG_PLAIN = 0, RG_AUGMENT = 1, RG_DEFLATE = 2 } rg_variant;
+/* RG_PLAIN    GMRES(m)
+ * RG_AUGMENT  min over x_c + span(W) + K_j(A, r_c)                (eq. def_aug_S_space, :205-217)
+ * RG_DEFLATE  Table 1 row 6 "deflated LS" = GCRO inner iteration  (:310, :332, :348)
+ * RG_OBLIQUE  Table 1 rows 5 / 2 "deflated / augmented oblique" (identical without a
+ *             preconditioner, eq. equivalence_oblique :325-330): GMRES(m) on M_D A with
+ *             M_D = I - A W E^{-1} W^T, E = W^T A W (:229-239), and the Galerkin start
+ *             x_c += W E^{-1} W^T r(x_c) (eq. projection_t_s, :289, :419) at every restart
+ *             (reading R15).  Requires k_eff <= 32; E singular -> RG_E_SINGULAR. */
+typedef enum { RG_PLAIN = 0, RG_AUGMENT = 1, RG_DEFLATE = 2, RG_OBLIQUE = 3 } rg_variant;
 typedef enum { RG_HOST = 0, RG_DEVICE = 1 } rg_mem;
 
 /* A sparse matrix handed to rg_create / rg_update_matrix.

@@ -27,7 +27,7 @@ constexpr int VEC_CTAS_PER_SM = 2;         // -> 296 CTAs: 32 resident warps / S
 enum KernelId {
   K_SPMV_STEP = 0, K_SPMV_RES, K_SPMV_PLAIN, K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN,
   K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_DK1, K_DK2,
-  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_COUNT
+  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_COUNT
 };
 
 struct KStatDev {
@@ -68,6 +68,7 @@ struct DevState {
   double Si[MAXM + 2][MAXM + 2];   // augment: S = T^{-1} (upper triangular), Si[col][row]
   double RCinv[MAXK][MAXK];        // R_C^{-1}, column-major [col][row]
   double RC[MAXK][MAXK];           // R_C, column-major [col][row]
+  double Einv[MAXK][MAXK];         // oblique: E^{-1}, E = W^T A W, column-major [col][row]
   double coef[MAXCOL];             // coefficients of the current CGS pass (absolute column)
   double hcol[MAXCOL];             // accumulated coefficients of the current column
   double coefx[MAXCOL];            // cycle-end x-update coefficients
@@ -78,6 +79,7 @@ struct DevState {
 
 // Basis layout (constant per context).  Z is n_pad x MAXCOL... column-major with leading
 // dimension ld; columns [0, maxk) hold W, [VB - k_eff, VB) hold Q, [VB, VB + m + 1) hold V.
+// The oblique variant keeps C = A W (not Q) in [k_eff, 2 k_eff), adjacent to W.
 struct Layout {
   double* Z;
   int64_t ld;      // = n_pad (multiple of 64)

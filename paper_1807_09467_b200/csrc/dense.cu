@@ -271,6 +271,67 @@ __global__ void k_inv(const double* sigma, int q, double* out) {
 
 // Cholesky G = R^T R (R upper, column-major R[c*k + r]) and R^{-1}, one CTA.
 constexpr int CLD = MAXK + 1;
+// E^{-1} by Gauss-Jordan elimination with partial pivoting on [E | I] in shared memory, one CTA
+// (k <= 32).  E(a, b) = W_a^T C_b = G[(k + b) * 2k + a] (the off-diagonal block of Gram([W | C])).
+constexpr int EK = 32;
+__global__ void __launch_bounds__(256) k_einv(const double* G, int k, DevState* st, int* fail) {
+  __shared__ double M[EK][2 * EK + 1];
+  __shared__ double f[EK];
+  __shared__ int s_p, s_bad;
+  __shared__ double s_emax;
+  const int tid = threadIdx.x, bd = blockDim.x, s = 2 * k;
+  for (int e = tid; e < k * 2 * k; e += bd) {
+    const int r = e / (2 * k), c = e % (2 * k);
+    M[r][c] = c < k ? G[(int64_t)(k + c) * s + r] : (c - k == r ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double mx = 0.0;
+    for (int r = 0; r < k; ++r)
+      for (int c = 0; c < k; ++c) mx = fmax(mx, fabs(M[r][c]));
+    s_emax = mx;
+    s_bad = !(mx > 0.0);
+  }
+  __syncthreads();
+  for (int c = 0; c < k && !s_bad; ++c) {
+    if (tid == 0) {
+      int p = c;
+      for (int r = c + 1; r < k; ++r)
+        if (fabs(M[r][c]) > fabs(M[p][c])) p = r;
+      s_p = p;
+      if (!(fabs(M[p][c]) > 1e-13 * s_emax)) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const int p = s_p;
+    if (p != c)
+      for (int cc = tid; cc < 2 * k; cc += bd) {
+        const double t = M[c][cc];
+        M[c][cc] = M[p][cc];
+        M[p][cc] = t;
+      }
+    __syncthreads();
+    const double piv = M[c][c];
+    __syncthreads();
+    for (int cc = tid; cc < 2 * k; cc += bd) M[c][cc] /= piv;
+    for (int r = tid; r < k; r += bd) f[r] = r == c ? 0.0 : M[r][c];  // multipliers vs the scaled pivot row
+    __syncthreads();
+    for (int e = tid; e < k * 2 * k; e += bd) {
+      const int r = e / (2 * k), cc = e % (2 * k);
+      if (r != c) M[r][cc] -= f[r] * M[c][cc];
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) fail[0] = 1;
+    return;
+  }
+  for (int e = tid; e < k * k; e += bd) {
+    const int r = e % k, c = e / k;
+    st->Einv[c][r] = M[r][k + c];
+  }
+}
+
 __global__ void __launch_bounds__(256) k_chol(const double* G, int k, double* R, double* Ri, int* fail) {
   __shared__ double Rs[MAXK * CLD];  // R(r, c) = Rs[c * CLD + r]
   __shared__ int bad;
@@ -427,6 +488,12 @@ cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const doub
 
 cudaError_t launch_inv(const double* sigma, int q, double* out, cudaStream_t strm) {
   k_inv<<<1, 64, 0, strm>>>(sigma, q, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_einv(const double* G, int k, DevState* st, int* fail, cudaStream_t strm) {
+  if (k < 1 || k > EK) return cudaErrorInvalidValue;
+  k_einv<<<1, 256, 0, strm>>>(G, k, st, fail);
   return cudaGetLastError();
 }
 

@@ -223,7 +223,7 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
     __syncthreads();
   }
   for (int i = tid; i <= jf; i += bd) st->coefx[VB + i] = -ys[i];  // x += V y
-  if (k > 0 && var != RG_PLAIN) {
+  if (k > 0 && (var == RG_DEFLATE || var == RG_AUGMENT)) {
     if (var == RG_DEFLATE) {  // x -= W R_C^{-1} B y
       for (int l = tid >> 5; l < k; l += nw) {
         double sacc = 0.0;
@@ -265,6 +265,20 @@ __device__ __forceinline__ void epi_cs_dq(DevState* st, const Layout& L, const d
   __syncthreads();
   rcinv_apply(st, k, us, zs);
   for (int l = threadIdx.x; l < k; l += blockDim.x) st->coefx[l] = -zs[l];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- oblique projection
+// tot[0..k) = W^T w.  t = E^{-1} W^T w -> coef[k + l] (the update w -= C t, C in columns [k, 2k));
+// at the cycle start also coefx[l] = -t_l (OP_XW: x += W t, the Galerkin start of PAPER.md:289).
+__device__ __forceinline__ void epi_ob(DevState* st, const double* tot, bool cycle_start) {
+  const int k = st->k_eff;
+  for (int a = threadIdx.x; a < k; a += blockDim.x) {
+    double t = 0.0;
+    for (int b = 0; b < k; ++b) t += st->Einv[b][a] * tot[b];
+    st->coef[k + a] = t;
+    if (cycle_start) st->coefx[a] = -t;
+  }
   __syncthreads();
 }
 

@@ -35,7 +35,14 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
 cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld, int k, DevState* st, unsigned* counter,
                         cudaStream_t s);
 
-enum OrthOp { OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB };
+enum OrthOp {
+  OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB,
+  // oblique variant (M_D = I - C E^{-1} W^T, C = A W in columns [k, 2k)):
+  OP_OB_CSD,  // cycle start: t = E^{-1} W^T r            (x += W t via OP_XW)
+  OP_OB_CSU,  // cycle start: r -= C t, ||r||^2 -> cycle-start epilogue
+  OP_OB_SD,   // Arnoldi step: t = E^{-1} W^T (A v_j)
+  OP_OB_SU    // Arnoldi step: A v_j -= C t               (the new column is M_D A v_j)
+};
 // cond != 0: cudaGraphConditionalHandle set to st->active by OP_UN's epilogue (graph WHILE node)
 cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond = 0);
 // DCGS2 Arnoldi step (dcgs.cu): phase 1 = dots + epilogue (sets the WHILE condition), 2 = update
@@ -49,6 +56,10 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
                               int k, int variant, cudaStream_t s);
 
 // ---- dense / recycle-build kernels (dense.cu)
+// E^{-1} (Gauss-Jordan, partial pivoting, one CTA) of E(a,b) = G[(k+b)*2k + a], the W^T C block of
+// the Gram matrix of [W | C] (G 2k x 2k column-major), into st->Einv; fail[0] = 1 if a pivot is
+// <= 1e-13 max|E_ab|.
+cudaError_t launch_einv(const double* G, int k, DevState* st, int* fail, cudaStream_t strm);
 // G = Y^T Y (s x s, column-major) for Y (n x s, leading dimension ld).
 cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G, double* partial,
                         unsigned* counter, DevState* st, cudaStream_t strm);

@@ -13,6 +13,8 @@
 // Cycle start (recycled variants): OP_CS_DQ a = Q^T r ; OP_XW x += W R_C^{-1} a ;
 // OP_CS_UN r -= Q a, ||r|| -> cycle-start epilogue.  Cycle end: OP_XUPD x += V y + W z.
 // OP_NORMB: ||b||.
+// Oblique variant (M_D = I - C E^{-1} W^T): OP_OB_CSD / OP_OB_SD t = E^{-1} W^T w,
+// OP_OB_CSU / OP_OB_SU w -= C t (+ ||w|| -> cycle-start epilogue at the cycle start).
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
@@ -42,12 +44,13 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
   DevState* st = a.st;
   const Layout& L = a.L;
   const int op = a.op;
-  static constexpr int kids[8] = {K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN, K_XW, K_XUPD, K_NORMB};
+  static constexpr int kids[12] = {K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN, K_XW, K_XUPD, K_NORMB,
+                                   K_OBD, K_OBU, K_OBD, K_OBU};
   const int kid = kids[op];
   bool go;
   switch (op) {
-    case OP_D1: case OP_UD2: case OP_UN: go = st->active != 0; break;
-    case OP_CS_DQ: case OP_CS_UN: case OP_XW: go = st->done == 0; break;
+    case OP_D1: case OP_UD2: case OP_UN: case OP_OB_SD: case OP_OB_SU: go = st->active != 0; break;
+    case OP_CS_DQ: case OP_CS_UN: case OP_XW: case OP_OB_CSD: case OP_OB_CSU: go = st->done == 0; break;
     case OP_XUPD: go = st->have_xupd != 0; break;
     default: go = true;
   }
@@ -76,8 +79,12 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
     case OP_XW: w = L.x; csrc = st->coefx; u0 = 0; u1 = k; break;
     case OP_XUPD:
       w = L.x; csrc = st->coefx; u0 = VB; u1 = VB + st->jfinal + 1;
-      if (var != RG_PLAIN) { u2 = 0; u3 = k; }
+      if (var == RG_AUGMENT || var == RG_DEFLATE) { u2 = 0; u3 = k; }
       break;
+    case OP_OB_CSD: w = L.Z + (int64_t)VB * ld; d0 = 0; d1 = k; break;
+    case OP_OB_CSU: w = L.Z + (int64_t)VB * ld; u0 = k; u1 = 2 * k; nrmflag = true; break;
+    case OP_OB_SD: w = L.Z + (int64_t)(VB + j + 1) * ld; d0 = 0; d1 = k; break;
+    case OP_OB_SU: w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = k; u1 = 2 * k; break;
     default: w = const_cast<double*>(L.b); nrmflag = true; break;  // OP_NORMB (read only)
   }
   const bool upd = (u1 > u0) || (u3 > u2);
@@ -158,7 +165,9 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
       if (a.use_cond && threadIdx.x == 0) cudaGraphSetConditional(a.cond, st->active ? 1u : 0u);
       break;
     case OP_CS_DQ: epi_cs_dq(st, L, tot); break;
-    case OP_CS_UN: epi_cycle_start(st, L, tot[0]); break;
+    case OP_CS_UN: case OP_OB_CSU: epi_cycle_start(st, L, tot[0]); break;
+    case OP_OB_CSD: epi_ob(st, tot, true); break;
+    case OP_OB_SD: epi_ob(st, tot, false); break;
     default:
       if (threadIdx.x == 0) {  // OP_NORMB
         st->bnorm = sqrt(tot[0]);

@@ -96,7 +96,10 @@ struct rg_ctx {
   int k_eff = 0;
   bool have_W = false;
   bool c_valid = false;
+  int c_kind = 0;           // what c_valid refers to: 0 Q / R_C (augment, deflate), 1 C / E^{-1} (oblique)
   bool use_dcgs = true;
+  bool dcgs_now = true;     // this solve uses DCGS2 (the oblique variant runs classical CGS2)
+  int cur_var = 0;          // variant of the kernel sequence being issued
   bool use_persist = true;  // one cooperative kernel per solve where supported (persistent.cu)
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -317,10 +320,40 @@ rg_status build_c(rg_ctx* c, bool sync) {
   return RG_OK;
 }
 
+// Oblique variant: C = A W into columns [k, 2k) (adjacent to W), E = W^T C from the Gram matrix of
+// [W | C], E^{-1} by Gauss-Jordan into the state (E_s = V_s^T A V_s).
+rg_status build_c_oblique(rg_ctx* c) {
+  const int k = c->k_eff;
+  if (2 * k > 64) return fail(RG_E_INVAL, "the oblique variant supports k_eff <= 32");
+  const int64_t ld = c->npad;
+  cudaStream_t s = c->stream;
+  double* C = c->Z + (int64_t)k * ld;
+  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported : launch_spmm(c->A, c->Z, C, ld, k, c->st, c->counter, s);
+  if (es == cudaErrorNotSupported) {
+    cudaGetLastError();
+    for (int l = 0; l < k; ++l)
+      CK(launch_spmv(c->A, c->L, c->st, SM_PLAIN, c->Z + (int64_t)l * ld, C + (int64_t)l * ld, 0, s));
+  } else {
+    CK(es);
+  }
+  double* G = c->small;
+  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
+  CK(launch_gram(c->Z, ld, c->n, 2 * k, G, c->partial, c->counter, c->st, s));
+  CK(launch_einv(G, k, c->st, c->dflag, s));
+  c->c_valid = true;
+  c->c_kind = 1;
+  return RG_OK;
+}
+
 // ---- the kernel sequences of one solve
 cudaError_t cycle_start(rg_ctx* c, int variant) {
   cudaError_t e = launch_spmv(c->A, c->L, c->st, SM_RES, nullptr, nullptr, variant == RG_PLAIN ? 1 : 0, c->stream);
   if (e != cudaSuccess || variant == RG_PLAIN) return e;
+  if (variant == RG_OBLIQUE) {  // Galerkin start x += W t, r -= C t, t = E^{-1} W^T r
+    if ((e = launch_orth(c->L, c->st, OP_OB_CSD, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_orth(c->L, c->st, OP_XW, c->stream)) != cudaSuccess) return e;
+    return launch_orth(c->L, c->st, OP_OB_CSU, c->stream);
+  }
   if ((e = launch_orth(c->L, c->st, OP_CS_DQ, c->stream)) != cudaSuccess) return e;
   if ((e = launch_orth(c->L, c->st, OP_XW, c->stream)) != cudaSuccess) return e;
   return launch_orth(c->L, c->st, OP_CS_UN, c->stream);
@@ -329,7 +362,11 @@ cudaError_t cycle_start(rg_ctx* c, int variant) {
 cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
   cudaError_t e;
   if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
-  if (c->use_dcgs) {  // delayed CGS2: one reduction + one update pass
+  if (c->cur_var == RG_OBLIQUE) {  // w = M_D A v_j = A v_j - C E^{-1} W^T A v_j
+    if ((e = launch_orth(c->L, c->st, OP_OB_SD, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_orth(c->L, c->st, OP_OB_SU, c->stream)) != cudaSuccess) return e;
+  }
+  if (c->dcgs_now) {  // delayed CGS2: one reduction + one update pass
     if ((e = launch_dcgs(c->L, c->st, 1, c->stream, cond)) != cudaSuccess) return e;
     return launch_dcgs(c->L, c->st, 2, c->stream);
   }
@@ -340,7 +377,7 @@ cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
 
 cudaError_t cycle_body(rg_ctx* c, int variant, int m) {
   cudaError_t e;
-  const int steps = m + (c->use_dcgs ? 1 : 0);  // DCGS2 finishes column j-1 in step j
+  const int steps = m + (c->dcgs_now ? 1 : 0);  // DCGS2 finishes column j-1 in step j
   for (int j = 0; j < steps; ++j)
     if ((e = arnoldi_step(c, 0)) != cudaSuccess) return e;
   if ((e = launch_orth(c->L, c->st, OP_XUPD, c->stream)) != cudaSuccess) return e;
@@ -657,7 +694,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (m < 1 || m > c->max_m) return fail(RG_E_INVAL, "m must be in 1..max_m");
   if (!(tol > 0.0)) return fail(RG_E_INVAL, "tol must be > 0");
   if (max_iters < 1) return fail(RG_E_INVAL, "max_iters must be >= 1");
-  if (v != RG_PLAIN && v != RG_AUGMENT && v != RG_DEFLATE) return fail(RG_E_INVAL, "unknown variant");
+  if (v != RG_PLAIN && v != RG_AUGMENT && v != RG_DEFLATE && v != RG_OBLIQUE) return fail(RG_E_INVAL, "unknown variant");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
   if (history_cap < 0) return fail(RG_E_INVAL, "history_cap < 0");
   cudaStream_t s = c->stream;
@@ -666,11 +703,15 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   const int k = eff == RG_PLAIN ? 0 : c->k_eff;
   int c_spmv = 0;
   bool check_c = false;
-  if (eff != RG_PLAIN && !c->c_valid) {
-    if ((rs = build_c(c, false)) != RG_OK) return rs;
+  const int want_kind = eff == RG_OBLIQUE ? 1 : 0;
+  if (eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind)) {
+    if ((rs = (eff == RG_OBLIQUE ? build_c_oblique(c) : build_c(c, false))) != RG_OK) return rs;
+    c->c_kind = want_kind;
     c_spmv = k;
     check_c = true;
   }
+  c->cur_var = eff;
+  c->dcgs_now = c->use_dcgs && eff != RG_OBLIQUE;
   if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
   if (x0) {
     if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
@@ -687,7 +728,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   h->profile = (c->flags & RG_FLAG_PROFILE) ? 1 : 0;
   h->tol = tol;
   h->jfinal = -1;
-  h->dcgs = c->use_dcgs ? 1 : 0;
+  h->dcgs = c->dcgs_now ? 1 : 0;
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
   c->L.augment = eff == RG_AUGMENT;
   CK(cudaEventRecord(c->e0, s));
@@ -696,7 +737,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
   // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
   const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
-  if (c->use_persist && persist_size && c->use_dcgs && !(c->flags & RG_FLAG_NO_GRAPH)) {
+  if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
     CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * 4, s));
     cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, m, k, eff, s);
     if (ep == cudaSuccess) done_persist = true;
@@ -722,7 +763,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     c->have_W = false;
     c->k_eff = 0;
     c->c_valid = false;
-    return fail(RG_E_SINGULAR, "A W is numerically rank deficient (R_C singular); recycle space cleared");
+    return fail(RG_E_SINGULAR, eff == RG_OBLIQUE ? "E = W^T A W is numerically singular; recycle space cleared"
+                                                 : "A W is numerically rank deficient (R_C singular); recycle space cleared");
   }
   if (h->bzero) {
     if (mem == RG_DEVICE) {
@@ -770,12 +812,12 @@ RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, in
   if (k == 0) return fail(RG_E_STATE, "no recycle space");
   const cudaMemcpyKind kind = mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   if (which == RG_EXPORT_W || which == RG_EXPORT_Q) {
-    if (which == RG_EXPORT_Q && !c->c_valid) return fail(RG_E_STATE, "Q is not built (run a recycled solve)");
+    if (which == RG_EXPORT_Q && !(c->c_valid && c->c_kind == 0)) return fail(RG_E_STATE, "Q is not built (run a recycled solve)");
     const int c0 = which == RG_EXPORT_W ? 0 : c->L.VB - k;
     CK(cudaMemcpy2DAsync(out, sizeof(double) * c->n, c->Z + (int64_t)c0 * c->npad, sizeof(double) * c->npad,
                          sizeof(double) * c->n, k, kind, c->stream));
   } else if (which == RG_EXPORT_RC) {
-    if (!c->c_valid) return fail(RG_E_STATE, "R_C is not built (run a recycled solve)");
+    if (!(c->c_valid && c->c_kind == 0)) return fail(RG_E_STATE, "R_C is not built (run a recycled solve)");
     CK(cudaMemcpy2DAsync(out, sizeof(double) * k, &c->st->RC[0][0], sizeof(double) * MAXK, sizeof(double) * k, k,
                          kind, c->stream));
   } else {
@@ -790,7 +832,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
-                                       "p_update"};
+                                       "p_update", "ob_dots", "ob_update"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));

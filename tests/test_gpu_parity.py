@@ -98,7 +98,7 @@ def test_spmv_full_size_sampled_rows(name, rng):
 
 
 # ------------------------------------------------------------------------------------- solves
-@pytest.mark.parametrize("variant", ["plain", "augment", "deflate"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
 @pytest.mark.parametrize("n,m,k", [(200, 10, 4), (1023, 25, 8), (64, 64, 3)])
 def test_solve_random_vs_oracle(variant, n, m, k, rng):
     hm = random_csr(n, rng, per_row=(2, 8), diag=2.2)
@@ -127,6 +127,10 @@ def test_solve_random_vs_oracle(variant, n, m, k, rng):
     assert np.linalg.norm(Wg @ Wg.T - W @ W.T, 2) <= 1e-10
     h = rep["history"]
     assert len(h) == rep["iterations"]
+    if variant == "oblique":  # final Galerkin/oblique correction: W^T (b - A x) = 0
+        assert np.linalg.norm(W.T @ r) <= 1e-11 * np.linalg.norm(b)
+        kk = min(len(h), len(ref["history"]))   # Givens estimates vs the oracle's explicit minima
+        assert np.allclose(h[:kk], ref["history"][:kk], rtol=1e-5, atol=1e-11)
 
 
 def test_b_zero_and_converged_x0(rng):
@@ -160,7 +164,7 @@ def test_rhs_in_image_of_recycle_space(rng):
     ctx.build_recycle(k)
     c = rng.standard_normal(k)
     b = hm.to_scipy() @ (W @ c)
-    for v in ("augment", "deflate"):
+    for v in ("augment", "deflate", "oblique"):
         x = torch.zeros(n, dtype=torch.float64, device=DEV)
         rep = ctx.solve(t(b), x, m=10, variant=v)
         assert rep["iterations"] == 0 and rep["converged"]
@@ -320,7 +324,8 @@ def test_update_matrix_new_pattern_and_validation(rng):
     spmv_check(h2, xx, y.cpu().numpy())
 
 
-def test_singular_recycle_operator_reported(rng):
+@pytest.mark.parametrize("variant", ["deflate", "oblique"])
+def test_singular_recycle_operator_reported(variant, rng):
     """A W rank deficient (A annihilates part of span W) -> RG_E_SINGULAR and the recycle space is
     cleared (E_s may be singular)."""
     from paper_1807_09467_b200 import rg as rgb
@@ -338,7 +343,7 @@ def test_singular_recycle_operator_reported(rng):
     assert ke == 4
     x = torch.zeros(n, dtype=torch.float64, device=DEV)
     with pytest.raises(rgb.RgError) as e:
-        ctx.solve(t(rng.standard_normal(n)), x, m=10, variant="deflate")
+        ctx.solve(t(rng.standard_normal(n)), x, m=10, variant=variant)
     assert e.value.status == rgb.RG_E_SINGULAR
     W = np.zeros((4, n))
     with pytest.raises(rgb.RgError) as e:

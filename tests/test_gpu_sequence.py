@@ -56,12 +56,12 @@ def run(cfg, variant, T, k=None):
     return rows
 
 
-@pytest.mark.parametrize("variant", ["plain", "augment", "deflate"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
 def test_c1_full_sequence(variant):
     run(synth.CONFIGS["C1"], variant, 10)
 
 
-@pytest.mark.parametrize("variant", ["augment", "deflate"])
+@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
 def test_c2_reduced(variant):
     run(synth.CONFIGS["C2"].reduced(96), variant, 6)
 
@@ -70,13 +70,18 @@ def test_c3_reduced_sell_deflate():
     run(synth.CONFIGS["C3"].reduced(96), "deflate", 5)
 
 
-@pytest.mark.parametrize("variant", ["augment", "deflate"])
+@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
 def test_c4_reduced(variant):
     run(synth.CONFIGS["C4"].reduced(20), variant, 5, k=8)
 
 
-def test_c5_reduced_bsr():
-    run(synth.CONFIGS["C5"].reduced(3), "deflate", 5)
+@pytest.mark.parametrize("variant", ["deflate", "oblique"])
+def test_c5_reduced_bsr(variant):
+    run(synth.CONFIGS["C5"].reduced(3), variant, 5)
+
+
+def test_c3_reduced_sell_oblique():
+    run(synth.CONFIGS["C3"].reduced(96), "oblique", 5)
 
 
 def run_schedule(cfg, variant, T, ell=1, modes="largest", k=None):
