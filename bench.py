@@ -7,7 +7,7 @@ space is rebuilt from the snapshot window (a3; C = A W and its QR are rebuilt in
 the system is solved with the recycled variant (a5-a10), and x_t is pushed as a snapshot (a2).
 
 Default workload: BASELINE.json configs[1] (C2, n = 262,144, GMRES(50), k = 10 from 20
-snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|augment|deflate.
+snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|augment|deflate|oblique.
 
   value      seconds per system (device time, CUDA events on the library's stream), whole job:
              max-over-ranks time / (systems solved by all ranks)
@@ -411,7 +411,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate"])
+    ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate", "oblique"])
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--sell", type=int, default=-1, help="1: pack CSR to SELL-32 inside the library, "
                     "0: keep CSR, -1: config default")

@@ -17,6 +17,12 @@
 // algorithms", 2020, and Bielich et al. 2022 describe the delayed re-orthogonalisation idea; the
 // recycled (Q) bookkeeping here follows the GCRO relation of PAPER.md:332.)  The A Q a_Q term is
 // dropped: a_Q = Q^T u is at rounding level because u was projected against Q.
+//
+// Oblique variant (operator M_D A, M_D = I - C E^{-1} W^T, C = A W in columns [k, 2k)): DK1 also
+// reduces W^T y and C^T u; the epilogue forms t = E^{-1} W^T y, appends the row v_j^T C =
+// (C^T u - (V_j^T C)^T a)/nu to the maintained V^T C (state Gm), and corrects the first-pass
+// coefficients by -(V_{j+1}^T C) t / nu; DK2 adds -C t / nu to the next u.  No extra pass or
+// reduction: M_D A v_j is never formed explicitly.
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
@@ -24,12 +30,16 @@ namespace rg {
 namespace {
 
 constexpr int DT = 512;
+// values one DK1 reduction returns: [a | b] over P = [Q | V] (<= MAXK + MAXM columns each), u.u,
+// u.y and up to 2 MAXK extras; also the row stride of its partials (fits the partial buffer)
+constexpr int DK1RED = 2 * (MAXK + MAXM) + 2 + 2 * MAXK;
 
 // ---------------------------------------------------------------- DK1 epilogue
-// tot = [a (p) | b (p) | s | g | q (k, augment)],  P = columns [lo, VB + j).
+// tot = [a (p) | b (p) | s | g | q (k, augment) or W^T y (k), C^T u (k) (oblique)],
+// P = columns [lo, VB + j).
 __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p) {
   __shared__ double lst[MAXK + 2];
-  __shared__ double Ha[MAXM + 2], Ba[MAXK];
+  __shared__ double Ha[MAXM + 2], Ba[MAXK], ob_t[MAXK], ob_ct[MAXM + 2];
   __shared__ double s_nu, s_d, s_aj;
   __shared__ int s_go;
   const int tid = threadIdx.x, bd = blockDim.x;
@@ -86,6 +96,31 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   }
   // ---- coefficients of DK2 and the first-pass coefficients of column j
   const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
+  const bool obl = var == RG_OBLIQUE && k > 0;
+  if (obl) {
+    const double* wy = tot + 2 * p + 2;  // W^T y
+    const double* cu = wy + k;           // C^T u
+    for (int l = tid; l < k; l += bd) {
+      double t = 0.0;
+      for (int b2 = 0; b2 < k; ++b2) t += st->Einv[b2][l] * wy[b2];
+      ob_t[l] = t;
+      double g = cu[l];                  // v_j^T C = (u - V_j a)^T C / nu
+      for (int i = 0; i < j; ++i) g -= a[i] * st->Gm[i][l];
+      st->Gm[j][l] = g * inv;
+    }
+    __syncthreads();
+    {
+      const int lane = tid & 31, nw = bd >> 5;
+      for (int i = tid >> 5; i <= j; i += nw) {  // ct_i = (V^T C t)_i
+        double s = 0.0;
+        for (int l = lane; l < k; l += 32) s += st->Gm[i][l] * ob_t[l];
+        s = warp_sum(s);
+        if (lane == 0) ob_ct[i] = s;
+      }
+    }
+    for (int l = tid; l < k; l += bd) st->coef[k + l] = -ob_t[l] * inv;
+    __syncthreads();
+  }
   // (H a_V)_c over the final columns 0..j-1 (Hessenberg) and (B a_V)_l: one warp per output,
   // lanes over the summation index (all loads of a warp in flight), fixed shuffle tree.
   {
@@ -109,7 +144,7 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   if (tid == 0) {
     const double aj = j >= 1 ? a[nq + j - 1] : 0.0;
     s_aj = aj;
-    s_d = ((gg - ab) * inv - nu * aj) * inv;  // v_j^T w
+    s_d = ((gg - ab) * inv - nu * aj - (obl ? ob_ct[j] : 0.0)) * inv;  // v_j^T w
     st->k2_inv_nu = inv;
     st->k2_y = inv;
     st->k2_u_next = -(aj + s_d) * inv;
@@ -118,7 +153,7 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   __syncthreads();
   const double f = (s_aj + s_d) * inv;
   for (int c = tid; c < j; c += bd) {  // V columns
-    const double cv = (b[nq + c] - Ha[c]) * inv;
+    const double cv = (b[nq + c] - Ha[c] - (obl ? ob_ct[c] : 0.0)) * inv;
     st->hcol[VB + c] = cv;
     st->coef[VB + c] = -Ha[c] * inv - cv + f * a[nq + c];
     st->coefv[VB + c] = -a[nq + c] * inv;
@@ -137,14 +172,14 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
 // tree, warp-owned shared-memory accumulators (deterministic).
 __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned long long cond) {
   __shared__ double us[DT], ys[DT];
-  __shared__ double dpart[MAXRED];
-  __shared__ double tot[MAXRED];
+  __shared__ double dpart[DK1RED];
+  __shared__ double tot[DK1RED];
   __shared__ double bsh[33];
   if (!st->active) { prof_noop(st, K_DK1); return; }
   prof_begin(st, K_DK1);
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
-  const int nqd = (var == RG_AUGMENT) ? k : 0;  // extra Q^T u dots
+  const int nqd = (var == RG_AUGMENT) ? k : (var == RG_OBLIQUE ? 2 * k : 0);  // extra dots
   const bool have_y = j < st->m;                // no SpMV was run at j == m
   const bool keep = L.keep_l2 != 0;  // basis fits L2: let DK2 re-hit what DK1 streamed
   const int64_t ld = L.ld;
@@ -172,7 +207,8 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
     __syncthreads();
     const int cnt = (int)((r1 - base) < DT ? (r1 - base) : DT);
     for (int c = wid; c < p + nqd; c += 16) {
-      const int col = c < p ? lo + c : QB + (c - p);
+      const bool obl = var == RG_OBLIQUE;  // extras: W^T y (cols [0,k)), C^T u (cols [k,2k))
+      const int col = c < p ? lo + c : (obl ? c - p : QB + (c - p));
       const double* __restrict__ zc = Z + (int64_t)col * ld + base + lane;
       double zv[RPL];
 #pragma unroll
@@ -190,8 +226,10 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
           dpart[c] += su;
           dpart[p + c] += sy;
         }
-      } else if (lane == 0) {
-        dpart[2 * p + 2 + (c - p)] += su;
+      } else {
+        const bool wy = obl && (c - p) < k;
+        if (wy) sy = warp_sum(sy);
+        if (lane == 0) dpart[2 * p + 2 + (c - p)] += wy ? sy : su;
       }
     }
   }
@@ -203,7 +241,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
     dpart[2 * p + 1] = t2;
   }
   __syncthreads();
-  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot)) return;
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot, DK1RED)) return;
   prof_tail(st, K_DK1);
   epi_dcgs(st, L, tot, p);
   if (threadIdx.x == 0) {
@@ -215,7 +253,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
 
 // ---------------------------------------------------------------- DK2: v_j and the next u
 __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
-  __shared__ double cv[MAXCOL], cn[MAXCOL];
+  __shared__ double cv[MAXCOL], cn[MAXCOL], cc2[MAXK];
   if (!st->active) { prof_noop(st, K_DK2); return; }
   prof_begin(st, K_DK2);
   const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
@@ -229,6 +267,8 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
     cv[c] = st->coefv[lo + c];
     cn[c] = st->coef[lo + c];
   }
+  const int k2 = var == RG_OBLIQUE ? k : 0;  // oblique: next u also gets -C t / nu (C = cols [k, 2k))
+  for (int l = threadIdx.x; l < k2; l += DT) cc2[l] = st->coef[k + l];
   const double inv = st->k2_inv_nu, fy = st->k2_y, fu = st->k2_u_next;
   __syncthreads();
   const int64_t ng = ld >> 5;
@@ -253,10 +293,11 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
       sv += cv[c] * z;
       sn += cn[c] * z;
     }
+    for (int l = 0; l < k2; ++l) sn += cc2[l] * (keep ? Z[(int64_t)(k + l) * ld + r] : __ldcs(Z + (int64_t)(k + l) * ld + r));
     u[r] = ur * inv + sv;
     y[r] = yr * fy + ur * fu + sn;
   }
-  if (st->profile && grid_last(L.counter) && threadIdx.x == 0) prof_end(st, K_DK2, 8.0 * (double)L.n * (p + 4));
+  if (st->profile && grid_last(L.counter) && threadIdx.x == 0) prof_end(st, K_DK2, 8.0 * (double)L.n * (p + k2 + 4));
 }
 
 }  // namespace

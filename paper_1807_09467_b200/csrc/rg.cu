@@ -362,7 +362,7 @@ cudaError_t cycle_start(rg_ctx* c, int variant) {
 cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
   cudaError_t e;
   if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
-  if (c->cur_var == RG_OBLIQUE) {  // w = M_D A v_j = A v_j - C E^{-1} W^T A v_j
+  if (c->cur_var == RG_OBLIQUE && !c->dcgs_now) {  // w = M_D A v_j = A v_j - C E^{-1} W^T A v_j
     if ((e = launch_orth(c->L, c->st, OP_OB_SD, c->stream)) != cudaSuccess) return e;
     if ((e = launch_orth(c->L, c->st, OP_OB_SU, c->stream)) != cudaSuccess) return e;
   }
@@ -711,7 +711,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     check_c = true;
   }
   c->cur_var = eff;
-  c->dcgs_now = c->use_dcgs && eff != RG_OBLIQUE;
+  c->dcgs_now = c->use_dcgs;
   if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
   if (x0) {
     if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;

@@ -349,3 +349,52 @@ def test_singular_recycle_operator_reported(variant, rng):
     with pytest.raises(rgb.RgError) as e:
         ctx.export(0, W)                             # cleared
     assert e.value.status == rgb.RG_E_STATE
+
+
+@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
+def test_dcgs2_and_cgs2_paths_agree(variant, rng):
+    """Delayed CGS2 (one reduction per step; the oblique projection folded into its coefficients)
+    and classical CGS2 (explicit M_D A v_j) give the same iterates."""
+    from paper_1807_09467_b200 import rg as rgb
+    cfg = synth.CONFIGS["C2"].reduced(160)
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    hm = seq.matrix(1, u)
+    b = seq.rhs(1, u)
+    snaps = [rng.standard_normal(cfg.n) for _ in range(6)]
+    out = []
+    for flags in (rgb.RG_FLAG_NO_PERSIST, rgb.RG_FLAG_CGS2):
+        ctx = make_ctx(hm, max_m=cfg.m, s=8, k=6, flags=flags)
+        for v in snaps:
+            ctx.push_snapshot(t(v))
+        ctx.build_recycle(6)
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=cfg.m, variant=variant, history_cap=1000)
+        out.append((rep, x.cpu().numpy()))
+        ctx.close()
+    (r0, x0), (r1, x1) = out
+    assert r0["converged"] and r1["converged"]
+    assert abs(r0["iterations"] - r1["iterations"]) <= 1
+    assert np.linalg.norm(x0 - x1) <= 1e-8 * np.linalg.norm(x1)
+
+
+@pytest.mark.parametrize("variant,k", [("plain", 0), ("augment", 64), ("deflate", 64), ("oblique", 32)])
+def test_maximum_restart_and_recycle_dimension(variant, k, rng):
+    """max_m = 128 and max_k = 64 (32 for oblique): the largest reductions ([Q|V] dots of 2(k+m)+2
+    values) and the largest least-squares state, against the oracle."""
+    n, m = 3000, 128
+    hm = random_csr(n, rng, per_row=(2, 8), diag=1.3)
+    kk = max(k, 1)
+    W = np.linalg.qr(rng.standard_normal((n, kk)))[0]
+    b = rng.standard_normal(n)
+    ctx = make_ctx(hm, max_m=m, s=64, k=64)
+    if k:
+        for i in range(k):
+            ctx.push_snapshot(t(W[:, i] * (k - i)))
+        assert ctx.build_recycle(k)[0] == k
+    x = torch.zeros(n, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), x, m=m, variant=variant, tol=1e-10, history_cap=5000)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=m, variant=variant, W=W if k else None, tol=1e-10)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["iterations"] - ref["iterations"]) <= 2
+    assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
