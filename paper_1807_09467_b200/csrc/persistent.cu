@@ -1,4 +1,5 @@
-// persistent.cu — the whole restarted solve in ONE cooperative kernel (plain / deflate, CSR / SELL).
+// persistent.cu — the whole restarted solve in ONE cooperative kernel (plain / deflate / oblique,
+// CSR / SELL).
 //
 // Why: at the sizes of configs C1-C2 every kernel boundary of the graph path costs a launch ramp
 // plus a single-CTA epilogue tail (~10 us per Arnoldi step).  Here every CTA of a co-resident grid
@@ -8,6 +9,8 @@
 // see dcgs.cu): barrier, SpMV y = A u + local dots [P^T u, P^T y, u.u, u.y], two-barrier
 // deterministic reduction, replicated epilogue, row update of v_j and the next u.
 // CTA 0 alone writes the solve report (iterations, history, status) to the device state.
+// Oblique (obl): P = V only; the Galerkin cycle start and the M_D projection folded into the DCGS2
+// coefficients exactly as dcgs.cu does it (V^T C replicated in shared memory).
 #include "epilogue.cuh"
 #include "kernels.cuh"
 #include <cstdlib>
@@ -27,6 +30,7 @@ struct PArgs {
   double* tot_g;        // reduced totals (MAXRED)
   unsigned* bar;        // [0] arrival count, [1] generation
   int m, k;             // m <= PM, k <= PK (k = 0: plain)
+  int obl;              // oblique variant (k = k_eff > 0, C = A W in columns [k, 2k))
 };
 
 // ---- grid barrier (all CTAs co-resident: cooperative launch).  Spins with a timeout so that a
@@ -143,14 +147,17 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   const Layout& L = pa.L;
   const MatDev& A = pa.A;
   DevState* st = pa.st;
-  const int m = pa.m, k = pa.k, VB = L.VB, QB = VB - k, lo = QB, nq = k;
+  const int m = pa.m, k = pa.k, VB = L.VB, QB = VB - k;
+  const bool obl = pa.obl != 0;
+  const int lo = obl ? VB : QB, nq = obl ? 0 : k;  // P = [Q | V] (deflate) or V (plain, oblique)
+  const int nx = obl ? 2 * k : 0;                   // extra dots per step: W^T y, C^T u
   const int64_t ld = L.ld;
   double* Z = L.Z;
   // ---- shared-memory layout (replicated least-squares state + staging)
   double* Hs = sm;                           // [m][m+2]  H(r, i) = Hs[i*(m+2) + r]
   double* Rs = Hs + m * (m + 2);             // [m][m+1]
-  double* Bs = Rs + m * (m + 1);             // [m][k]    B(l, i) = Bs[i*k + l]
-  double* cs = Bs + m * (k > 0 ? k : 1);
+  double* Bs = Rs + m * (m + 1);             // [m+1][k]  B(l, i) = Bs[i*k + l]; oblique: (V^T C)(i, l)
+  double* cs = Bs + (m + 1) * (k > 0 ? k : 1);
   double* sn = cs + PM;
   double* gg = sn + PM;                      // PM + 2
   double* h1 = gg + PM + 2;                  // PCOL: first-pass coefficients of the pending column
@@ -223,6 +230,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       if (cta0) bytes += A.bytes + 8.0 * L.n;
     }
     if (k > 0) {  // LS projection onto span(W): a = Q^T r, x += W R_C^{-1} a, r -= Q a
+                  // (oblique: Galerkin start a = W^T r, t = E^{-1} a, x += W t, r -= C t)
       for (int c = tid; c < k; c += PT) dpart[c] = 0.0;
       __syncthreads();
       for (int64_t base = r0; base < r1; base += PT) {
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         __syncthreads();
         const int cnt = (int)min((int64_t)PT, r1 - base);
         for (int c = wid; c < k; c += PT / 32) {
-          const double* zc = Z + (int64_t)(QB + c) * ld + base;
+          const double* zc = Z + (int64_t)((obl ? 0 : QB) + c) * ld + base;
           double s = 0.0;
           for (int q = lane; q < cnt; q += 32) s += zc[q] * us[q];
           s = warp_sum(s);
@@ -240,18 +248,24 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         __syncthreads();
       }
       if (!greduce(dpart, k, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
-      for (int l = tid; l < k; l += PT) {  // z = R_C^{-1} a
+      for (int l = tid; l < k; l += PT) {  // z = R_C^{-1} a  (oblique: t = E^{-1} a)
         double s = 0.0;
-        for (int c = l; c < k; ++c) s += st->RCinv[c][l] * tot[c];
+        if (obl) {
+          for (int c = 0; c < k; ++c) s += st->Einv[c][l] * tot[c];
+        } else {
+          for (int c = l; c < k; ++c) s += st->RCinv[c][l] * tot[c];
+        }
         zk[l] = s;
       }
       __syncthreads();
+      const double* rq = obl ? zk : tot;            // r -= Q a  or  r -= C t
+      const int rb = obl ? k : QB;
       double s2 = 0.0;
       for (int64_t r = r0 + tid; r < r1; r += PT) {
         double xr = x[r], rr = u0[r];
         for (int l = 0; l < k; ++l) {
           xr += zk[l] * Z[(int64_t)l * ld + r];
-          rr -= tot[l] * Z[(int64_t)(QB + l) * ld + r];
+          rr -= rq[l] * Z[(int64_t)(rb + l) * ld + r];
         }
         x[r] = xr;
         u0[r] = rr;
@@ -282,7 +296,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       unsigned long long tph = (st->profile && cta0 && tid == 0) ? gtimer() : 0ull;
       if (j > 0 && !gbar(pa.bar, &s_fail)) goto fail;  // u complete
       ptick(st, K_PB1, tph);
-      const int nv = 2 * p + 2;
+      const int nv = 2 * p + 2 + nx;
       for (int c = tid; c < nv; c += PT) dpart[c] = 0.0;
       double s_uu = 0.0, s_uy = 0.0;
       if (have_y)  // SpMV over this CTA's rows first (many rows in flight), then the dot pass
@@ -302,8 +316,8 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         __syncthreads();
         const int cnt = (int)min((int64_t)PT, r1 - base);
         constexpr int RPL = PT / 32;
-        for (int c = wid; c < p; c += PT / 32) {
-          const double* zc = Z + (int64_t)(lo + c) * ld + base + lane;
+        for (int c = wid; c < p + nx; c += PT / 32) {
+          const double* zc = Z + (int64_t)(c < p ? lo + c : c - p) * ld + base + lane;
           double zv[RPL];
 #pragma unroll
           for (int q = 0; q < RPL; ++q)  // 16 independent loads in flight per lane
@@ -317,8 +331,12 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
           su = warp_sum(su);
           sy = warp_sum(sy);
           if (lane == 0) {
-            dpart[c] += su;
-            dpart[p + c] += sy;
+            if (c < p) {
+              dpart[c] += su;
+              dpart[p + c] += sy;
+            } else {  // oblique extras: [W^T y (k) | C^T u (k)] after [a | b | s | g]
+              dpart[2 * p + 2 + (c - p)] += (c - p) < k ? sy : su;
+            }
           }
         }
       }
@@ -331,7 +349,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       ptick(st, K_PB2, tph);
       if (!greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
       ptick(st, K_PB3, tph);
-      if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + 2);
+      if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + nx + 2);
       // ---- replicated epilogue: delayed second pass, column j-1, least squares
       const double* a = tot;
       const double* bb = tot + p;
@@ -392,7 +410,29 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
       const double aj = j >= 1 ? a[nq + j - 1] : 0.0;
       const double d = ((gm - ab) * inv - nu * aj) * inv;
-      const double f = (aj + d) * inv;
+      if (obl) {  // t = E^{-1} W^T y -> wk[0,k) = -t/nu (C coefficients of the next u); row j of V^T C
+        const double* wy = tot + 2 * p + 2;
+        const double* cu = wy + k;
+        for (int l = tid; l < k; l += PT) {
+          double t = 0.0;
+          for (int c = 0; c < k; ++c) t += st->Einv[c][l] * wy[c];
+          zk[l] = t;
+          double g = cu[l];
+          for (int i = 0; i < j; ++i) g -= a[i] * Bs[i * k + l];
+          Bs[j * k + l] = g * inv;
+        }
+        __syncthreads();
+        for (int i = wid; i <= j; i += PT / 32) {  // ct_i = (V^T C t)_i -> ys[i] (free until cycle end)
+          double s = 0.0;
+          for (int l = lane; l < k; l += 32) s += Bs[i * k + l] * zk[l];
+          s = warp_sum(s);
+          if (lane == 0) ys[i] = s;
+        }
+        for (int l = tid; l < k; l += PT) wk[l] = -zk[l] * inv;
+        __syncthreads();
+      }
+      const double dob = obl ? ((gm - ab) * inv - nu * aj - ys[j]) * inv : d;
+      const double f = (aj + dob) * inv;
       for (int o = wid; o < j + nq; o += PT / 32) {  // (H a_V)_c and (B a_V)_l
         double s = 0.0;
         if (o < j) {
@@ -406,7 +446,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       __syncthreads();
       for (int c = tid; c < j; c += PT) {
         const double Ha = wk[PK + c];
-        const double cvv = (bb[nq + c] - Ha) * inv;
+        const double cvv = (bb[nq + c] - Ha - (obl ? ys[c] : 0.0)) * inv;
         cn[nq + c] = -Ha * inv - cvv + f * a[nq + c];
         cv[nq + c] = -a[nq + c] * inv;
         h1[nq + c] = cvv;
@@ -416,11 +456,11 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         cv[l] = -a[l] * inv;
         h1[l] = (bb[l] - wk[l]) * inv;
       }
-      if (tid == 0) h1[nq + j] = d;
+      if (tid == 0) h1[nq + j] = dob;
       __syncthreads();
       ptick(st, K_PB4, tph);
-      // ---- update pass: v_j = u/nu + P cv, u_next = y/nu - f u + P cn  (own rows)
-      const double fu = -(aj + d) * inv;
+      // ---- update pass: v_j = u/nu + P cv, u_next = y/nu - f u + P cn (- C t/nu)  (own rows)
+      const double fu = -(aj + dob) * inv;
       for (int64_t r = r0 + tid; r < r1; r += PT) {
         const double ur = u[r], yr = y[r];
         double sv = 0.0, sn2 = 0.0;
@@ -443,10 +483,12 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
           sv += cv[c] * z;
           sn2 += cn[c] * z;
         }
+        if (obl)
+          for (int l = 0; l < k; ++l) sn2 += wk[l] * Z[(int64_t)(k + l) * ld + r];
         u[r] = ur * inv + sv;
         y[r] = yr * inv + ur * fu + sn2;
       }
-      if (cta0) bytes += 8.0 * L.n * (p + 4);
+      if (cta0) bytes += 8.0 * L.n * (p + (obl ? k : 0) + 4);
       __syncthreads();
       ptick(st, K_PB5, tph);
     }
@@ -460,7 +502,8 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         }
       }
       __syncthreads();
-      if (k > 0) {
+      const int kx = obl ? 0 : k;  // oblique: x += V y (the next cycle start applies the W part)
+      if (kx > 0) {
         for (int l = tid; l < k; l += PT) {
           double s = 0.0;
           for (int i = 0; i <= jf; ++i) s += Bs[i * k + l] * ys[i];
@@ -477,10 +520,10 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       for (int64_t r = r0 + tid; r < r1; r += PT) {
         double xr = x[r];
         for (int i = 0; i <= jf; ++i) xr += ys[i] * Z[(int64_t)(VB + i) * ld + r];
-        for (int l = 0; l < k; ++l) xr -= zk[l] * Z[(int64_t)l * ld + r];
+        for (int l = 0; l < kx; ++l) xr -= zk[l] * Z[(int64_t)l * ld + r];
         x[r] = xr;
       }
-      if (cta0) bytes += 8.0 * L.n * (jf + 1 + k + 2);
+      if (cta0) bytes += 8.0 * L.n * (jf + 1 + kx + 2);
     }
     if (status) break;
   }
@@ -509,14 +552,14 @@ fail:
 }  // namespace
 
 size_t persistent_smem(int m, int k) {
-  return sizeof(double) * ((size_t)m * (m + 2) + (size_t)m * (m + 1) + (size_t)m * (k > 0 ? k : 1) + 2 * PM +
+  return sizeof(double) * ((size_t)m * (m + 2) + (size_t)m * (m + 1) + (size_t)(m + 1) * (k > 0 ? k : 1) + 2 * PM +
                            (PM + 2) + 3 * PCOL + 2 * PT + 2 * MAXRED + (PM + 2) + 2 * PK + PM + 2);
 }
 
 // Returns cudaErrorNotSupported when the configuration is outside this path.
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar, int m,
                               int k, int variant, cudaStream_t s) {
-  if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE) || A.fmt == 2)
+  if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE && variant != RG_OBLIQUE) || A.fmt == 2)
     return cudaErrorNotSupported;
   const size_t smem = persistent_smem(m, k);
   static int max_smem = -1;
@@ -535,7 +578,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : 2;
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_DEFLATE ? k : 0};
+  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k, variant == RG_OBLIQUE && k > 0 ? 1 : 0};
   void* args[] = {&pa};
   return cudaLaunchCooperativeKernel((const void*)k_solve_persistent, dim3(G), dim3(PT), args, smem, s);
 }

@@ -240,7 +240,7 @@ def test_recycle_operator_thin_qr(name, N, sell, rng):
     assert np.allclose(np.tril(R, -1), 0.0)
 
 
-@pytest.mark.parametrize("variant", ["plain", "deflate"])
+@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique"])
 def test_persistent_and_graph_paths_agree(variant, rng):
     """The single cooperative-kernel solve and the CUDA-graph solve compute the same iterates
     (same DCGS2 arithmetic, different reduction trees): same iteration counts, x within 1e-10."""
