@@ -14,6 +14,11 @@ Parity status of each function:
                       space K_j(M_D A, M_D r_0), rows 2 = 5 (eq. equivalence_oblique), b = A W c
                       special case, W^T r = 0 on return, dense LU solution; obproj pinned by the
                       projector's defining properties (M_D A W = 0, W^T M_D = 0, M_D^2 = M_D, rank)
+  ssor / solve(precond) pinned: M^{-1} equals the inverse of the explicitly assembled SSOR matrix
+                      (D + wL) D^{-1} (D + wU)/(w(2-w)) of the permuted matrix, w = 1 diagonal A
+                      closed form, symmetric A -> symmetric M^{-1}, triangular A in the order ->
+                      forward sweep exact; right-preconditioned solves = lstsq over the explicit
+                      space x_c + [span W] + M^{-1} K_j(op A M^{-1}, v) (all variants)
   svd / recycle_basis pinned: [3,4,0] closed form, orthonormal input, Eckart-Young tail,
                       numpy.linalg.svd brute force
 """
@@ -62,6 +67,10 @@ def lib():
         L.or_solve.argtypes = [ctypes.POINTER(_Mat), _f64p, _f64p, ctypes.c_int, ctypes.c_int, _f64p,
                                ctypes.c_int, ctypes.c_double, ctypes.c_int, _f64p, ctypes.POINTER(_Rep),
                                _f64p, ctypes.c_int]
+        L.or_solve_pc.restype = ctypes.c_int
+        L.or_solve_pc.argtypes = L.or_solve.argtypes + [_i32p, ctypes.c_double]
+        L.or_ssor.restype = ctypes.c_int
+        L.or_ssor.argtypes = [ctypes.POINTER(_Mat), _i32p, ctypes.c_double, _f64p, _f64p]
         L.or_lsproj.restype = ctypes.c_int
         L.or_lsproj.argtypes = [ctypes.POINTER(_Mat), _f64p, ctypes.c_int, _f64p, ctypes.c_int]
         L.or_obproj.restype = ctypes.c_int
@@ -121,10 +130,28 @@ def spmv_row(A: Matrix, row: int, x: np.ndarray) -> float:
     return lib().or_spmv_row(ctypes.byref(A._m), int(row), _f(x))
 
 
+def ssor_order(colors):
+    """Row order of a multicolour SSOR: rows sorted by colour, natural order inside a colour."""
+    colors = np.asarray(colors)
+    return np.ascontiguousarray(np.argsort(colors, kind="stable"), dtype=np.int32)
+
+
+def ssor(A: Matrix, order, omega, z):
+    """M^{-1} z for SSOR(omega) in the given row order (oracle.c or_ssor)."""
+    order = np.ascontiguousarray(order, dtype=np.int32)
+    z = np.ascontiguousarray(z, dtype=np.float64)
+    out = np.empty(A.n)
+    if lib().or_ssor(ctypes.byref(A._m), order.ctypes.data_as(_i32p), float(omega), _f(z), _f(out)):
+        raise np.linalg.LinAlgError("oracle: zero diagonal entry")
+    return out
+
+
 def solve(A: Matrix, b, x0=None, m=30, variant="plain", W=None, tol=1e-8, max_iters=20000,
-          hist_cap=None):
-    """Restarted min-residual solve (plain / augment / deflate).  W: n x k array (columns span the
-    recycle space) or None.  Returns dict(x, iterations, cycles, converged, rel_residual, history)."""
+          hist_cap=None, precond=None):
+    """Restarted min-residual solve (plain / augment / deflate / oblique / oblique_aug).  W: n x k
+    array (columns span the recycle space) or None.  precond: None or (order, omega) = right SSOR
+    preconditioner in that row order.  Returns dict(x, iterations, cycles, converged, rel_residual,
+    history)."""
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     b = np.ascontiguousarray(b, dtype=np.float64)
     x = np.empty(A.n)
@@ -143,12 +170,18 @@ def solve(A: Matrix, b, x0=None, m=30, variant="plain", W=None, tol=1e-8, max_it
     if x0 is not None:
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
         x0p = _f(x0)
-    st = lib().or_solve(ctypes.byref(A._m), _f(b), x0p, int(m), v,
-                        Wf.ctypes.data_as(_f64p) if Wf is not None and k > 0 else None, k, float(tol),
-                        int(max_iters), _f(x), ctypes.byref(rep), _f(hist), hist_cap)
+    args = [ctypes.byref(A._m), _f(b), x0p, int(m), v, Wf.ctypes.data_as(_f64p) if Wf is not None and k > 0 else None,
+            k, float(tol), int(max_iters), _f(x), ctypes.byref(rep), _f(hist), hist_cap]
+    if precond is None:
+        st = lib().or_solve(*args)
+    else:
+        order = np.ascontiguousarray(precond[0], dtype=np.int32)
+        st = lib().or_solve_pc(*args, order.ctypes.data_as(_i32p), float(precond[1]))
     if st == 1:
         raise np.linalg.LinAlgError("oracle: A W is (numerically) rank deficient" if v < OBLIQUE
                                     else "oracle: E = W^T A W is (numerically) singular")
+    if st == 3:
+        raise np.linalg.LinAlgError("oracle: zero diagonal entry (SSOR)")
     if st != 0:
         raise MemoryError("oracle: allocation failed")
     return dict(x=x, iterations=rep.iterations, cycles=rep.cycles, converged=bool(rep.converged),

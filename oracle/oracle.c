@@ -24,6 +24,12 @@
  *               A*[W, v_0..v_j] is grown by modified Gram-Schmidt applied twice (MGS2), the residual
  *               is r - U_Z U_Z^T r and the coefficients are R_Z^{-1} U_Z^T r.  This is the plain
  *               definition, not the GPU's Hessenberg/Givens/GCRO algebra.
+ *   - or_ssor / or_solve_pc: SSOR(omega) preconditioner ("Symmetric Successive Over-Relaxation")
+ *               in a given row ORDER (a permutation: the GPU's multicolour ordering is one such
+ *               order), M = (D + wL) D^{-1} (D + wU) / (w(2-w)) with L/U the parts of A before/after
+ *               each row in that order; applied as a RIGHT preconditioner ("A M y = b,
+ *               x = M^{-1} y"): every Krylov direction v enters the search space as M^{-1} v and the
+ *               Krylov operator is (projector) A M^{-1}.  DESIGN.md reading R18.
  *   - or_svd:   thin SVD by one-sided (Hestenes) Jacobi directly on X, long-double dot products;
  *               sorted non-increasing; rank = #{sigma > 1e-12 sigma_1} (PAPER.md:524-537, 552-553,
  *               Algorithm 1; Schmidt-Eckart-Young eq. opt_svd).
@@ -123,15 +129,111 @@ static void residual(const or_mat* A, const double* b, const double* x, double* 
   for (int64_t i = 0; i < A->n; ++i) r[i] = b[i] - r[i];
 }
 
+/* SSOR preconditioner in a row order: order[idx] = row processed idx-th (a permutation of 0..n-1). */
+typedef struct {
+  const int32_t* order;
+  double omega;
+  int32_t* pos;      /* pos[order[idx]] = idx */
+  double* tmp;       /* n scratch */
+} or_prec;
+
+/* out = M^{-1} z, M = (D + wL) D^{-1} (D + wU) / (w(2-w)) in the order of pc (Saad, "Iterative
+ * Methods for Sparse Linear Systems", SSOR preconditioner): forward sweep w = (D + wL)^{-1} w(2-w) z,
+ * then backward sweep t = (D + wU)^{-1} D w.  CSR only.  Returns 0, or 3 if a diagonal entry is
+ * missing or zero. */
+static int ssor_apply(const or_mat* A, const or_prec* pc, const double* z, double* out) {
+  const int64_t n = A->n;
+  const double om = pc->omega, sc = om * (2.0 - om);
+  for (int64_t idx = 0; idx < n; ++idx) {          /* forward: rows in order */
+    const int32_t r = pc->order[idx];
+    double s = sc * z[r], d = 0.0;
+    for (int32_t p = A->rp[r]; p < A->rp[r + 1]; ++p) {
+      const int32_t j = A->ci[p];
+      if (j == r) d = A->v[p];
+      else if (pc->pos[j] < idx) s -= om * A->v[p] * out[j];
+    }
+    if (d == 0.0) return 3;
+    out[r] = s / d;
+  }
+  for (int64_t idx = n - 1; idx >= 0; --idx) {     /* backward: rows in reverse order */
+    const int32_t r = pc->order[idx];
+    double s = 0.0, d = 0.0;
+    for (int32_t p = A->rp[r]; p < A->rp[r + 1]; ++p) {
+      const int32_t j = A->ci[p];
+      if (j == r) d = A->v[p];
+      else if (pc->pos[j] > idx) s += om * A->v[p] * out[j];
+    }
+    out[r] = (d * out[r] - s) / d;
+  }
+  return 0;
+}
+
+/* y = A M^{-1} v (pc != NULL) or A v */
+static int op_apply(const or_mat* A, const or_prec* pc, const double* v, double* y) {
+  if (!pc) { or_spmv(A, v, y); return 0; }
+  int st = ssor_apply(A, pc, v, pc->tmp);
+  or_spmv(A, pc->tmp, y);
+  return st;
+}
+
+/* x += M^{-1} (V c) over q columns of V (n x q, column-major); scratch t (n) */
+static int add_krylov_part(const or_mat* A, const or_prec* pc, const double* V, const double* c, int q,
+                           double* t, double* x) {
+  const int64_t n = A->n;
+  if (!pc) {
+    for (int i = 0; i < q; ++i) axpy(n, c[i], V + (int64_t)i * n, x);
+    return 0;
+  }
+  memset(t, 0, sizeof(double) * n);
+  for (int i = 0; i < q; ++i) axpy(n, c[i], V + (int64_t)i * n, t);
+  int st = ssor_apply(A, pc, t, pc->tmp);
+  axpy(n, 1.0, pc->tmp, x);
+  return st;
+}
+
 static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2,
                          const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
-                         double* hist, int hist_cap);
+                         double* hist, int hist_cap, const or_prec* pc);
+static int solve_impl(const or_mat* A, const double* b, const double* x0, int m, int variant,
+                      const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+                      double* hist, int hist_cap, const or_prec* pc);
 
 int or_solve(const or_mat* A, const double* b, const double* x0, int m, int variant,
              const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
              double* hist, int hist_cap) {
+  return solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, NULL);
+}
+
+/* or_solve with a right SSOR(omega) preconditioner in the row order `order` (NULL: none). */
+int or_solve_pc(const or_mat* A, const double* b, const double* x0, int m, int variant,
+                const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+                double* hist, int hist_cap, const int32_t* order, double omega) {
+  if (!order) return solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, NULL);
+  or_prec pc = {order, omega, malloc(sizeof(int32_t) * A->n), malloc(sizeof(double) * A->n)};
+  int st = 2;
+  if (pc.pos && pc.tmp) {
+    for (int64_t i = 0; i < A->n; ++i) pc.pos[order[i]] = (int32_t)i;
+    st = solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, &pc);
+  }
+  free(pc.pos); free(pc.tmp);
+  return st;
+}
+
+/* out = M^{-1} z for the SSOR(omega) preconditioner in row order `order` (0, or 3: zero diagonal) */
+int or_ssor(const or_mat* A, const int32_t* order, double omega, const double* z, double* out) {
+  or_prec pc = {order, omega, malloc(sizeof(int32_t) * A->n), NULL};
+  if (!pc.pos) return 2;
+  for (int64_t i = 0; i < A->n; ++i) pc.pos[order[i]] = (int32_t)i;
+  int st = ssor_apply(A, &pc, z, out);
+  free(pc.pos);
+  return st;
+}
+
+static int solve_impl(const or_mat* A, const double* b, const double* x0, int m, int variant,
+                      const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+                      double* hist, int hist_cap, const or_prec* pc) {
   if ((variant == 3 || variant == 4) && W != NULL && k > 0)
-    return solve_oblique(A, b, x0, m, variant == 4, W, k, tol, max_iters, x, rep, hist, hist_cap);
+    return solve_oblique(A, b, x0, m, variant == 4, W, k, tol, max_iters, x, rep, hist, hist_cap, pc);
   if (variant == 3 || variant == 4) variant = 0;   /* no recycle space: plain GMRES */
   const int64_t n = A->n;
   memset(rep, 0, sizeof(*rep));
@@ -206,7 +308,7 @@ int or_solve(const or_mat* A, const double* b, const double* x0, int m, int vari
     int q = kk;   /* current image-basis size */
     for (int j = 0; j < m; ++j) {
       double* vj = V + (int64_t)j * n;
-      or_spmv(A, vj, w);                    /* w = A v_j */
+      if (op_apply(A, pc, vj, w)) { rep->status = 3; goto out; }  /* w = A v_j  (A M^{-1} v_j) */
       /* image column A v_j -> U_Z by MGS2 */
       memcpy(z, w, sizeof(double) * n);
       double wn = nrm2(n, w);
@@ -235,7 +337,7 @@ int or_solve(const or_mat* A, const double* b, const double* x0, int m, int vari
       /* coefficients over the search basis [W, v_0, ..., v_{q-kk-1}] */
       backsolve(q, RZ, qmax + 1, e, c);
       for (int l = 0; l < kk; ++l) axpy(n, c[l], W + (int64_t)l * n, x);
-      for (int i = kk; i < q; ++i) axpy(n, c[i], V + (int64_t)(i - kk) * n, x);
+      add_krylov_part(A, pc, V, c + kk, q - kk, z, x);   /* x += (M^{-1}) V c_V */
       break;
     }
   }
@@ -361,7 +463,7 @@ static void ob_galerkin(const or_mat* A, const oblique_ctx* o, const double* b, 
  * identity eq. equivalence_oblique). */
 static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2,
                          const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
-                         double* hist, int hist_cap) {
+                         double* hist, int hist_cap, const or_prec* pc) {
   const int64_t n = A->n;
   memset(rep, 0, sizeof(*rep));
   rep->k_used = k;
@@ -403,7 +505,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
     for (int64_t i = 0; i < n; ++i) V[i] = w[i] / v0n;
     int q = 0;
     for (int j = 0; j < m; ++j) {
-      or_spmv(A, V + (int64_t)j * n, w);              /* w = M_D A v_j */
+      if (op_apply(A, pc, V + (int64_t)j * n, w)) { rep->status = 3; goto out; }  /* w = M_D A (M^{-1}) v_j */
       ob_apply(&o, w, t);
       memcpy(z, w, sizeof(double) * n);
       double wn = nrm2(n, w);
@@ -428,7 +530,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
         continue;
       }
       backsolve(q, RZ, m + 1, e, c);
-      for (int i = 0; i < q; ++i) axpy(n, c[i], V + (int64_t)i * n, x);
+      add_krylov_part(A, pc, V, c, q, z, x);          /* x += (M^{-1}) V c */
       break;
     }
   }

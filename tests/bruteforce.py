@@ -20,11 +20,28 @@ def _orth_append(K, v):
     return [Q[:, i] for i in range(Q.shape[1])]
 
 
-def restarted_minres(A, b, m, variant="plain", W=None, tol=1e-8, max_iters=2000, x0=None):
-    """x_{c,j} = argmin over x_c (+ span W) + K_j(op, v) of ||b - A x||, cycle by cycle.
+def ssor_matrix(A, order, omega):
+    """The SSOR preconditioner matrix, assembled literally: in the row order `order`,
+    M_p = (D + wL) D^{-1} (D + wU) / (w (2 - w)) with A_p = A[order][:, order] = D + L + U;
+    returned in the original indexing (M[order][:, order] = M_p)."""
+    order = np.asarray(order)
+    Ap = A[np.ix_(order, order)]
+    D = np.diag(np.diag(Ap))
+    L = np.tril(Ap, -1)
+    U = np.triu(Ap, 1)
+    Mp = (D + omega * L) @ np.linalg.inv(D) @ (D + omega * U) / (omega * (2.0 - omega))
+    M = np.empty_like(Mp)
+    M[np.ix_(order, order)] = Mp
+    return M
 
-    op/v: plain, augment -> (A, r_c); deflate -> (P A, P r_c).  Start for recycled variants:
-    x_0 <- x0 + W lstsq(AW, r(x0)).  Returns (x, iterations, history)."""
+
+def restarted_minres(A, b, m, variant="plain", W=None, tol=1e-8, max_iters=2000, x0=None, Minv=None):
+    """x_{c,j} = argmin over x_c (+ span W) + Minv K_j(op, v) of ||b - A x||, cycle by cycle.
+
+    op/v: plain, augment -> (A Minv, r_c); deflate -> (P A Minv, P r_c) (Minv = I without a
+    preconditioner).  Start for recycled variants: x_0 <- x0 + W lstsq(AW, r(x0)).
+    Returns (x, iterations, history)."""
+    Mi = np.eye(A.shape[0]) if Minv is None else Minv
     n = A.shape[0]
     bn = np.linalg.norm(b)
     x = np.zeros(n) if x0 is None else np.array(x0, dtype=float)
@@ -39,12 +56,12 @@ def restarted_minres(A, b, m, variant="plain", W=None, tol=1e-8, max_iters=2000,
         if np.linalg.norm(r) / bn <= tol or iters >= max_iters:
             break
         if variant == "deflate" and rec:
-            op, v = P @ A, P @ r
+            op, v = P @ A @ Mi, P @ r
         else:
-            op, v = A, r
+            op, v = A @ Mi, r
         K = [v / np.linalg.norm(v)]
         for j in range(m):
-            S = np.column_stack(([W[:, i] for i in range(W.shape[1])] if rec else []) + K)
+            S = np.column_stack(([W[:, i] for i in range(W.shape[1])] if rec else []) + [Mi @ q for q in K])
             y = np.linalg.lstsq(A @ S, r, rcond=None)[0]
             res = np.linalg.norm(r - A @ S @ y)
             hist.append(res / bn)
@@ -61,7 +78,7 @@ def oblique_projector(A, W):
     return np.eye(A.shape[0]) - A @ W @ np.linalg.inv(W.T @ A @ W) @ W.T
 
 
-def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False):
+def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False, Minv=None):
     """Table 1 rows 5 (row2=False) / 2 (row2=True) with the Galerkin start at every cycle
     (R15): x_c <- x_c + W E^{-1} W^T r(x_c); z = argmin over K_j(M_D A, v) of
     ||M_D r_c - M_D A z|| with v = M_D r_c (row 5) or r_c (row 2).  Returns (x, iterations, history)."""
@@ -70,7 +87,8 @@ def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False):
     x = np.zeros(n)
     E = W.T @ A @ W
     M = oblique_projector(A, W)
-    MA = M @ A
+    Mi = np.eye(A.shape[0]) if Minv is None else Minv
+    MA = M @ A @ Mi
     hist, iters = [], 0
     while True:
         x = x + W @ np.linalg.solve(E, W.T @ (b - A @ x))
@@ -87,7 +105,7 @@ def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False):
             hist.append(res / bn)
             iters += 1
             if res / bn <= tol or j == m - 1 or iters >= max_iters:
-                x = x + S @ y
+                x = x + Mi @ (S @ y)
                 break
             K = _orth_append(K, MA @ K[-1])
     return x, iters, np.array(hist)
