@@ -165,7 +165,7 @@ class ClockSampler:
 class GpuRun:
     """One replica: the library context plus the device-side sequence generator."""
 
-    def __init__(self, cfg, variant, k, device, stream, profile, sell):
+    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None):
         import torch
 
         import synth
@@ -183,6 +183,8 @@ class GpuRun:
                            fmt="bsr" if cfg.kind == "bsr" else "csr", block=cfg.B if cfg.kind == "bsr" else 1,
                            sell_C=32 if sell else 0, max_m=cfg.m, max_snapshots=cfg.s,
                            max_k=max(k, 1), stream=stream.cuda_stream, flags=flags)
+        if precond:
+            self.ctx.set_preconditioner("ssor", precond)   # library greedy multicolour order
         self.t = 0
         self.iters = []
         self.nsnap = 0
@@ -212,7 +214,7 @@ class GpuRun:
 class HostE2ERun:
     """The same sequence through the public API with HOST buffers (pinned), host generator."""
 
-    def __init__(self, cfg, variant, k, device, stream, sell):
+    def __init__(self, cfg, variant, k, device, stream, sell, precond=None):
         import torch
 
         import synth
@@ -230,6 +232,8 @@ class HostE2ERun:
                            fmt="bsr" if cfg.kind == "bsr" else "csr", block=cfg.B if cfg.kind == "bsr" else 1,
                            sell_C=32 if sell else 0, max_m=cfg.m, max_snapshots=cfg.s,
                            max_k=max(k, 1), stream=stream.cuda_stream)
+        if precond:
+            self.ctx.set_preconditioner("ssor", precond)
         self.t = 0
         self.nsnap = 0
         self.h2d = 0
@@ -257,12 +261,19 @@ def flush_l2(buf):
     buf.add_(1.0)   # 256 MiB write > 126 MB L2
 
 
-def oracle_time(cfg, variant, k, systems, budget_s=30.0):
-    """The oracle (plain C, 1 thread) on the first `systems` systems of its own sequence."""
+def oracle_time(cfg, variant, k, systems, budget_s=30.0, precond=None):
+    """The oracle (plain C, 1 thread) on the first `systems` systems of its own sequence
+    (precond = omega: right SSOR in the greedy multicolour order of tests/coloring.py)."""
     import oracle
     import synth
     seq = synth.HostSequence(cfg)
     u = seq.initial()
+    pc = None
+    if precond:
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from coloring import greedy_colors
+        A1 = seq.matrix(1, u)
+        pc = (oracle.ssor_order(greedy_colors(A1.n, A1.row_ptr, A1.col_idx)), precond)
     X = []
     times = []
     its = []
@@ -273,7 +284,7 @@ def oracle_time(cfg, variant, k, systems, budget_s=30.0):
         W = None
         if variant != "plain" and X:
             W, _, _ = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), k)
-        r = oracle.solve(A, b, m=cfg.m, variant=variant, W=W, tol=cfg.tol)
+        r = oracle.solve(A, b, m=cfg.m, variant=variant, W=W, tol=cfg.tol, precond=pc)
         times.append(time.perf_counter() - t0)
         its.append(r["iterations"])
         u = r["x"]
@@ -297,7 +308,8 @@ def run_ours(args, cfg):
     flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=device)
     with torch.cuda.stream(stream):
         sell = (cfg.fmt == "sell") if args.sell < 0 else bool(args.sell)
-        run = GpuRun(cfg, args.variant, k, device, stream, profile=not args.no_profile, sell=sell)
+        run = GpuRun(cfg, args.variant, k, device, stream, profile=not args.no_profile, sell=sell,
+                     precond=args.omega if args.precond == "ssor" else None)
         for _ in range(args.warmup):
             run.step()
         torch.cuda.synchronize()
@@ -312,7 +324,8 @@ def run_ours(args, cfg):
         # e2e through the public API with host buffers
         e2e = None
         if not args.no_e2e:
-            hrun = HostE2ERun(cfg, args.variant, k, device, stream, sell)
+            hrun = HostE2ERun(cfg, args.variant, k, device, stream, sell,
+                              precond=args.omega if args.precond == "ssor" else None)
             for _ in range(min(args.warmup, 2)):
                 hrun.step()
             torch.cuda.synchronize()
@@ -355,7 +368,8 @@ def run_ours(args, cfg):
     launches = sum(s["launches"] + s["noop"] for kname, s in kstats.items() if not kname.startswith("p_"))
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        times, its = oracle_time(cfg, args.variant, k, args.cpu_systems, budget_s=args.cpu_budget)
+        times, its = oracle_time(cfg, args.variant, k, args.cpu_systems, budget_s=args.cpu_budget,
+                                 precond=args.omega if args.precond == "ssor" else None)
         cpu = {"value": sum(times) / len(times), "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{cfg.name} systems 1..{len(times)} of the oracle's own sequence ({args.variant}, "
                          f"iterations {its}), plain C fp64 single thread"}
@@ -364,6 +378,7 @@ def run_ours(args, cfg):
         "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, synth/)",
         "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.cid - 1}]", "variant": args.variant,
+                   "precond": f"right SSOR(omega={args.omega}), multicolour" if args.precond == "ssor" else "none",
                    "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "fmt": cfg.fmt,
                    "device_format": "SELL-32" if sell else ("BSR-64" if cfg.kind == "bsr" else "CSR"),
                    "tol": cfg.tol,
@@ -390,7 +405,8 @@ def run_reference(args, cfg):
         return
     k = args.k or cfg.k
     n_sys = args.warmup + args.steps
-    times, its = oracle_time(cfg, args.variant, k, n_sys, budget_s=1e9)
+    times, its = oracle_time(cfg, args.variant, k, n_sys, budget_s=1e9,
+                             precond=args.omega if args.precond == "ssor" else None)
     timed = times[args.warmup:]
     v = sum(timed) / len(timed)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -413,6 +429,9 @@ def main(argv=None):
     ap.add_argument("--config", default="C2")
     ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate", "oblique"])
     ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--precond", default="none", choices=["none", "ssor"],
+                    help="right SSOR preconditioner in a multicolour order (SURVEY NEXT #2)")
+    ap.add_argument("--omega", type=float, default=1.0)
     ap.add_argument("--sell", type=int, default=-1, help="1: pack CSR to SELL-32 inside the library, "
                     "0: keep CSR, -1: config default")
     ap.add_argument("--no-profile", action="store_true")

@@ -178,6 +178,29 @@ RG_API rg_status rg_solve(rg_ctx* ctx, const double* b, const double* x0, int32_
                           double tol, int32_t max_iters, double* x_out, rg_mem mem, double* history,
                           int32_t history_cap, rg_report* rep);
 
+/* Preconditioning (R18).
+ *   kind = RG_PREC_SSOR: SSOR(omega), 0 < omega < 2, in a MULTICOLOUR row order, applied as a
+ *     RIGHT preconditioner ("A M y = b, x = M^{-1} y") by every later rg_solve of every
+ *     variant: the Arnoldi operator becomes (projector) A M^{-1} and the Krylov part of x is
+ *     M^{-1} V y, so GMRES still minimises (and the stop test still uses) the TRUE residual.
+ *     M = (D + wL) D^{-1} (D + wU) / (w(2-w)), L / U = couplings to rows of lower / higher colour.
+ *   colors     NULL: the library colours the symmetrised pattern greedily in natural order (5-point
+ *              and 7-point grids get red-black, 9-point grids 4 colours); else n int32 colours in
+ *              0..63 (host or device per `mem`) that must not give two coupled rows the same colour.
+ *   ncolors_out nullable; receives the number of colours.
+ *   kind = RG_PREC_NONE removes the preconditioner.
+ * Errors: RG_E_INVAL for a BSR matrix, omega outside (0, 2), an invalid colouring or a row without a
+ * stored diagonal entry (nothing is changed).  A later pattern change (rg_update_matrix with
+ * row_ptr != NULL) removes the preconditioner; values-only updates keep it.  Solves with a
+ * preconditioner run on the CUDA-graph path. */
+#define RG_PREC_NONE 0
+#define RG_PREC_SSOR 1
+RG_API rg_status rg_set_preconditioner(rg_ctx* ctx, int32_t kind, double omega, const int32_t* colors,
+                                       rg_mem mem, int32_t* ncolors_out);
+
+/* y = M^{-1} x for the current preconditioner (x, y length n in `mem`); RG_E_STATE if none. */
+RG_API rg_status rg_apply_preconditioner(rg_ctx* ctx, const double* x, double* y, rg_mem mem);
+
 /* y = A x with the context's current matrix (x, y length n in `mem`). */
 RG_API rg_status rg_apply(rg_ctx* ctx, const double* x, double* y, rg_mem mem);
 

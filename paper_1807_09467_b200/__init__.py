@@ -54,6 +54,21 @@ class Context:
     def apply(self, x, y):
         rg.rg_apply(self.ctx, x, y)
 
+    def set_preconditioner(self, kind="ssor", omega=1.0, colors=None):
+        """Right SSOR(omega) preconditioner in a multicolour order (None kind removes it); returns
+        the number of colours."""
+        if colors is not None:
+            if hasattr(colors, "is_cuda"):        # torch tensor
+                import torch
+                colors = colors.to(dtype=torch.int32).contiguous()
+            else:
+                import numpy as np
+                colors = np.ascontiguousarray(colors, dtype=np.int32)
+        return rg.rg_set_preconditioner(self.ctx, kind, omega, colors)
+
+    def apply_preconditioner(self, x, y):
+        rg.rg_apply_preconditioner(self.ctx, x, y)
+
     def export(self, which, out):
         return rg.rg_export(self.ctx, which, out)
 

@@ -27,7 +27,7 @@ constexpr int VEC_CTAS_PER_SM = 2;         // -> 296 CTAs: 32 resident warps / S
 enum KernelId {
   K_SPMV_STEP = 0, K_SPMV_RES, K_SPMV_PLAIN, K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN,
   K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_DK1, K_DK2,
-  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_COUNT
+  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_SSOR, K_COUNT
 };
 
 struct KStatDev {
@@ -94,6 +94,9 @@ struct Layout {
   int cgs_ok;      // [Q|V] (max_k + max_m + 1 columns) fits k_cgs (16 chunks of 8 columns)
   int augment;     // variant of the graph being built / launched is augment
   int keep_l2;     // the whole basis [W|Q|V] is L2-sized: DCGS2 passes use cached (not streaming) loads
+  int prec;        // right preconditioner active (precond.cu): cycle end adds pz = M^{-1} (V y)
+  double* pz;      // preconditioner output (M^{-1} u of the Arnoldi step, M^{-1} V y at the cycle end)
+  double* pt;      // cycle-end scratch: V y
 };
 
 // ---------------------------------------------------------------- small device helpers

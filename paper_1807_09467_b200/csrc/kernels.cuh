@@ -23,10 +23,10 @@ struct MatDev {
   double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
 };
 
-enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2 };
+enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2, SM_STEP_PC = 3 };
 
 // w = A v_j (STEP), r = b - A x (RES; epi != 0 runs the cycle-start epilogue on ||r||^2),
-// y = A x (PLAIN).
+// y = A x (PLAIN), w = A pz (STEP_PC: pz = M^{-1} v_j from launch_ssor, same gating as STEP).
 cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode, const double* x,
                         double* y, int res_epi, cudaStream_t s);
 
@@ -41,7 +41,8 @@ enum OrthOp {
   OP_OB_CSD,  // cycle start: t = E^{-1} W^T r            (x += W t via OP_XW)
   OP_OB_CSU,  // cycle start: r -= C t, ||r||^2 -> cycle-start epilogue
   OP_OB_SD,   // Arnoldi step: t = E^{-1} W^T (A v_j)
-  OP_OB_SU    // Arnoldi step: A v_j -= C t               (the new column is M_D A v_j)
+  OP_OB_SU,   // Arnoldi step: A v_j -= C t               (the new column is M_D A v_j)
+  OP_VY       // cycle end, preconditioned: pt = V y      (then pz = M^{-1} pt, OP_XUPD adds pz)
 };
 // cond != 0: cudaGraphConditionalHandle set to st->active by OP_UN's epilogue (graph WHILE node)
 cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond = 0);
@@ -54,6 +55,25 @@ cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cud
 // k <= 64.  cudaErrorNotSupported when outside that scope (caller uses the graph path).
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar, int m,
                               int k, int variant, cudaStream_t s);
+
+// ---- multicolour SSOR(omega) preconditioner (precond.cu)
+constexpr int MAXCOLORS = 64;
+struct PrecDev {
+  const int32_t* rp = nullptr;   // CSR pattern and values of the current matrix
+  const int32_t* ci = nullptr;
+  const double* v = nullptr;
+  const uint8_t* color = nullptr;
+  const int32_t* perm = nullptr; // rows grouped by colour
+  const int32_t* diag = nullptr; // position of a_rr
+  int ncolors = 0;
+  double omega = 1.0;
+  int64_t coff[MAXCOLORS + 1] = {};  // colour c = perm[coff[c] .. coff[c+1])
+  int64_t cnnz[MAXCOLORS] = {};      // stored entries of the rows of colour c (byte model)
+};
+// out = M^{-1} in.  gate 0: always; 1: Arnoldi step (in = the state's u, noop as SM_STEP);
+// 2: cycle end (noop unless st->have_xupd).
+cudaError_t launch_ssor(const PrecDev& P, const Layout& L, DevState* st, const double* in, double* out, int gate,
+                        cudaStream_t s);
 
 // ---- dense / recycle-build kernels (dense.cu)
 // E^{-1} (Gauss-Jordan, partial pivoting, one CTA) of E(a,b) = G[(k+b)*2k + a], the W^T C block of

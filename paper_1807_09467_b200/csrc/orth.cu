@@ -44,14 +44,14 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
   DevState* st = a.st;
   const Layout& L = a.L;
   const int op = a.op;
-  static constexpr int kids[12] = {K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN, K_XW, K_XUPD, K_NORMB,
-                                   K_OBD, K_OBU, K_OBD, K_OBU};
+  static constexpr int kids[13] = {K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN, K_XW, K_XUPD, K_NORMB,
+                                   K_OBD, K_OBU, K_OBD, K_OBU, K_XUPD};
   const int kid = kids[op];
   bool go;
   switch (op) {
     case OP_D1: case OP_UD2: case OP_UN: case OP_OB_SD: case OP_OB_SU: go = st->active != 0; break;
     case OP_CS_DQ: case OP_CS_UN: case OP_XW: case OP_OB_CSD: case OP_OB_CSU: go = st->done == 0; break;
-    case OP_XUPD: go = st->have_xupd != 0; break;
+    case OP_XUPD: case OP_VY: go = st->have_xupd != 0; break;
     default: go = true;
   }
   if (!go) { prof_noop(st, kid); return; }
@@ -77,17 +77,19 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
     case OP_CS_DQ: w = L.Z + (int64_t)VB * ld; d0 = QB; d1 = VB; break;
     case OP_CS_UN: w = L.Z + (int64_t)VB * ld; u0 = QB; u1 = VB; nrmflag = true; break;
     case OP_XW: w = L.x; csrc = st->coefx; u0 = 0; u1 = k; break;
-    case OP_XUPD:
-      w = L.x; csrc = st->coefx; u0 = VB; u1 = VB + st->jfinal + 1;
+    case OP_XUPD:  // x += V y (+ W part); preconditioned: x += pz (= M^{-1} V y, OP_VY + SSOR) + W part
+      w = L.x; csrc = st->coefx;
+      if (!L.prec) { u0 = VB; u1 = VB + st->jfinal + 1; }
       if (var == RG_AUGMENT || var == RG_DEFLATE) { u2 = 0; u3 = k; }
       break;
+    case OP_VY: w = L.pt; csrc = st->coefx; u0 = VB; u1 = VB + st->jfinal + 1; break;
     case OP_OB_CSD: w = L.Z + (int64_t)VB * ld; d0 = 0; d1 = k; break;
     case OP_OB_CSU: w = L.Z + (int64_t)VB * ld; u0 = k; u1 = 2 * k; nrmflag = true; break;
     case OP_OB_SD: w = L.Z + (int64_t)(VB + j + 1) * ld; d0 = 0; d1 = k; break;
     case OP_OB_SU: w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = k; u1 = 2 * k; break;
     default: w = const_cast<double*>(L.b); nrmflag = true; break;  // OP_NORMB (read only)
   }
-  const bool upd = (u1 > u0) || (u3 > u2);
+  const bool upd = (u1 > u0) || (u3 > u2) || (op == OP_XUPD && L.prec) || op == OP_VY;
   const bool dots = d1 > d0;
   const int nd = d1 - d0;
   for (int c = u0 + threadIdx.x; c < u1; c += OT) cf[c] = csrc[c] * st->sc[c];
@@ -107,7 +109,8 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
     const bool in = r < r1;
     double acc = 0.0;
     if (in) {
-      acc = w[r];
+      acc = op == OP_VY ? 0.0 : w[r];
+      if (op == OP_XUPD && L.prec) acc += L.pz[r];
       if (upd) {
         int c = u0;
         for (; c + 8 <= u1; c += 8) {   // 8 independent loads in flight, applied in order

@@ -43,8 +43,12 @@ constexpr int HIST_CAP = 1 << 16;
 constexpr int SMALL = MAXS * MAXS;  // doubles per small-matrix slot
 
 struct GraphKey {
-  int variant, m;
-  bool operator<(const GraphKey& o) const { return variant != o.variant ? variant < o.variant : m < o.m; }
+  int variant, m, prec;
+  bool operator<(const GraphKey& o) const {
+    if (variant != o.variant) return variant < o.variant;
+    if (m != o.m) return m < o.m;
+    return prec < o.prec;
+  }
 };
 
 }  // namespace
@@ -100,6 +104,14 @@ struct rg_ctx {
   bool use_dcgs = true;
   bool dcgs_now = true;     // this solve uses DCGS2 (the oblique variant runs classical CGS2)
   int cur_var = 0;          // variant of the kernel sequence being issued
+  // right preconditioner (precond.cu): kind 0 none, 1 SSOR(omega) in a multicolour order
+  int prec_kind = 0;
+  PrecDev P;
+  uint8_t* d_color = nullptr;
+  int32_t* d_perm = nullptr;
+  int32_t* d_diag = nullptr;
+  double* pz = nullptr;
+  double* pt = nullptr;
   bool use_persist = true;  // one cooperative kernel per solve where supported (persistent.cu)
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -113,6 +125,14 @@ size_t header_bytes() { return offsetof(DevState, cs); }
 void clear_graphs(rg_ctx* c) {
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   c->graphs.clear();
+}
+
+void drop_preconditioner(rg_ctx* c) {
+  cudaFree(c->d_color); cudaFree(c->d_perm); cudaFree(c->d_diag);
+  c->d_color = nullptr; c->d_perm = nullptr; c->d_diag = nullptr;
+  c->prec_kind = 0;
+  c->P = PrecDev();
+  c->L.prec = 0;
 }
 
 void free_matrix(rg_ctx* c) {
@@ -194,6 +214,10 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
       if (bad) return fail(RG_E_INVAL, "invalid sparsity pattern (device check code " + std::to_string(bad) + ")");
     }
     const bool realloc = first || A->nnz != c->nnz || newfmt != c->fmt || b != c->block;
+    if (c->prec_kind) {  // the colouring / diagonal positions belong to the old pattern
+      clear_graphs(c);
+      drop_preconditioner(c);
+    }
     if (realloc) {
       clear_graphs(c);
       free_matrix(c);
@@ -359,9 +383,24 @@ cudaError_t cycle_start(rg_ctx* c, int variant) {
   return launch_orth(c->L, c->st, OP_CS_UN, c->stream);
 }
 
+// x += V y (+ W part); with a right preconditioner x += M^{-1} (V y) (+ W part)
+cudaError_t cycle_end(rg_ctx* c) {
+  cudaError_t e;
+  if (c->L.prec) {
+    if ((e = launch_orth(c->L, c->st, OP_VY, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_ssor(c->P, c->L, c->st, c->pt, c->pz, 2, c->stream)) != cudaSuccess) return e;
+  }
+  return launch_orth(c->L, c->st, OP_XUPD, c->stream);
+}
+
 cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
   cudaError_t e;
-  if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
+  if (c->L.prec) {  // y = A M^{-1} u
+    if ((e = launch_ssor(c->P, c->L, c->st, nullptr, c->pz, 1, c->stream)) != cudaSuccess) return e;
+    if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP_PC, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
+  } else if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) {
+    return e;
+  }
   if (c->cur_var == RG_OBLIQUE && !c->dcgs_now) {  // w = M_D A v_j = A v_j - C E^{-1} W^T A v_j
     if ((e = launch_orth(c->L, c->st, OP_OB_SD, c->stream)) != cudaSuccess) return e;
     if ((e = launch_orth(c->L, c->st, OP_OB_SU, c->stream)) != cudaSuccess) return e;
@@ -380,7 +419,7 @@ cudaError_t cycle_body(rg_ctx* c, int variant, int m) {
   const int steps = m + (c->dcgs_now ? 1 : 0);  // DCGS2 finishes column j-1 in step j
   for (int j = 0; j < steps; ++j)
     if ((e = arnoldi_step(c, 0)) != cudaSuccess) return e;
-  if ((e = launch_orth(c->L, c->st, OP_XUPD, c->stream)) != cudaSuccess) return e;
+  if ((e = cycle_end(c)) != cudaSuccess) return e;
   return cycle_start(c, variant);
 }
 
@@ -433,7 +472,7 @@ rg_status build_solve_graph(rg_ctx* c, int variant, cudaGraphExec_t* out) {
   CKG(cudaStreamEndCapture(c->stream, &tmp));
   CKG(e1);
   CKG(cudaStreamBeginCaptureToGraph(c->stream, bodyO, &inner, nullptr, 1, cudaStreamCaptureModeThreadLocal));
-  e1 = launch_orth(c->L, c->st, OP_XUPD, c->stream);
+  e1 = cycle_end(c);
   if (e1 == cudaSuccess) e1 = cycle_start(c, variant);
   if (e1 == cudaSuccess) e1 = launch_cond(c->st, hout, 1, c->stream);
   CKG(cudaStreamEndCapture(c->stream, &tmp));
@@ -455,7 +494,7 @@ rg_status run_solve(rg_ctx* c, int variant, int m) {
       CK(cycle_body(c, variant, m));
     }
   }
-  GraphKey key{variant, 0};
+  GraphKey key{variant, 0, c->L.prec};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     cudaGraphExec_t ge;
@@ -490,6 +529,8 @@ RG_API void rg_destroy(rg_ctx* c) {
   cudaFree(c->Z); cudaFree(c->x); cudaFree(c->b); cudaFree(c->X); cudaFree(c->Y);
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
   cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar);
+  drop_preconditioner(c);
+  cudaFree(c->pz); cudaFree(c->pt);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->hhist) cudaFreeHost(c->hhist);
   if (c->hflag) cudaFreeHost(c->hflag);
@@ -737,7 +778,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
   // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
   const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
-  if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
+  c->L.prec = c->prec_kind ? 1 : 0;
+  if (c->use_persist && persist_size && c->dcgs_now && !c->L.prec && !(c->flags & RG_FLAG_NO_GRAPH)) {
     CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * 4, s));
     cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, m, k, eff, s);
     if (ep == cudaSuccess) done_persist = true;
@@ -804,6 +846,134 @@ RG_API rg_status rg_apply(rg_ctx* c, const double* x, double* y, rg_mem mem) {
   return RG_OK;
 }
 
+RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, const int32_t* colors, rg_mem mem,
+                                       int32_t* ncolors_out) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  if (kind == RG_PREC_NONE) {
+    if (c->prec_kind) {
+      CK(cudaStreamSynchronize(c->stream));
+      clear_graphs(c);
+      drop_preconditioner(c);
+    }
+    if (ncolors_out) *ncolors_out = 0;
+    return RG_OK;
+  }
+  if (kind != RG_PREC_SSOR) return fail(RG_E_INVAL, "unknown preconditioner kind");
+  if (!(omega > 0.0 && omega < 2.0)) return fail(RG_E_INVAL, "SSOR needs 0 < omega < 2");
+  if (c->fmt == 2) return fail(RG_E_INVAL, "SSOR is implemented for CSR (and SELL-packed CSR) matrices only");
+  if (colors && mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  const int64_t n = c->n;
+  std::vector<int32_t> rp(n + 1), ci(std::max<int64_t>(c->nnz, 1));
+  CK(cudaMemcpyAsync(rp.data(), c->rp, sizeof(int32_t) * (n + 1), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(ci.data(), c->ci, sizeof(int32_t) * c->nnz, cudaMemcpyDeviceToHost, c->stream));
+  std::vector<int32_t> col(n);
+  if (colors) {
+    CK(cudaMemcpyAsync(col.data(), colors, sizeof(int32_t) * n,
+                       mem == RG_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost, c->stream));
+  }
+  CK(cudaStreamSynchronize(c->stream));
+  int nc = 0;
+  if (colors) {
+    for (int64_t r = 0; r < n; ++r) {
+      if (col[r] < 0 || col[r] >= MAXCOLORS) return fail(RG_E_INVAL, "colours must be in 0..63");
+      nc = std::max(nc, col[r] + 1);
+    }
+  } else {
+    // greedy colouring of the symmetrised pattern in natural order (smallest colour not used by a
+    // coloured neighbour); neighbours of r = row r's columns and column r's rows (transpose)
+    std::vector<int64_t> tp(n + 1, 0);
+    for (int64_t p = 0; p < c->nnz; ++p) tp[ci[p] + 1]++;
+    for (int64_t i = 0; i < n; ++i) tp[i + 1] += tp[i];
+    std::vector<int32_t> tr(std::max<int64_t>(c->nnz, 1));
+    {
+      std::vector<int64_t> fill(tp.begin(), tp.end() - 1);
+      for (int64_t r = 0; r < n; ++r)
+        for (int32_t p = rp[r]; p < rp[r + 1]; ++p) tr[fill[ci[p]]++] = (int32_t)r;
+    }
+    std::fill(col.begin(), col.end(), -1);
+    for (int64_t r = 0; r < n; ++r) {
+      uint64_t used = 0;
+      for (int32_t p = rp[r]; p < rp[r + 1]; ++p)
+        if (ci[p] != r && col[ci[p]] >= 0) used |= 1ull << col[ci[p]];
+      for (int64_t p = tp[r]; p < tp[r + 1]; ++p)
+        if (tr[p] != r && col[tr[p]] >= 0) used |= 1ull << col[tr[p]];
+      int cc = 0;
+      while (cc < MAXCOLORS && (used >> cc & 1ull)) ++cc;
+      if (cc >= MAXCOLORS) return fail(RG_E_INVAL, "greedy colouring needs more than 64 colours");
+      col[r] = cc;
+      nc = std::max(nc, cc + 1);
+    }
+  }
+  // validity (no coupled rows share a colour) and the diagonal positions
+  std::vector<int32_t> diag(n, -1);
+  for (int64_t r = 0; r < n; ++r)
+    for (int32_t p = rp[r]; p < rp[r + 1]; ++p) {
+      if (ci[p] == r) diag[r] = p;
+      else if (col[ci[p]] == col[r]) return fail(RG_E_INVAL, "not a valid colouring: row " + std::to_string(r) +
+                                                              " and column " + std::to_string(ci[p]) + " share a colour");
+    }
+  for (int64_t r = 0; r < n; ++r)
+    if (diag[r] < 0) return fail(RG_E_INVAL, "SSOR needs a stored diagonal entry in every row (row " + std::to_string(r) + ")");
+  // rows grouped by colour (stable), entries per colour
+  PrecDev P;
+  P.ncolors = nc;
+  P.omega = omega;
+  std::vector<int32_t> perm(n);
+  {
+    std::vector<int64_t> cnt(nc + 1, 0);
+    for (int64_t r = 0; r < n; ++r) {
+      cnt[col[r] + 1]++;
+      P.cnnz[col[r]] += rp[r + 1] - rp[r];
+    }
+    for (int i = 0; i < nc; ++i) cnt[i + 1] += cnt[i];
+    for (int i = 0; i <= nc; ++i) P.coff[i] = cnt[i];
+    for (int64_t r = 0; r < n; ++r) perm[cnt[col[r]]++] = (int32_t)r;
+  }
+  std::vector<uint8_t> col8(n);
+  for (int64_t r = 0; r < n; ++r) col8[r] = (uint8_t)col[r];
+  CK(cudaStreamSynchronize(c->stream));
+  clear_graphs(c);
+  drop_preconditioner(c);
+  rg_status s;
+  if ((s = dalloc(&c->d_color, (size_t)n, "colours")) != RG_OK || (s = dalloc(&c->d_perm, (size_t)n, "perm")) != RG_OK ||
+      (s = dalloc(&c->d_diag, (size_t)n, "diag")) != RG_OK) {
+    drop_preconditioner(c);
+    return s;
+  }
+  if (!c->pz) {
+    if ((s = dalloc(&c->pz, (size_t)c->npad, "pz")) != RG_OK || (s = dalloc(&c->pt, (size_t)c->npad, "pt")) != RG_OK) {
+      drop_preconditioner(c);
+      return s;
+    }
+    CK(cudaMemsetAsync(c->pz, 0, sizeof(double) * c->npad, c->stream));
+    CK(cudaMemsetAsync(c->pt, 0, sizeof(double) * c->npad, c->stream));
+  }
+  CK(cudaMemcpyAsync(c->d_color, col8.data(), n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_perm, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->d_diag, diag.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  P.rp = c->rp; P.ci = c->ci; P.v = c->v;
+  P.color = c->d_color; P.perm = c->d_perm; P.diag = c->d_diag;
+  c->P = P;
+  c->prec_kind = RG_PREC_SSOR;
+  c->L.pz = c->pz;
+  c->L.pt = c->pt;
+  if (ncolors_out) *ncolors_out = nc;
+  return RG_OK;
+}
+
+RG_API rg_status rg_apply_preconditioner(rg_ctx* c, const double* x, double* y, rg_mem mem) {
+  if (!c || !x || !y) return fail(RG_E_INVAL, "NULL argument");
+  if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  if (!c->prec_kind) return fail(RG_E_STATE, "no preconditioner set");
+  rg_status s = copy_in(c->t1, x, sizeof(double) * c->n, mem, c->stream);
+  if (s != RG_OK) return s;
+  CK(launch_ssor(c->P, c->L, c->st, c->t1, c->t2, 0, c->stream));
+  CK(cudaMemcpyAsync(y, c->t2, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return RG_OK;
+}
+
 RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, int32_t* k_eff) {
   if (!c || !out) return fail(RG_E_INVAL, "NULL argument");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
@@ -832,7 +1002,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
-                                       "p_update", "ob_dots", "ob_update"};
+                                       "p_update", "ob_dots", "ob_update", "ssor"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));

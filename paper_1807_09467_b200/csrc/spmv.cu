@@ -37,13 +37,14 @@ __device__ __forceinline__ bool setup(const SpmvArgs& a, Io& io, int& kid) {
   io.res = false;
   io.b = nullptr;
   io.xs = 1.0;
-  if (a.mode == SM_STEP) {
+  if (a.mode == SM_STEP || a.mode == SM_STEP_PC) {
     kid = K_SPMV_STEP;
     const int j = st->j;
     if (!st->active || (st->dcgs && j >= st->m)) { prof_noop(st, kid); return false; }
-    io.x = L.Z + (int64_t)(L.VB + j) * L.ld;
+    io.x = a.mode == SM_STEP_PC ? L.pz : L.Z + (int64_t)(L.VB + j) * L.ld;
     io.y = L.Z + (int64_t)(L.VB + j + 1) * L.ld;
-    io.xs = st->dcgs ? 1.0 : st->sc[L.VB + j];  // DCGS2: y = A u on the raw vector
+    // DCGS2: y = A u on the raw vector; STEP_PC: the SSOR sweep already applied the column scale
+    io.xs = (st->dcgs || a.mode == SM_STEP_PC) ? 1.0 : st->sc[L.VB + j];
   } else if (a.mode == SM_RES) {
     kid = K_SPMV_RES;
     if (st->done) { prof_noop(st, kid); return false; }

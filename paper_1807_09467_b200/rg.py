@@ -22,6 +22,8 @@ RG_HOST, RG_DEVICE = 0, 1
 RG_FLAG_NO_GRAPH, RG_FLAG_PROFILE, RG_FLAG_CGS2, RG_FLAG_NO_PERSIST = 1, 2, 4, 8
 RG_EXPORT_W, RG_EXPORT_Q, RG_EXPORT_RC = 0, 1, 2
 RG_MODES_LARGEST, RG_MODES_SMALLEST = 0, 1
+RG_PREC_NONE, RG_PREC_SSOR = 0, 1
+PRECS = {None: RG_PREC_NONE, "none": RG_PREC_NONE, "ssor": RG_PREC_SSOR}
 MODES = {"largest": RG_MODES_LARGEST, "smallest": RG_MODES_SMALLEST}
 VARIANTS = {"plain": RG_PLAIN, "augment": RG_AUGMENT, "deflate": RG_DEFLATE, "oblique": RG_OBLIQUE}
 STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E_STATE",
@@ -29,8 +31,8 @@ STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E
 
 # Symbols declared in include/rg.h (tests check the .so exports exactly these).
 SYMBOLS = ("rg_create", "rg_update_matrix", "rg_matrix_values", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle", "rg_build_recycle_modes",
-           "rg_solve", "rg_apply", "rg_export", "rg_kernel_stats", "rg_reset_kernel_stats", "rg_destroy",
-           "rg_last_error")
+           "rg_solve", "rg_apply", "rg_set_preconditioner", "rg_apply_preconditioner", "rg_export",
+           "rg_kernel_stats", "rg_reset_kernel_stats", "rg_destroy", "rg_last_error")
 
 
 class RgError(RuntimeError):
@@ -80,6 +82,8 @@ def load(path: str = LIB_PATH):
     L.rg_solve.argtypes = [vp, vp, vp, i32, ctypes.c_int, d, i32, vp, ctypes.c_int, vp, i32,
                            ctypes.POINTER(rg_report)]
     L.rg_apply.argtypes = [vp, vp, vp, ctypes.c_int]
+    L.rg_set_preconditioner.argtypes = [vp, i32, d, vp, ctypes.c_int, ctypes.POINTER(i32)]
+    L.rg_apply_preconditioner.argtypes = [vp, vp, vp, ctypes.c_int]
     L.rg_export.argtypes = [vp, i32, vp, ctypes.c_int, ctypes.POINTER(i32)]
     L.rg_kernel_stats.argtypes = [vp, ctypes.POINTER(rg_kstat), i32, ctypes.POINTER(i32)]
     L.rg_reset_kernel_stats.argtypes = [vp]
@@ -207,6 +211,20 @@ def rg_solve(ctx, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=
 def rg_apply(ctx, x, y):
     mem = _mem_of(x, y)
     _check(_lib.rg_apply(ctx, _ptr(x)[0], _ptr(y)[0], mem))
+
+
+def rg_set_preconditioner(ctx, kind="ssor", omega=1.0, colors=None):
+    """colors: None (library greedy colouring) or an int32 array / tensor of length n."""
+    kd = PRECS[kind] if (kind is None or isinstance(kind, str)) else int(kind)
+    nc = ctypes.c_int32(0)
+    p, mem = _ptr(colors)
+    _check(_lib.rg_set_preconditioner(ctx, kd, float(omega), p, RG_HOST if mem is None else mem, ctypes.byref(nc)))
+    return nc.value
+
+
+def rg_apply_preconditioner(ctx, x, y):
+    mem = _mem_of(x, y)
+    _check(_lib.rg_apply_preconditioner(ctx, _ptr(x)[0], _ptr(y)[0], mem))
 
 
 def rg_export(ctx, which, out):
