@@ -58,18 +58,32 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
 
 // ---- multicolour SSOR(omega) preconditioner (precond.cu)
 constexpr int MAXCOLORS = 64;
+// The matrix is stored a second time for the sweeps, rows in colour order (index idx = position in
+// perm) and split by the colour of the column: L = couplings to lower colours (forward sweep), U =
+// to higher colours (backward sweep), dinv = 1 / a_rr.  Each sweep then streams a contiguous slab
+// and reads every off-diagonal entry exactly once per application (no colour tests).  The values
+// are re-gathered from the CSR values after every matrix update (launch_ssor_values).
 struct PrecDev {
-  const int32_t* rp = nullptr;   // CSR pattern and values of the current matrix
-  const int32_t* ci = nullptr;
-  const double* v = nullptr;
-  const uint8_t* color = nullptr;
-  const int32_t* perm = nullptr; // rows grouped by colour
-  const int32_t* diag = nullptr; // position of a_rr
+  const int32_t* perm = nullptr;  // rows grouped by colour
+  const int32_t* Lrp = nullptr;   // [n + 1] over idx
+  const int32_t* Lci = nullptr;   // original column index
+  double* Lv = nullptr;
+  const int32_t* Lmap = nullptr;  // position of each L entry in the CSR values
+  const int32_t* Urp = nullptr;
+  const int32_t* Uci = nullptr;
+  double* Uv = nullptr;
+  const int32_t* Umap = nullptr;
+  double* dinv = nullptr;         // [n] over idx
+  const int32_t* dmap = nullptr;  // position of a_rr (over idx)
+  int64_t nL = 0, nU = 0;
   int ncolors = 0;
   double omega = 1.0;
   int64_t coff[MAXCOLORS + 1] = {};  // colour c = perm[coff[c] .. coff[c+1])
-  int64_t cnnz[MAXCOLORS] = {};      // stored entries of the rows of colour c (byte model)
+  int64_t cL[MAXCOLORS] = {};        // L / U entries of the rows of colour c (byte model)
+  int64_t cU[MAXCOLORS] = {};
 };
+// Lv / Uv / dinv from the CSR values v.
+cudaError_t launch_ssor_values(const PrecDev& P, const double* v, int64_t n, cudaStream_t s);
 // out = M^{-1} in.  gate 0: always; 1: Arnoldi step (in = the state's u, noop as SM_STEP);
 // 2: cycle end (noop unless st->have_xupd).
 cudaError_t launch_ssor(const PrecDev& P, const Layout& L, DevState* st, const double* in, double* out, int gate,

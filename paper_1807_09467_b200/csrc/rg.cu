@@ -107,9 +107,7 @@ struct rg_ctx {
   // right preconditioner (precond.cu): kind 0 none, 1 SSOR(omega) in a multicolour order
   int prec_kind = 0;
   PrecDev P;
-  uint8_t* d_color = nullptr;
-  int32_t* d_perm = nullptr;
-  int32_t* d_diag = nullptr;
+  std::vector<void*> prec_bufs;  // device arrays owned by P
   double* pz = nullptr;
   double* pt = nullptr;
   bool use_persist = true;  // one cooperative kernel per solve where supported (persistent.cu)
@@ -128,8 +126,8 @@ void clear_graphs(rg_ctx* c) {
 }
 
 void drop_preconditioner(rg_ctx* c) {
-  cudaFree(c->d_color); cudaFree(c->d_perm); cudaFree(c->d_diag);
-  c->d_color = nullptr; c->d_perm = nullptr; c->d_diag = nullptr;
+  for (void* p : c->prec_bufs) cudaFree(p);
+  c->prec_bufs.clear();
   c->prec_kind = 0;
   c->P = PrecDev();
   c->L.prec = 0;
@@ -265,6 +263,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
       if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
     }
     if (c->fmt == 1) CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 0, c->stream));
+    if (c->prec_kind) CK(launch_ssor_values(c->P, c->v, c->n, c->stream));  // SSOR copies follow the values
   }
   // device descriptor and byte model
   MatDev& M = c->A;
@@ -905,7 +904,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
     }
   }
   // validity (no coupled rows share a colour) and the diagonal positions
-  std::vector<int32_t> diag(n, -1);
+  std::vector<int64_t> diag(n, -1);
   for (int64_t r = 0; r < n; ++r)
     for (int32_t p = rp[r]; p < rp[r + 1]; ++p) {
       if (ci[p] == r) diag[r] = p;
@@ -914,32 +913,71 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
     }
   for (int64_t r = 0; r < n; ++r)
     if (diag[r] < 0) return fail(RG_E_INVAL, "SSOR needs a stored diagonal entry in every row (row " + std::to_string(r) + ")");
-  // rows grouped by colour (stable), entries per colour
+  // rows grouped by colour (stable); the L / U split copies in that order (PrecDev)
   PrecDev P;
   P.ncolors = nc;
   P.omega = omega;
   std::vector<int32_t> perm(n);
   {
     std::vector<int64_t> cnt(nc + 1, 0);
-    for (int64_t r = 0; r < n; ++r) {
-      cnt[col[r] + 1]++;
-      P.cnnz[col[r]] += rp[r + 1] - rp[r];
-    }
+    for (int64_t r = 0; r < n; ++r) cnt[col[r] + 1]++;
     for (int i = 0; i < nc; ++i) cnt[i + 1] += cnt[i];
     for (int i = 0; i <= nc; ++i) P.coff[i] = cnt[i];
     for (int64_t r = 0; r < n; ++r) perm[cnt[col[r]]++] = (int32_t)r;
   }
-  std::vector<uint8_t> col8(n);
-  for (int64_t r = 0; r < n; ++r) col8[r] = (uint8_t)col[r];
+  std::vector<int32_t> Lrp(n + 1, 0), Urp(n + 1, 0), Lci, Uci, Lmap, Umap, dmap(n);
+  Lci.reserve(c->nnz); Uci.reserve(c->nnz); Lmap.reserve(c->nnz); Umap.reserve(c->nnz);
+  for (int64_t idx = 0; idx < n; ++idx) {
+    const int32_t r = perm[idx];
+    dmap[idx] = (int32_t)diag[r];
+    for (int32_t p = rp[r]; p < rp[r + 1]; ++p) {
+      const int32_t j = ci[p];
+      if (j == r) continue;
+      if (col[j] < col[r]) { Lci.push_back(j); Lmap.push_back(p); P.cL[col[r]]++; }
+      else { Uci.push_back(j); Umap.push_back(p); P.cU[col[r]]++; }
+    }
+    Lrp[idx + 1] = (int32_t)Lci.size();
+    Urp[idx + 1] = (int32_t)Uci.size();
+  }
+  P.nL = (int64_t)Lci.size();
+  P.nU = (int64_t)Uci.size();
   CK(cudaStreamSynchronize(c->stream));
   clear_graphs(c);
   drop_preconditioner(c);
+  // device copies
+  auto up = [&](const void* h, size_t bytes, const char* what, void** out) -> rg_status {
+    void* d = nullptr;
+    if (cudaMalloc(&d, std::max<size_t>(bytes, 8)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(RG_E_NOMEM, std::string("device allocation failed: ") + what);
+    }
+    c->prec_bufs.push_back(d);
+    if (h && bytes && cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+      return fail(RG_E_CUDA, std::string("upload failed: ") + what);
+    *out = d;
+    return RG_OK;
+  };
   rg_status s;
-  if ((s = dalloc(&c->d_color, (size_t)n, "colours")) != RG_OK || (s = dalloc(&c->d_perm, (size_t)n, "perm")) != RG_OK ||
-      (s = dalloc(&c->d_diag, (size_t)n, "diag")) != RG_OK) {
+  void *d_perm, *d_Lrp, *d_Lci, *d_Lmap, *d_Lv, *d_Urp, *d_Uci, *d_Umap, *d_Uv, *d_dinv, *d_dmap;
+  if ((s = up(perm.data(), sizeof(int32_t) * n, "perm", &d_perm)) != RG_OK ||
+      (s = up(Lrp.data(), sizeof(int32_t) * (n + 1), "L row pointer", &d_Lrp)) != RG_OK ||
+      (s = up(Lci.data(), sizeof(int32_t) * P.nL, "L columns", &d_Lci)) != RG_OK ||
+      (s = up(Lmap.data(), sizeof(int32_t) * P.nL, "L map", &d_Lmap)) != RG_OK ||
+      (s = up(nullptr, sizeof(double) * P.nL, "L values", &d_Lv)) != RG_OK ||
+      (s = up(Urp.data(), sizeof(int32_t) * (n + 1), "U row pointer", &d_Urp)) != RG_OK ||
+      (s = up(Uci.data(), sizeof(int32_t) * P.nU, "U columns", &d_Uci)) != RG_OK ||
+      (s = up(Umap.data(), sizeof(int32_t) * P.nU, "U map", &d_Umap)) != RG_OK ||
+      (s = up(nullptr, sizeof(double) * P.nU, "U values", &d_Uv)) != RG_OK ||
+      (s = up(nullptr, sizeof(double) * n, "1/diag", &d_dinv)) != RG_OK ||
+      (s = up(dmap.data(), sizeof(int32_t) * n, "diag map", &d_dmap)) != RG_OK) {
+    cudaStreamSynchronize(c->stream);
     drop_preconditioner(c);
     return s;
   }
+  P.perm = (const int32_t*)d_perm;
+  P.Lrp = (const int32_t*)d_Lrp; P.Lci = (const int32_t*)d_Lci; P.Lmap = (const int32_t*)d_Lmap; P.Lv = (double*)d_Lv;
+  P.Urp = (const int32_t*)d_Urp; P.Uci = (const int32_t*)d_Uci; P.Umap = (const int32_t*)d_Umap; P.Uv = (double*)d_Uv;
+  P.dinv = (double*)d_dinv; P.dmap = (const int32_t*)d_dmap;
   if (!c->pz) {
     if ((s = dalloc(&c->pz, (size_t)c->npad, "pz")) != RG_OK || (s = dalloc(&c->pt, (size_t)c->npad, "pt")) != RG_OK) {
       drop_preconditioner(c);
@@ -948,12 +986,8 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
     CK(cudaMemsetAsync(c->pz, 0, sizeof(double) * c->npad, c->stream));
     CK(cudaMemsetAsync(c->pt, 0, sizeof(double) * c->npad, c->stream));
   }
-  CK(cudaMemcpyAsync(c->d_color, col8.data(), n, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->d_perm, perm.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
-  CK(cudaMemcpyAsync(c->d_diag, diag.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+  CK(launch_ssor_values(P, c->v, n, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  P.rp = c->rp; P.ci = c->ci; P.v = c->v;
-  P.color = c->d_color; P.perm = c->d_perm; P.diag = c->d_diag;
   c->P = P;
   c->prec_kind = RG_PREC_SSOR;
   c->L.pz = c->pz;
