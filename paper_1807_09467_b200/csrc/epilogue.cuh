@@ -163,11 +163,14 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
     int iters = s_ic[1];
     int stop = 0, jf = j;
     if (!s_tb) {
-      for (int i = 0; i < j; ++i) {  // apply the previous rotations
-        const double a = h[i], b = h[i + 1];
-        h[i] = csS[i] * a + snS[i] * b;
-        h[i + 1] = -snS[i] * a + csS[i] * b;
+      double carry = h[0];  // apply the previous rotations; the rotated entry stays in a register
+#pragma unroll 4
+      for (int i = 0; i < j; ++i) {
+        const double b = h[i + 1], ci = csS[i], si = snS[i];
+        h[i] = ci * carry + si * b;
+        carry = -si * carry + ci * b;
       }
+      h[j] = carry;
       if (!(hypot(h[j], h[j + 1]) > 0.0)) s_tb = 1;  // A v_j = 0 within span: no progress possible
     }
     if (s_tb) {

@@ -13,6 +13,7 @@
 // coefficients exactly as dcgs.cu does it (V^T C replicated in shared memory).
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include <climits>
 #include <cstdlib>
 
 namespace rg {
@@ -31,21 +32,25 @@ struct PArgs {
   unsigned* bar;        // [0] arrival count, [1] generation
   int m, k;             // m <= PM, k <= PK (k = 0: plain)
   int obl;              // oblique variant (k = k_eff > 0, C = A W in columns [k, 2k))
+  unsigned* flags;      // [gridDim.x] neighbour-sync epochs (zeroed before the launch)
+  int nbsync;           // 1: point-to-point neighbour sync before the SpMVs instead of grid barriers
 };
 
 // ---- grid barrier (all CTAs co-resident: cooperative launch).  Spins with a timeout so that a
 // bug cannot hang the GPU: after ~2 s every CTA gives up and the solve reports RG_E_CUDA.
+// Words (unsigned): [0] arrival counter, [32] generation (separate 128-B lines).  (Measured: a
+// two-level arrival tree with per-group counters made no difference at 296 CTAs.)
 __device__ __forceinline__ bool gbar(unsigned* bar, int* s_fail) {
   __syncthreads();
   if (gridDim.x == 1) return true;  // single-CTA solve (tiny systems): a CTA barrier suffices
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
+    volatile unsigned* gen = bar + 32;
     const unsigned g = *gen;
     __threadfence();
     if (atomicAdd(bar, 1u) == gridDim.x - 1) {
       bar[0] = 0u;
       __threadfence();
-      atomicAdd(bar + 1, 1u);
+      atomicAdd(bar + 32, 1u);
     } else {
       const long long t0 = clock64();
       unsigned ns = 32;
@@ -61,24 +66,79 @@ __device__ __forceinline__ bool gbar(unsigned* bar, int* s_fail) {
   return *s_fail == 0;
 }
 
+// ---- neighbour synchronisation.  The SpMV of a CTA reads only the rows of the CTAs that own the
+// columns of its rows ([c_lo, c_hi], computed once from the pattern).  After writing the vector the
+// next SpMV reads (u, or x at a cycle end), every CTA publishes an epoch; before the SpMV a CTA
+// waits only for the epochs of its column owners instead of a grid-wide barrier.  Every CTA runs the
+// same sequence of publish points (the control flow is replicated), so epochs agree.  Write-after-
+// read hazards on those rows are excluded by the grid barriers inside the reduction that separates
+// a SpMV from the next write of the same column.
+__device__ __forceinline__ void nb_publish(unsigned* flags, unsigned epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicExch(flags + blockIdx.x, epoch);
+  }
+}
+
+__device__ __forceinline__ bool nb_wait(const unsigned* flags, int lo, int hi, unsigned epoch, int* s_fail) {
+  for (int c = lo + (int)threadIdx.x; c <= hi; c += blockDim.x) {  // one polling thread per owner CTA
+    volatile const unsigned* f = flags + c;
+    const long long t0 = clock64();
+    unsigned ns = 32;
+    while (*f < epoch) {
+      __nanosleep(ns);
+      if (ns < 256) ns <<= 1;
+      if (clock64() - t0 > 4000000000LL) { *s_fail = 1; break; }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  return *s_fail == 0;
+}
+
+// owner CTA of a row under the even 32-row-granule split used by the kernel
+__device__ __forceinline__ int row_owner(int64_t row, int64_t ng, int G) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {  // largest b with r0(b) <= row
+    const int mid = (lo + hi + 1) >> 1;
+    if ((((int64_t)mid * ng / G) << 5) <= row) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 // ---- deterministic grid reduction: every CTA writes its nv partials; CTA c sums columns
 // c, c+G, ... over CTAs in index order; every CTA then reads the nv totals into `tot`.
 // (Measured: a single "last CTA reduces" wave is slower here — the reducing CTA competes with ~300
-// pollers — so the work is spread over all CTAs between two barriers.)
+// pollers — and so is a one-barrier variant in which every CTA reduces all columns itself (296 CTAs
+// x all partials from L2: C2 reduce phase 6.8 -> 23.8 ms per 10 systems); the work is spread over
+// all CTAs between two barriers.)
 __device__ __forceinline__ bool greduce(const double* vals, int nv, double* partial, double* tot_g, double* tot,
-                                        unsigned* bar, int* s_fail) {
+                                        unsigned* bar, int* s_fail, DevState* st = nullptr) {
   if (gridDim.x == 1) {  // single CTA: the CTA's values are the totals
     __syncthreads();
     for (int i = threadIdx.x; i < nv; i += PT) tot[i] = vals[i];
     __syncthreads();
     return true;
   }
-  for (int i = threadIdx.x; i < nv; i += PT) partial[(size_t)blockIdx.x * MAXRED + i] = vals[i];
-  if (!gbar(bar, s_fail)) return false;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, G = gridDim.x;
+  for (int i = threadIdx.x; i < nv; i += PT) partial[(size_t)blockIdx.x * MAXRED + i] = vals[i];
+  const unsigned long long ta = (st && st->profile && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
+  if (!gbar(bar, s_fail)) return false;
+  if (ta) {  // profiling: time CTA 0 waits in the first barrier (skew + arrival) -> p_reduce_arrive
+    st->kstat[K_PB6].ns += gtimer() - ta;
+    st->kstat[K_PB6].launches++;
+  }
   for (int col = blockIdx.x + G * wid; col < nv; col += G * (PT / 32)) {
     double a = 0.0;
-    for (int b = lane; b < G; b += 32) a += __ldcg(partial + (size_t)b * MAXRED + col);
+    for (int b0 = lane; b0 < G; b0 += 32 * 8) {  // 8 independent L2 loads in flight per lane
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < G ? __ldcg(partial + (size_t)(b0 + 32 * u) * MAXRED + col) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a += v[u];
+    }
     a = warp_sum(a);
     if (lane == 0) tot_g[col] = a;
   }
@@ -187,6 +247,36 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   const double* __restrict__ b = L.b;
   double bytes = 0.0;  // algorithmic bytes (CTA 0 accounts them)
   const bool keep = L.keep_l2 != 0;  // basis L2-sized: cached loads (the update pass re-hits them)
+  // ---- column owners of this CTA's rows (neighbour sync): min / max column of its CSR entries
+  __shared__ int s_clo, s_chi;
+  unsigned epoch = 0;
+  const bool nbs = pa.nbsync != 0 && gridDim.x > 1;
+  if (nbs) {
+    int cmin = INT_MAX, cmax = -1;
+    const int64_t re = r1 < L.n ? r1 : L.n;
+    if (r0 < re) {
+      const int32_t p0 = A.rp[r0], p1 = A.rp[re];
+      for (int32_t p = p0 + tid; p < p1; p += PT) {
+        const int c = A.ci[p];
+        cmin = min(cmin, c);
+        cmax = max(cmax, c);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      cmin = min(cmin, __shfl_xor_sync(0xffffffffu, cmin, o));
+      cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+    }
+    if (tid == 0) { s_clo = INT_MAX; s_chi = -1; }
+    __syncthreads();
+    if (lane == 0) { atomicMin(&s_clo, cmin); atomicMax(&s_chi, cmax); }
+    __syncthreads();
+    if (tid == 0) {
+      const int G = gridDim.x;
+      s_clo = s_chi < 0 ? (int)blockIdx.x : row_owner(s_clo, ng, G);
+      s_chi = s_chi < 0 ? (int)blockIdx.x : row_owner(s_chi, ng, G);
+    }
+    __syncthreads();
+  }
 
   // ---- ||b||
   {
@@ -213,7 +303,11 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   double beta = 0.0, relres = 0.0;
   for (;;) {
     // ================= cycle start: r = b - A x into V column 0 (+ Q^T r, ||r||^2)
-    if (!gbar(pa.bar, &s_fail)) goto fail;  // x complete
+    if (nbs) {  // x of the column owners complete
+      if (!nb_wait(pa.flags, s_clo, s_chi, epoch, &s_fail)) goto fail;
+    } else if (!gbar(pa.bar, &s_fail)) {
+      goto fail;
+    }
     double* __restrict__ u0 = Z + (int64_t)VB * ld;
     {
       double s = 0.0;
@@ -294,7 +388,13 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       double* __restrict__ y = Z + (int64_t)(VB + j + 1) * ld;
       const bool have_y = j < m;
       unsigned long long tph = (st->profile && cta0 && tid == 0) ? gtimer() : 0ull;
-      if (j > 0 && !gbar(pa.bar, &s_fail)) goto fail;  // u complete
+      if (j > 0) {  // u complete (on the column owners' rows)
+        if (nbs) {
+          if (!nb_wait(pa.flags, s_clo, s_chi, epoch, &s_fail)) goto fail;
+        } else if (!gbar(pa.bar, &s_fail)) {
+          goto fail;
+        }
+      }
       ptick(st, K_PB1, tph);
       const int nv = 2 * p + 2 + nx;
       for (int c = tid; c < nv; c += PT) dpart[c] = 0.0;
@@ -347,7 +447,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         __syncthreads();
       }
       ptick(st, K_PB2, tph);
-      if (!greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      if (!greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, st)) goto fail;
       ptick(st, K_PB3, tph);
       if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + nx + 2);
       // ---- replicated epilogue: delayed second pass, column j-1, least squares
@@ -370,23 +470,27 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         if (tid == 0) Hs[col * (m + 2) + j] = nu;
         __syncthreads();
         if (tid == 0) {  // Givens on column col (same arithmetic in every CTA)
-          double hv[PM + 2];
-          for (int i = 0; i <= j; ++i) hv[i] = Hs[col * (m + 2) + i];
+          // the rotated entry travels in a register; the loads of H, cs, sn do not depend on the
+          // chain, so the unrolled loop keeps them in flight (2 FMAs per rotation on the chain)
+          const double* Hc = Hs + col * (m + 2);
+          double* Rc = Rs + col * (m + 1);
+          double carry = Hc[0];
+#pragma unroll 4
           for (int i = 0; i < col; ++i) {
-            const double x0 = hv[i], x1 = hv[i + 1];
-            hv[i] = cs[i] * x0 + sn[i] * x1;
-            hv[i + 1] = -sn[i] * x0 + cs[i] * x1;
+            const double x1 = Hc[i + 1], ci = cs[i], si = sn[i];
+            Rc[i] = ci * carry + si * x1;
+            carry = -si * carry + ci * x1;
           }
-          const double den = hypot(hv[col], hv[col + 1]);
+          const double hlast = Hc[col + 1];
+          const double den = hypot(carry, hlast);
           int stop = 0;
           if (!(den > 0.0)) {
             stop = 2;  // no progress possible: end the cycle at the previous column
           } else {
-            const double c = hv[col] / den, s = hv[col + 1] / den;
+            const double c = carry / den, s = hlast / den;
             cs[col] = c;
             sn[col] = s;
-            hv[col] = den;
-            for (int i = 0; i <= col; ++i) Rs[col * (m + 1) + i] = hv[i];
+            Rc[col] = den;
             const double gj = gg[col];
             gg[col] = c * gj;
             gg[col + 1] = -s * gj;
@@ -489,7 +593,8 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         y[r] = yr * inv + ur * fu + sn2;
       }
       if (cta0) bytes += 8.0 * L.n * (p + (obl ? k : 0) + 4);
-      __syncthreads();
+      if (nbs) nb_publish(pa.flags, ++epoch);  // u complete on this CTA's rows
+      else __syncthreads();
       ptick(st, K_PB5, tph);
     }
     // ================= cycle end: y = R^{-1} g, x += V y - W R_C^{-1} B y (own rows)
@@ -524,6 +629,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         x[r] = xr;
       }
       if (cta0) bytes += 8.0 * L.n * (jf + 1 + kx + 2);
+      if (nbs) nb_publish(pa.flags, ++epoch);  // x complete on this CTA's rows
     }
     if (status) break;
   }
@@ -557,8 +663,8 @@ size_t persistent_smem(int m, int k) {
 }
 
 // Returns cudaErrorNotSupported when the configuration is outside this path.
-cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar, int m,
-                              int k, int variant, cudaStream_t s) {
+cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
+                              unsigned* flags, int m, int k, int variant, cudaStream_t s) {
   if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE && variant != RG_OBLIQUE) || A.fmt == 2)
     return cudaErrorNotSupported;
   const size_t smem = persistent_smem(m, k);
@@ -578,7 +684,8 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : 2;
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k, variant == RG_OBLIQUE && k > 0 ? 1 : 0};
+  static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
+  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k, variant == RG_OBLIQUE && k > 0 ? 1 : 0, flags, nbsync};
   void* args[] = {&pa};
   return cudaLaunchCooperativeKernel((const void*)k_solve_persistent, dim3(G), dim3(PT), args, smem, s);
 }

@@ -90,6 +90,7 @@ struct rg_ctx {
   int* dflag = nullptr;
   double* tot_g = nullptr;   // persistent solve: reduced totals
   unsigned* gbar = nullptr;  // persistent solve: grid-barrier words
+  unsigned* pflags = nullptr;  // persistent solve: neighbour-sync epochs (NSM * 8)
   DevState* st = nullptr;
   DevState* hst = nullptr;  // pinned host mirror
   double* hhist = nullptr;  // pinned history staging
@@ -527,7 +528,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   free_matrix(c);
   cudaFree(c->Z); cudaFree(c->x); cudaFree(c->b); cudaFree(c->X); cudaFree(c->Y);
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
-  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar);
+  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar); cudaFree(c->pflags);
   drop_preconditioner(c);
   cudaFree(c->pz); cudaFree(c->pt);
   if (c->hst) cudaFreeHost(c->hst);
@@ -582,7 +583,8 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
       (s = dalloc(&c->t2, np, "t2")) != RG_OK || (s = dalloc(&c->hist, (size_t)HIST_CAP, "hist")) != RG_OK ||
       (s = dalloc(&c->partial, part, "partial")) != RG_OK || (s = dalloc(&c->counter, 4, "counter")) != RG_OK ||
       (s = dalloc(&c->small, (size_t)SMALL * 16, "small")) != RG_OK || (s = dalloc(&c->dflag, 4, "flag")) != RG_OK ||
-      (s = dalloc(&c->tot_g, (size_t)MAXRED, "totals")) != RG_OK || (s = dalloc(&c->gbar, 4, "barrier")) != RG_OK ||
+      (s = dalloc(&c->tot_g, (size_t)MAXRED, "totals")) != RG_OK || (s = dalloc(&c->gbar, (size_t)BAR_WORDS, "barrier")) != RG_OK ||
+      (s = dalloc(&c->pflags, (size_t)NSM * 8, "sync flags")) != RG_OK ||
       (s = dalloc(&c->st, 1, "state")) != RG_OK) {
     rg_destroy(c);
     return s;
@@ -779,8 +781,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
   c->L.prec = c->prec_kind ? 1 : 0;
   if (c->use_persist && persist_size && c->dcgs_now && !c->L.prec && !(c->flags & RG_FLAG_NO_GRAPH)) {
-    CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * 4, s));
-    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, m, k, eff, s);
+    CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
+    CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 8, s));
+    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, m, k, eff, s);
     if (ep == cudaSuccess) done_persist = true;
     else if (ep == cudaErrorNotSupported || ep == cudaErrorCooperativeLaunchTooLarge) cudaGetLastError();
     else CK(ep);
@@ -1036,7 +1039,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
-                                       "p_update", "ob_dots", "ob_update", "ssor"};
+                                       "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));
