@@ -723,7 +723,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
     const int off = modes == RG_MODES_SMALLEST ? rank - ke : 0;
     CK(launch_inv(sig + off, ke, inv, st));
     CK(launch_xm(c->Y, ld, c->n, s, V2 + (int64_t)off * s, s, ke, inv, c->Z, ld, c->st, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());  // stream-ordered: the solve (or rg_export) consumes W on the same stream
   }
   return RG_OK;
 }
