@@ -14,6 +14,9 @@ Parity status of each function:
                       space K_j(M_D A, M_D r_0), rows 2 = 5 (eq. equivalence_oblique), b = A W c
                       special case, W^T r = 0 on return, dense LU solution; obproj pinned by the
                       projector's defining properties (M_D A W = 0, W^T M_D = 0, M_D^2 = M_D, rank)
+  solve (orthogonal)  pinned: brute-force lstsq over the explicit Krylov space of (I - WW^T) A
+                      (rows 1 and 4, restarts, with the R19 per-cycle Galerkin completion), row 1 =
+                      row 4, b = AWc, W^T r = 0 on return, LU solution
   ssor / solve(precond) pinned: M^{-1} equals the inverse of the explicitly assembled SSOR matrix
                       (D + wL) D^{-1} (D + wU)/(w(2-w)) of the permuted matrix, w = 1 diagonal A
                       closed form, symmetric A -> symmetric M^{-1}, triangular A in the order ->
@@ -35,10 +38,11 @@ _LIB = None
 _i32p = ctypes.POINTER(ctypes.c_int32)
 _f64p = ctypes.POINTER(ctypes.c_double)
 
-PLAIN, AUGMENT, DEFLATE, OBLIQUE, OBLIQUE_AUG = 0, 1, 2, 3, 4
-# "oblique" = Table 1 row 5 (deflated oblique), "oblique_aug" = row 2 (augmented oblique)
+PLAIN, AUGMENT, DEFLATE, OBLIQUE, OBLIQUE_AUG, ORTHOGONAL, ORTHOGONAL_AUG = 0, 1, 2, 3, 4, 5, 6
+# "oblique" = Table 1 row 5 (deflated oblique), "oblique_aug" = row 2 (augmented oblique),
+# "orthogonal" = row 4 (deflated orthogonal), "orthogonal_aug" = row 1 (augmented orthogonal)
 VARIANTS = {"plain": PLAIN, "augment": AUGMENT, "deflate": DEFLATE, "oblique": OBLIQUE,
-            "oblique_aug": OBLIQUE_AUG}
+            "oblique_aug": OBLIQUE_AUG, "orthogonal": ORTHOGONAL, "orthogonal_aug": ORTHOGONAL_AUG}
 
 
 class _Mat(ctypes.Structure):

@@ -17,6 +17,8 @@
  *                           P = I - AW((AW)^T AW)^{-1}(AW)^T          PAPER.md:310, 348; eq. def_S_k_projected)
  *               with the start x_0 <- x0 + W (C^T C)^{-1} C^T r(x0), C = AW (the j = 0 case of the
  *               same minimisation; min-residual analogue of eq. projection_t_s).
+ *                 orthogonal: Table 1 rows 4 / 1: as oblique with the Krylov projector I - W W^T
+ *                            and the same per-cycle Galerkin start (R19)
  *                 oblique : Table 1 rows 5 / 2 (deflated / augmented oblique):
  *                           GMRES(m) on M_D A, M_D = I - AW E^{-1} W^T, E = W^T A W,
  *                           Galerkin start x_c += W E^{-1} W^T r(x_c) at every cycle (reading R15)
@@ -191,7 +193,7 @@ static int add_krylov_part(const or_mat* A, const or_prec* pc, const double* V, 
   return st;
 }
 
-static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2,
+static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2, int orth,
                          const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
                          double* hist, int hist_cap, const or_prec* pc);
 static int solve_impl(const or_mat* A, const double* b, const double* x0, int m, int variant,
@@ -232,9 +234,10 @@ int or_ssor(const or_mat* A, const int32_t* order, double omega, const double* z
 static int solve_impl(const or_mat* A, const double* b, const double* x0, int m, int variant,
                       const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
                       double* hist, int hist_cap, const or_prec* pc) {
-  if ((variant == 3 || variant == 4) && W != NULL && k > 0)
-    return solve_oblique(A, b, x0, m, variant == 4, W, k, tol, max_iters, x, rep, hist, hist_cap, pc);
-  if (variant == 3 || variant == 4) variant = 0;   /* no recycle space: plain GMRES */
+  if (variant >= 3 && variant <= 6 && W != NULL && k > 0)
+    return solve_oblique(A, b, x0, m, variant == 4 || variant == 6, variant >= 5, W, k, tol, max_iters, x, rep,
+                         hist, hist_cap, pc);
+  if (variant >= 3 && variant <= 6) variant = 0;   /* no recycle space: plain GMRES */
   const int64_t n = A->n;
   memset(rep, 0, sizeof(*rep));
   const int kk = (variant != 0 && W != NULL) ? k : 0;
@@ -448,8 +451,21 @@ static void ob_galerkin(const or_mat* A, const oblique_ctx* o, const double* b, 
   for (int l = 0; l < o->k; ++l) axpy(o->n, t[l], o->W + (int64_t)l * o->n, x);
 }
 
-/* Table 1 rows 5 ("deflated oblique", row2 = 0) and 2 ("augmented oblique", row2 = 1):
- * GMRES(m) on the Krylov operator M_D A, each restart cycle c being
+/* y <- (I - W W^T) y, the orthogonal projector of Table 1 rows 1 / 4 (W has
+ * orthonormal columns, "V_s any orthogonal matrix"), written as its formula: t = W^T y,
+ * y -= W t. */
+static void orth_apply(const oblique_ctx* o, double* y, double* t) {
+  for (int l = 0; l < o->k; ++l) t[l] = dot(o->n, o->W + (int64_t)l * o->n, y);
+  for (int l = 0; l < o->k; ++l) axpy(o->n, -t[l], o->W + (int64_t)l * o->n, y);
+}
+
+/* Table 1 rows 5 ("deflated oblique", row2 = 0) and 2 ("augmented oblique", row2 = 1); with
+ * orth = 1 rows 4 ("deflated orthogonal") and 1 ("augmented orthogonal"), whose Krylov operator is
+ * (I - W W^T) A instead of M_D A and whose minimised quantity is ||(I - WW^T)(r_c - A z)||.
+ * For orth the per-cycle Galerkin start is the COMPLETION of DESIGN.md R19: without it the W
+ * component of the residual is never reduced (true residual stalls at 3.7e-4).  Rows 1
+ * and 4 then coincide for the same reason rows 2 and 5 do (W^T r_c = 0 after the start).
+ * Oblique: GMRES(m) on the Krylov operator M_D A, each restart cycle c being
  *   x_c <- x_c + W E^{-1} W^T r(x_c)                  (Galerkin start of the cycle)
  *   r_c = b - A x_c  (recomputed; equals M_D r of the un-projected iterate)
  *   stop if ||r_c|| / ||b|| <= tol                    (TRUE residual)
@@ -461,7 +477,7 @@ static void ob_galerkin(const or_mat* A, const oblique_ctx* o, const double* b, 
  * start also serves as the final oblique correction, so on return V^T (b - A x) = 0.
  * reading R15 (Galerkin start at every restart; makes rows 2 and 5 coincide at every cycle, the
  * identity eq. equivalence_oblique). */
-static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2,
+static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2, int orth,
                          const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
                          double* hist, int hist_cap, const or_prec* pc) {
   const int64_t n = A->n;
@@ -498,7 +514,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
     if (rep->iterations >= max_iters) break;
     rep->cycles++;
     memcpy(rho, r, sizeof(double) * n);               /* target M_D r_c */
-    ob_apply(&o, rho, t);
+    if (orth) orth_apply(&o, rho, t); else ob_apply(&o, rho, t);
     memcpy(w, row2 ? r : rho, sizeof(double) * n);   /* Krylov initial vector */
     double v0n = nrm2(n, w);
     if (!(v0n > 0.0)) break;
@@ -506,7 +522,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
     int q = 0;
     for (int j = 0; j < m; ++j) {
       if (op_apply(A, pc, V + (int64_t)j * n, w)) { rep->status = 3; goto out; }  /* w = M_D A (M^{-1}) v_j */
-      ob_apply(&o, w, t);
+      if (orth) orth_apply(&o, w, t); else ob_apply(&o, w, t);
       memcpy(z, w, sizeof(double) * n);
       double wn = nrm2(n, w);
       double zn = mgs2(n, q, UZ, z, coef);

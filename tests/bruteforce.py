@@ -78,7 +78,7 @@ def oblique_projector(A, W):
     return np.eye(A.shape[0]) - A @ W @ np.linalg.inv(W.T @ A @ W) @ W.T
 
 
-def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False, Minv=None):
+def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False, Minv=None, orth=False):
     """Table 1 rows 5 (row2=False) / 2 (row2=True) with the Galerkin start at every cycle
     (R15): x_c <- x_c + W E^{-1} W^T r(x_c); z = argmin over K_j(M_D A, v) of
     ||M_D r_c - M_D A z|| with v = M_D r_c (row 5) or r_c (row 2).  Returns (x, iterations, history)."""
@@ -86,7 +86,8 @@ def restarted_oblique(A, b, m, W, tol=1e-8, max_iters=2000, row2=False, Minv=Non
     bn = np.linalg.norm(b)
     x = np.zeros(n)
     E = W.T @ A @ W
-    M = oblique_projector(A, W)
+    # Krylov projector: oblique M_D (rows 2/5) or the literal orthogonal I - W W^T (rows 1/4)
+    M = np.eye(A.shape[0]) - W @ W.T if orth else oblique_projector(A, W)
     Mi = np.eye(A.shape[0]) if Minv is None else Minv
     MA = M @ A @ Mi
     hist, iters = [], 0

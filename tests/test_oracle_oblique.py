@@ -128,3 +128,48 @@ def test_empty_recycle_space_is_plain(rng):
     p = oracle.solve(A, b, m=6, variant="plain")
     q = oracle.solve(A, b, m=6, variant="oblique", W=None)
     assert p["iterations"] == q["iterations"] and np.array_equal(p["x"], q["x"])
+
+
+# ------------------------------------------------------------------ orthogonal rows (1 and 4)
+@pytest.mark.parametrize("row1", [False, True])
+@pytest.mark.parametrize("m,k", [(5, 3), (9, 1), (6, 5)])
+def test_orthogonal_matches_brute_force(rng, row1, m, k):
+    """Table 1 rows 4 / 1 (Krylov operator (I - WW^T) A) with the per-cycle Galerkin
+    completion (R19): per-step equality with lstsq over the explicit space."""
+    n = 36
+    D = random_nonsym(n, rng, shift=1.6)
+    W = _orthonormal(n, k, rng)
+    b = rng.standard_normal(n)
+    var = "orthogonal_aug" if row1 else "orthogonal"
+    r = oracle.solve(oracle.Matrix.from_dense(D), b, m=m, variant=var, W=W, tol=1e-9, max_iters=800)
+    xb, itb, hb = restarted_oblique(D, b, m, W, tol=1e-9, max_iters=800, row2=row1, orth=True)
+    assert r["converged"]
+    assert r["iterations"] == itb
+    kk = min(len(hb), len(r["history"]))
+    assert np.allclose(r["history"][:kk], hb[:kk], rtol=1e-7, atol=1e-12)
+    assert np.linalg.norm(r["x"] - xb) <= 1e-7 * np.linalg.norm(xb)
+
+
+def test_orthogonal_rows_1_and_4_coincide_and_converge(rng):
+    n, k = 80, 5
+    D = random_nonsym(n, rng, shift=1.3)
+    W = _orthonormal(n, k, rng)
+    b = rng.standard_normal(n)
+    A = oracle.Matrix.from_dense(D)
+    p = oracle.solve(A, b, m=6, variant="orthogonal", W=W, tol=1e-10, max_iters=3000)
+    q = oracle.solve(A, b, m=6, variant="orthogonal_aug", W=W, tol=1e-10, max_iters=3000)
+    assert p["converged"] and q["converged"] and p["iterations"] == q["iterations"]
+    assert np.linalg.norm(p["x"] - q["x"]) <= 1e-9 * np.linalg.norm(p["x"])
+    xs = np.linalg.solve(D, b)
+    assert np.linalg.norm(p["x"] - xs) <= 1e-8 * np.linalg.norm(xs)
+    assert np.linalg.norm(W.T @ (b - D @ p["x"])) <= 1e-13 * np.linalg.norm(b)
+
+
+def test_orthogonal_rhs_in_image_of_recycle_space(rng):
+    n, k = 30, 4
+    D = random_nonsym(n, rng)
+    W = _orthonormal(n, k, rng)
+    c = rng.standard_normal(k)
+    r = oracle.solve(oracle.Matrix.from_dense(D), D @ W @ c, m=10, variant="orthogonal", W=W)
+    assert r["iterations"] == 0 and r["converged"]
+    assert np.linalg.norm(r["x"] - W @ c) <= 1e-12 * np.linalg.norm(c)
