@@ -7,7 +7,7 @@ space is rebuilt from the snapshot window (a3; C = A W and its QR are rebuilt in
 the system is solved with the recycled variant (a5-a10), and x_t is pushed as a snapshot (a2).
 
 Default workload: BASELINE.json configs[1] (C2, n = 262,144, GMRES(50), k = 10 from 20
-snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|augment|deflate|oblique.
+snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|augment|deflate|oblique|orthogonal.
 
   value      seconds per system (device time, CUDA events on the library's stream), whole job:
              max-over-ranks time / (systems solved by all ranks)
@@ -441,7 +441,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate", "oblique"])
+    ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate", "oblique", "orthogonal"])
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--precond", default="none", choices=["none", "ssor"],
                     help="right SSOR preconditioner in a multicolour order (SURVEY NEXT #2)")

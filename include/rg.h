@@ -62,8 +62,12 @@ typedef enum { RG_CSR = 0, RG_BSR = 1 } rg_format;
  *             preconditioner, eq. equivalence_oblique :325-330): GMRES(m) on M_D A with
  *             M_D = I - A W E^{-1} W^T, E = W^T A W (:229-239), and the Galerkin start
  *             x_c += W E^{-1} W^T r(x_c) (eq. projection_t_s, :289, :419) at every restart
- *             (reading R15).  Requires k_eff <= 32; E singular -> RG_E_SINGULAR. */
-typedef enum { RG_PLAIN = 0, RG_AUGMENT = 1, RG_DEFLATE = 2, RG_OBLIQUE = 3 } rg_variant;
+ *             (reading R15).  Requires k_eff <= 32; E singular -> RG_E_SINGULAR.
+ * RG_ORTHOGONAL Table 1 rows 4 / 1 "deflated / augmented orthogonal" (:341, :346): GMRES(m) on
+ *             (I - W W^T) A with the same per-restart Galerkin start, which is the completion that
+ *             makes the TRUE residual converge (R19); rows 1 and 4 coincide under it.
+ *             Same requirements as RG_OBLIQUE (the start needs E). */
+typedef enum { RG_PLAIN = 0, RG_AUGMENT = 1, RG_DEFLATE = 2, RG_OBLIQUE = 3, RG_ORTHOGONAL = 4 } rg_variant;
 typedef enum { RG_HOST = 0, RG_DEVICE = 1 } rg_mem;
 
 /* A sparse matrix handed to rg_create / rg_update_matrix.

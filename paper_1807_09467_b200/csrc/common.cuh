@@ -99,6 +99,12 @@ struct Layout {
   double* pt;      // cycle-end scratch: V y
 };
 
+// Galerkin-start variants (oblique, orthogonal): C = A W in columns [k, 2k), E^{-1} in the state.
+// The Krylov projector is I - P T W^T with P = C, T = E^{-1} (oblique) or P = W, T = I (orthogonal);
+// proj_base() is the first column of P.
+__host__ __device__ __forceinline__ bool galerkin_variant(int v) { return v == RG_OBLIQUE || v == RG_ORTHOGONAL; }
+__host__ __device__ __forceinline__ int proj_base(int v, int k) { return v == RG_ORTHOGONAL ? 0 : k; }
+
 // ---------------------------------------------------------------- small device helpers
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;

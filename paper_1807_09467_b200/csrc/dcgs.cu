@@ -96,13 +96,16 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   }
   // ---- coefficients of DK2 and the first-pass coefficients of column j
   const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
-  const bool obl = var == RG_OBLIQUE && k > 0;
+  const bool obl = galerkin_variant(var) && k > 0;  // oblique / orthogonal (P = C / W, T = E^{-1} / I)
+  const int pbase = proj_base(var, k);
   if (obl) {
     const double* wy = tot + 2 * p + 2;  // W^T y
-    const double* cu = wy + k;           // C^T u
+    const double* cu = wy + k;           // P^T u
     for (int l = tid; l < k; l += bd) {
       double t = 0.0;
-      for (int b2 = 0; b2 < k; ++b2) t += st->Einv[b2][l] * wy[b2];
+      if (var == RG_ORTHOGONAL) t = wy[l];
+      else
+        for (int b2 = 0; b2 < k; ++b2) t += st->Einv[b2][l] * wy[b2];
       ob_t[l] = t;
       double g = cu[l];                  // v_j^T C = (u - V_j a)^T C / nu
       for (int i = 0; i < j; ++i) g -= a[i] * st->Gm[i][l];
@@ -118,7 +121,7 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
         if (lane == 0) ob_ct[i] = s;
       }
     }
-    for (int l = tid; l < k; l += bd) st->coef[k + l] = -ob_t[l] * inv;
+    for (int l = tid; l < k; l += bd) st->coef[pbase + l] = -ob_t[l] * inv;
     __syncthreads();
   }
   // (H a_V)_c over the final columns 0..j-1 (Hessenberg) and (B a_V)_l: one warp per output,
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
   prof_begin(st, K_DK1);
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
-  const int nqd = (var == RG_AUGMENT) ? k : (var == RG_OBLIQUE ? 2 * k : 0);  // extra dots
+  const int nqd = (var == RG_AUGMENT) ? k : (galerkin_variant(var) ? 2 * k : 0);  // extra dots
   const bool have_y = j < st->m;                // no SpMV was run at j == m
   const bool keep = L.keep_l2 != 0;  // basis fits L2: let DK2 re-hit what DK1 streamed
   const int64_t ld = L.ld;
@@ -207,8 +210,9 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
     __syncthreads();
     const int cnt = (int)((r1 - base) < DT ? (r1 - base) : DT);
     for (int c = wid; c < p + nqd; c += 16) {
-      const bool obl = var == RG_OBLIQUE;  // extras: W^T y (cols [0,k)), C^T u (cols [k,2k))
-      const int col = c < p ? lo + c : (obl ? c - p : QB + (c - p));
+      // extras: W^T y (cols [0,k)), P^T u (P = C: cols [k,2k); P = W: cols [0,k) again)
+      const bool obl = galerkin_variant(var);
+      const int col = c < p ? lo + c : (obl ? ((c - p) < k ? c - p : proj_base(var, k) + (c - p - k)) : QB + (c - p));
       const double* __restrict__ zc = Z + (int64_t)col * ld + base + lane;
       double zv[RPL];
 #pragma unroll
@@ -267,8 +271,9 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
     cv[c] = st->coefv[lo + c];
     cn[c] = st->coef[lo + c];
   }
-  const int k2 = var == RG_OBLIQUE ? k : 0;  // oblique: next u also gets -C t / nu (C = cols [k, 2k))
-  for (int l = threadIdx.x; l < k2; l += DT) cc2[l] = st->coef[k + l];
+  const int k2 = galerkin_variant(var) ? k : 0;  // next u also gets -P t / nu (P = C or W)
+  const int pb2 = proj_base(var, k);
+  for (int l = threadIdx.x; l < k2; l += DT) cc2[l] = st->coef[pb2 + l];
   const double inv = st->k2_inv_nu, fy = st->k2_y, fu = st->k2_u_next;
   __syncthreads();
   const int64_t ng = ld >> 5;
@@ -293,7 +298,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
       sv += cv[c] * z;
       sn += cn[c] * z;
     }
-    for (int l = 0; l < k2; ++l) sn += cc2[l] * (keep ? Z[(int64_t)(k + l) * ld + r] : __ldcs(Z + (int64_t)(k + l) * ld + r));
+    for (int l = 0; l < k2; ++l) sn += cc2[l] * (keep ? Z[(int64_t)(pb2 + l) * ld + r] : __ldcs(Z + (int64_t)(pb2 + l) * ld + r));
     u[r] = ur * inv + sv;
     y[r] = yr * fy + ur * fu + sn;
   }

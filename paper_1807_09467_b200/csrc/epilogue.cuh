@@ -274,12 +274,19 @@ __device__ __forceinline__ void epi_cs_dq(DevState* st, const Layout& L, const d
 // ---------------------------------------------------------------- oblique projection
 // tot[0..k) = W^T w.  t = E^{-1} W^T w -> coef[k + l] (the update w -= C t, C in columns [k, 2k));
 // at the cycle start also coefx[l] = -t_l (OP_XW: x += W t, the Galerkin start of PAPER.md:289).
+// Orthogonal variant, Arnoldi step: t = W^T w -> coef[l] (w -= W t: the projector I - W W^T).
 __device__ __forceinline__ void epi_ob(DevState* st, const double* tot, bool cycle_start) {
   const int k = st->k_eff;
+  const bool orth = !cycle_start && st->variant == RG_ORTHOGONAL;
+  const int pb = orth ? 0 : k;
   for (int a = threadIdx.x; a < k; a += blockDim.x) {
     double t = 0.0;
-    for (int b = 0; b < k; ++b) t += st->Einv[b][a] * tot[b];
-    st->coef[k + a] = t;
+    if (orth) {
+      t = tot[a];
+    } else {
+      for (int b = 0; b < k; ++b) t += st->Einv[b][a] * tot[b];
+    }
+    st->coef[pb + a] = t;
     if (cycle_start) st->coefx[a] = -t;
   }
   __syncthreads();

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
     case OP_OB_CSD: w = L.Z + (int64_t)VB * ld; d0 = 0; d1 = k; break;
     case OP_OB_CSU: w = L.Z + (int64_t)VB * ld; u0 = k; u1 = 2 * k; nrmflag = true; break;
     case OP_OB_SD: w = L.Z + (int64_t)(VB + j + 1) * ld; d0 = 0; d1 = k; break;
-    case OP_OB_SU: w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = k; u1 = 2 * k; break;
+    case OP_OB_SU: w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = proj_base(var, k); u1 = u0 + k; break;
     default: w = const_cast<double*>(L.b); nrmflag = true; break;  // OP_NORMB (read only)
   }
   const bool upd = (u1 > u0) || (u3 > u2) || (op == OP_XUPD && L.prec) || op == OP_VY;

@@ -210,7 +210,9 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   const int m = pa.m, k = pa.k, VB = L.VB, QB = VB - k;
   const bool obl = pa.obl != 0;
   const int lo = obl ? VB : QB, nq = obl ? 0 : k;  // P = [Q | V] (deflate) or V (plain, oblique)
-  const int nx = obl ? 2 * k : 0;                   // extra dots per step: W^T y, C^T u
+  const int nx = obl ? 2 * k : 0;                   // extra dots per step: W^T y, P^T u
+  const bool orthp = pa.obl == 2;                   // orthogonal: projector I - W W^T (P = W, T = I)
+  const int pbase = orthp ? 0 : k;                  // first column of P (C = A W at [k, 2k) or W)
   const int64_t ld = L.ld;
   double* Z = L.Z;
   // ---- shared-memory layout (replicated least-squares state + staging)
@@ -417,7 +419,8 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         const int cnt = (int)min((int64_t)PT, r1 - base);
         constexpr int RPL = PT / 32;
         for (int c = wid; c < p + nx; c += PT / 32) {
-          const double* zc = Z + (int64_t)(c < p ? lo + c : c - p) * ld + base + lane;
+          const int zcol = c < p ? lo + c : ((c - p) < k ? c - p : pbase + (c - p - k));
+          const double* zc = Z + (int64_t)zcol * ld + base + lane;
           double zv[RPL];
 #pragma unroll
           for (int q = 0; q < RPL; ++q)  // 16 independent loads in flight per lane
@@ -519,7 +522,9 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         const double* cu = wy + k;
         for (int l = tid; l < k; l += PT) {
           double t = 0.0;
-          for (int c = 0; c < k; ++c) t += st->Einv[c][l] * wy[c];
+          if (orthp) t = wy[l];
+          else
+            for (int c = 0; c < k; ++c) t += st->Einv[c][l] * wy[c];
           zk[l] = t;
           double g = cu[l];
           for (int i = 0; i < j; ++i) g -= a[i] * Bs[i * k + l];
@@ -588,7 +593,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
           sn2 += cn[c] * z;
         }
         if (obl)
-          for (int l = 0; l < k; ++l) sn2 += wk[l] * Z[(int64_t)(k + l) * ld + r];
+          for (int l = 0; l < k; ++l) sn2 += wk[l] * Z[(int64_t)(pbase + l) * ld + r];
         u[r] = ur * inv + sv;
         y[r] = yr * inv + ur * fu + sn2;
       }
@@ -665,7 +670,7 @@ size_t persistent_smem(int m, int k) {
 // Returns cudaErrorNotSupported when the configuration is outside this path.
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
                               unsigned* flags, int m, int k, int variant, cudaStream_t s) {
-  if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE && variant != RG_OBLIQUE) || A.fmt == 2)
+  if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE && !galerkin_variant(variant)) || A.fmt == 2)
     return cudaErrorNotSupported;
   const size_t smem = persistent_smem(m, k);
   static int max_smem = -1;
@@ -685,7 +690,8 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
-  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k, variant == RG_OBLIQUE && k > 0 ? 1 : 0, flags, nbsync};
+  PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k,
+           galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, flags, nbsync};
   void* args[] = {&pa};
   return cudaLaunchCooperativeKernel((const void*)k_solve_persistent, dim3(G), dim3(PT), args, smem, s);
 }

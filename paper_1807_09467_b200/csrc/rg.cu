@@ -373,7 +373,7 @@ rg_status build_c_oblique(rg_ctx* c) {
 cudaError_t cycle_start(rg_ctx* c, int variant) {
   cudaError_t e = launch_spmv(c->A, c->L, c->st, SM_RES, nullptr, nullptr, variant == RG_PLAIN ? 1 : 0, c->stream);
   if (e != cudaSuccess || variant == RG_PLAIN) return e;
-  if (variant == RG_OBLIQUE) {  // Galerkin start x += W t, r -= C t, t = E^{-1} W^T r
+  if (galerkin_variant(variant)) {  // Galerkin start x += W t, r -= C t, t = E^{-1} W^T r
     if ((e = launch_orth(c->L, c->st, OP_OB_CSD, c->stream)) != cudaSuccess) return e;
     if ((e = launch_orth(c->L, c->st, OP_XW, c->stream)) != cudaSuccess) return e;
     return launch_orth(c->L, c->st, OP_OB_CSU, c->stream);
@@ -401,7 +401,7 @@ cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
   } else if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP, nullptr, nullptr, 0, c->stream)) != cudaSuccess) {
     return e;
   }
-  if (c->cur_var == RG_OBLIQUE && !c->dcgs_now) {  // w = M_D A v_j = A v_j - C E^{-1} W^T A v_j
+  if (galerkin_variant(c->cur_var) && !c->dcgs_now) {  // w = M_D A v_j = A v_j - C E^{-1} W^T A v_j (or (I-WW^T) A v_j)
     if ((e = launch_orth(c->L, c->st, OP_OB_SD, c->stream)) != cudaSuccess) return e;
     if ((e = launch_orth(c->L, c->st, OP_OB_SU, c->stream)) != cudaSuccess) return e;
   }
@@ -736,7 +736,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (m < 1 || m > c->max_m) return fail(RG_E_INVAL, "m must be in 1..max_m");
   if (!(tol > 0.0)) return fail(RG_E_INVAL, "tol must be > 0");
   if (max_iters < 1) return fail(RG_E_INVAL, "max_iters must be >= 1");
-  if (v != RG_PLAIN && v != RG_AUGMENT && v != RG_DEFLATE && v != RG_OBLIQUE) return fail(RG_E_INVAL, "unknown variant");
+  if (v != RG_PLAIN && v != RG_AUGMENT && v != RG_DEFLATE && v != RG_OBLIQUE && v != RG_ORTHOGONAL)
+    return fail(RG_E_INVAL, "unknown variant");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
   if (history_cap < 0) return fail(RG_E_INVAL, "history_cap < 0");
   cudaStream_t s = c->stream;
@@ -745,9 +746,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   const int k = eff == RG_PLAIN ? 0 : c->k_eff;
   int c_spmv = 0;
   bool check_c = false;
-  const int want_kind = eff == RG_OBLIQUE ? 1 : 0;
+  const int want_kind = galerkin_variant(eff) ? 1 : 0;
   if (eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind)) {
-    if ((rs = (eff == RG_OBLIQUE ? build_c_oblique(c) : build_c(c, false))) != RG_OK) return rs;
+    if ((rs = (galerkin_variant(eff) ? build_c_oblique(c) : build_c(c, false))) != RG_OK) return rs;
     c->c_kind = want_kind;
     c_spmv = k;
     check_c = true;
@@ -807,7 +808,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     c->have_W = false;
     c->k_eff = 0;
     c->c_valid = false;
-    return fail(RG_E_SINGULAR, eff == RG_OBLIQUE ? "E = W^T A W is numerically singular; recycle space cleared"
+    return fail(RG_E_SINGULAR, galerkin_variant(eff) ? "E = W^T A W is numerically singular; recycle space cleared"
                                                  : "A W is numerically rank deficient (R_C singular); recycle space cleared");
   }
   if (h->bzero) {

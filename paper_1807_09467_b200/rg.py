@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "lib", "librg.so")
 
 RG_OK, RG_E_INVAL, RG_E_NOMEM, RG_E_CUDA, RG_E_STATE, RG_E_SINGULAR, RG_E_NUMERIC = range(7)
 RG_CSR, RG_BSR = 0, 1
-RG_PLAIN, RG_AUGMENT, RG_DEFLATE, RG_OBLIQUE = 0, 1, 2, 3
+RG_PLAIN, RG_AUGMENT, RG_DEFLATE, RG_OBLIQUE, RG_ORTHOGONAL = 0, 1, 2, 3, 4
 RG_HOST, RG_DEVICE = 0, 1
 RG_FLAG_NO_GRAPH, RG_FLAG_PROFILE, RG_FLAG_CGS2, RG_FLAG_NO_PERSIST = 1, 2, 4, 8
 RG_EXPORT_W, RG_EXPORT_Q, RG_EXPORT_RC = 0, 1, 2
@@ -25,7 +25,8 @@ RG_MODES_LARGEST, RG_MODES_SMALLEST = 0, 1
 RG_PREC_NONE, RG_PREC_SSOR = 0, 1
 PRECS = {None: RG_PREC_NONE, "none": RG_PREC_NONE, "ssor": RG_PREC_SSOR}
 MODES = {"largest": RG_MODES_LARGEST, "smallest": RG_MODES_SMALLEST}
-VARIANTS = {"plain": RG_PLAIN, "augment": RG_AUGMENT, "deflate": RG_DEFLATE, "oblique": RG_OBLIQUE}
+VARIANTS = {"plain": RG_PLAIN, "augment": RG_AUGMENT, "deflate": RG_DEFLATE, "oblique": RG_OBLIQUE,
+            "orthogonal": RG_ORTHOGONAL}
 STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E_STATE",
           5: "RG_E_SINGULAR", 6: "RG_E_NUMERIC"}
 

@@ -98,7 +98,7 @@ def test_spmv_full_size_sampled_rows(name, rng):
 
 
 # ------------------------------------------------------------------------------------- solves
-@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique", "orthogonal"])
 @pytest.mark.parametrize("n,m,k", [(200, 10, 4), (1023, 25, 8), (64, 64, 3)])
 def test_solve_random_vs_oracle(variant, n, m, k, rng):
     hm = random_csr(n, rng, per_row=(2, 8), diag=2.2)
@@ -127,7 +127,7 @@ def test_solve_random_vs_oracle(variant, n, m, k, rng):
     assert np.linalg.norm(Wg @ Wg.T - W @ W.T, 2) <= 1e-10
     h = rep["history"]
     assert len(h) == rep["iterations"]
-    if variant == "oblique":  # final Galerkin/oblique correction: W^T (b - A x) = 0
+    if variant in ("oblique", "orthogonal"):  # final Galerkin correction: W^T (b - A x) = 0
         assert np.linalg.norm(W.T @ r) <= 1e-11 * np.linalg.norm(b)
         kk = min(len(h), len(ref["history"]))   # Givens estimates vs the oracle's explicit minima
         assert np.allclose(h[:kk], ref["history"][:kk], rtol=1e-5, atol=1e-11)
@@ -164,7 +164,7 @@ def test_rhs_in_image_of_recycle_space(rng):
     ctx.build_recycle(k)
     c = rng.standard_normal(k)
     b = hm.to_scipy() @ (W @ c)
-    for v in ("augment", "deflate", "oblique"):
+    for v in ("augment", "deflate", "oblique", "orthogonal"):
         x = torch.zeros(n, dtype=torch.float64, device=DEV)
         rep = ctx.solve(t(b), x, m=10, variant=v)
         assert rep["iterations"] == 0 and rep["converged"]
@@ -240,7 +240,7 @@ def test_recycle_operator_thin_qr(name, N, sell, rng):
     assert np.allclose(np.tril(R, -1), 0.0)
 
 
-@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique", "orthogonal"])
 def test_persistent_and_graph_paths_agree(variant, rng):
     """The single cooperative-kernel solve and the CUDA-graph solve compute the same iterates
     (same DCGS2 arithmetic, different reduction trees): same iteration counts, x within 1e-10."""
@@ -351,7 +351,7 @@ def test_singular_recycle_operator_reported(variant, rng):
     assert e.value.status == rgb.RG_E_STATE
 
 
-@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique", "orthogonal"])
 def test_dcgs2_and_cgs2_paths_agree(variant, rng):
     """Delayed CGS2 (one reduction per step; the oblique projection folded into its coefficients)
     and classical CGS2 (explicit M_D A v_j) give the same iterates."""

@@ -57,7 +57,7 @@ def test_ssor_apply_vs_oracle(rng, n, omega):
     assert torch.equal(y, y2)
 
 
-@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique", "orthogonal"])
 def test_preconditioned_solve_vs_oracle(rng, variant):
     n, m, k = 1500, 20, 6
     hm = random_csr(n, rng, diag=1.6)

@@ -56,12 +56,12 @@ def run(cfg, variant, T, k=None):
     return rows
 
 
-@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique", "orthogonal"])
 def test_c1_full_sequence(variant):
     run(synth.CONFIGS["C1"], variant, 10)
 
 
-@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique", "orthogonal"])
 def test_c2_reduced(variant):
     run(synth.CONFIGS["C2"].reduced(96), variant, 6)
 
@@ -80,8 +80,9 @@ def test_c5_reduced_bsr(variant):
     run(synth.CONFIGS["C5"].reduced(3), variant, 5)
 
 
-def test_c3_reduced_sell_oblique():
-    run(synth.CONFIGS["C3"].reduced(96), "oblique", 5)
+@pytest.mark.parametrize("variant", ["oblique", "orthogonal"])
+def test_c3_reduced_sell_galerkin(variant):
+    run(synth.CONFIGS["C3"].reduced(96), variant, 5)
 
 
 def run_schedule(cfg, variant, T, ell=1, modes="largest", k=None):
