@@ -1,0 +1,3 @@
+for c in C1 C2 C3 C4; do for v in deflate oblique orthogonal plain; do
+  timeout 300 python bench.py --config $c --variant $v --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c','$v', round(d['value']*1e3,4), sum(d['config']['iterations_timed']), d['roofline']['kernel'], d['roofline']['frac'])" || echo "$c $v FAILED"
+done; done
