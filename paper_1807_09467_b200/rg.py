@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librg.so")
+LIB_PATH = os.environ.get("RG_LIB_PATH") or os.path.join(_HERE, "lib", "librg.so")  # override: A/B experiments
 
 RG_OK, RG_E_INVAL, RG_E_NOMEM, RG_E_CUDA, RG_E_STATE, RG_E_SINGULAR, RG_E_NUMERIC = range(7)
 RG_CSR, RG_BSR = 0, 1
