@@ -53,10 +53,12 @@ cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cud
 
 // Whole solve in one cooperative kernel (persistent.cu): plain / deflate, CSR / SELL, m <= 64,
 // k <= 64.  cudaErrorNotSupported when outside that scope (caller uses the graph path).
-// bar: [BAR_WORDS] zeroed barrier words; flags: [NSM * 8] zeroed neighbour-sync epochs.
+// bar: [BAR_WORDS] zeroed barrier words; flags: [NSM * 8] zeroed neighbour-sync epochs;
+// P: right SSOR preconditioner (nullptr: none; needs L.pz, L.pt).
 constexpr int BAR_WORDS = 64;
+struct PrecDev;
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
-                              unsigned* flags, int m, int k, int variant, cudaStream_t s);
+                              unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s);
 
 // ---- multicolour SSOR(omega) preconditioner (precond.cu)
 constexpr int MAXCOLORS = 64;

@@ -34,6 +34,11 @@ struct PArgs {
   int obl;              // oblique variant (k = k_eff > 0, C = A W in columns [k, 2k))
   unsigned* flags;      // [gridDim.x] neighbour-sync epochs (zeroed before the launch)
   int nbsync;           // 1: point-to-point neighbour sync before the SpMVs instead of grid barriers
+  int prec;             // right multicolour SSOR preconditioner (precond.cu's colour-ordered L/U copies)
+  PrecDev P;
+  double* pz;           // M^{-1} u (step) / M^{-1} V y (cycle end)
+  double* pt;           // V y (cycle end)
+  double pc_bytes;      // algorithmic bytes of one SSOR application
 };
 
 // ---- grid barrier (all CTAs co-resident: cooperative launch).  Spins with a timeout so that a
@@ -280,6 +285,58 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
     __syncthreads();
   }
 
+  // ---- SSOR: this CTA's rows of colour c are perm[s_ilo[c] .. s_ihi[c]) (perm is row-sorted per colour)
+  __shared__ int s_ilo[MAXCOLORS], s_ihi[MAXCOLORS];
+  const bool prec = pa.prec != 0;
+  if (prec) {
+    const int64_t rend = r1 < L.n ? r1 : L.n;
+    for (int c = tid; c < pa.P.ncolors; c += PT) {
+      auto lower = [&](int64_t row) {  // first idx of colour c with perm[idx] >= row
+        int64_t lo2 = pa.P.coff[c], hi2 = pa.P.coff[c + 1];
+        while (lo2 < hi2) {
+          const int64_t mid = (lo2 + hi2) >> 1;
+          if (pa.P.perm[mid] < row) lo2 = mid + 1;
+          else hi2 = mid;
+        }
+        return (int)lo2;
+      };
+      s_ilo[c] = lower(r0 < rend ? r0 : rend);
+      s_ihi[c] = lower(rend);
+    }
+    __syncthreads();
+  }
+  // out = M^{-1} in on this CTA's rows; `in` is read on own rows only.  Sweep c waits for the
+  // neighbours' previous sweep (their rows of the colours it reads are final), then publishes.
+  auto ssor_apply = [&](const double* in, double* out) -> bool {
+    const int nc = pa.P.ncolors;
+    const double om = pa.P.omega, sc = om * (2.0 - om);
+    for (int pass = 0; pass < 2 * nc - 1; ++pass) {
+      const bool bwd = pass >= nc;
+      const int c = bwd ? 2 * nc - 2 - pass : pass;
+      if (pass > 0) {
+        if (nbs) {
+          if (!nb_wait(pa.flags, s_clo, s_chi, epoch, &s_fail)) return false;
+        } else if (!gbar(pa.bar, &s_fail)) {
+          return false;
+        }
+      }
+      const int32_t* __restrict__ rp = bwd ? pa.P.Urp : pa.P.Lrp;
+      const int32_t* __restrict__ ci = bwd ? pa.P.Uci : pa.P.Lci;
+      const double* __restrict__ vv = bwd ? pa.P.Uv : pa.P.Lv;
+      for (int idx = s_ilo[c] + tid; idx < s_ihi[c]; idx += PT) {
+        const int32_t r = pa.P.perm[idx];
+        double s = 0.0;
+        for (int32_t q = rp[idx]; q < rp[idx + 1]; ++q) s += vv[q] * out[ci[q]];
+        const double di = pa.P.dinv[idx];
+        out[r] = bwd ? out[r] - om * s * di : (sc * in[r] - om * s) * di;
+      }
+      if (nbs) nb_publish(pa.flags, ++epoch);
+      else __syncthreads();
+    }
+    if (nbs) return nb_wait(pa.flags, s_clo, s_chi, epoch, &s_fail);  // out complete on the owners
+    return gbar(pa.bar, &s_fail);
+  };
+
   // ---- ||b||
   {
     double s = 0.0;
@@ -401,8 +458,15 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       const int nv = 2 * p + 2 + nx;
       for (int c = tid; c < nv; c += PT) dpart[c] = 0.0;
       double s_uu = 0.0, s_uy = 0.0;
-      if (have_y)  // SpMV over this CTA's rows first (many rows in flight), then the dot pass
-        for (int64_t r = r0 + tid; r < r1; r += PT) y[r] = r < L.n ? row_dot(A, r, u) : 0.0;
+      if (have_y) {  // SpMV over this CTA's rows first (many rows in flight), then the dot pass
+        const double* sx = u;
+        if (prec) {  // y = A M^{-1} u
+          if (!ssor_apply(u, pa.pz)) goto fail;
+          sx = pa.pz;
+          if (cta0) bytes += pa.pc_bytes;
+        }
+        for (int64_t r = r0 + tid; r < r1; r += PT) y[r] = r < L.n ? row_dot(A, r, sx) : 0.0;
+      }
       for (int64_t base = r0; base < r1; base += PT) {
         const int64_t r = base + tid;
         double ur = 0.0, yr = 0.0;
@@ -627,9 +691,23 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         }
         __syncthreads();
       }
+      if (prec) {  // x += M^{-1} (V y) - W part
+        for (int64_t r = r0 + tid; r < r1; r += PT) {
+          double t = 0.0;
+          for (int i = 0; i <= jf; ++i) t += ys[i] * Z[(int64_t)(VB + i) * ld + r];
+          pa.pt[r] = t;
+        }
+        __syncthreads();
+        if (!ssor_apply(pa.pt, pa.pz)) goto fail;
+        if (cta0) bytes += pa.pc_bytes + 16.0 * L.n;
+      }
       for (int64_t r = r0 + tid; r < r1; r += PT) {
         double xr = x[r];
-        for (int i = 0; i <= jf; ++i) xr += ys[i] * Z[(int64_t)(VB + i) * ld + r];
+        if (prec) {
+          xr += pa.pz[r];
+        } else {
+          for (int i = 0; i <= jf; ++i) xr += ys[i] * Z[(int64_t)(VB + i) * ld + r];
+        }
         for (int l = 0; l < kx; ++l) xr -= zk[l] * Z[(int64_t)l * ld + r];
         x[r] = xr;
       }
@@ -669,7 +747,7 @@ size_t persistent_smem(int m, int k) {
 
 // Returns cudaErrorNotSupported when the configuration is outside this path.
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
-                              unsigned* flags, int m, int k, int variant, cudaStream_t s) {
+                              unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s) {
   if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE && !galerkin_variant(variant)) || A.fmt == 2)
     return cudaErrorNotSupported;
   const size_t smem = persistent_smem(m, k);
@@ -691,7 +769,13 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
   PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k,
-           galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, flags, nbsync};
+           galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, flags, nbsync,
+           P ? 1 : 0, P ? *P : PrecDev(), L.pz, L.pt, 0.0};
+  if (P) {
+    double b2 = 0.0;
+    for (int c = 0; c < P->ncolors; ++c) b2 += 12.0 * (double)(P->cL[c] + P->cU[c]);
+    pa.pc_bytes = b2 + 8.0 * (double)L.n * 6.0;  // + perm, row pointers, 1/a_rr, in, out (fwd), out r/w (bwd)
+  }
   void* args[] = {&pa};
   return cudaLaunchCooperativeKernel((const void*)k_solve_persistent, dim3(G), dim3(PT), args, smem, s);
 }

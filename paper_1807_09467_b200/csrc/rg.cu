@@ -781,10 +781,11 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
   const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
   c->L.prec = c->prec_kind ? 1 : 0;
-  if (c->use_persist && persist_size && c->dcgs_now && !c->L.prec && !(c->flags & RG_FLAG_NO_GRAPH)) {
+  if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
     CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
     CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 8, s));
-    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, m, k, eff, s);
+    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, m, k, eff,
+                                       c->L.prec ? &c->P : nullptr, s);
     if (ep == cudaSuccess) done_persist = true;
     else if (ep == cudaErrorNotSupported || ep == cudaErrorCooperativeLaunchTooLarge) cudaGetLastError();
     else CK(ep);

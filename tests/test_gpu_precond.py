@@ -183,3 +183,31 @@ def test_invalid_inputs_and_pattern_change(rng):
     with pytest.raises(rgb.RgError) as e:
         ctx.apply_preconditioner(t(np.ones(200)), y)
     assert e.value.status == rgb.RG_E_STATE
+
+
+@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique"])
+def test_persistent_and_graph_paths_agree_preconditioned(rng, variant):
+    """SSOR sweeps inside the cooperative solve (neighbour-synchronised colour sweeps) and the
+    per-colour launches of the graph path give the same iterates."""
+    from paper_1807_09467_b200 import rg as rgb
+    cfg = synth.CONFIGS["C2"].reduced(160)
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    hm = seq.matrix(1, u)
+    b = seq.rhs(1, u)
+    snaps = [rng.standard_normal(cfg.n) for _ in range(4)]
+    out = []
+    for flags in (0, rgb.RG_FLAG_NO_PERSIST):
+        ctx = ctx_for(hm, max_m=cfg.m, s=8, k=4, flags=flags)
+        ctx.set_preconditioner("ssor", 1.1)
+        for v in snaps:
+            ctx.push_snapshot(t(v))
+        ctx.build_recycle(4)
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=cfg.m, variant=variant, history_cap=1000)
+        out.append((rep, x.cpu().numpy()))
+        ctx.close()
+    (r0, x0), (r1, x1) = out
+    assert r0["converged"] and r1["converged"]
+    assert abs(r0["iterations"] - r1["iterations"]) <= 1
+    assert np.linalg.norm(x0 - x1) <= 1e-9 * np.linalg.norm(x1)
