@@ -110,18 +110,47 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML polled
+    every 2 ms from a background thread (nvidia-smi's 100 ms loop would see one sample of a
+    ~0.1 s region); falls back to `nvidia-smi -lms 100` when NVML is unavailable."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
+        self.thread = None
+        self.samples = []
         self.path = os.path.join("/tmp", f"rg_clocks_{os.getpid()}.csv")
 
+    def _poll(self, pynvml, h):
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop:
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), {n for n, b in bits.items() if rs & b}))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
     def __enter__(self):
+        self.stop = False
+        try:
+            import threading
+
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.thread = threading.Thread(target=self._poll, args=(pynvml, h), daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.thread = None
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
@@ -132,6 +161,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *a):
+        self.stop = True
+        if self.thread is not None:
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -141,10 +173,16 @@ class ClockSampler:
             self.f.close()
 
     def summary(self):
+        if self.thread is not None:
+            if not self.samples:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no NVML samples"], "samples": 0}
+            reasons = set().union(*[r for _, _, r in self.samples])
+            return {"sm_mhz": statistics.median([s for s, _, _ in self.samples]),
+                    "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": sorted(reasons),
+                    "samples": len(self.samples), "source": "nvml, 2 ms"}
         if self.proc is None or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             p = [x.strip() for x in line.split(",")]
             if len(p) < 7:
@@ -154,11 +192,11 @@ class ClockSampler:
                 mx.append(float(p[1]))
             except ValueError:
                 continue
-            for nm, v in zip(names, p[3:7]):
-                if v.lower().startswith("active"):
+            for nm, v in zip(self.NAMES, p[3:7]):
+                if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi, 100 ms"}
 
 
 # ---------------------------------------------------------------------------------------- our arm
@@ -437,7 +475,9 @@ def run_reference(args, cfg):
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed systems; default: the rest of the config's sequence after the warm-up "
+                         "(C2: 47 of 50) for our arm, 3 for --impl reference")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2")
@@ -459,6 +499,8 @@ def main(argv=None):
         print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
     import synth
     cfg = synth.CONFIGS[args.config]
+    if args.steps is None:
+        args.steps = 3 if args.impl == "reference" else max(1, cfg.systems - args.warmup)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:
