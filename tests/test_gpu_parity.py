@@ -398,3 +398,50 @@ def test_maximum_restart_and_recycle_dimension(variant, k, rng):
     assert rep["converged"] and ref["converged"]
     assert abs(rep["iterations"] - ref["iterations"]) <= 2
     assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-8 * np.linalg.norm(ref["x"])
+
+
+def test_variant_switching_on_one_context(rng):
+    """One context, one recycle space, the variants in turn: the C = A W / Q / E^{-1} state is
+    rebuilt whenever the variant family changes (LS projection vs Galerkin start)."""
+    n, m, k = 3000, 20, 5
+    hm = random_csr(n, rng, per_row=(2, 8), diag=2.0)
+    W = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    ctx = make_ctx(hm, max_m=m, s=k, k=k)
+    for i in range(k):
+        ctx.push_snapshot(t(W[:, i] * (k - i)))
+    assert ctx.build_recycle(k)[0] == k
+    M = oracle.Matrix.from_host(hm)
+    for variant in ("deflate", "oblique", "augment", "orthogonal", "deflate", "oblique", "plain"):
+        b = rng.standard_normal(n)
+        x = torch.zeros(n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=m, variant=variant, tol=1e-9)
+        ref = oracle.solve(M, b, m=m, variant=variant, W=None if variant == "plain" else W, tol=1e-9)
+        assert rep["converged"] and ref["converged"], variant
+        assert abs(rep["iterations"] - ref["iterations"]) <= 2, (variant, rep["iterations"], ref["iterations"])
+        assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"]), variant
+
+
+@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique"])
+def test_persistent_multi_cta_wide_pattern(variant, rng):
+    """A random pattern couples every row range with every other one, so the persistent solve's
+    neighbour synchronisation must wait on all CTAs (n = 20,000: many CTAs)."""
+    from paper_1807_09467_b200 import rg as rgb
+    n, m, k = 20000, 25, 4
+    hm = random_csr(n, rng, per_row=(3, 7), diag=2.4)
+    W = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    b = rng.standard_normal(n)
+    outs = []
+    for flags in (0, rgb.RG_FLAG_NO_PERSIST):
+        ctx = make_ctx(hm, max_m=m, s=k, k=k, flags=flags)
+        for i in range(k):
+            ctx.push_snapshot(t(W[:, i] * (k - i)))
+        ctx.build_recycle(k)
+        x = torch.zeros(n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=m, variant=variant, tol=1e-9)
+        outs.append((rep, x.cpu().numpy()))
+        ctx.close()
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=m, variant=variant, W=None if variant == "plain" else W,
+                       tol=1e-9)
+    for rep, xg in outs:
+        assert rep["converged"] and abs(rep["iterations"] - ref["iterations"]) <= 2
+        assert np.linalg.norm(xg - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
