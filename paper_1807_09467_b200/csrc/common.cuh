@@ -188,17 +188,29 @@ __device__ __forceinline__ bool grid_reduce(const double* vals, int nv, double* 
   const int G = gridDim.x;
   const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   (void)scr;
-  if (nv > 2 * nw) {  // many columns (Gram): thread per column, CTAs summed in index order
-    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+  if (nv > 2 * nw) {
+    // many columns: S consecutive threads per column (S = largest power of two <= 32 with
+    // S * nv <= blockDim); thread `sub` of a column sums the partials of CTAs sub, sub + S, ...
+    // with 16 independent L2 loads in flight, then a fixed shuffle tree of width S.  (A thread
+    // per column summing all G partials in batches of 8 was ~37 dependent L2 round trips: ~10 us
+    // of last-CTA tail per launch at G = 296.)
+    int S = 1;
+    while (S < 32 && 2 * S * nv <= (int)blockDim.x) S <<= 1;
+    const int sub = threadIdx.x % S, groups = blockDim.x / S;
+    for (int c0 = 0; c0 < nv; c0 += groups) {
+      const int c = c0 + (int)threadIdx.x / S;
       double a = 0.0;
-      for (int b = 0; b < G; b += 8) {
-        double v[8];
+      if (c < nv) {
+        for (int b = sub; b < G; b += S * 16) {
+          double v[16];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = b + u < G ? __ldcg(&partial[(size_t)(b + u) * ldp + c]) : 0.0;
+          for (int u = 0; u < 16; ++u) v[u] = b + u * S < G ? __ldcg(&partial[(size_t)(b + u * S) * ldp + c]) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a += v[u];
+          for (int u = 0; u < 16; ++u) a += v[u];
+        }
       }
-      tot[c] = a;
+      for (int o = S >> 1; o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o, S);
+      if (c < nv && sub == 0) tot[c] = a;
     }
     __syncthreads();
     if (threadIdx.x == 0) *counter = 0u;
