@@ -239,7 +239,7 @@ class GpuRun:
             self.gen.fill(self.t, self.x, val_ptr=self.vals_ptr)   # the solver's value buffer (a1)
             self.ctx.update_values_inplace(self.nnz)
         if self.variant != "plain" and self.nsnap > 0:
-            self.ctx.build_recycle(self.k)             # a3 (a4 happens inside the solve)
+            self.k_eff, self.sigma = self.ctx.build_recycle(self.k)   # a3 (a4 happens inside the solve)
         rep = self.ctx.solve(self.gen.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol)
         if not rep["converged"]:
             raise RuntimeError(f"system {self.t} did not converge: {rep}")
