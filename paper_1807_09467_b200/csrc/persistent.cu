@@ -117,8 +117,10 @@ __device__ __forceinline__ int row_owner(int64_t row, int64_t ng, int G) {
 // c, c+G, ... over CTAs in index order; every CTA then reads the nv totals into `tot`.
 // (Measured: a single "last CTA reduces" wave is slower here — the reducing CTA competes with ~300
 // pollers — and so is a one-barrier variant in which every CTA reduces all columns itself (296 CTAs
-// x all partials from L2: C2 reduce phase 6.8 -> 23.8 ms per 10 systems); the work is spread over
-// all CTAs between two barriers.)
+// x all partials from L2: C2 reduce phase 6.8 -> 23.8 ms per 10 systems), and so is a thread-block-
+// cluster variant (DSMEM sum inside clusters of 2/4/8 CTAs, one grid barrier, every CTA summing the
+// G/CS cluster partials: reduce phase +40..140 %: every CTA reading the same few KB hot-spots the
+// same L2 lines); the work is spread over all CTAs between two barriers.)
 __device__ __forceinline__ bool greduce(const double* vals, int nv, double* partial, double* tot_g, double* tot,
                                         unsigned* bar, int* s_fail, DevState* st = nullptr) {
   if (gridDim.x == 1) {  // single CTA: the CTA's values are the totals
