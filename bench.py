@@ -358,10 +358,12 @@ def run_ours(args, cfg):
             run.step()
         torch.cuda.synchronize()
         run.ctx.reset_kernel_stats()
+        gen0 = run.gen.launches
         with ClockSampler(local) as clk:
             per, t_local, t_max = timed_replicas(run.step, args.steps, 0, dist_on, device, "cuda",
                                                  between=lambda: flush_l2(flush), stream=stream)
         kstats = run.ctx.kernel_stats()
+        gen_launches = run.gen.launches - gen0
         value = t_max / (args.steps * ws)
         timed_iters = run.iters[args.warmup:]
 
@@ -416,8 +418,13 @@ def run_ours(args, cfg):
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": bytes_per, "avg_launch_us": ms_per * 1e3,
                 "share_of_step": round(s["ms"] / 1e3 / t_local, 4)}
-    # device-counted kernel launches (the p_* entries are phase timers inside the persistent solve)
-    launches = sum(s["launches"] + s["noop"] for kname, s in kstats.items() if not kname.startswith("p_"))
+    # kernel launches in the timed region: device-counted executions (incl. launches that found nothing
+    # to do), the library's host-launched kernels, and the input generator's kernels.  Not summed:
+    # the p_* phase timers inside the persistent solve and "ssor" (per application; its kernels are
+    # counted in "ssor_sweep_kernels").  Under profiling, a "gram" entry counts its two kernels as one
+    # (the second is in "host_launched").
+    launches = sum(s["launches"] + s["noop"] for kname, s in kstats.items()
+                   if not kname.startswith("p_") and kname != "ssor") + gen_launches
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
         times, its = oracle_time(cfg, args.variant, k, args.cpu_systems, budget_s=args.cpu_budget,

@@ -451,6 +451,7 @@ __global__ void k_validate(const int32_t* rp, const int32_t* ci, int64_t nrows, 
 
 cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G, double* partial,
                         unsigned* counter, DevState* st, cudaStream_t strm) {
+  note_host_launches(1);
   int64_t g = (n + GTR - 1) / GTR;
   if (g > GRAM_CTAS) g = GRAM_CTAS;
   const int gi = (int)(g < 1 ? 1 : g);
@@ -474,6 +475,7 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
 
 cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const double* M, int ldm, int q,
                       const double* colscale, double* Y, int64_t ldy, DevState* st, cudaStream_t strm) {
+  note_host_launches(1);
   const size_t smem = sizeof(double) * (S8MAX * XMS + XTR * GTS + XTR * XMS);
   static bool init = false;
   if (!init) {
@@ -487,28 +489,33 @@ cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const doub
 }
 
 cudaError_t launch_inv(const double* sigma, int q, double* out, cudaStream_t strm) {
+  note_host_launches(1);
   k_inv<<<1, 64, 0, strm>>>(sigma, q, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_einv(const double* G, int k, DevState* st, int* fail, cudaStream_t strm) {
+  note_host_launches(1);
   if (k < 1 || k > EK) return cudaErrorInvalidValue;
   k_einv<<<1, 256, 0, strm>>>(G, k, st, fail);
   return cudaGetLastError();
 }
 
 cudaError_t launch_chol(const double* G, int k, double* R, double* Rinv, int* fail, cudaStream_t strm) {
+  note_host_launches(1);
   k_chol<<<1, 256, 0, strm>>>(G, k, R, Rinv, fail);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rc_finish(const double* R1, const double* R1i, const double* R2, const double* R2i,
                              int k, DevState* st, int* fail, cudaStream_t strm) {
+  note_host_launches(1);
   k_rc_finish<<<1, 256, 0, strm>>>(R1, R1i, R2, R2i, k, st, fail);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaStream_t strm) {
+  note_host_launches(1);
   k_sell_widths<<<NSM * 4, 256, 0, strm>>>(rp, n, sw);
   return cudaGetLastError();
 }
@@ -516,12 +523,14 @@ cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaSt
 cudaError_t launch_sell_pack(const int32_t* rp, const int32_t* ci, const double* v, int64_t n,
                              const int64_t* sp, const int32_t* sw, int32_t* sci, double* sv,
                              int pattern, cudaStream_t strm) {
+  note_host_launches(1);
   k_sell_pack<<<NSM * 8, 256, 0, strm>>>(rp, ci, v, n, sp, sw, sci, sv, pattern);
   return cudaGetLastError();
 }
 
 cudaError_t launch_validate(const int32_t* rp, const int32_t* ci, int64_t nrows, int64_t ncols,
                             int64_t nnz, int* bad, cudaStream_t strm) {
+  note_host_launches(1);
   k_validate<<<NSM * 4, 256, 0, strm>>>(rp, ci, nrows, ncols, nnz, bad);
   return cudaGetLastError();
 }

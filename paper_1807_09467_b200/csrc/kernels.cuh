@@ -23,6 +23,11 @@ struct MatDev {
   double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
 };
 
+// Kernels launched directly by the host without a device-side counter (recycle build, CholQR2,
+// E^{-1}, SELL packing, validation, SSOR value refresh) are counted here; rg_kernel_stats reports
+// the total as the entry "host_launched".
+void note_host_launches(int n);
+
 enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2, SM_STEP_PC = 3 };
 
 // w = A v_j (STEP), r = b - A x (RES; epi != 0 runs the cycle-start epilogue on ||r||^2),

@@ -31,8 +31,11 @@ struct OrthArgs {
 
 // Sets a WHILE-node condition from the device state: which = 0 -> st->active (Arnoldi loop),
 // which = 1 -> !st->done (restart-cycle loop).
-__global__ void k_cond(const DevState* st, cudaGraphConditionalHandle h, int which) {
-  if (threadIdx.x == 0) cudaGraphSetConditional(h, which == 0 ? (st->active ? 1u : 0u) : (st->done ? 0u : 1u));
+__global__ void k_cond(DevState* st, cudaGraphConditionalHandle h, int which) {
+  if (threadIdx.x == 0) {
+    cudaGraphSetConditional(h, which == 0 ? (st->active ? 1u : 0u) : (st->done ? 0u : 1u));
+    if (st->profile) st->kstat[K_COND].launches++;
+  }
 }
 
 __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(CT, 2) k_cgs(Layout L, DevState* st, unsigned 
 }  // namespace
 
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s) {
-  k_cond<<<1, 32, 0, s>>>(st, (cudaGraphConditionalHandle)h, which);
+  k_cond<<<1, 32, 0, s>>>(const_cast<DevState*>(st), (cudaGraphConditionalHandle)h, which);
   return cudaGetLastError();
 }
 

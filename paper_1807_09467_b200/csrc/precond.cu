@@ -81,8 +81,9 @@ __global__ void __launch_bounds__(ST) k_ssor(SsorArgs a) {
 }
 
 // closes the K_SSOR timing interval after the last sweep of one application
-__global__ void k_ssor_done(DevState* st, int gate) {
+__global__ void k_ssor_done(DevState* st, int gate, int nsweeps) {
   if (!st->profile) return;
+  st->kstat[K_SSORK].launches += nsweeps + 1;  // kernel launches of this application (incl. this one)
   if (gate == 1 && (!st->active || (st->dcgs && st->j >= st->m))) return;
   if (gate == 2 && !st->have_xupd) return;
   KStatDev& k = st->kstat[K_SSOR];
@@ -101,6 +102,7 @@ __global__ void k_ssor_values(PrecDev P, const double* __restrict__ v, int64_t n
 }  // namespace
 
 cudaError_t launch_ssor_values(const PrecDev& P, const double* v, int64_t n, cudaStream_t s) {
+  note_host_launches(1);
   const int64_t work = std::max(std::max(P.nL, P.nU), n);
   int64_t g = (work + ST - 1) / ST;
   if (g > (int64_t)NSM * 8) g = (int64_t)NSM * 8;
@@ -129,7 +131,7 @@ cudaError_t launch_ssor(const PrecDev& P, const Layout& L, DevState* st, const d
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
-  k_ssor_done<<<1, 1, 0, s>>>(st, gate);
+  k_ssor_done<<<1, 1, 0, s>>>(st, gate, 2 * P.ncolors - 1);
   return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstddef>
 #include <cstdio>
@@ -22,9 +23,14 @@
 
 using namespace rg;
 
+namespace rg {
+void note_host_launches(int n);
+}
+
 namespace {
 
 thread_local std::string g_err;
+std::atomic<long long> g_host_launches{0};
 
 rg_status fail(rg_status s, const std::string& msg) {
   g_err = msg;
@@ -52,6 +58,8 @@ struct GraphKey {
 };
 
 }  // namespace
+
+void rg::note_host_launches(int n) { g_host_launches += n; }
 
 struct rg_ctx {
   int dev = 0;
@@ -1041,7 +1049,8 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
-                                       "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive"};
+                                       "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
+                                       "ssor_sweep_kernels"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));
@@ -1058,7 +1067,13 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
     o.tail_ms = ks[i].tail_ns * 1e-6;
     o.bytes = ks[i].bytes;
   }
-  *count = out ? n : K_COUNT;
+  if (out && n < cap) {  // kernels launched directly by the host (no device counter)
+    rg_kstat& o = out[n++];
+    memset(&o, 0, sizeof(o));
+    strncpy(o.name, "host_launched", sizeof(o.name) - 1);
+    o.launches = (int64_t)g_host_launches.load();
+  }
+  *count = out ? n : K_COUNT + 1;
   return RG_OK;
 }
 
@@ -1066,6 +1081,7 @@ RG_API rg_status rg_reset_kernel_stats(rg_ctx* c) {
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
   CK(cudaMemsetAsync(&c->st->kstat[0], 0, sizeof(KStatDev) * K_COUNT, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  g_host_launches = 0;
   return RG_OK;
 }
 

@@ -556,6 +556,7 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
   if (g > NSM * 8) g = NSM * 8;
   for (int k0 = 0; k0 < k; k0 += 16) {
     k_spmm_rows<16><<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(A, W, Y, ld, k0, k - k0 < 16 ? k - k0 : 16);
+    note_host_launches(1);
   }
   return cudaGetLastError();
 }

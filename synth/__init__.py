@@ -331,6 +331,8 @@ class DeviceSequence:
                 self.val.copy_(torch.from_numpy(h._fixed))
         self.b = torch.empty(self.n, dtype=torch.float64, device=device)
 
+    launches = 0  # device kernels launched by fill() (one per generator call)
+
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream().cuda_stream)
 
@@ -343,25 +345,32 @@ class DeviceSequence:
         dst = vp(val_ptr if val_ptr is not None else self.val.data_ptr())
         if cfg.kind == "bsr":
             if self._t == 0 or t < self._t:
+                self.launches += 1
                 C.syd_c5_values(self.host.col_idx.shape[0], cfg.B, cfg.seed, vp(self.kind.data_ptr()),
                                 0.1 * 1.5, 0.1 * 0.5, dst, st)
                 self._t = 1
+                self.launches += 1
                 C.syd_normal_vec(self.n, cfg.seed, 0xB, vp(self.b.data_ptr()), st)
             while self._t < t:
                 self._t += 1
+                self.launches += 1
                 C.syd_c5_perturb(self.val.numel(), cfg.seed, self._t, dst, st)
             return
         sc = self.host.scalars()
         if cfg.kind == "5pt":
             if cfg.cid == 2:
+                self.launches += 1
                 C.syd_fill5_values(cfg.N, sc["cd"], sc["ih"], sc["idt"], 0.0, 0.0, vp(u_prev_dev.data_ptr()),
                                    vp(self.row_ptr.data_ptr()), dst, st)
             else:
                 bx, by = velocity(cfg, t)
+                self.launches += 1
                 C.syd_fill5_values(cfg.N, sc["cd"], sc["ih"], sc["idt"], bx, by, None,
                                    vp(self.row_ptr.data_ptr()), dst, st)
         elif cfg.kind == "7pt":
             bx, by, bz = velocity(cfg, t)
+            self.launches += 1
             C.syd_fill7_values(cfg.N, sc["cd"], sc["ih"], sc["idt"], bx, by, bz,
                                vp(self.row_ptr.data_ptr()), dst, st)
+        self.launches += 1
         C.syd_rhs(self.n, vp(u_prev_dev.data_ptr()), cfg.dt, cfg.forcing, vp(self.b.data_ptr()), st)
