@@ -8,7 +8,9 @@
  * window of previous solutions (Algorithm 1), used through
  *   augmentation: search space x_c + span(W) + K_j(A, r_c)
  *   deflation   : x_c + span(W) + K_j(P A, P r_c), P = I - AW((AW)^T AW)^{-1}(AW)^T
- *                 (Table 1 row "deflated LS" :348; = GCRO inner iteration :332).
+ *                 (Table 1 row "deflated LS" :348; = GCRO inner iteration :332),
+ * or through the Galerkin start and the oblique / orthogonal projectors of Table 1 rows 1, 2, 4, 5
+ * (rg_variant), optionally with a right SSOR preconditioner (rg_set_preconditioner).
  * Every step runs in hand-written fp64 CUDA kernels for sm_100a; there is no CPU fallback.
  *
  * Conventions shared by all entry points
@@ -111,8 +113,9 @@ typedef struct {
 #define RG_FLAG_PROFILE 2  /* record per-kernel device time (%globaltimer) for rg_kernel_stats */
 #define RG_FLAG_CGS2 4     /* classical CGS2 (3 reductions per Arnoldi step) instead of the default
                               delayed CGS2 (1 reduction per step); same iterates in exact arithmetic */
-#define RG_FLAG_NO_PERSIST 8 /* never use the single cooperative-kernel solve (plain/deflate, CSR/SELL,
-                                m <= 64); always use the CUDA-graph path */
+#define RG_FLAG_NO_PERSIST 8 /* never use the single cooperative-kernel solve (every variant but
+                                augment, CSR/SELL, m <= 64, k <= 64, n_pad <= 1.6M); always use the
+                                CUDA-graph path */
 
 /* Solve report (fields follow SPEC.md's SolveReport).
  *   iterations   Arnoldi steps summed over restart cycles (residual and C = AW products are
