@@ -108,6 +108,7 @@ struct rg_ctx {
   int s_count = 0, s_head = 0;
   int k_eff = 0;
   bool have_W = false;
+  int v1prev_s = 0;         // size of the stored first-pass eigenvectors (Jacobi warm start), 0 = none
   bool c_valid = false;
   int c_kind = 0;           // what c_valid refers to: 0 Q / R_C (augment, deflate), 1 C / E^{-1} (oblique)
   bool use_dcgs = true;
@@ -683,6 +684,7 @@ RG_API rg_status rg_push_snapshot(rg_ctx* c, const double* x, rg_mem mem) {
 RG_API rg_status rg_clear_snapshots(rg_ctx* c) {
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
   c->s_count = c->s_head = 0;
+  c->v1prev_s = 0;
   c->have_W = false;
   c->k_eff = 0;
   c->c_valid = false;
@@ -707,9 +709,12 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   double* V2 = c->small + 3 * SMALL;
   double* sig = c->small + 4 * SMALL;
   double* inv = c->small + 5 * SMALL;
-  // pass 1: G = X^T X, Jacobi -> V1 ; Y = X V1
+  // pass 1: G = X^T X, Jacobi -> V1 (warm-started from the previous build's V1) ; Y = X V1
+  double* V1prev = c->small + 8 * SMALL;
   CK(launch_gram(c->X, ld, c->n, s, G, c->partial, c->counter, c->st, st));
-  CK(launch_jacobi(G, s, lam, V1, nullptr, c->st, st));
+  CK(launch_jacobi(G, s, lam, V1, nullptr, c->st, st, V1prev, c->v1prev_s <= s ? c->v1prev_s : 0));
+  CK(cudaMemcpyAsync(V1prev, V1, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
+  c->v1prev_s = s;
   CK(launch_xm(c->X, ld, c->n, s, V1, s, s, nullptr, c->Y, ld, c->st, st));
   // pass 2: Y^T Y (nearly diagonal, column-scaled) -> V2, sigma
   CK(launch_gram(c->Y, ld, c->n, s, G, c->partial, c->counter, c->st, st));
@@ -717,6 +722,11 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   std::vector<double> hs(s);
   CK(cudaMemcpyAsync(hs.data(), sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (getenv("RG_DEBUG")) {
+    double sw[2] = {0.0, 0.0};
+    cudaMemcpy(sw, lam + s, 2 * sizeof(double), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "rg_build_recycle: s=%d, Jacobi sweeps %.0f (pass 1) %.0f (pass 2)\n", s, sw[0], sw[1]);
+  }
   int rank = 0;
   for (int i = 0; i < s; ++i)
     if (hs[0] > 0.0 && hs[i] > 1e-12 * hs[0]) ++rank;
