@@ -26,11 +26,25 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // Stage GTR rows x s8 columns of the column-major Y into a row-major shared tile (zero padded).
-__device__ __forceinline__ void stage_tile(double* tile, const double* __restrict__ Y, int64_t ld, int64_t n,
-                                           int s, int s8, int64_t r0) {
-  for (int e = threadIdx.x; e < GTR * s8; e += blockDim.x) {
+// All of a thread's loads are issued before its shared-memory stores (one memory round trip per
+// tile; a load-then-store loop made it one round trip per element: k_gram_mma / k_xm ran at
+// ~0.65 TB/s).  Requires blockDim.x == 256.
+// The kernels keep the NEXT tile's registers in flight while they compute on the current one.
+constexpr int STG_PER_THREAD = GTR * S8MAX / 256;
+__device__ __forceinline__ void tile_load(double* v, const double* __restrict__ Y, int64_t ld, int64_t n, int s,
+                                          int s8, int64_t r0) {
+#pragma unroll
+  for (int u = 0; u < STG_PER_THREAD; ++u) {
+    const int e = threadIdx.x + u * 256;
     const int c = e / GTR, r = e % GTR;  // consecutive threads: consecutive rows (coalesced)
-    tile[r * GTS + c] = (c < s && r0 + r < n) ? __ldcs(Y + (int64_t)c * ld + r0 + r) : 0.0;
+    v[u] = (e < GTR * s8 && c < s && r0 + r < n) ? __ldcs(Y + (int64_t)c * ld + r0 + r) : 0.0;
+  }
+}
+__device__ __forceinline__ void tile_store(double* tile, const double* v, int s8) {
+#pragma unroll
+  for (int u = 0; u < STG_PER_THREAD; ++u) {
+    const int e = threadIdx.x + u * 256;
+    if (e < GTR * s8) tile[(e % GTR) * GTS + e / GTR] = v[u];
   }
 }
 
@@ -55,10 +69,13 @@ __global__ void __launch_bounds__(GT) k_gram_mma(const double* __restrict__ Y, i
   }
   const int nq = (np - wid + 7) / 8;
   const int64_t ntiles = (n + GTR - 1) / GTR;
+  double v[STG_PER_THREAD];
+  if ((int64_t)blockIdx.x < ntiles) tile_load(v, Y, ld, n, s, s8, (int64_t)blockIdx.x * GTR);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     __syncthreads();
-    stage_tile(tile, Y, ld, n, s, s8, t * GTR);
+    tile_store(tile, v, s8);
     __syncthreads();
+    if (t + gridDim.x < ntiles) tile_load(v, Y, ld, n, s, s8, (t + gridDim.x) * GTR);  // next tile in flight
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       if (q < nq) {
@@ -260,11 +277,15 @@ __global__ void __launch_bounds__(XT) k_xm(const double* __restrict__ X, int64_t
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t ntiles = (n + XTR - 1) / XTR;
+  static_assert(XTR == GTR, "k_xm stages GTR-row tiles");
+  double v[STG_PER_THREAD];
+  if ((int64_t)blockIdx.x < ntiles) tile_load(v, X, ldx, n, s, s8, (int64_t)blockIdx.x * XTR);
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t r0 = t * XTR;
     __syncthreads();
-    stage_tile(tile, X, ldx, n, s, s8, r0);
+    tile_store(tile, v, s8);
     __syncthreads();
+    if (t + gridDim.x < ntiles) tile_load(v, X, ldx, n, s, s8, (t + gridDim.x) * XTR);  // next tile in flight
     double acc[S8MAX / 8][2];
 #pragma unroll
     for (int cb = 0; cb < S8MAX / 8; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
