@@ -14,7 +14,7 @@ namespace {
 constexpr int GT = 256;         // threads of the Gram kernel (8 warps)
 constexpr int GTR = 64;         // rows per Gram tile
 constexpr int S8MAX = 64;       // s rounded up to a multiple of 8
-constexpr int GTS = S8MAX + 1;  // tile row stride (odd: spreads banks)
+
 constexpr int GRAM_CTAS = NSM * 2;
 constexpr int GPL = S8MAX * S8MAX;  // partial stride per CTA
 
@@ -25,26 +25,27 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// Stage GTR rows x s8 columns of the column-major Y into a row-major shared tile (zero padded).
-// All of a thread's loads are issued before its shared-memory stores (one memory round trip per
-// tile; a load-then-store loop made it one round trip per element: k_gram_mma / k_xm ran at
-// ~0.65 TB/s).  Requires blockDim.x == 256.
-// The kernels keep the NEXT tile's registers in flight while they compute on the current one.
-constexpr int STG_PER_THREAD = GTR * S8MAX / 256;
-__device__ __forceinline__ void tile_load(double* v, const double* __restrict__ Y, int64_t ld, int64_t n, int s,
-                                          int s8, int64_t r0) {
-#pragma unroll
-  for (int u = 0; u < STG_PER_THREAD; ++u) {
-    const int e = threadIdx.x + u * 256;
-    const int c = e / GTR, r = e % GTR;  // consecutive threads: consecutive rows (coalesced)
-    v[u] = (e < GTR * s8 && c < s && r0 + r < n) ? __ldcs(Y + (int64_t)c * ld + r0 + r) : 0.0;
-  }
+// ---- cp.async ring of column-major tiles: stage[c * TS + r] = Y(r0 + r, c), 64 rows, s8 columns
+// (columns >= s zero-filled by a 0-byte source).  16-byte copies of row pairs; NST tiles in flight
+// per CTA without holding registers (the register-staged version above kept one).
+constexpr int TS = GTR + 4;   // column stride (doubles): fragment reads hit 16 distinct 8-byte banks
+constexpr int NST = 3;        // ring stages
+__device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  if (valid)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, 0;" ::"r"(d), "l"(src) : "memory");
 }
-__device__ __forceinline__ void tile_store(double* tile, const double* v, int s8) {
-#pragma unroll
-  for (int u = 0; u < STG_PER_THREAD; ++u) {
-    const int e = threadIdx.x + u * 256;
-    if (e < GTR * s8) tile[(e % GTR) * GTS + e / GTR] = v[u];
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_stages() { asm volatile("cp.async.wait_group %0;" ::"n"(NST - 2) : "memory"); }
+// rows r0 .. r0+63 exist in the column-major buffer (n_pad is a multiple of 64; padding rows are 0)
+__device__ __forceinline__ void tile_issue(double* stage, const double* __restrict__ Y, int64_t ld, int s, int s8,
+                                           int64_t r0) {
+  for (int e = threadIdx.x; e < s8 * (GTR / 2); e += blockDim.x) {
+    const int c = e / (GTR / 2), i = e % (GTR / 2);
+    const bool ok = c < s;
+    cp16(stage + c * TS + 2 * i, Y + (int64_t)(ok ? c : 0) * ld + r0 + 2 * i, ok);
   }
 }
 
@@ -52,7 +53,7 @@ __device__ __forceinline__ void tile_store(double* tile, const double* v, int s8
 // DMMA; warp w owns pairs w, w+8, ... and keeps their 8x8 accumulators in registers across tiles.
 __global__ void __launch_bounds__(GT) k_gram_mma(const double* __restrict__ Y, int64_t ld, int64_t n, int s,
                                                  double* __restrict__ partial, DevState* st) {
-  __shared__ double tile[GTR * GTS];
+  extern __shared__ double ring[];     // NST x s8 x TS
   if (st) prof_begin(st, K_GRAM);
   const int s8 = (s + 7) & ~7, nb = s8 / 8, np = nb * (nb + 1) / 2;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -69,23 +70,31 @@ __global__ void __launch_bounds__(GT) k_gram_mma(const double* __restrict__ Y, i
   }
   const int nq = (np - wid + 7) / 8;
   const int64_t ntiles = (n + GTR - 1) / GTR;
-  double v[STG_PER_THREAD];
-  if ((int64_t)blockIdx.x < ntiles) tile_load(v, Y, ld, n, s, s8, (int64_t)blockIdx.x * GTR);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    __syncthreads();
-    tile_store(tile, v, s8);
-    __syncthreads();
-    if (t + gridDim.x < ntiles) tile_load(v, Y, ld, n, s, s8, (t + gridDim.x) * GTR);  // next tile in flight
+  const int sstride = s8 * TS;
+  for (int i = 0; i < NST - 1; ++i) {  // prologue: the first NST-1 tiles of this CTA
+    const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
+    if (t < ntiles) tile_issue(ring + i * sstride, Y, ld, s, s8, t * GTR);
+    cp_commit();
+  }
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    cp_wait_stages();
+    __syncthreads();  // tile `it` complete for every thread; stage (it-1) % NST free again
+    const int64_t tn = t + (int64_t)(NST - 1) * gridDim.x;
+    if (tn < ntiles) tile_issue(ring + ((it + NST - 1) % NST) * sstride, Y, ld, s, s8, tn * GTR);
+    cp_commit();
+    const double* tile = ring + (it % NST) * sstride;
 #pragma unroll
     for (int q = 0; q < MAXQ; ++q) {
       if (q < nq) {
-        const double* ta = tile + (lane & 3) * GTS + pi[q] * 8 + (lane >> 2);
-        const double* tb = tile + (lane & 3) * GTS + pj[q] * 8 + (lane >> 2);
+        const double* ta = tile + (pi[q] * 8 + (lane >> 2)) * TS + (lane & 3);
+        const double* tb = tile + (pj[q] * 8 + (lane >> 2)) * TS + (lane & 3);
 #pragma unroll
-        for (int kk = 0; kk < GTR / 4; ++kk) dmma(acc[q][0], acc[q][1], ta[kk * 4 * GTS], tb[kk * 4 * GTS]);
+        for (int kk = 0; kk < GTR / 4; ++kk) dmma(acc[q][0], acc[q][1], ta[kk * 4], tb[kk * 4]);
       }
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   double* P = partial + (size_t)blockIdx.x * GPL;
 #pragma unroll
   for (int q = 0; q < MAXQ; ++q) {
@@ -266,9 +275,10 @@ __global__ void __launch_bounds__(XT) k_xm(const double* __restrict__ X, int64_t
                                            const double* __restrict__ colscale, double* Y, int64_t ldy,
                                            DevState* st) {
   extern __shared__ double sm[];
-  double* Ms = sm;                     // S8MAX x XMS : Ms[a * XMS + c]
-  double* tile = Ms + S8MAX * XMS;     // XTR x GTS   : tile[r * GTS + a]
-  double* out = tile + XTR * GTS;      // XTR x XMS   : out[r * XMS + c]
+  const int s8_ = (s + 7) & ~7;
+  double* Ms = sm;                     // s8 x XMS    : Ms[a * XMS + c]
+  double* out = Ms + s8_ * XMS;        // XTR x XMS   : out[r * XMS + c]
+  double* ring = out + XTR * XMS;      // NST x s8 x TS column-major tiles
   (void)st;
   const int s8 = (s + 7) & ~7, q8 = (q + 7) & ~7, ncb = q8 / 8;
   for (int e = threadIdx.x; e < s8 * q8; e += XT) {
@@ -278,20 +288,27 @@ __global__ void __launch_bounds__(XT) k_xm(const double* __restrict__ X, int64_t
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t ntiles = (n + XTR - 1) / XTR;
   static_assert(XTR == GTR, "k_xm stages GTR-row tiles");
-  double v[STG_PER_THREAD];
-  if ((int64_t)blockIdx.x < ntiles) tile_load(v, X, ldx, n, s, s8, (int64_t)blockIdx.x * XTR);
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  const int sstride = s8 * TS;
+  for (int i = 0; i < NST - 1; ++i) {
+    const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
+    if (t < ntiles) tile_issue(ring + i * sstride, X, ldx, s, s8, t * XTR);
+    cp_commit();
+  }
+  int it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
     const int64_t r0 = t * XTR;
-    __syncthreads();
-    tile_store(tile, v, s8);
-    __syncthreads();
-    if (t + gridDim.x < ntiles) tile_load(v, X, ldx, n, s, s8, (t + gridDim.x) * XTR);  // next tile in flight
+    cp_wait_stages();
+    __syncthreads();  // tile `it` complete; the previous tile's output staging has been written out
+    const int64_t tn = t + (int64_t)(NST - 1) * gridDim.x;
+    if (tn < ntiles) tile_issue(ring + ((it + NST - 1) % NST) * sstride, X, ldx, s, s8, tn * XTR);
+    cp_commit();
+    const double* tile = ring + (it % NST) * sstride;
     double acc[S8MAX / 8][2];
 #pragma unroll
     for (int cb = 0; cb < S8MAX / 8; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
-    const double* ta = tile + (wid * 8 + (lane >> 2)) * GTS + (lane & 3);
+    const double* ta = tile + (lane & 3) * TS + wid * 8 + (lane >> 2);
     for (int k4 = 0; k4 < s8; k4 += 4) {
-      const double a = ta[k4];
+      const double a = ta[k4 * TS];
       const double* mb = Ms + (k4 + (lane & 3)) * XMS + (lane >> 2);
 #pragma unroll
       for (int cb = 0; cb < S8MAX / 8; ++cb)
@@ -311,6 +328,7 @@ __global__ void __launch_bounds__(XT) k_xm(const double* __restrict__ X, int64_t
       if (r0 + r < n) Y[(int64_t)c * ldy + r0 + r] = out[r * XMS + c];
     }
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 __global__ void k_inv(const double* sigma, int q, double* out) {
@@ -500,10 +518,17 @@ __global__ void k_validate(const int32_t* rp, const int32_t* ci, int64_t nrows, 
 cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G, double* partial,
                         unsigned* counter, DevState* st, cudaStream_t strm) {
   note_host_launches(1);
+  const int s8 = (s + 7) & ~7;
+  const size_t smem = sizeof(double) * NST * s8 * TS;
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(k_gram_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * NST * S8MAX * TS));
+    init = true;
+  }
   int64_t g = (n + GTR - 1) / GTR;
   if (g > GRAM_CTAS) g = GRAM_CTAS;
   const int gi = (int)(g < 1 ? 1 : g);
-  k_gram_mma<<<gi, GT, 0, strm>>>(Y, ld, n, s, partial, st);
+  k_gram_mma<<<gi, GT, smem, strm>>>(Y, ld, n, s, partial, st);
   const int P = s * (s + 1) / 2;
   k_gram_reduce<<<(P + 7) / 8, 256, 0, strm>>>(partial, gi, s, G, counter, st, 8.0 * (double)n * s);
   return cudaGetLastError();
@@ -524,14 +549,19 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
 cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const double* M, int ldm, int q,
                       const double* colscale, double* Y, int64_t ldy, DevState* st, cudaStream_t strm) {
   note_host_launches(1);
-  const size_t smem = sizeof(double) * (S8MAX * XMS + XTR * GTS + XTR * XMS);
+  const int s8 = (s + 7) & ~7;
+  const size_t smem = sizeof(double) * (s8 * XMS + XTR * XMS + NST * s8 * TS);
   static bool init = false;
   if (!init) {
-    cudaFuncSetAttribute(k_xm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_xm, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (S8MAX * XMS + XTR * XMS + NST * S8MAX * TS)));
     init = true;
   }
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xm, XT, smem);
   int64_t g = (n + XTR - 1) / XTR;
-  if (g > NSM * 2) g = NSM * 2;
+  const int64_t cap = (int64_t)NSM * (occ < 1 ? 1 : (occ > 4 ? 4 : occ));
+  if (g > cap) g = cap;
   k_xm<<<(int)(g < 1 ? 1 : g), XT, smem, strm>>>(X, ldx, n, s, M, ldm, q, colscale, Y, ldy, st);
   return cudaGetLastError();
 }
