@@ -772,7 +772,11 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     check_c = true;
   }
   c->cur_var = eff;
-  c->dcgs_now = c->use_dcgs;
+  // DCGS2 saves two reductions and one basis pass per Arnoldi step but spends one extra SpMV per
+  // cycle (the step after the stopping column).  When one SpMV moves more bytes than a whole pass
+  // over the basis (C5: 7.3 GB vs ~0.8 GB), classical CGS2 is cheaper (measured C5: see DESIGN.md).
+  const double basis_pass = 8.0 * (double)c->n * (double)(k + m + 2);
+  c->dcgs_now = c->use_dcgs && !(c->A.bytes > basis_pass && !getenv("RG_FORCE_DCGS"));
   if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
   if (x0) {
     if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
