@@ -557,8 +557,12 @@ cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const doub
                          (int)(sizeof(double) * (S8MAX * XMS + XTR * XMS + NST * S8MAX * TS)));
     init = true;
   }
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xm, XT, smem);
+  static int occ_s8[S8MAX / 8 + 1] = {0};  // occupancy per panel width (queried once each)
+  int& occ = occ_s8[s8 / 8];
+  if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xm, XT, smem) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 1;
+  }
   int64_t g = (n + XTR - 1) / XTR;
   const int64_t cap = (int64_t)NSM * (occ < 1 ? 1 : (occ > 4 ? 4 : occ));
   if (g > cap) g = cap;

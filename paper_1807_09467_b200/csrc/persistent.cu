@@ -761,8 +761,17 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
     max_smem = 200 * 1024;
   }
   if (smem > (size_t)max_smem) return cudaErrorNotSupported;
-  int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_solve_persistent, PT, smem);
+  static size_t occ_smem = 0;  // occupancy of the last shared-memory size (queried once per size)
+  static int occ_last = 0;
+  if (occ_smem != smem) {
+    occ_last = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last, k_solve_persistent, PT, smem) != cudaSuccess) {
+      cudaGetLastError();
+      occ_last = 0;
+    }
+    occ_smem = smem;
+  }
+  const int occ = occ_last;
   if (occ < 1) return cudaErrorNotSupported;
   // tiny systems (<= 8 rows per thread of one CTA) run on ONE CTA: no grid barriers at all
   int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;

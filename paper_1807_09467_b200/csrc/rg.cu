@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstddef>
 #include <cstdio>
@@ -103,6 +104,7 @@ struct rg_ctx {
   DevState* hst = nullptr;  // pinned host mirror
   double* hhist = nullptr;  // pinned history staging
   int* hflag = nullptr;     // pinned flag staging
+  double* hsig = nullptr;   // pinned singular-value staging (MAXS)
   Layout L;
   // snapshots / recycle space
   int s_count = 0, s_head = 0;
@@ -543,6 +545,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   if (c->hst) cudaFreeHost(c->hst);
   if (c->hhist) cudaFreeHost(c->hhist);
   if (c->hflag) cudaFreeHost(c->hflag);
+  if (c->hsig) cudaFreeHost(c->hsig);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -600,7 +603,8 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   }
   if (cudaMallocHost(&c->hst, sizeof(DevState)) != cudaSuccess ||
       cudaMallocHost(&c->hhist, sizeof(double) * HIST_CAP) != cudaSuccess ||
-      cudaMallocHost(&c->hflag, sizeof(int) * 4) != cudaSuccess) {
+      cudaMallocHost(&c->hflag, sizeof(int) * 4) != cudaSuccess ||
+      cudaMallocHost(&c->hsig, sizeof(double) * (MAXS + 2)) != cudaSuccess) {
     cudaGetLastError();
     rg_destroy(c);
     return fail(RG_E_NOMEM, "pinned host allocation failed");
@@ -703,6 +707,9 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   const int s = c->s_count;
   const int64_t ld = c->npad;
   cudaStream_t st = c->stream;
+  static const bool timing = getenv("RG_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
   double* G = c->small;
   double* V1 = c->small + 1 * SMALL;
   double* lam = c->small + 2 * SMALL;
@@ -719,9 +726,11 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   // pass 2: Y^T Y (nearly diagonal, column-scaled) -> V2, sigma
   CK(launch_gram(c->Y, ld, c->n, s, G, c->partial, c->counter, c->st, st));
   CK(launch_jacobi(G, s, lam, V2, sig, c->st, st));
-  std::vector<double> hs(s);
-  CK(cudaMemcpyAsync(hs.data(), sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+  const auto t1 = now();
+  double* hs = c->hsig;  // pinned
+  CK(cudaMemcpyAsync(hs, sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  const auto t2 = now();
   if (getenv("RG_DEBUG")) {
     double sw[2] = {0.0, 0.0};
     cudaMemcpy(sw, lam + s, 2 * sizeof(double), cudaMemcpyDeviceToHost);
@@ -731,7 +740,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   for (int i = 0; i < s; ++i)
     if (hs[0] > 0.0 && hs[i] > 1e-12 * hs[0]) ++rank;
   const int ke = std::min(std::min(k, s), rank);
-  if (sigma) memcpy(sigma, hs.data(), sizeof(double) * s);
+  if (sigma) memcpy(sigma, hs, sizeof(double) * s);
   if (k_eff) *k_eff = ke;
   c->k_eff = ke;
   c->have_W = ke > 0;
@@ -742,6 +751,11 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
     CK(launch_inv(sig + off, ke, inv, st));
     CK(launch_xm(c->Y, ld, c->n, s, V2 + (int64_t)off * s, s, ke, inv, c->Z, ld, c->st, st));
     CK(cudaGetLastError());  // stream-ordered: the solve (or rg_export) consumes W on the same stream
+  }
+  if (timing) {
+    const auto t3 = now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    fprintf(stderr, "rg_build_recycle host us: launch %.1f, wait %.1f, tail %.1f\n", us(t0, t1), us(t1, t2), us(t2, t3));
   }
   return RG_OK;
 }
