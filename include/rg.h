@@ -113,9 +113,8 @@ typedef struct {
 #define RG_FLAG_PROFILE 2  /* record per-kernel device time (%globaltimer) for rg_kernel_stats */
 #define RG_FLAG_CGS2 4     /* classical CGS2 (3 reductions per Arnoldi step) instead of the default
                               delayed CGS2 (1 reduction per step); same iterates in exact arithmetic */
-#define RG_FLAG_NO_PERSIST 8 /* never use the single cooperative-kernel solve (every variant but
-                                augment, CSR/SELL, m <= 64, k <= 64, n_pad <= 1.6M); always use the
-                                CUDA-graph path */
+#define RG_FLAG_NO_PERSIST 8 /* never use the single cooperative-kernel solve (any variant, CSR/SELL,
+                                m <= 64, k <= 64, n_pad <= 1.6M); always use the CUDA-graph path */
 
 /* Solve report (fields follow SPEC.md's SolveReport).
  *   iterations   Arnoldi steps summed over restart cycles (residual and C = AW products are

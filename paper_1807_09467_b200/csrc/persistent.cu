@@ -1,5 +1,4 @@
-// persistent.cu — the whole restarted solve in ONE cooperative kernel (plain / deflate / oblique,
-// CSR / SELL).
+// persistent.cu — the whole restarted solve in ONE cooperative kernel (every variant, CSR / SELL).
 //
 // Why: at the sizes of configs C1-C2 every kernel boundary of the graph path costs a launch ramp
 // plus a single-CTA epilogue tail (~10 us per Arnoldi step).  Here every CTA of a co-resident grid
@@ -32,6 +31,7 @@ struct PArgs {
   unsigned* bar;        // [0] arrival count, [1] generation
   int m, k;             // m <= PM, k <= PK (k = 0: plain)
   int obl;              // oblique variant (k = k_eff > 0, C = A W in columns [k, 2k))
+  int aug;              // augment variant (k > 0): least squares on M = T H-bar (epilogue.cuh epi_ls)
   unsigned* flags;      // [gridDim.x] neighbour-sync epochs (zeroed before the launch)
   int nbsync;           // 1: point-to-point neighbour sync before the SpMVs instead of grid barriers
   int prec;             // right multicolour SSOR preconditioner (precond.cu's colour-ordered L/U copies)
@@ -216,8 +216,9 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   DevState* st = pa.st;
   const int m = pa.m, k = pa.k, VB = L.VB, QB = VB - k;
   const bool obl = pa.obl != 0;
-  const int lo = obl ? VB : QB, nq = obl ? 0 : k;  // P = [Q | V] (deflate) or V (plain, oblique)
-  const int nx = obl ? 2 * k : 0;                   // extra dots per step: W^T y, P^T u
+  const bool aug = pa.aug != 0;
+  const int lo = (obl || aug) ? VB : QB, nq = (obl || aug) ? 0 : k;  // P = [Q | V] (deflate) or V
+  const int nx = obl ? 2 * k : (aug ? k : 0);       // extra dots per step: W^T y, P^T u / Q^T u
   const bool orthp = pa.obl == 2;                   // orthogonal: projector I - W W^T (P = W, T = I)
   const int pbase = orthp ? 0 : k;                  // first column of P (C = A W at [k, 2k) or W)
   const int64_t ld = L.ld;
@@ -239,6 +240,9 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   double* ys = tot + MAXRED;                 // PM + 2: cycle-end y
   double* zk = ys + PM + 2;                  // PK
   double* wk = zk + PK;                      // PK (+ PM+2 behind it: (H a)_c at wk[PK + c])
+  // augment only: G (rows v_0..v_{m+1}: Q^T v_i) in Bs (sized (m+2) k), T and S = T^{-1} ([col][row])
+  double* Ts = wk + PK + PM + 2;             // [(m+2)][(m+2)] when aug
+  double* Ss = Ts + (aug ? (m + 2) * (m + 2) : 0);
   __shared__ double bsh[33];
   __shared__ int s_fail, s_stop;
   __shared__ double s_sc[8];
@@ -440,6 +444,10 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
     ++cycles;
     if (tid == 0) gg[0] = beta;
     for (int i = tid; i < PCOL; i += PT) h1[i] = 0.0;
+    if (aug) {  // v_0 = r_c / beta with Q^T r_c = 0 after the cycle-start projection: G[0,:] = 0, T00 = S00 = 1
+      for (int l = tid; l < k; l += PT) Bs[l] = 0.0;
+      if (tid == 0) { Ts[0] = 1.0; Ss[0] = 1.0; }
+    }
     __syncthreads();
     // ================= Arnoldi steps (DCGS2), u = V column j (raw), y -> V column j+1
     int jf = -1;
@@ -485,7 +493,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         const int cnt = (int)min((int64_t)PT, r1 - base);
         constexpr int RPL = PT / 32;
         for (int c = wid; c < p + nx; c += PT / 32) {
-          const int zcol = c < p ? lo + c : ((c - p) < k ? c - p : pbase + (c - p - k));
+          const int zcol = c < p ? lo + c : (aug ? QB + (c - p) : ((c - p) < k ? c - p : pbase + (c - p - k)));
           const double* zc = Z + (int64_t)zcol * ld + base + lane;
           double zv[RPL];
 #pragma unroll
@@ -503,8 +511,8 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
             if (c < p) {
               dpart[c] += su;
               dpart[p + c] += sy;
-            } else {  // oblique extras: [W^T y (k) | C^T u (k)] after [a | b | s | g]
-              dpart[2 * p + 2 + (c - p)] += (c - p) < k ? sy : su;
+            } else {  // extras after [a | b | s | g]: oblique [W^T y (k) | P^T u (k)], augment Q^T u (k)
+              dpart[2 * p + 2 + (c - p)] += (!aug && (c - p) < k) ? sy : su;
             }
           }
         }
@@ -538,10 +546,67 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         for (int l = tid; l < nq; l += PT) Bs[col * k + l] = h1[l] + a[l];
         if (tid == 0) Hs[col * (m + 2) + j] = nu;
         __syncthreads();
+        const int M2 = m + 2;
+        int aug_tb = 0;  // augment: v_j (numerically) in span(Q) + span(V_j): end the cycle at col - 1
+        if (aug) {
+          // G row j = Q^T v_j = (Q^T u - G_j^T a) / nu; then the new column of T (Cholesky factor of
+          // M = I - G^T G) and of S = T^{-1}; the least squares runs on M H-bar column col = T h.
+          const double* qu = tot + 2 * p + 2;
+          for (int l = tid; l < k; l += PT) {
+            double g = qu[l];
+            for (int i = 0; i < j; ++i) g -= Bs[i * k + l] * a[i];
+            Bs[j * k + l] = nu > 0.0 ? g / nu : 0.0;
+          }
+          __syncthreads();
+          for (int i = wid; i <= j; i += PT / 32) {  // mc_i = delta_ij - G_i . G_j  -> cv[i]
+            double sacc = 0.0;
+            for (int l = lane; l < k; l += 32) sacc += Bs[i * k + l] * Bs[j * k + l];
+            sacc = warp_sum(sacc);
+            if (lane == 0) cv[i] = (i == j ? 1.0 : 0.0) - sacc;
+          }
+          __syncthreads();
+          for (int i = wid; i < j; i += PT / 32) {  // t_i = sum_{l <= i} S(l, i) mc_l -> cn[i]
+            double sacc = 0.0;
+            for (int l = lane; l <= i; l += 32) sacc += Ss[i * M2 + l] * cv[l];
+            sacc = warp_sum(sacc);
+            if (lane == 0) cn[i] = sacc;
+          }
+          __syncthreads();
+          if (tid == 0) {
+            double t2 = 0.0;
+            for (int i = 0; i < j; ++i) t2 += cn[i] * cn[i];
+            const double tau2 = cv[j] - t2;
+            s_sc[2] = tau2 > 1e-14 ? sqrt(tau2) : 0.0;
+          }
+          __syncthreads();
+          aug_tb = !(s_sc[2] > 0.0);
+          if (!aug_tb) {
+            const double tau = s_sc[2];
+            for (int l = wid; l < j; l += PT / 32) {  // S(l, j) = -(sum_{i >= l} S(l, i) t_i) / tau
+              double sacc = 0.0;
+              for (int i = l + lane; i < j; i += 32) sacc += Ss[i * M2 + l] * cn[i];
+              sacc = warp_sum(sacc);
+              if (lane == 0) Ss[j * M2 + l] = -sacc / tau;
+            }
+            for (int i = tid; i < j; i += PT) Ts[j * M2 + i] = cn[i];
+            if (tid == 0) {
+              Ts[j * M2 + j] = tau;
+              Ss[j * M2 + j] = 1.0 / tau;
+            }
+            __syncthreads();
+            for (int i = wid; i <= j; i += PT / 32) {  // column col of M = T H: sum_{l >= i} T(i, l) h_l -> ys[i]
+              double sacc = 0.0;
+              for (int l = i + lane; l <= j; l += 32) sacc += Ts[l * M2 + i] * Hs[col * M2 + l];
+              sacc = warp_sum(sacc);
+              if (lane == 0) ys[i] = sacc;
+            }
+            __syncthreads();
+          }
+        }
         if (tid == 0) {  // Givens on column col (same arithmetic in every CTA)
           // the rotated entry travels in a register; the loads of H, cs, sn do not depend on the
           // chain, so the unrolled loop keeps them in flight (2 FMAs per rotation on the chain)
-          const double* Hc = Hs + col * (m + 2);
+          const double* Hc = aug ? ys : Hs + col * (m + 2);
           double* Rc = Rs + col * (m + 1);
           double carry = Hc[0];
 #pragma unroll 4
@@ -553,7 +618,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
           const double hlast = Hc[col + 1];
           const double den = hypot(carry, hlast);
           int stop = 0;
-          if (!(den > 0.0)) {
+          if (aug_tb || !(den > 0.0)) {
             stop = 2;  // no progress possible: end the cycle at the previous column
           } else {
             const double c = carry / den, s = hlast / den;
@@ -679,7 +744,28 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       }
       __syncthreads();
       const int kx = obl ? 0 : k;  // oblique: x += V y (the next cycle start applies the W part)
-      if (kx > 0) {
+      if (kx > 0 && aug) {  // x -= W R_C^{-1} G H-bar y
+        for (int i = wid; i <= jf + 1; i += PT / 32) {  // (H-bar y)_i -> cv[i] (Hessenberg)
+          double s = 0.0;
+          for (int c2 = (i > 0 ? i - 1 : 0) + lane; c2 <= jf; c2 += 32) s += Hs[c2 * (m + 2) + i] * ys[c2];
+          s = warp_sum(s);
+          if (lane == 0) cv[i] = s;
+        }
+        __syncthreads();
+        for (int l = wid; l < k; l += PT / 32) {
+          double s = 0.0;
+          for (int i = lane; i <= jf + 1; i += 32) s += Bs[i * k + l] * cv[i];
+          s = warp_sum(s);
+          if (lane == 0) wk[l] = s;
+        }
+        __syncthreads();
+        for (int l = tid; l < k; l += PT) {
+          double s = 0.0;
+          for (int c = l; c < k; ++c) s += st->RCinv[c][l] * wk[c];
+          zk[l] = s;
+        }
+        __syncthreads();
+      } else if (kx > 0) {
         for (int l = tid; l < k; l += PT) {
           double s = 0.0;
           for (int i = 0; i <= jf; ++i) s += Bs[i * k + l] * ys[i];
@@ -742,17 +828,18 @@ fail:
 
 }  // namespace
 
-size_t persistent_smem(int m, int k) {
+size_t persistent_smem(int m, int k, bool aug) {
   return sizeof(double) * ((size_t)m * (m + 2) + (size_t)m * (m + 1) + (size_t)(m + 1) * (k > 0 ? k : 1) + 2 * PM +
-                           (PM + 2) + 3 * PCOL + 2 * PT + 2 * MAXRED + (PM + 2) + 2 * PK + PM + 2);
+                           (PM + 2) + 3 * PCOL + 2 * PT + 2 * MAXRED + (PM + 2) + 2 * PK + PM + 2 +
+                           (aug ? 2 * (size_t)(m + 2) * (m + 2) : 0));
 }
 
 // Returns cudaErrorNotSupported when the configuration is outside this path.
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
                               unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s) {
-  if (m > PM || k > PK || (variant != RG_PLAIN && variant != RG_DEFLATE && !galerkin_variant(variant)) || A.fmt == 2)
-    return cudaErrorNotSupported;
-  const size_t smem = persistent_smem(m, k);
+  if (m > PM || k > PK || A.fmt == 2) return cudaErrorNotSupported;
+  const bool aug = variant == RG_AUGMENT && k > 0;
+  const size_t smem = persistent_smem(m, k, aug);
   static int max_smem = -1;
   if (max_smem < 0) {
     cudaFuncSetAttribute(k_solve_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -780,7 +867,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
   PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k,
-           galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, flags, nbsync,
+           galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, aug ? 1 : 0, flags, nbsync,
            P ? 1 : 0, P ? *P : PrecDev(), L.pz, L.pt, 0.0};
   if (P) {
     double b2 = 0.0;

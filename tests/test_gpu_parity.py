@@ -240,7 +240,7 @@ def test_recycle_operator_thin_qr(name, N, sell, rng):
     assert np.allclose(np.tril(R, -1), 0.0)
 
 
-@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique", "orthogonal"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique", "orthogonal"])
 def test_persistent_and_graph_paths_agree(variant, rng):
     """The single cooperative-kernel solve and the CUDA-graph solve compute the same iterates
     (same DCGS2 arithmetic, different reduction trees): same iteration counts, x within 1e-10."""
@@ -421,7 +421,7 @@ def test_variant_switching_on_one_context(rng):
         assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"]), variant
 
 
-@pytest.mark.parametrize("variant", ["plain", "deflate", "oblique"])
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
 def test_persistent_multi_cta_wide_pattern(variant, rng):
     """A random pattern couples every row range with every other one, so the persistent solve's
     neighbour synchronisation must wait on all CTAs (n = 20,000: many CTAs)."""
