@@ -56,7 +56,7 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
 // WHILE-node condition from the state: which 0 -> active, 1 -> !done
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s);
 
-// Whole solve in one cooperative kernel (persistent.cu): plain / deflate, CSR / SELL, m <= 64,
+// Whole solve in one cooperative kernel (persistent.cu): every variant, CSR / SELL, m <= 64,
 // k <= 64.  cudaErrorNotSupported when outside that scope (caller uses the graph path).
 // bar: [BAR_WORDS] zeroed barrier words; flags: [NSM * 8] zeroed neighbour-sync epochs;
 // P: right SSOR preconditioner (nullptr: none; needs L.pz, L.pt).
