@@ -60,7 +60,7 @@ cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cud
 // k <= 64.  cudaErrorNotSupported when outside that scope (caller uses the graph path).
 // bar: [BAR_WORDS] zeroed barrier words; flags: [NSM * 8] zeroed neighbour-sync epochs;
 // P: right SSOR preconditioner (nullptr: none; needs L.pz, L.pt).
-constexpr int BAR_WORDS = 64;
+constexpr int BAR_WORDS = 64 + 32 * NSM * 8;
 struct PrecDev;
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
                               unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s);

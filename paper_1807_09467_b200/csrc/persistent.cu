@@ -34,6 +34,7 @@ struct PArgs {
   int aug;              // augment variant (k > 0): least squares on M = T H-bar (epilogue.cuh epi_ls)
   unsigned* flags;      // [gridDim.x] neighbour-sync epochs (zeroed before the launch)
   int nbsync;           // 1: point-to-point neighbour sync before the SpMVs instead of grid barriers
+  int skew;             // experiment: record per-CTA "dots done" timestamps
   int prec;             // right multicolour SSOR preconditioner (precond.cu's colour-ordered L/U copies)
   PrecDev P;
   double* pz;           // M^{-1} u (step) / M^{-1} V y (cycle end)
@@ -43,23 +44,25 @@ struct PArgs {
 
 // ---- grid barrier (all CTAs co-resident: cooperative launch).  Spins with a timeout so that a
 // bug cannot hang the GPU: after ~2 s every CTA gives up and the solve reports RG_E_CUDA.
-// Words (unsigned): [0] arrival counter, [32] generation (separate 128-B lines).  (Measured: a
-// two-level arrival tree with per-group counters made no difference at 296 CTAs.)
+// Words (unsigned): [0] monotonic arrival counter, [64 + 32 b] CTA b's barrier count (zeroed per
+// launch).  (Measured: a two-level arrival tree with per-group counters made no difference at 296
+// CTAs.)
 __device__ __forceinline__ bool gbar(unsigned* bar, int* s_fail) {
   __syncthreads();
   if (gridDim.x == 1) return true;  // single-CTA solve (tiny systems): a CTA barrier suffices
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 32;
-    const unsigned g = *gen;
+    // monotonic arrival counter: the n-th barrier of this launch completes when the counter reaches
+    // n * G (every CTA passes the same barriers in the same order), so the last arrival's own atomic
+    // is the release — no reset and no separate generation bump (one L2 round trip less)
+    unsigned* nb = bar + 64 + blockIdx.x * 32;  // this CTA's barrier count (own 128-B line; thread 0 only)
+    const unsigned target = (*nb + 1u) * gridDim.x;
+    *nb += 1u;
     __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(bar + 32, 1u);
-    } else {
+    if (atomicAdd(bar, 1u) + 1u < target) {
+      volatile unsigned* cnt = bar;
       const long long t0 = clock64();
       unsigned ns = 32;
-      while (*gen == g) {  // exponential back-off keeps ~300 pollers off the barrier's L2 line
+      while (*cnt < target) {  // exponential back-off keeps ~300 pollers off the barrier's L2 line
         __nanosleep(ns);
         if (ns < 256) ns <<= 1;
         if (clock64() - t0 > 4000000000LL) { *s_fail = 1; break; }
@@ -524,6 +527,10 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         __syncthreads();
       }
       ptick(st, K_PB2, tph);
+      if (pa.skew && cycles == 1 && j >= 5 && j < 9 && tid == 0) {
+        const unsigned tnow = (unsigned)(gtimer() & 0xffffffffu);
+        pa.flags[NSM * 2 + (j - 5) * NSM * 2 + blockIdx.x] = tnow;  // dots done
+      }
       if (!greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, st)) goto fail;
       ptick(st, K_PB3, tph);
       if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + nx + 2);
@@ -868,6 +875,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
   PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k,
            galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, aug ? 1 : 0, flags, nbsync,
+           getenv("RG_SKEW") ? 1 : 0,
            P ? 1 : 0, P ? *P : PrecDev(), L.pz, L.pt, 0.0};
   if (P) {
     double b2 = 0.0;

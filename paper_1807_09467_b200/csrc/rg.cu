@@ -596,7 +596,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
       (s = dalloc(&c->partial, part, "partial")) != RG_OK || (s = dalloc(&c->counter, 4, "counter")) != RG_OK ||
       (s = dalloc(&c->small, (size_t)SMALL * 16, "small")) != RG_OK || (s = dalloc(&c->dflag, 4, "flag")) != RG_OK ||
       (s = dalloc(&c->tot_g, (size_t)MAXRED, "totals")) != RG_OK || (s = dalloc(&c->gbar, (size_t)BAR_WORDS, "barrier")) != RG_OK ||
-      (s = dalloc(&c->pflags, (size_t)NSM * 8, "sync flags")) != RG_OK ||
+      (s = dalloc(&c->pflags, (size_t)NSM * 16, "sync flags")) != RG_OK ||
       (s = dalloc(&c->st, 1, "state")) != RG_OK) {
     rg_destroy(c);
     return s;
@@ -819,7 +819,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   c->L.prec = c->prec_kind ? 1 : 0;
   if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
     CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
-    CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 8, s));
+    CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 16, s));
     cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, m, k, eff,
                                        c->L.prec ? &c->P : nullptr, s);
     if (ep == cudaSuccess) done_persist = true;
@@ -841,6 +841,29 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (history && hcap > 0) CK(cudaMemcpyAsync(c->hhist, c->hist, sizeof(double) * hcap, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (check_c) bad = c->hflag[0];
+  if (done_persist && getenv("RG_SKEW")) {  // experiment: per-CTA "dots done" spread, steps 5..8
+    std::vector<unsigned> ts((size_t)NSM * 8);
+    cudaMemcpy(ts.data(), c->pflags + NSM * 2, sizeof(unsigned) * NSM * 8, cudaMemcpyDeviceToHost);
+    for (int q = 0; q < 4; ++q) {
+      unsigned mn = 0xffffffffu, mx = 0;
+      int imx = -1, cnt = 0;
+      for (int b2 = 0; b2 < NSM * 2; ++b2) {
+        const unsigned v = ts[(size_t)q * NSM * 2 + b2];
+        if (!v) continue;
+        ++cnt;
+        if (v < mn) mn = v;
+        if (v > mx) { mx = v; imx = b2; }
+      }
+      if (cnt) {
+        std::vector<unsigned> vs;
+        for (int b2 = 0; b2 < NSM * 2; ++b2) if (ts[(size_t)q * NSM * 2 + b2]) vs.push_back(ts[(size_t)q * NSM * 2 + b2] - mn);
+        std::sort(vs.begin(), vs.end());
+        fprintf(stderr, "skew step %d: CTAs %d spread %.2f us (p50 %.2f p90 %.2f), last CTA %d, CTA0 %.2f\n", q + 5, cnt,
+                (mx - mn) * 1e-3, vs[vs.size() / 2] * 1e-3, vs[vs.size() * 9 / 10] * 1e-3, imx,
+                ts[(size_t)q * NSM * 2] ? (ts[(size_t)q * NSM * 2] - mn) * 1e-3 : -1.0);
+      }
+    }
+  }
   if (bad) {
     c->have_W = false;
     c->k_eff = 0;
