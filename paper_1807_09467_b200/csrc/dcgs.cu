@@ -26,6 +26,8 @@
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 namespace rg {
 namespace {
 
@@ -169,6 +171,19 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   __syncthreads();
 }
 
+// grid reduction of DK1's partial vector, the DCGS2 epilogue in the last CTA, state advance
+__device__ __forceinline__ void dk1_finish(const Layout& L, DevState* st, double* dpart, double* tot, int nv, int p,
+                                           int nqd, int j, bool have_y, unsigned long long cond) {
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot, DK1RED)) return;
+  prof_tail(st, K_DK1);
+  epi_dcgs(st, L, tot, p);
+  if (threadIdx.x == 0) {
+    if (st->active) st->j = j + 1;  // next iteration (DK2 of this one uses st->j - 1)
+    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
+    prof_end(st, K_DK1, 8.0 * (double)L.n * (p + nqd + (have_y ? 2 : 1)));
+  }
+}
+
 // ---------------------------------------------------------------- DK1: dots of u and y with P
 // Rows are split evenly over the CTAs; per 512-row sub-tile u and y are staged in shared memory,
 // warp w owns columns w, w+16, ...: 16 independent loads per lane, two products, fixed shuffle
@@ -245,14 +260,109 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
     dpart[2 * p + 1] = t2;
   }
   __syncthreads();
-  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot, DK1RED)) return;
-  prof_tail(st, K_DK1);
-  epi_dcgs(st, L, tot, p);
-  if (threadIdx.x == 0) {
-    if (st->active) st->j = j + 1;  // next iteration (DK2 of this one uses st->j - 1)
-    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
-    prof_end(st, K_DK1, 8.0 * (double)L.n * (p + nqd + (have_y ? 2 : 1)));
+  dk1_finish(L, st, dpart, tot, nv, p, nqd, j, have_y, cond);
+}
+
+// ---------------------------------------------------------------- DK1, streaming variant
+// The DK2 access pattern (thread per row, stride = CTA size, all loads of a row independent) with the
+// dot columns taken in chunks of SCH: per chunk every thread keeps 2 * SCH partial sums (u and y) in
+// registers over all of the CTA's rows and the chunk ends with ONE block reduction; u and y are
+// re-read per chunk (L2 hits).  No per-sub-tile barrier and no shared-memory staging.
+template <int SCH, int RU>  // SCH columns per chunk, RU rows per thread per iteration (loads in flight)
+__global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, unsigned long long cond) {
+  __shared__ double dpart[DK1RED];
+  __shared__ double tot[DK1RED];
+  __shared__ double wred[DT / 32][2 * SCH];
+  __shared__ double bsh[33];
+  if (!st->active) { prof_noop(st, K_DK1); return; }
+  prof_begin(st, K_DK1);
+  const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
+  const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
+  const int nqd = (var == RG_AUGMENT) ? k : (galerkin_variant(var) ? 2 * k : 0);
+  const bool have_y = j < st->m;
+  const bool keep = L.keep_l2 != 0;
+  const int64_t ld = L.ld;
+  const double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;
+  const double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;
+  const double* __restrict__ Z = L.Z;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int nv = 2 * p + 2 + nqd, ncols = p + nqd;
+  const bool obl = galerkin_variant(var);
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  double s_uu = 0.0, s_uy = 0.0;
+  for (int c0 = 0; c0 < ncols || c0 == 0; c0 += SCH) {
+    const int nc = min(SCH, ncols - c0);
+    const double* zp[SCH];
+#pragma unroll
+    for (int kk = 0; kk < SCH; ++kk) {
+      const int c = c0 + (kk < nc ? kk : 0);
+      const int col = c < p ? lo + c : (obl ? ((c - p) < k ? c - p : proj_base(var, k) + (c - p - k)) : QB + (c - p));
+      zp[kk] = Z + (int64_t)col * ld;
+    }
+    double su[SCH], sy[SCH];
+#pragma unroll
+    for (int kk = 0; kk < SCH; ++kk) su[kk] = sy[kk] = 0.0;
+    for (int64_t rb = r0 + threadIdx.x; rb < r1; rb += DT * RU) {
+      double ur[RU], yr[RU], z[RU][SCH];
+#pragma unroll
+      for (int q = 0; q < RU; ++q) {  // all loads of RU rows issued before any use
+        const int64_t r = rb + (int64_t)q * DT;
+        const bool ok = r < r1;
+        ur[q] = ok ? u[r] : 0.0;
+        yr[q] = (ok && have_y) ? y[r] : 0.0;
+#pragma unroll
+        for (int kk = 0; kk < SCH; ++kk) z[q][kk] = (ok && kk < nc) ? (keep ? zp[kk][r] : __ldcs(zp[kk] + r)) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < RU; ++q) {
+#pragma unroll
+        for (int kk = 0; kk < SCH; ++kk) {
+          su[kk] += z[q][kk] * ur[q];
+          sy[kk] += z[q][kk] * yr[q];
+        }
+        if (c0 == 0) {
+          s_uu += ur[q] * ur[q];
+          s_uy += ur[q] * yr[q];
+        }
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < SCH; ++kk) {
+      const double a = warp_sum(su[kk]), b = warp_sum(sy[kk]);
+      if (lane == 0) {
+        wred[wid][kk] = a;
+        wred[wid][SCH + kk] = b;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * SCH) {
+      const int kk = threadIdx.x % SCH;
+      const bool isy = threadIdx.x >= SCH;
+      double sacc = 0.0;
+      for (int w = 0; w < DT / 32; ++w) sacc += wred[w][threadIdx.x];
+      const int c = c0 + kk;
+      if (kk < nc) {
+        if (c < p) {
+          dpart[isy ? p + c : c] = sacc;
+        } else {
+          const bool wy = obl && (c - p) < k;  // extras: W^T y, P^T u (galerkin) / Q^T u (augment)
+          if (isy == wy) dpart[2 * p + 2 + (c - p)] = sacc;
+        }
+      }
+    }
+    __syncthreads();
+    if (ncols == 0) break;
   }
+  const double t1 = block_sum(s_uu, bsh);
+  const double t2 = block_sum(s_uy, bsh);
+  if (threadIdx.x == 0) {
+    dpart[2 * p] = t1;
+    dpart[2 * p + 1] = t2;
+  }
+  __syncthreads();
+  dk1_finish(L, st, dpart, tot, nv, p, nqd, j, have_y, cond);
 }
 
 // ---------------------------------------------------------------- DK2: v_j and the next u
@@ -315,7 +425,13 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
     init = true;
   }
   if (phase == 1) {
-    k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
+    // streaming variant by default (C4: 3.90 -> 4.54 TB/s; (SCH, RU) = (4, 2) and (6, 2) measured
+    // equal, (4, 4) spills); RG_DK1_TILES=1 selects the shared-memory sub-tile kernel
+    static const int tiles = getenv("RG_DK1_TILES") ? 1 : 0;
+    if (!tiles)
+      k_dk1_stream<8, 1><<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
+    else
+      k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
     return cudaGetLastError();
   }
   k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
