@@ -212,17 +212,21 @@ __device__ __forceinline__ void ptick(DevState* st, int kid, unsigned long long&
   }
 }
 
+// VK selects the code the instantiation contains: 0 plain / deflate, 1 oblique / orthogonal, 2 augment
+// (one kernel with every variant's code carried more live registers and spilled in the hot loops:
+// C2 deflate +1.7 %).
+template <int VK>
 __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   extern __shared__ double sm[];
   const Layout& L = pa.L;
   const MatDev& A = pa.A;
   DevState* st = pa.st;
   const int m = pa.m, k = pa.k, VB = L.VB, QB = VB - k;
-  const bool obl = pa.obl != 0;
-  const bool aug = pa.aug != 0;
+  const bool obl = VK == 1 && pa.obl != 0;
+  constexpr bool aug = VK == 2;
   const int lo = (obl || aug) ? VB : QB, nq = (obl || aug) ? 0 : k;  // P = [Q | V] (deflate) or V
   const int nx = obl ? 2 * k : (aug ? k : 0);       // extra dots per step: W^T y, P^T u / Q^T u
-  const bool orthp = pa.obl == 2;                   // orthogonal: projector I - W W^T (P = W, T = I)
+  const bool orthp = VK == 1 && pa.obl == 2;        // orthogonal: projector I - W W^T (P = W, T = I)
   const int pbase = orthp ? 0 : k;                  // first column of P (C = A W at [k, 2k) or W)
   const int64_t ld = L.ld;
   double* Z = L.Z;
@@ -846,26 +850,31 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
                               unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s) {
   if (m > PM || k > PK || A.fmt == 2) return cudaErrorNotSupported;
   const bool aug = variant == RG_AUGMENT && k > 0;
+  const int vk = aug ? 2 : ((galerkin_variant(variant) && k > 0) ? 1 : 0);
+  const void* fn = vk == 2 ? (const void*)k_solve_persistent<2>
+                           : (vk == 1 ? (const void*)k_solve_persistent<1> : (const void*)k_solve_persistent<0>);
   const size_t smem = persistent_smem(m, k, aug);
   static int max_smem = -1;
   if (max_smem < 0) {
-    cudaFuncSetAttribute(k_solve_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_solve_persistent, cudaFuncAttributePreferredSharedMemoryCarveout,
-                         cudaSharedmemCarveoutMaxShared);
+    for (const void* f : {(const void*)k_solve_persistent<0>, (const void*)k_solve_persistent<1>,
+                          (const void*)k_solve_persistent<2>}) {
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    }
     max_smem = 200 * 1024;
   }
   if (smem > (size_t)max_smem) return cudaErrorNotSupported;
-  static size_t occ_smem = 0;  // occupancy of the last shared-memory size (queried once per size)
-  static int occ_last = 0;
-  if (occ_smem != smem) {
-    occ_last = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last, k_solve_persistent, PT, smem) != cudaSuccess) {
+  static size_t occ_smem[3] = {0, 0, 0};  // occupancy per instantiation and shared-memory size (queried once)
+  static int occ_last[3] = {0, 0, 0};
+  if (occ_smem[vk] != smem) {
+    occ_last[vk] = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last[vk], fn, PT, smem) != cudaSuccess) {
       cudaGetLastError();
-      occ_last = 0;
+      occ_last[vk] = 0;
     }
-    occ_smem = smem;
+    occ_smem[vk] = smem;
   }
-  const int occ = occ_last;
+  const int occ = occ_last[vk];
   if (occ < 1) return cudaErrorNotSupported;
   // tiny systems (<= 8 rows per thread of one CTA) run on ONE CTA: no grid barriers at all
   int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;
@@ -883,7 +892,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
     pa.pc_bytes = b2 + 8.0 * (double)L.n * 6.0;  // + perm, row pointers, 1/a_rr, in, out (fwd), out r/w (bwd)
   }
   void* args[] = {&pa};
-  return cudaLaunchCooperativeKernel((const void*)k_solve_persistent, dim3(G), dim3(PT), args, smem, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(PT), args, smem, s);
 }
 
 }  // namespace rg
