@@ -645,6 +645,19 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
             else if (res <= tol || nu <= 1e-14 * beta || col + 1 >= m || iters + 1 >= max_iters) stop = 1;
           }
           s_stop = stop;
+        } else if (wid > 0) {
+          // meanwhile warps 1..: the products (H a_V)_c and (B a_V)_l of the coefficient step below
+          // (they read the unrotated H and B only, not the rotation thread 0 is computing)
+          for (int o = wid - 1; o < j + nq; o += PT / 32 - 1) {
+            double s = 0.0;
+            if (o < j) {
+              for (int i = (o > 0 ? o - 1 : 0) + lane; i < j; i += 32) s += Hs[i * (m + 2) + o] * a[nq + i];
+            } else {
+              for (int i = lane; i < j; i += 32) s += Bs[i * k + (o - j)] * a[nq + i];
+            }
+            s = warp_sum(s);
+            if (lane == 0) wk[o < j ? PK + o : o - j] = s;  // reuse: [0,k) Ba, [PK, PK+j) Ha
+          }
         }
         __syncthreads();
         ++iters;
@@ -684,15 +697,17 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       }
       const double dob = obl ? ((gm - ab) * inv - nu * aj - ys[j]) * inv : d;
       const double f = (aj + dob) * inv;
-      for (int o = wid; o < j + nq; o += PT / 32) {  // (H a_V)_c and (B a_V)_l
-        double s = 0.0;
-        if (o < j) {
-          for (int i = (o > 0 ? o - 1 : 0) + lane; i < j; i += 32) s += Hs[i * (m + 2) + o] * a[nq + i];
-        } else {
-          for (int i = lane; i < j; i += 32) s += Bs[i * k + (o - j)] * a[nq + i];
+      if (j == 0) {  // (for j >= 1 computed during the Givens step above)
+        for (int o = wid; o < j + nq; o += PT / 32) {  // (H a_V)_c and (B a_V)_l
+          double s = 0.0;
+          if (o < j) {
+            for (int i = (o > 0 ? o - 1 : 0) + lane; i < j; i += 32) s += Hs[i * (m + 2) + o] * a[nq + i];
+          } else {
+            for (int i = lane; i < j; i += 32) s += Bs[i * k + (o - j)] * a[nq + i];
+          }
+          s = warp_sum(s);
+          if (lane == 0) wk[o < j ? PK + o : o - j] = s;  // reuse: [0,k) Ba, [PK, PK+j) Ha
         }
-        s = warp_sum(s);
-        if (lane == 0) wk[o < j ? PK + o : o - j] = s;  // reuse: [0,k) Ba, [PK, PK+j) Ha
       }
       __syncthreads();
       for (int c = tid; c < j; c += PT) {
