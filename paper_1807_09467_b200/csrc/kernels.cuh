@@ -21,6 +21,7 @@ struct MatDev {
   int64_t nslices = 0;
   int tma = 1;                  // BSR-64: stream blocks with TMA bulk copies
   double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
+  int64_t nnz = 0;              // CSR entries
 };
 
 // Kernels launched directly by the host without a device-side counter (recycle build, CholQR2,
@@ -59,11 +60,14 @@ cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cud
 // Whole solve in one cooperative kernel (persistent.cu): every variant, CSR / SELL, m <= 64,
 // k <= 64.  cudaErrorNotSupported when outside that scope (caller uses the graph path).
 // bar: [BAR_WORDS] zeroed barrier words; flags: [NSM * 8] zeroed neighbour-sync epochs;
-// P: right SSOR preconditioner (nullptr: none; needs L.pz, L.pt).
+// P: right SSOR preconditioner (nullptr: none; needs L.pz, L.pt).  ll: [ll_words()] reduction words,
+// zeroed once at allocation and never again (their epochs continue in DevState::red_epoch).
 constexpr int BAR_WORDS = 64 + 32 * NSM * 8;
 struct PrecDev;
+size_t ll_words();
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
-                              unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s);
+                              unsigned* flags, unsigned long long* ll, int m, int k, int variant, const PrecDev* P,
+                              cudaStream_t s);
 
 // ---- multicolour SSOR(omega) preconditioner (precond.cu)
 constexpr int MAXCOLORS = 64;

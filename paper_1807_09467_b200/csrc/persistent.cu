@@ -12,13 +12,18 @@
 // coefficients exactly as dcgs.cu does it (V^T C replicated in shared memory).
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
 namespace rg {
 namespace {
 
-constexpr int PT = 512;       // threads per CTA
+#ifndef RG_PT
+#define RG_PT 512
+#endif
+constexpr int PT = RG_PT;     // threads per CTA
+constexpr int PCTA = 1024 / PT;  // resident CTAs per SM
 constexpr int PM = 64;        // max restart length on this path
 constexpr int PK = 64;        // max recycle dimension on this path
 constexpr int PCOL = PK + PM + 2;
@@ -34,12 +39,15 @@ struct PArgs {
   int aug;              // augment variant (k > 0): least squares on M = T H-bar (epilogue.cuh epi_ls)
   unsigned* flags;      // [gridDim.x] neighbour-sync epochs (zeroed before the launch)
   int nbsync;           // 1: point-to-point neighbour sync before the SpMVs instead of grid barriers
-  int skew;             // experiment: record per-CTA "dots done" timestamps
+  int skew;             // experiment (RG_SKEW=j): per-CTA start / dots done / reduced timestamps and SM of step j
   int prec;             // right multicolour SSOR preconditioner (precond.cu's colour-ordered L/U copies)
   PrecDev P;
   double* pz;           // M^{-1} u (step) / M^{-1} V y (cycle end)
   double* pt;           // V y (cycle end)
   double pc_bytes;      // algorithmic bytes of one SSOR application
+  int rcap, ccap;       // CSR pattern cache in shared memory: row pointers / column indices capacity (0: off)
+  unsigned long long* ll;  // flag-carrying reduction words (LL_WORDS; zeroed once at allocation)
+  int llred;            // 1: reductions through `ll` (greduce_ll), 0: two-barrier greduce
 };
 
 // ---- grid barrier (all CTAs co-resident: cooperative launch).  Spins with a timeout so that a
@@ -158,6 +166,81 @@ __device__ __forceinline__ bool greduce(const double* vals, int nv, double* part
   return true;
 }
 
+// ---- flag-carrying ("LL") deterministic grid reduction, no barrier at all.  Every value travels as
+// two 64-bit words {low half | epoch, high half | epoch}; an aligned 64-bit store is single-copy
+// atomic, so a reader that sees the current epoch in both words holds the value — data and flag
+// arrive together, no fence, no counter.  CTA b publishes its nv partials; CTA c sums columns
+// c, c+G, ... (thread t polls CTA t's partial, fixed-tree block sum: deterministic) and publishes
+// the total; every CTA polls the nv totals.  Latency after the last partial: one poll round trip,
+// a block sum, one poll round trip (the two-barrier version adds two atomic arrivals, four fences
+// and the barrier polls).  Epochs increase by one per reduction and persist across launches in
+// DevState::red_epoch; partials and totals are double-buffered by epoch parity, so a slot is
+// rewritten only two reductions later, after every CTA has consumed it (each CTA must have read
+// every total of the reduction in between).  Requires G <= PT and G <= LL_GMAX.  Each total is
+// written to LL_R replicas (CTA b polls replica b % LL_R): ~300 CTAs polling the same few lines
+// queue at their L2 slices (micro-benchmark, nv = 92: 4.8 -> 3.8 us per reduction with 16 replicas).
+constexpr int LL_GMAX = NSM * 2;
+constexpr int LL_R = 16;
+}  // namespace
+size_t ll_words() { return (size_t)2 * 2 * ((size_t)LL_GMAX * MAXRED + (size_t)LL_R * MAXRED); }
+namespace {
+
+__device__ __forceinline__ void ll_st(unsigned long long* p, double v, unsigned ep) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned long long e = (unsigned long long)ep << 32;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"((b & 0xffffffffull) | e), "l"((b >> 32) | e)
+               : "memory");
+}
+
+__device__ __forceinline__ bool ll_ld(const unsigned long long* p, unsigned ep, double& v) {
+  unsigned long long w0, w1;
+  long long t0 = 0;
+  for (int it = 0;; ++it) {
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    if ((unsigned)(w0 >> 32) == ep && (unsigned)(w1 >> 32) == ep) break;
+    if (it == 0) {
+      t0 = clock64();
+    } else if (clock64() - t0 > 4000000000LL) {
+      return false;
+    }
+    __nanosleep(32);
+  }
+  v = __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
+  return true;
+}
+
+__device__ __forceinline__ bool greduce_ll(const double* vals, int nv, unsigned long long* ll, double* tot,
+                                           unsigned& ep, double* bsh, int* s_fail, DevState* st = nullptr) {
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  ++ep;
+  const int buf = (int)(ep & 1u);
+  unsigned long long* part = ll + (size_t)buf * LL_GMAX * MAXRED * 2;
+  unsigned long long* totw = ll + (size_t)2 * LL_GMAX * MAXRED * 2 + (size_t)buf * LL_R * MAXRED * 2;
+  __syncthreads();  // vals complete
+  for (int i = tid; i < nv; i += PT) ll_st(part + ((size_t)b * MAXRED + i) * 2, vals[i], ep);
+  const unsigned long long ta = (st && st->profile && b == 0 && tid == 0) ? gtimer() : 0ull;
+  bool ok = true;
+  for (int col = b; col < nv; col += G) {
+    double a = 0.0;
+    if (tid < G && !ll_ld(part + ((size_t)tid * MAXRED + col) * 2, ep, a)) ok = false;
+    a = block_sum(a, bsh);
+    if (ta && col == b) {  // profiling: CTA 0 waits for its column's partials (skew + latency) -> p_reduce_arrive
+      st->kstat[K_PB6].ns += gtimer() - ta;
+      st->kstat[K_PB6].launches++;
+    }
+    if (tid < LL_R) ll_st(totw + ((size_t)tid * MAXRED + col) * 2, a, ep);
+  }
+  const unsigned long long* mine = totw + (size_t)(b % LL_R) * MAXRED * 2;
+  for (int i = tid; i < nv; i += PT) {
+    double v = 0.0;
+    if (!ll_ld(mine + (size_t)i * 2, ep, v)) ok = false;
+    tot[i] = v;
+  }
+  if (!ok) *s_fail = 1;
+  __syncthreads();
+  return *s_fail == 0;
+}
+
 // y_r = (A x)_r for one row (CSR thread-per-row / SELL).  x is written INSIDE this kernel (V columns
 // are reused every cycle, x is updated at every cycle end), so it is gathered with ordinary coherent
 // loads — never through the non-coherent read-only path (__ldg / ld.global.nc).  Visibility of other
@@ -202,6 +285,29 @@ __device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const do
   return s;
 }
 
+// CSR row from the CTA's shared-memory copy of its pattern (row pointers relative to the CTA's first
+// entry): the column indices no longer need a global load, so a row costs one dependent round trip
+// (value and x gathers in parallel) instead of three (row pointer -> index -> x).  Same order as row_dot.
+__device__ __forceinline__ double row_dot_sc(const MatDev& A, int64_t lr, const int32_t* s_rp, const int32_t* s_ci,
+                                            const double* __restrict__ vb, const double* __restrict__ x) {
+  const int32_t p0 = s_rp[lr], p1 = s_rp[lr + 1];
+  double s = 0.0;
+  for (int32_t p = p0; p < p1; p += 8) {
+    int32_t cc[8];
+    double vv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = p + u < p1;
+      cc[u] = ok ? s_ci[p + u] : 0;
+      vv[u] = ok ? __ldcs(vb + p + u) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p + u < p1) s += vv[u] * x[cc[u]];
+  }
+  return s;
+}
+
 // phase timer (CTA 0, thread 0, profiling only): adds now - *t0 to the phase slot and resets t0
 __device__ __forceinline__ void ptick(DevState* st, int kid, unsigned long long& t0) {
   if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -216,7 +322,7 @@ __device__ __forceinline__ void ptick(DevState* st, int kid, unsigned long long&
 // (one kernel with every variant's code carried more live registers and spilled in the hot loops:
 // C2 deflate +1.7 %).
 template <int VK>
-__global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
+__global__ void __launch_bounds__(PT, PCTA) k_solve_persistent(PArgs pa) {
   extern __shared__ double sm[];
   const Layout& L = pa.L;
   const MatDev& A = pa.A;
@@ -250,6 +356,8 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   // augment only: G (rows v_0..v_{m+1}: Q^T v_i) in Bs (sized (m+2) k), T and S = T^{-1} ([col][row])
   double* Ts = wk + PK + PM + 2;             // [(m+2)][(m+2)] when aug
   double* Ss = Ts + (aug ? (m + 2) * (m + 2) : 0);
+  int32_t* s_rp = (int32_t*)(Ss + (aug ? (m + 2) * (m + 2) : 0));  // CSR cache (pa.rcap / pa.ccap entries)
+  int32_t* s_ci = s_rp + pa.rcap;
   __shared__ double bsh[33];
   __shared__ int s_fail, s_stop;
   __shared__ double s_sc[8];
@@ -258,6 +366,11 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   __syncthreads();
   const bool cta0 = blockIdx.x == 0;
   if (cta0) prof_begin(st, K_MISC);
+  unsigned rep = pa.llred ? *(volatile unsigned*)&st->red_epoch : 0u;  // reduction epoch (LL)
+  auto gred = [&](int nv, DevState* pst) -> bool {
+    return pa.llred ? greduce_ll(dpart, nv, pa.ll, tot, rep, bsh, &s_fail, pst)
+                    : greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, pst);
+  };
   const int64_t ng = ld >> 5;
   const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
   const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
@@ -267,6 +380,22 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   const double* __restrict__ b = L.b;
   double bytes = 0.0;  // algorithmic bytes (CTA 0 accounts them)
   const bool keep = L.keep_l2 != 0;  // basis L2-sized: cached loads (the update pass re-hits them)
+  // ---- this CTA's CSR pattern into shared memory when it fits (the SpMVs then read only values and x)
+  bool sc = false;
+  const double* __restrict__ sc_v = A.v;
+  {
+    const int64_t re = r1 < L.n ? r1 : L.n;
+    if (pa.ccap > 0 && A.fmt == 0 && r0 < re && re - r0 + 1 <= pa.rcap) {
+      const int32_t e0 = A.rp[r0], cnt = A.rp[re] - e0;
+      if (cnt <= pa.ccap) {
+        for (int64_t i = tid; i <= re - r0; i += PT) s_rp[i] = A.rp[r0 + i] - e0;
+        for (int32_t e = tid; e < cnt; e += PT) s_ci[e] = A.ci[e0 + e];
+        sc = true;
+        sc_v = A.v + e0;
+      }
+    }
+    __syncthreads();
+  }
   // ---- column owners of this CTA's rows (neighbour sync): min / max column of its CSR entries
   __shared__ int s_clo, s_chi;
   unsigned epoch = 0;
@@ -357,7 +486,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
     s = block_sum(s, bsh);
     if (tid == 0) dpart[0] = s;
     __syncthreads();
-    if (!greduce(dpart, 1, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+    if (!gred(1, nullptr)) goto fail;
   }
   {
   const double bnorm = sqrt(tot[0]);
@@ -384,14 +513,14 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
     {
       double s = 0.0;
       for (int64_t r = r0 + tid; r < r1; r += PT) {
-        const double rr = r < L.n ? b[r] - row_dot(A, r, x) : 0.0;
+        const double rr = r < L.n ? b[r] - (sc ? row_dot_sc(A, r - r0, s_rp, s_ci, sc_v, x) : row_dot(A, r, x)) : 0.0;
         u0[r] = rr;
         s += rr * rr;
       }
       s = block_sum(s, bsh);
       if (tid == 0) dpart[0] = s;
       __syncthreads();
-      if (!greduce(dpart, 1, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      if (!gred(1, nullptr)) goto fail;
       beta = sqrt(tot[0]);
       if (cta0) bytes += A.bytes + 8.0 * L.n;
     }
@@ -413,7 +542,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         }
         __syncthreads();
       }
-      if (!greduce(dpart, k, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      if (!gred(k, nullptr)) goto fail;
       for (int l = tid; l < k; l += PT) {  // z = R_C^{-1} a  (oblique: t = E^{-1} a)
         double s = 0.0;
         if (obl) {
@@ -440,7 +569,7 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       s2 = block_sum(s2, bsh);
       if (tid == 0) dpart[0] = s2;
       __syncthreads();
-      if (!greduce(dpart, 1, L.partial, pa.tot_g, tot, pa.bar, &s_fail)) goto fail;
+      if (!gred(1, nullptr)) goto fail;
       beta = sqrt(tot[0]);
       if (cta0) bytes += 8.0 * L.n * (4 * k + 4);
     }
@@ -472,6 +601,12 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         }
       }
       ptick(st, K_PB1, tph);
+      if (pa.skew && cycles == 1 && j == pa.skew && tid == 0) {  // experiment: step start, SM id
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        pa.flags[NSM * 2 + 1 * NSM * 2 + blockIdx.x] = (unsigned)(gtimer() & 0xffffffffu);
+        pa.flags[NSM * 2 + 3 * NSM * 2 + blockIdx.x] = smid;
+      }
       const int nv = 2 * p + 2 + nx;
       for (int c = tid; c < nv; c += PT) dpart[c] = 0.0;
       double s_uu = 0.0, s_uy = 0.0;
@@ -482,7 +617,15 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
           sx = pa.pz;
           if (cta0) bytes += pa.pc_bytes;
         }
-        for (int64_t r = r0 + tid; r < r1; r += PT) y[r] = r < L.n ? row_dot(A, r, sx) : 0.0;
+        if (sc) {
+          for (int64_t r = r0 + tid; r < r1; r += PT) y[r] = r < L.n ? row_dot_sc(A, r - r0, s_rp, s_ci, sc_v, sx) : 0.0;
+        } else {
+          for (int64_t r = r0 + tid; r < r1; r += PT) y[r] = r < L.n ? row_dot(A, r, sx) : 0.0;
+        }
+      }
+      if (st->profile && cta0 && tid == 0) {  // sub-interval of p_spmv_dots: the SpMV alone
+        st->kstat[K_PB7].ns += gtimer() - tph;
+        st->kstat[K_PB7].launches++;
       }
       for (int64_t base = r0; base < r1; base += PT) {
         const int64_t r = base + tid;
@@ -498,19 +641,23 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         s_uy += ur * yr;
         __syncthreads();
         const int cnt = (int)min((int64_t)PT, r1 - base);
-        constexpr int RPL = PT / 32;
+        constexpr int RPL = 16;
         for (int c = wid; c < p + nx; c += PT / 32) {
           const int zcol = c < p ? lo + c : (aug ? QB + (c - p) : ((c - p) < k ? c - p : pbase + (c - p - k)));
-          const double* zc = Z + (int64_t)zcol * ld + base + lane;
-          double zv[RPL];
-#pragma unroll
-          for (int q = 0; q < RPL; ++q)  // 16 independent loads in flight per lane
-            zv[q] = (lane + 32 * q < cnt) ? (keep ? zc[32 * q] : __ldcs(zc + 32 * q)) : 0.0;
           double su = 0.0, sy = 0.0;
+#pragma unroll 1
+          for (int h = 0; h < PT / (32 * RPL); ++h) {
+            const int lh = lane + 32 * RPL * h;
+            const double* zc = Z + (int64_t)zcol * ld + base + lh;
+            double zv[RPL];
 #pragma unroll
-          for (int q = 0; q < RPL; ++q) {
-            su += zv[q] * us[lane + 32 * q];
-            sy += zv[q] * ysm[lane + 32 * q];
+            for (int q = 0; q < RPL; ++q)  // 16 independent loads in flight per lane
+              zv[q] = (lh + 32 * q < cnt) ? (keep ? zc[32 * q] : __ldcs(zc + 32 * q)) : 0.0;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+              su += zv[q] * us[lh + 32 * q];
+              sy += zv[q] * ysm[lh + 32 * q];
+            }
           }
           su = warp_sum(su);
           sy = warp_sum(sy);
@@ -531,11 +678,13 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
         __syncthreads();
       }
       ptick(st, K_PB2, tph);
-      if (pa.skew && cycles == 1 && j >= 5 && j < 9 && tid == 0) {
-        const unsigned tnow = (unsigned)(gtimer() & 0xffffffffu);
-        pa.flags[NSM * 2 + (j - 5) * NSM * 2 + blockIdx.x] = tnow;  // dots done
+      if (pa.skew && cycles == 1 && j == pa.skew && tid == 0) {  // experiment: dots done
+        pa.flags[NSM * 2 + blockIdx.x] = (unsigned)(gtimer() & 0xffffffffu);
       }
-      if (!greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, st)) goto fail;
+      if (!gred(nv, st)) goto fail;
+      if (pa.skew && cycles == 1 && j == pa.skew && tid == 0) {  // experiment: reduction done
+        pa.flags[NSM * 2 + 2 * NSM * 2 + blockIdx.x] = (unsigned)(gtimer() & 0xffffffffu);
+      }
       ptick(st, K_PB3, tph);
       if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + nx + 2);
       // ---- replicated epilogue: delayed second pass, column j-1, least squares
@@ -730,24 +879,25 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
       for (int64_t r = r0 + tid; r < r1; r += PT) {
         const double ur = u[r], yr = y[r];
         double sv = 0.0, sn2 = 0.0;
-        int c = 0;
-        for (; c + 8 <= p; c += 8) {  // 8 independent loads in flight
+        int c = p;  // columns in DESCENDING order: the dot pass just streamed them ascending, so the
+                    // most recently touched ones come first (LRU-friendly when the basis nears the L2 size)
+        for (; c >= 8; c -= 8) {  // 8 independent loads in flight
           double z[8];
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            const double* zp = Z + (int64_t)(lo + c + t) * ld + r;
+            const double* zp = Z + (int64_t)(lo + c - 1 - t) * ld + r;
             z[t] = keep ? *zp : __ldcs(zp);
           }
 #pragma unroll
           for (int t = 0; t < 8; ++t) {
-            sv += cv[c + t] * z[t];
-            sn2 += cn[c + t] * z[t];
+            sv += cv[c - 1 - t] * z[t];
+            sn2 += cn[c - 1 - t] * z[t];
           }
         }
-        for (; c < p; ++c) {
-          const double z = Z[(int64_t)(lo + c) * ld + r];
-          sv += cv[c] * z;
-          sn2 += cn[c] * z;
+        for (; c > 0; --c) {
+          const double z = Z[(int64_t)(lo + c - 1) * ld + r];
+          sv += cv[c - 1] * z;
+          sn2 += cn[c - 1] * z;
         }
         if (obl)
           for (int l = 0; l < k; ++l) sn2 += wk[l] * Z[(int64_t)(pbase + l) * ld + r];
@@ -844,11 +994,13 @@ __global__ void __launch_bounds__(PT, 2) k_solve_persistent(PArgs pa) {
   }
   }
 out:
+  if (pa.llred && cta0 && tid == 0) st->red_epoch = rep;
   return;
 fail:
   if (cta0 && tid == 0) {
     st->status = RG_E_CUDA;
     st->done = 1;
+    if (pa.llred) st->red_epoch = rep + 16u;  // past anything a CTA may have published
   }
 }
 
@@ -862,13 +1014,28 @@ size_t persistent_smem(int m, int k, bool aug) {
 
 // Returns cudaErrorNotSupported when the configuration is outside this path.
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
-                              unsigned* flags, int m, int k, int variant, const PrecDev* P, cudaStream_t s) {
+                              unsigned* flags, unsigned long long* ll, int m, int k, int variant, const PrecDev* P,
+                              cudaStream_t s) {
   if (m > PM || k > PK || A.fmt == 2) return cudaErrorNotSupported;
   const bool aug = variant == RG_AUGMENT && k > 0;
   const int vk = aug ? 2 : ((galerkin_variant(variant) && k > 0) ? 1 : 0);
   const void* fn = vk == 2 ? (const void*)k_solve_persistent<2>
                            : (vk == 1 ? (const void*)k_solve_persistent<1> : (const void*)k_solve_persistent<0>);
-  const size_t smem = persistent_smem(m, k, aug);
+  const size_t smem0 = persistent_smem(m, k, aug);
+  // CSR pattern cache: what keeps PCTA CTAs per SM resident (228 KB per SM, 1 KB per CTA reserved,
+  // ~1 KB static), sized for this CTA count's rows and ~1.5x its share of the entries
+  int rcap = 0, ccap = 0;
+  if (A.fmt == 0 && !getenv("RG_NO_SMEM_CSR")) {
+    const int64_t G0 = std::min<int64_t>((int64_t)NSM * PCTA, std::max<int64_t>(1, (L.ld + PT - 1) / PT));
+    const int64_t rows = ((L.ld >> 5) / G0 + 2) * 32 + 1;
+    const int64_t ents = A.nnz / G0 * 3 / 2 + 1024;
+    const int64_t budget = ((int64_t)228 * 1024 / PCTA - 2 * 1024 - (int64_t)smem0) / 4;
+    if (budget >= rows + ents) {
+      rcap = (int)rows;
+      ccap = (int)ents;
+    }
+  }
+  const size_t smem = smem0 + sizeof(int32_t) * (size_t)(rcap + ccap);
   static int max_smem = -1;
   if (max_smem < 0) {
     for (const void* f : {(const void*)k_solve_persistent<0>, (const void*)k_solve_persistent<1>,
@@ -893,14 +1060,15 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   if (occ < 1) return cudaErrorNotSupported;
   // tiny systems (<= 8 rows per thread of one CTA) run on ONE CTA: no grid barriers at all
   int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;
-  static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : 2;
+  static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : PCTA;
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
   PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k,
            galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, aug ? 1 : 0, flags, nbsync,
-           getenv("RG_SKEW") ? 1 : 0,
-           P ? 1 : 0, P ? *P : PrecDev(), L.pz, L.pt, 0.0};
+           getenv("RG_SKEW") ? atoi(getenv("RG_SKEW")) : 0,
+           P ? 1 : 0, P ? *P : PrecDev(), L.pz, L.pt, 0.0, rcap, ccap, ll,
+           (ll && G > 1 && G <= LL_GMAX && G <= PT && !getenv("RG_NO_LLRED")) ? 1 : 0};
   if (P) {
     double b2 = 0.0;
     for (int c = 0; c < P->ncolors; ++c) b2 += 12.0 * (double)(P->cL[c] + P->cU[c]);

@@ -100,6 +100,7 @@ struct rg_ctx {
   double* tot_g = nullptr;   // persistent solve: reduced totals
   unsigned* gbar = nullptr;  // persistent solve: grid-barrier words
   unsigned* pflags = nullptr;  // persistent solve: neighbour-sync epochs (NSM * 8)
+  unsigned long long* llw = nullptr;  // persistent solve: flag-carrying reduction words (ll_words())
   DevState* st = nullptr;
   DevState* hst = nullptr;  // pinned host mirror
   double* hhist = nullptr;  // pinned history staging
@@ -287,6 +288,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
     const double avg = c->n > 0 ? (double)c->nnz / (double)c->n : 0.0;
     M.lpr = avg <= 12.0 ? 1 : avg <= 24.0 ? 8 : avg <= 48.0 ? 16 : 32;
     M.bytes = 12.0 * c->nnz + 4.0 * (c->n + 1) + 16.0 * c->n;
+    M.nnz = c->nnz;
   } else if (c->fmt == 1) {
     M.sp = c->sp; M.sw = c->sw; M.sci = c->sci; M.sv = c->sv; M.nslices = c->nslices;
     M.bytes = 12.0 * c->sell_len + 12.0 * c->nslices + 16.0 * c->n;
@@ -539,7 +541,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   free_matrix(c);
   cudaFree(c->Z); cudaFree(c->x); cudaFree(c->b); cudaFree(c->X); cudaFree(c->Y);
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
-  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar); cudaFree(c->pflags);
+  cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar); cudaFree(c->pflags); cudaFree(c->llw);
   drop_preconditioner(c);
   cudaFree(c->pz); cudaFree(c->pt);
   if (c->hst) cudaFreeHost(c->hst);
@@ -597,6 +599,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
       (s = dalloc(&c->small, (size_t)SMALL * 16, "small")) != RG_OK || (s = dalloc(&c->dflag, 4, "flag")) != RG_OK ||
       (s = dalloc(&c->tot_g, (size_t)MAXRED, "totals")) != RG_OK || (s = dalloc(&c->gbar, (size_t)BAR_WORDS, "barrier")) != RG_OK ||
       (s = dalloc(&c->pflags, (size_t)NSM * 16, "sync flags")) != RG_OK ||
+      (s = dalloc(&c->llw, ll_words(), "reduction words")) != RG_OK ||
       (s = dalloc(&c->st, 1, "state")) != RG_OK) {
     rg_destroy(c);
     return s;
@@ -621,6 +624,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   ok(cudaMemsetAsync(c->t2, 0, sizeof(double) * np, c->stream));
   ok(cudaMemsetAsync(c->counter, 0, sizeof(unsigned) * 4, c->stream));
   ok(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
+  ok(cudaMemsetAsync(c->llw, 0, sizeof(unsigned long long) * ll_words(), c->stream));
   for (int i = 0; i < MAXCOL; ++i) c->hst->sc[i] = i < VB ? 1.0 : 0.0;
   ok(cudaMemcpyAsync(&c->st->sc[0], &c->hst->sc[0], sizeof(double) * MAXCOL, cudaMemcpyHostToDevice, c->stream));
   ok(cudaEventCreate(&c->e0));
@@ -820,7 +824,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
     CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
     CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 16, s));
-    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, m, k, eff,
+    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, c->llw, m, k, eff,
                                        c->L.prec ? &c->P : nullptr, s);
     if (ep == cudaSuccess) done_persist = true;
     else if (ep == cudaErrorNotSupported || ep == cudaErrorCooperativeLaunchTooLarge) cudaGetLastError();
@@ -841,28 +845,15 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (history && hcap > 0) CK(cudaMemcpyAsync(c->hhist, c->hist, sizeof(double) * hcap, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (check_c) bad = c->hflag[0];
-  if (done_persist && getenv("RG_SKEW")) {  // experiment: per-CTA "dots done" spread, steps 5..8
+  if (done_persist && getenv("RG_SKEW")) {  // experiment: per-CTA step start / dots done / reduction done / SM
     std::vector<unsigned> ts((size_t)NSM * 8);
     cudaMemcpy(ts.data(), c->pflags + NSM * 2, sizeof(unsigned) * NSM * 8, cudaMemcpyDeviceToHost);
-    for (int q = 0; q < 4; ++q) {
-      unsigned mn = 0xffffffffu, mx = 0;
-      int imx = -1, cnt = 0;
-      for (int b2 = 0; b2 < NSM * 2; ++b2) {
-        const unsigned v = ts[(size_t)q * NSM * 2 + b2];
-        if (!v) continue;
-        ++cnt;
-        if (v < mn) mn = v;
-        if (v > mx) { mx = v; imx = b2; }
-      }
-      if (cnt) {
-        std::vector<unsigned> vs;
-        for (int b2 = 0; b2 < NSM * 2; ++b2) if (ts[(size_t)q * NSM * 2 + b2]) vs.push_back(ts[(size_t)q * NSM * 2 + b2] - mn);
-        std::sort(vs.begin(), vs.end());
-        fprintf(stderr, "skew step %d: CTAs %d spread %.2f us (p50 %.2f p90 %.2f), last CTA %d, CTA0 %.2f\n", q + 5, cnt,
-                (mx - mn) * 1e-3, vs[vs.size() / 2] * 1e-3, vs[vs.size() * 9 / 10] * 1e-3, imx,
-                ts[(size_t)q * NSM * 2] ? (ts[(size_t)q * NSM * 2] - mn) * 1e-3 : -1.0);
-      }
-    }
+    unsigned mn = 0xffffffffu;
+    for (int b2 = 0; b2 < NSM * 2; ++b2) mn = std::min(mn, ts[NSM * 2 + b2]);
+    fprintf(stderr, "skewcsv cta,sm,start,dots,reduced\n");
+    for (int b2 = 0; b2 < NSM * 2; ++b2)
+      fprintf(stderr, "skewcsv %d,%u,%.3f,%.3f,%.3f\n", b2, ts[3 * NSM * 2 + b2], (int)(ts[NSM * 2 + b2] - mn) * 1e-3,
+              (int)(ts[b2] - mn) * 1e-3, (int)(ts[2 * NSM * 2 + b2] - mn) * 1e-3);
   }
   if (bad) {
     c->have_W = false;
@@ -1101,7 +1092,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
                                        "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
-                                       "ssor_sweep_kernels"};
+                                       "ssor_sweep_kernels", "p_spmv"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));
