@@ -394,6 +394,30 @@ def run_ours(args, cfg):
                             "rg_build_recycle, rg_solve (H2D b, D2H x), rg_push_snapshot (H2D x); the host "
                             "generation of A_t, b_t (synthetic data source) is outside the clock"}
 
+        # the recycled sequence against plain GMRES(m) on the GPU (north_star: "the recycled solver's
+        # end-to-end sequence time reported against plain GMRES(m)"): the same config as a plain
+        # sequence, same warm-up, same timed systems, same device timing and L2 flushes
+        vs_plain = None
+        if not args.no_vs_plain and args.variant != "plain":
+            hrun = None
+            run.ctx.close()
+            prun = GpuRun(cfg, "plain", k, device, stream, profile=False, sell=sell,
+                          precond=args.omega if args.precond == "ssor" else None)
+            for _ in range(args.warmup):
+                prun.step()
+            torch.cuda.synchronize()
+            pper, _, pt_max = timed_replicas(prun.step, args.steps, 0, dist_on, device, "cuda",
+                                             between=lambda: flush_l2(flush), stream=stream)
+            pits = prun.iters[args.warmup:]
+            prun.ctx.close()
+            vs_plain = {"variant": "plain", "value": pt_max / (args.steps * ws), "unit": UNIT,
+                        "sequence_s": pt_max, "iterations_timed": pits,
+                        "iterations_total": sum(pits), "recycled_iterations_total": sum(timed_iters),
+                        "recycled_sequence_s": t_max,
+                        "sequence_speedup": round(pt_max / t_max, 4),
+                        "scope": "the same systems t of a free-running plain GMRES(m) sequence (its own "
+                                 "x_{t-1} drives A_t, b_t), timed like the main line"}
+
     if rank != 0:
         if dist_on:
             torch.distributed.destroy_process_group()
@@ -446,6 +470,8 @@ def run_ours(args, cfg):
                    "l2": "flushed (256 MiB write) between steps, outside the timed events",
                    "parallelism": f"replicas x{ws}"},
         "per_step_s": [round(p, 6) for p in per],
+        "sequence_s": t_max,
+        "vs_plain": vs_plain,
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
         "clocks": clk.summary(),
         "kernels": {kname: {"launches": s["launches"], "noop": s["noop"], "ms": round(s["ms"], 4),
@@ -497,6 +523,8 @@ def main(argv=None):
                     "0: keep CSR, -1: config default")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-vs-plain", action="store_true",
+                    help="skip the plain GMRES(m) sequence timed beside the recycled one")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-systems", type=int, default=3)

@@ -5,6 +5,8 @@
 // Gram/Jacobi pass on Y to restore the accuracy the squared conditioning costs (DESIGN.md
 // reading R-SVD), and W = Y V_2 Sigma^{-1}.  CholQR2 of C = A W uses the same Gram and X*M
 // kernels plus a one-CTA Cholesky.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -141,17 +143,16 @@ constexpr int JLD = MAXS + 1;
 // start is valid for Jacobi.  With the previous system's eigenvectors (the window changed by one
 // column) the sweep count at the 1e-14 stop is unchanged (7 at s = 20), but most pairs fall below
 // the rotation threshold early and are skipped: measured -40 us per build at C2.
-__global__ void __launch_bounds__(256) k_jacobi(const double* G, int s, double* lam, double* V,
+__global__ void __launch_bounds__(1024) k_jacobi(const double* G, int s, double* lam, double* V,
                                                 double* sigma_out, DevState* st, const double* V0, int s0) {
   extern __shared__ double jsm[];
   double* A_ = jsm;                    // JLD x JLD, A(r, c) = A_[r * JLD + c]
   double* V_ = jsm + JLD * JLD;
   double* B_ = jsm + 2 * JLD * JLD;    // warm start scratch: G V0
-  __shared__ double cs[MAXS / 2 + 1], sn[MAXS / 2 + 1];
-  __shared__ int pp[MAXS / 2 + 1], qq[MAXS / 2 + 1];
   __shared__ double ev[MAXS + 1];
   __shared__ int perm[MAXS + 1];
-  __shared__ double s_off, s_fro;
+  __shared__ double jred[33], jcs[MAXS / 2 + 1], jsn[MAXS / 2 + 1];
+  __shared__ unsigned short jpair[MAXS * MAXS / 2];  // round-robin pairing: (p | q << 8) per (round, i)
   const int tid = threadIdx.x, bd = blockDim.x;
   if (st) prof_begin(st, K_JACOBI);
   const int ne = s + (s & 1);  // even size (pad with a decoupled zero row/column)
@@ -178,64 +179,82 @@ __global__ void __launch_bounds__(256) k_jacobi(const double* G, int s, double* 
     __syncthreads();
   }
   const int half = ne / 2;
+  // Per round: the `half` rotation threads compute (c, s) of their pair from the current A (pairs
+  // from a table built once: no integer division in the loop), barrier, then thread (i, i2)
+  // updates the 2x2 block of rows {p_i, q_i} x columns {p_i2, q_i2} into the other buffer of a
+  // double-buffered A — rows first (J^T A), then columns (A J): the operation order of a full row
+  // pass followed by a column pass, so every entry gets the same arithmetic as before — and rows
+  // 2 i2, 2 i2 + 1 of V for pair i (in place: no other thread touches them in this round), barrier.
+  // The loop is latency-bound (one warp per SM sub-partition): ncu showed ~390 instructions per
+  // warp per round in the first version (integer modulo for the pairing, the rotation formula
+  // evaluated by every block thread); 1.16 us per round at s = 20.
+  for (int e = tid; e < (ne - 1) * half; e += bd) {
+    const int round = e / half, i = e % half;
+    int p, q;
+    if (i == 0) { p = round; q = ne - 1; }
+    else { p = (round + i) % (ne - 1); q = (round - i + (ne - 1)) % (ne - 1); }
+    if (p > q) { const int t = p; p = q; q = t; }
+    jpair[e] = (unsigned short)(p | (q << 8));
+  }
+  double* Ac = A_;
+  double* An = B_;
   int sweep = 0;
   for (; sweep < 40; ++sweep) {
-    if (tid == 0) {
-      double off = 0.0, fro = 0.0;
-      for (int r = 0; r < ne; ++r)
-        for (int c = 0; c < ne; ++c) {
-          const double v2 = A_[(r) * JLD + (c)] * A_[(r) * JLD + (c)];
-          fro += v2;
-          if (r != c) off += v2;
-        }
-      s_off = off;
-      s_fro = fro;
+    double off = 0.0, fro = 0.0;
+    for (int e = tid; e < ne * ne; e += bd) {
+      const int r = e / ne, c = e % ne;
+      const double v2 = Ac[(r) * JLD + (c)] * Ac[(r) * JLD + (c)];
+      fro += v2;
+      if (r != c) off += v2;
     }
-    __syncthreads();
-    if (!(s_off > 1e-28 * s_fro) || ne < 2) break;  // off(A)_F <= 1e-14 ||A||_F
+    off = block_sum(off, jred);
+    fro = block_sum(fro, jred);
+    if (!(off > 1e-28 * fro) || ne < 2) break;  // off(A)_F <= 1e-14 ||A||_F
     for (int round = 0; round < ne - 1; ++round) {
-      // circle method: fix player ne-1; pair (round, ne-1) and ((round+i)%(ne-1), (round-i)%(ne-1))
-      for (int i = tid; i < half; i += bd) {
-        int p, q;
-        if (i == 0) { p = round; q = ne - 1; }
-        else { p = (round + i) % (ne - 1); q = (round - i + (ne - 1)) % (ne - 1); }
-        if (p > q) { const int t = p; p = q; q = t; }
-        pp[i] = p; qq[i] = q;
-        const double apq = A_[(p) * JLD + (q)], app = A_[(p) * JLD + (p)], aqq = A_[(q) * JLD + (q)];
+      const unsigned short* pr = jpair + round * half;
+      if (tid < half) {
+        const int p = pr[tid] & 0xff, q = pr[tid] >> 8;
+        const double apq = Ac[(p) * JLD + (q)], app = Ac[(p) * JLD + (p)], aqq = Ac[(q) * JLD + (q)];
         double c = 1.0, sv = 0.0;
         if (fabs(apq) > 1e-300 && apq * apq > 1e-36 * fabs(app * aqq)) {
           // t = tan(theta) = sign(th) / (|th| + sqrt(1 + th^2)), th = (aqq - app) / (2 apq), written as
-          // t = b sign(a) / (|a| + sqrt(a^2 + b^2)) with a = aqq - app, b = 2 apq (one sqrt, one
-          // division, one reciprocal square root instead of three of each)
+          // t = b' / d with a = aqq - app, b = 2 apq, b' = b sign(a), d = |a| + sqrt(a^2 + b^2); then
+          // c = 1 / sqrt(1 + t^2) = d w and s = t c = b' w with w = 1 / sqrt(d^2 + b^2): one sqrt and
+          // one reciprocal square root on the dependent chain, no division (the loop is latency-bound)
           const double a = aqq - app, b = 2.0 * apq;
-          const double t = (a >= 0.0 ? b : -b) / (fabs(a) + sqrt(a * a + b * b));
-          c = rsqrt(1.0 + t * t);
-          sv = t * c;
+          const double d = fabs(a) + sqrt(a * a + b * b);
+          const double w = rsqrt(d * d + b * b);
+          c = d * w;
+          sv = (a >= 0.0 ? b : -b) * w;
         }
-        cs[i] = c; sn[i] = sv;
+        jcs[tid] = c;
+        jsn[tid] = sv;
       }
       __syncthreads();
-      for (int e = tid; e < half * ne; e += bd) {  // rows: A <- J^T A
-        const int i = e / ne, col = e % ne;
-        const int p = pp[i], q = qq[i];
-        const double ap = A_[(p) * JLD + (col)], aq = A_[(q) * JLD + (col)];
-        A_[(p) * JLD + (col)] = cs[i] * ap - sn[i] * aq;
-        A_[(q) * JLD + (col)] = sn[i] * ap + cs[i] * aq;
+      for (int e = tid; e < half * half; e += bd) {
+        const int i = e / half, i2 = e - i * half;
+        const int p = pr[i] & 0xff, q = pr[i] >> 8, p2 = pr[i2] & 0xff, q2 = pr[i2] >> 8;
+        const double c = jcs[i], sv = jsn[i], c2 = jcs[i2], s2 = jsn[i2];
+        const double a = Ac[(p) * JLD + (p2)], b = Ac[(p) * JLD + (q2)];
+        const double d = Ac[(q) * JLD + (p2)], f = Ac[(q) * JLD + (q2)];
+        const double a1 = c * a - sv * d, b1 = c * b - sv * f;   // rows p, q: J^T A
+        const double d1 = sv * a + c * d, f1 = sv * b + c * f;
+        An[(p) * JLD + (p2)] = c2 * a1 - s2 * b1;                // columns p2, q2: A J
+        An[(p) * JLD + (q2)] = s2 * a1 + c2 * b1;
+        An[(q) * JLD + (p2)] = c2 * d1 - s2 * f1;
+        An[(q) * JLD + (q2)] = s2 * d1 + c2 * f1;
+#pragma unroll
+        for (int row = 2 * i2; row < 2 * i2 + 2; ++row) {         // V <- V J (rows of pair i)
+          const double vp = V_[(row) * JLD + (p)], vq = V_[(row) * JLD + (q)];
+          V_[(row) * JLD + (p)] = c * vp - sv * vq;
+          V_[(row) * JLD + (q)] = sv * vp + c * vq;
+        }
       }
       __syncthreads();
-      for (int e = tid; e < half * ne; e += bd) {  // columns: A <- A J, V <- V J
-        const int i = e / ne, row = e % ne;
-        const int p = pp[i], q = qq[i];
-        const double ap = A_[(row) * JLD + (p)], aq = A_[(row) * JLD + (q)];
-        A_[(row) * JLD + (p)] = cs[i] * ap - sn[i] * aq;
-        A_[(row) * JLD + (q)] = sn[i] * ap + cs[i] * aq;
-        const double vp = V_[(row) * JLD + (p)], vq = V_[(row) * JLD + (q)];
-        V_[(row) * JLD + (p)] = cs[i] * vp - sn[i] * vq;
-        V_[(row) * JLD + (q)] = sn[i] * vp + cs[i] * vq;
-      }
-      __syncthreads();
+      double* t = Ac; Ac = An; An = t;
     }
   }
+  A_ = Ac;
   if (tid == 0) {  // sort eigenvalues of the first s (the pad is the zero eigenpair of the pad)
     int cnt = 0;
     for (int i = 0; i < ne; ++i) {
@@ -542,7 +561,9 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
     cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     init = true;
   }
-  k_jacobi<<<1, 256, smem, strm>>>(G, s, lam, V, sigma_out, st, s0 > 0 ? V0 : nullptr, s0);
+  const int half = (s + (s & 1)) / 2;  // one thread per 2x2 block of the rotation round (<= 1024)
+  const int nt = std::max(64, std::min(1024, (half * half + 31) / 32 * 32));
+  k_jacobi<<<1, nt, smem, strm>>>(G, s, lam, V, sigma_out, st, s0 > 0 ? V0 : nullptr, s0);
   return cudaGetLastError();
 }
 

@@ -68,6 +68,11 @@ size_t ll_words();
 cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
                               unsigned* flags, unsigned long long* ll, int m, int k, int variant, const PrecDev* P,
                               cudaStream_t s);
+// C = A W, CholQR2 -> Q (columns [VB - k, VB) of Z), R_C, R_C^{-1} (device state) in ONE cooperative
+// kernel; *cflag (zeroed by the caller) set on a singular factor.  CSR / SELL, k <= 16; otherwise
+// cudaErrorNotSupported (caller: build_c).  bar zeroed by the caller; ll as for launch_persistent.
+cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
+                          unsigned long long* ll, int k, int* cflag, cudaStream_t s);
 
 // ---- multicolour SSOR(omega) preconditioner (precond.cu)
 constexpr int MAXCOLORS = 64;

@@ -27,6 +27,7 @@ constexpr int PCTA = 1024 / PT;  // resident CTAs per SM
 constexpr int PM = 64;        // max restart length on this path
 constexpr int PK = 64;        // max recycle dimension on this path
 constexpr int PCOL = PK + PM + 2;
+constexpr int CBK = 16;       // max recycle dimension of the one-kernel operator build (k (k+1) / 2 <= MAXRED)
 
 struct PArgs {
   Layout L;
@@ -1004,6 +1005,256 @@ fail:
   }
 }
 
+// ---- recycle-operator build as ONE cooperative kernel (replaces build_c's chain of ~10 launches —
+// SpMM, 2 x (Gram, reduce, Cholesky, X*M), R_C finish — measured 165 us per C2 system, mostly launch
+// ramps and single-CTA tails).  P:310: the deflation projector uses an orthonormal basis of C = A W;
+// here C = A W (this CTA's rows, W complete from rg_build_recycle), CholQR2 with the two Gram
+// matrices grid-reduced (deterministic, fixed order) and the k x k Cholesky factors computed
+// REDUNDANTLY by every CTA (identical inputs and code: identical results, no broadcast), Q = C
+// R1^{-1} R2^{-1} in place in the Q columns; CTA 0 writes R_C = R2 R1 and R_C^{-1} = R1^{-1} R2^{-1}
+// to the device state and flags a singular factor (same tests as k_chol / k_rc_finish).  A separate
+// kernel, not a prologue of k_solve_persistent: inside it the extra code perturbed the register
+// allocation of the Arnoldi loop (update pass 8.8 -> 11.7 us per step at C2).
+// Thread per row (all k <= KC columns in registers: every load of a row is in flight at once);
+// rows staged in PT-row tiles [KC][PT] for the Gram, which is register-blocked: warp w < nblk owns a
+// 4 x 4 block (a-block <= b-block) of the k x k Gram and accumulates it over all of the CTA's rows
+// (lanes over rows), reduced across lanes once per pass.
+template <int KC>
+__global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs pa, int* cflag) {
+  constexpr int NB = KC / 4;                       // 4-column blocks
+  constexpr int NBLK = NB * (NB + 1) / 2;          // Gram blocks (a-block <= b-block), <= PT / 32
+  static_assert(NBLK <= PT / 32, "one warp per Gram block");
+  extern __shared__ double sm[];
+  double* tile = sm;                   // [KC][PT]
+  double* R1 = tile + KC * PT;         // [col][row], k x k each
+  double* R1i = R1 + CBK * CBK;
+  double* R2 = R1i + CBK * CBK;
+  double* R2i = R2 + CBK * CBK;
+  double* dpart = R2i + CBK * CBK;     // MAXRED
+  double* tot = dpart + MAXRED;        // MAXRED
+  __shared__ double bsh[33];
+  __shared__ int s_fail;
+  const Layout& L = pa.L;
+  const MatDev& A = pa.A;
+  DevState* st = pa.st;
+  const int k = pa.k, QB = L.VB - k, P2 = k * (k + 1) / 2;
+  const int64_t ld = L.ld;
+  double* Qc = L.Z + (int64_t)QB * ld;
+  const double* __restrict__ Wc = L.Z;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool cta0 = blockIdx.x == 0;
+  if (cta0) prof_begin(st, K_CBUILD);
+  if (tid == 0) s_fail = 0;
+  unsigned rep = pa.llred ? *(volatile unsigned*)&st->red_epoch : 0u;
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  auto gred = [&](int nv) -> bool {
+    return pa.llred ? greduce_ll(dpart, nv, pa.ll, tot, rep, bsh, &s_fail, nullptr)
+                    : greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, nullptr);
+  };
+  // this warp's Gram block (ab, bb): rows 4 ab.., columns 4 bb..
+  int ab = 0, bb = 0;
+  {
+    int q = wid;
+    while (q >= NB - ab && ab < NB) { q -= NB - ab; ++ab; }
+    bb = ab + q;
+  }
+  const bool gw = wid < NBLK && 4 * ab < k && 4 * bb < k;
+  double gacc[16];
+  auto gram_zero = [&]() {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) gacc[i] = 0.0;
+  };
+  auto gram_tile = [&](int cnt) {  // accumulate the staged tile's rows (lanes over rows)
+    if (!gw) return;
+    for (int t = lane; t < cnt; t += 32) {
+      double xa[4], xb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xa[i] = tile[(4 * ab + i) * PT + t];
+        xb[i] = tile[(4 * bb + i) * PT + t];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) gacc[4 * i + j] += xa[i] * xb[j];
+    }
+  };
+  auto gram_flush = [&]() {  // lane sums -> dpart (packed upper, index of (a, b), a <= b)
+    if (gw) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double v = warp_sum(gacc[4 * i + j]);
+          const int a2 = 4 * ab + i, b2 = 4 * bb + j;
+          if (lane == 0 && a2 < k && b2 < k && a2 <= b2) dpart[a2 * k - a2 * (a2 - 1) / 2 + (b2 - a2)] = v;
+        }
+    }
+    __syncthreads();
+  };
+  // upper Cholesky G = R^T R of the packed upper Gram in `tot` (warp 0), R^{-1} (lane c: column c)
+  auto chol = [&](double* R, double* Ri) {
+    if (wid == 0) {
+      auto g = [&](int a2, int b2) {
+        const int a3 = a2 < b2 ? a2 : b2, b3 = a2 < b2 ? b2 : a2;
+        return tot[a3 * k - a3 * (a3 - 1) / 2 + (b3 - a3)];
+      };
+      for (int jj = 0; jj < k; ++jj) {
+        if (lane == 0) {
+          double d = g(jj, jj);
+          for (int l = 0; l < jj; ++l) d -= R[jj * k + l] * R[jj * k + l];
+          if (!(d > 0.0)) { if (cta0) *cflag = 1; d = 1.0; }
+          R[jj * k + jj] = sqrt(d);
+        }
+        __syncwarp();
+        for (int i = jj + 1 + lane; i < k; i += 32) {
+          double v = g(i, jj);
+          for (int l = 0; l < jj; ++l) v -= R[jj * k + l] * R[i * k + l];
+          R[i * k + jj] = v / R[jj * k + jj];
+        }
+        __syncwarp();
+      }
+      for (int c = lane; c < k; c += 32) {
+        for (int r = k - 1; r >= 0; --r) {
+          double v = (r == c) ? 1.0 : 0.0;
+          for (int l = r + 1; l <= c; ++l) v -= R[l * k + r] * Ri[c * k + l];
+          Ri[c * k + r] = r <= c ? v / R[r * k + r] : 0.0;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  // row r of the Q columns times an upper-triangular inverse, in place (this thread owns the row)
+  auto row_tri = [&](int64_t r, const double* Ri, double* out) {
+    double x[KC];
+#pragma unroll
+    for (int l = 0; l < KC; ++l) x[l] = l < k ? Qc[(int64_t)l * ld + r] : 0.0;
+#pragma unroll
+    for (int c = 0; c < KC; ++c) {
+      double acc = 0.0;
+#pragma unroll
+      for (int l = 0; l <= c; ++l) acc += x[l] * Ri[c * k + l];
+      out[c] = acc;
+    }
+  };
+  for (int i = tid; i < MAXRED; i += PT) dpart[i] = 0.0;
+  for (int i = tid; i < 4 * CBK * CBK; i += PT) R1[i] = 0.0;
+  __syncthreads();
+  // pass 1: C = A W into the Q columns (padding rows stay 0), Gram of C
+  gram_zero();
+  for (int64_t base = r0; base < r1; base += PT) {
+    const int64_t r = base + tid;
+    const int cnt = (int)min((int64_t)PT, r1 - base);
+    if (tid < cnt) {
+      double acc[KC];
+#pragma unroll
+      for (int u = 0; u < KC; ++u) acc[u] = 0.0;
+      if (r < L.n) {
+        // 8 (value, column) pairs in flight, then the W gathers of every column in flight
+        int64_t e0, est;
+        int ne;
+        if (A.fmt == 1) {
+          const int64_t sl = r >> 5;
+          ne = __ldg(A.sw + sl);
+          e0 = __ldg(A.sp + sl) + (r & 31);
+          est = 32;
+        } else {
+          e0 = __ldg(A.rp + r);
+          ne = __ldg(A.rp + r + 1) - (int32_t)e0;
+          est = 1;
+        }
+        const double* __restrict__ av = A.fmt == 1 ? A.sv : A.v;
+        const int32_t* __restrict__ ac = A.fmt == 1 ? A.sci : A.ci;
+        for (int q0 = 0; q0 < ne; q0 += 8) {
+          double vv[8];
+          int32_t cc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const bool okq = q0 + q < ne;
+            vv[q] = okq ? __ldcs(av + e0 + (int64_t)(q0 + q) * est) : 0.0;
+            cc[q] = okq ? __ldcs(ac + e0 + (int64_t)(q0 + q) * est) : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (q0 + q < ne) {
+#pragma unroll
+              for (int u = 0; u < KC; ++u)
+                if (u < k) acc[u] += vv[q] * __ldg(Wc + (int64_t)u * ld + cc[q]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < KC; ++u) {
+        if (u < k) Qc[(int64_t)u * ld + r] = acc[u];
+        tile[u * PT + tid] = acc[u];
+      }
+    }
+    __syncthreads();
+    gram_tile(cnt);
+    __syncthreads();
+  }
+  gram_flush();
+  bool ok = gred(P2);
+  if (ok) chol(R1, R1i);
+  // pass 2: Q1 = C R1^{-1} in place, Gram of Q1
+  gram_zero();
+  for (int64_t base = r0; ok && base < r1; base += PT) {
+    const int64_t r = base + tid;
+    const int cnt = (int)min((int64_t)PT, r1 - base);
+    if (tid < cnt) {
+      double y[KC];
+      row_tri(r, R1i, y);
+#pragma unroll
+      for (int u = 0; u < KC; ++u) {
+        if (u < k) Qc[(int64_t)u * ld + r] = y[u];
+        tile[u * PT + tid] = u < k ? y[u] : 0.0;
+      }
+    }
+    __syncthreads();
+    gram_tile(cnt);
+    __syncthreads();
+  }
+  gram_flush();
+  if (ok) ok = gred(P2);
+  if (ok) chol(R2, R2i);
+  // pass 3: Q = Q1 R2^{-1} in place (no staging)
+  for (int64_t r = r0 + tid; ok && r < r1; r += PT) {
+    double y[KC];
+    row_tri(r, R2i, y);
+#pragma unroll
+    for (int u = 0; u < KC; ++u)
+      if (u < k) Qc[(int64_t)u * ld + r] = y[u];
+  }
+  if (cta0) {
+    // R_C = R2 R1, R_C^{-1} = R1^{-1} R2^{-1} ([col][row]), and k_rc_finish's singularity test
+    for (int e = tid; e < k * k; e += PT) {
+      const int c = e / k, r = e % k;
+      double v = 0.0, vi = 0.0;
+      for (int l = 0; l < k; ++l) {
+        v += R2[l * k + r] * R1[c * k + l];
+        vi += R1i[l * k + r] * R2i[c * k + l];
+      }
+      st->RC[c][r] = v;
+      st->RCinv[c][r] = vi;
+      if (r == c) tot[c] = fabs(v);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double dmax = 0.0, dmin = 1e308;
+      for (int i = 0; i < k; ++i) {
+        dmax = tot[i] > dmax ? tot[i] : dmax;
+        dmin = tot[i] < dmin ? tot[i] : dmin;
+      }
+      if (!ok || !(dmin > 1e-12 * dmax)) *cflag = 1;
+      if (pa.llred) st->red_epoch = ok ? rep : rep + 16u;  // past anything a CTA may have published
+      prof_end(st, K_CBUILD, A.bytes + 8.0 * (double)L.n * 6.0 * k);
+    }
+  }
+}
+
 }  // namespace
 
 size_t persistent_smem(int m, int k, bool aug) {
@@ -1075,6 +1326,39 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
     pa.pc_bytes = b2 + 8.0 * (double)L.n * 6.0;  // + perm, row pointers, 1/a_rr, in, out (fwd), out r/w (bwd)
   }
   void* args[] = {&pa};
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(PT), args, smem, s);
+}
+
+// One cooperative launch building C = A W, Q, R_C, R_C^{-1} (k_cbuild).  cudaErrorNotSupported when
+// outside its scope (BSR, k > CBK, not co-resident): the caller runs build_c's kernel chain instead.
+cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
+                          unsigned long long* ll, int k, int* cflag, cudaStream_t s) {
+  if (k < 1 || k > CBK || A.fmt == 2) return cudaErrorNotSupported;
+  const int nch = (k + 7) / 8;
+  const void* fn = nch == 1 ? (const void*)k_cbuild<8> : (const void*)k_cbuild<16>;
+  const size_t smem = sizeof(double) * ((size_t)8 * nch * PT + 4 * CBK * CBK + 2 * MAXRED);
+  static int occ[3] = {-1, -1, -1};
+  if (occ[nch] < 0) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[nch], fn, PT, smem) != cudaSuccess) {
+      cudaGetLastError();
+      occ[nch] = 0;
+    }
+  }
+  if (occ[nch] < 1) return cudaErrorNotSupported;
+  const int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;
+  const int64_t cap = (int64_t)NSM * (occ[nch] >= PCTA ? PCTA : occ[nch]);
+  const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+  PArgs pa{};
+  pa.L = L;
+  pa.A = A;
+  pa.st = st;
+  pa.tot_g = tot_g;
+  pa.bar = bar;
+  pa.k = k;
+  pa.ll = ll;
+  pa.llred = (ll && G > 1 && G <= LL_GMAX && G <= PT && !getenv("RG_NO_LLRED")) ? 1 : 0;
+  void* args[] = {&pa, &cflag};
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(PT), args, smem, s);
 }
 

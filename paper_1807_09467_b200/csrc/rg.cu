@@ -783,8 +783,36 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   int c_spmv = 0;
   bool check_c = false;
   const int want_kind = galerkin_variant(eff) ? 1 : 0;
-  if (eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind)) {
-    if ((rs = (galerkin_variant(eff) ? build_c_oblique(c) : build_c(c, false))) != RG_OK) return rs;
+  // RG_TIMING: device-side phase split of one solve (events on the solve's stream)
+  static const bool timing = getenv("RG_TIMING") != nullptr;
+  static cudaEvent_t tev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (timing && !tev[0])
+    for (auto& e : tev) cudaEventCreate(&e);
+  if (timing) cudaEventRecord(tev[0], s);
+  // C = A W is rebuilt when stale.  On the persistent path (deflate / augment, k <= 16) the solve
+  // kernel builds it itself (fuse_c); otherwise the build_c kernel chain runs first.
+  const bool need_c = eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind);
+  const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
+  const double basis_pass0 = 8.0 * (double)c->n * (double)(k + m + 2);
+  const bool dcgs_next = c->use_dcgs && !(c->A.bytes > basis_pass0 && !getenv("RG_FORCE_DCGS"));
+  static const bool no_fuse = getenv("RG_NO_FUSE_C") != nullptr;
+  bool fuse_c = need_c && !galerkin_variant(eff) && !no_fuse && c->use_persist && persist_size && dcgs_next &&
+                !(c->flags & RG_FLAG_NO_GRAPH);
+  if (need_c) {
+    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
+    if (fuse_c) {  // one cooperative kernel (persistent.cu k_cbuild) instead of build_c's ~10 launches
+      CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
+      const cudaError_t eb = launch_cbuild(c->L, c->A, c->st, c->tot_g, c->gbar, c->llw, k, c->dflag, s);
+      if (eb == cudaSuccess) {
+        c->c_valid = true;
+      } else if (eb == cudaErrorNotSupported || eb == cudaErrorCooperativeLaunchTooLarge) {
+        cudaGetLastError();
+        fuse_c = false;
+      } else {
+        CK(eb);
+      }
+    }
+    if (!fuse_c && (rs = (galerkin_variant(eff) ? build_c_oblique(c) : build_c(c, false))) != RG_OK) return rs;
     c->c_kind = want_kind;
     c_spmv = k;
     check_c = true;
@@ -814,12 +842,12 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   h->dcgs = c->dcgs_now ? 1 : 0;
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
   c->L.augment = eff == RG_AUGMENT;
+  if (timing) cudaEventRecord(tev[1], s);
   CK(cudaEventRecord(c->e0, s));
   bool done_persist = false;
   // Measured on B200: the single cooperative kernel wins while kernel-boundary
   // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
   // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
-  const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
   c->L.prec = c->prec_kind ? 1 : 0;
   if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
     CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
@@ -838,12 +866,22 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   CK(cudaEventRecord(c->e1, s));
   // one synchronisation per solve: header, C=AW singularity flag, x and the history together
   int bad = 0;
+  if (timing) cudaEventRecord(tev[2], s);
   CK(cudaMemcpyAsync(h, c->st, header_bytes(), cudaMemcpyDeviceToHost, s));
   if (check_c) CK(cudaMemcpyAsync(c->hflag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(x_out, c->x, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   const int hcap = std::min(history_cap, HIST_CAP);
   if (history && hcap > 0) CK(cudaMemcpyAsync(c->hhist, c->hist, sizeof(double) * hcap, cudaMemcpyDeviceToHost, s));
+  if (timing) cudaEventRecord(tev[3], s);
   CK(cudaStreamSynchronize(s));
+  if (timing) {
+    float a = 0.f, b2 = 0.f, d = 0.f;
+    cudaEventElapsedTime(&a, tev[0], tev[1]);
+    cudaEventElapsedTime(&b2, tev[1], tev[2]);
+    cudaEventElapsedTime(&d, tev[2], tev[3]);
+    fprintf(stderr, "rg_solve device us: setup (C = A W, QR, copies) %.1f, solve %.1f, copy-out %.1f\n", a * 1e3,
+            b2 * 1e3, d * 1e3);
+  }
   if (check_c) bad = c->hflag[0];
   if (done_persist && getenv("RG_SKEW")) {  // experiment: per-CTA step start / dots done / reduction done / SM
     std::vector<unsigned> ts((size_t)NSM * 8);
@@ -1092,7 +1130,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
                                        "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
-                                       "ssor_sweep_kernels", "p_spmv"};
+                                       "ssor_sweep_kernels", "p_spmv", "cbuild"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));

@@ -236,9 +236,9 @@ def rg_export(ctx, which, out):
 
 
 def rg_kernel_stats(ctx):
-    buf = (rg_kstat * 32)()
+    buf = (rg_kstat * 64)()
     cnt = ctypes.c_int32(0)
-    _check(_lib.rg_kernel_stats(ctx, buf, 32, ctypes.byref(cnt)))
+    _check(_lib.rg_kernel_stats(ctx, buf, 64, ctypes.byref(cnt)))
     return {buf[i].name.decode(): dict(launches=buf[i].launches, noop=buf[i].noop_launches,
                                        ms=buf[i].total_ms, tail_ms=buf[i].tail_ms, bytes=buf[i].bytes)
             for i in range(cnt.value)}
