@@ -203,12 +203,13 @@ class ClockSampler:
 class GpuRun:
     """One replica: the library context plus the device-side sequence generator."""
 
-    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None):
+    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None, sync_build=False):
         import torch
 
         import synth
         from paper_1807_09467_b200 import Context, rg
         self.torch, self.cfg, self.variant, self.k = torch, cfg, variant, k
+        self.sync_build = sync_build   # True: rg_build_recycle returns k_eff, sigma (host sync)
         self.dev = device
         self.stream = stream
         self.gen = synth.DeviceSequence(cfg, device)
@@ -239,7 +240,10 @@ class GpuRun:
             self.gen.fill(self.t, self.x, val_ptr=self.vals_ptr)   # the solver's value buffer (a1)
             self.ctx.update_values_inplace(self.nnz)
         if self.variant != "plain" and self.nsnap > 0:
-            self.k_eff, self.sigma = self.ctx.build_recycle(self.k)   # a3 (a4 happens inside the solve)
+            if self.sync_build:
+                self.k_eff, self.sigma = self.ctx.build_recycle(self.k)
+            else:                                      # a3, asynchronous (a4 happens inside the solve)
+                self.ctx.build_recycle(self.k, deferred=True)
         rep = self.ctx.solve(self.gen.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol)
         if not rep["converged"]:
             raise RuntimeError(f"system {self.t} did not converge: {rep}")
@@ -292,7 +296,7 @@ class HostE2ERun:
         cfg = self.cfg
         self.ctx.update_matrix(self.val)
         if self.variant != "plain" and self.nsnap > 0:
-            self.ctx.build_recycle(self.k)
+            self.ctx.build_recycle(self.k, deferred=True)
         rep = self.ctx.solve(self.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol)
         self.ctx.push_snapshot(self.x)
         self.nsnap += 1

@@ -158,7 +158,11 @@ RG_API rg_status rg_clear_snapshots(rg_ctx* ctx);
  *   k       requested dimension, 1..max_k
  *   k_eff   (out, nullable) dimension kept
  *   sigma   (out, nullable, host) the #snapshots singular values, non-increasing
- * RG_E_STATE if the window is empty. */
+ * RG_E_STATE if the window is empty.
+ * With k_eff == NULL and sigma == NULL the call is ASYNCHRONOUS: it enqueues the SVD on the stream
+ * and returns without waiting; the next call that needs W (rg_solve, rg_export, a further build)
+ * waits for the singular values, fixes k_eff and forms W.  The window may be pushed to meanwhile
+ * (the build reads it in stream order).  Errors of the deferred part are reported by that call. */
 RG_API rg_status rg_build_recycle(rg_ctx* ctx, int32_t k, int32_t* k_eff, double* sigma);
 
 /* As rg_build_recycle, choosing which singular modes span W (PAPER.md:673-676 compares both):

@@ -43,9 +43,9 @@ class Context:
     def clear_snapshots(self):
         rg.rg_clear_snapshots(self.ctx)
 
-    def build_recycle(self, k, modes="largest"):
+    def build_recycle(self, k, modes="largest", deferred=False):
         if modes == "largest":
-            return rg.rg_build_recycle(self.ctx, k, self.max_snapshots)
+            return rg.rg_build_recycle(self.ctx, k, self.max_snapshots, deferred)
         return rg.rg_build_recycle_modes(self.ctx, k, modes, self.max_snapshots)
 
     def solve(self, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=20000, history_cap=0):

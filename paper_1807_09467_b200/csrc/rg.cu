@@ -127,6 +127,11 @@ struct rg_ctx {
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // asynchronous recycle build (rg_build_recycle with k_eff = sigma = NULL): finished by the next
+  // call that needs W (finish_build)
+  cudaEvent_t ebuild = nullptr;
+  bool pend = false;
+  int pend_k = 0, pend_modes = 0, pend_s = 0;
 };
 
 namespace {
@@ -550,6 +555,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   if (c->hsig) cudaFreeHost(c->hsig);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
+  if (c->ebuild) cudaEventDestroy(c->ebuild);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -629,6 +635,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   ok(cudaMemcpyAsync(&c->st->sc[0], &c->hst->sc[0], sizeof(double) * MAXCOL, cudaMemcpyHostToDevice, c->stream));
   ok(cudaEventCreate(&c->e0));
   ok(cudaEventCreate(&c->e1));
+  ok(cudaEventCreateWithFlags(&c->ebuild, cudaEventDisableTiming));
   ok(cudaStreamSynchronize(c->stream));
   if (e != cudaSuccess) {
     rg_destroy(c);
@@ -691,6 +698,10 @@ RG_API rg_status rg_push_snapshot(rg_ctx* c, const double* x, rg_mem mem) {
 
 RG_API rg_status rg_clear_snapshots(rg_ctx* c) {
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  if (c->pend) {  // drop a pending asynchronous build
+    CK(cudaEventSynchronize(c->ebuild));
+    c->pend = false;
+  }
   c->s_count = c->s_head = 0;
   c->v1prev_s = 0;
   c->have_W = false;
@@ -699,47 +710,14 @@ RG_API rg_status rg_clear_snapshots(rg_ctx* c) {
   return RG_OK;
 }
 
-RG_API rg_status rg_build_recycle(rg_ctx* c, int32_t k, int32_t* k_eff, double* sigma) {
-  return rg_build_recycle_modes(c, k, RG_MODES_LARGEST, k_eff, sigma);
-}
-
-RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int32_t* k_eff, double* sigma) {
-  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
-  if (modes != RG_MODES_LARGEST && modes != RG_MODES_SMALLEST) return fail(RG_E_INVAL, "unknown modes");
-  if (k < 1 || k > c->max_k) return fail(RG_E_INVAL, "k must be in 1..max_k");
-  if (c->s_count == 0) return fail(RG_E_STATE, "no snapshots");
-  const int s = c->s_count;
+// Second half of a recycle build, once sigma is on the host: rank, k_eff, W = Y V2 Sigma^{-1}.
+rg_status finish_build(rg_ctx* c, int k, int modes, int s, int32_t* k_eff, double* sigma) {
   const int64_t ld = c->npad;
   cudaStream_t st = c->stream;
-  static const bool timing = getenv("RG_TIMING") != nullptr;
-  auto now = [] { return std::chrono::steady_clock::now(); };
-  const auto t0 = now();
-  double* G = c->small;
-  double* V1 = c->small + 1 * SMALL;
-  double* lam = c->small + 2 * SMALL;
   double* V2 = c->small + 3 * SMALL;
   double* sig = c->small + 4 * SMALL;
   double* inv = c->small + 5 * SMALL;
-  // pass 1: G = X^T X, Jacobi -> V1 (warm-started from the previous build's V1) ; Y = X V1
-  double* V1prev = c->small + 8 * SMALL;
-  CK(launch_gram(c->X, ld, c->n, s, G, c->partial, c->counter, c->st, st));
-  CK(launch_jacobi(G, s, lam, V1, nullptr, c->st, st, V1prev, c->v1prev_s <= s ? c->v1prev_s : 0));
-  CK(cudaMemcpyAsync(V1prev, V1, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
-  c->v1prev_s = s;
-  CK(launch_xm(c->X, ld, c->n, s, V1, s, s, nullptr, c->Y, ld, c->st, st));
-  // pass 2: Y^T Y (nearly diagonal, column-scaled) -> V2, sigma
-  CK(launch_gram(c->Y, ld, c->n, s, G, c->partial, c->counter, c->st, st));
-  CK(launch_jacobi(G, s, lam, V2, sig, c->st, st));
-  const auto t1 = now();
-  double* hs = c->hsig;  // pinned
-  CK(cudaMemcpyAsync(hs, sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  const auto t2 = now();
-  if (getenv("RG_DEBUG")) {
-    double sw[2] = {0.0, 0.0};
-    cudaMemcpy(sw, lam + s, 2 * sizeof(double), cudaMemcpyDeviceToHost);
-    fprintf(stderr, "rg_build_recycle: s=%d, Jacobi sweeps %.0f (pass 1) %.0f (pass 2)\n", s, sw[0], sw[1]);
-  }
+  double* hs = c->hsig;
   int rank = 0;
   for (int i = 0; i < s; ++i)
     if (hs[0] > 0.0 && hs[i] > 1e-12 * hs[0]) ++rank;
@@ -756,12 +734,76 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
     CK(launch_xm(c->Y, ld, c->n, s, V2 + (int64_t)off * s, s, ke, inv, c->Z, ld, c->st, st));
     CK(cudaGetLastError());  // stream-ordered: the solve (or rg_export) consumes W on the same stream
   }
+  return RG_OK;
+}
+
+// Complete a pending asynchronous build (no-op otherwise).
+rg_status resolve_build(rg_ctx* c) {
+  if (!c->pend) return RG_OK;
+  c->pend = false;
+  CK(cudaEventSynchronize(c->ebuild));
+  return finish_build(c, c->pend_k, c->pend_modes, c->pend_s, nullptr, nullptr);
+}
+
+RG_API rg_status rg_build_recycle(rg_ctx* c, int32_t k, int32_t* k_eff, double* sigma) {
+  return rg_build_recycle_modes(c, k, RG_MODES_LARGEST, k_eff, sigma);
+}
+
+RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int32_t* k_eff, double* sigma) {
+  if (!c) return fail(RG_E_INVAL, "ctx is NULL");
+  if (modes != RG_MODES_LARGEST && modes != RG_MODES_SMALLEST) return fail(RG_E_INVAL, "unknown modes");
+  if (k < 1 || k > c->max_k) return fail(RG_E_INVAL, "k must be in 1..max_k");
+  if (c->s_count == 0) return fail(RG_E_STATE, "no snapshots");
+  if (rg_status r0 = resolve_build(c)) return r0;  // a previous asynchronous build completes first
+  const int s = c->s_count;
+  const int64_t ld = c->npad;
+  cudaStream_t st = c->stream;
+  static const bool timing = getenv("RG_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  const auto t0 = now();
+  double* G = c->small;
+  double* V1 = c->small + 1 * SMALL;
+  double* lam = c->small + 2 * SMALL;
+  double* V2 = c->small + 3 * SMALL;
+  double* sig = c->small + 4 * SMALL;
+  // pass 1: G = X^T X, Jacobi -> V1 (warm-started from the previous build's V1) ; Y = X V1
+  double* V1prev = c->small + 8 * SMALL;
+  CK(launch_gram(c->X, ld, c->n, s, G, c->partial, c->counter, c->st, st));
+  CK(launch_jacobi(G, s, lam, V1, nullptr, c->st, st, V1prev, c->v1prev_s <= s ? c->v1prev_s : 0));
+  CK(cudaMemcpyAsync(V1prev, V1, sizeof(double) * s * s, cudaMemcpyDeviceToDevice, st));
+  c->v1prev_s = s;
+  CK(launch_xm(c->X, ld, c->n, s, V1, s, s, nullptr, c->Y, ld, c->st, st));
+  // pass 2: Y^T Y (nearly diagonal, column-scaled) -> V2, sigma
+  CK(launch_gram(c->Y, ld, c->n, s, G, c->partial, c->counter, c->st, st));
+  CK(launch_jacobi(G, s, lam, V2, sig, c->st, st));
+  const auto t1 = now();
+  double* hs = c->hsig;  // pinned
+  CK(cudaMemcpyAsync(hs, sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
+  if (!k_eff && !sigma && !getenv("RG_SYNC_BUILD")) {
+    // asynchronous: nothing to return now; the next call that needs W waits for sigma (finish_build)
+    CK(cudaEventRecord(c->ebuild, st));
+    c->pend = true;
+    c->pend_k = k;
+    c->pend_modes = modes;
+    c->pend_s = s;
+    c->have_W = false;
+    c->c_valid = false;
+    return RG_OK;
+  }
+  CK(cudaStreamSynchronize(st));
+  const auto t2 = now();
+  if (getenv("RG_DEBUG")) {
+    double sw[2] = {0.0, 0.0};
+    cudaMemcpy(sw, lam + s, 2 * sizeof(double), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "rg_build_recycle: s=%d, Jacobi sweeps %.0f (pass 1) %.0f (pass 2)\n", s, sw[0], sw[1]);
+  }
+  const rg_status rs = finish_build(c, k, modes, s, k_eff, sigma);
   if (timing) {
     const auto t3 = now();
-    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    auto us = [](auto a2, auto b2) { return std::chrono::duration<double, std::micro>(b2 - a2).count(); };
     fprintf(stderr, "rg_build_recycle host us: launch %.1f, wait %.1f, tail %.1f\n", us(t0, t1), us(t1, t2), us(t2, t3));
   }
-  return RG_OK;
+  return rs;
 }
 
 RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t m, rg_variant v, double tol,
@@ -778,6 +820,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (history_cap < 0) return fail(RG_E_INVAL, "history_cap < 0");
   cudaStream_t s = c->stream;
   rg_status rs;
+  if ((rs = resolve_build(c)) != RG_OK) return rs;
   const int eff = (v != RG_PLAIN && c->have_W && c->k_eff > 0) ? (int)v : (int)RG_PLAIN;
   const int k = eff == RG_PLAIN ? 0 : c->k_eff;
   int c_spmv = 0;
@@ -1104,6 +1147,7 @@ RG_API rg_status rg_apply_preconditioner(rg_ctx* c, const double* x, double* y, 
 RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, int32_t* k_eff) {
   if (!c || !out) return fail(RG_E_INVAL, "NULL argument");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  if (rg_status r0 = resolve_build(c)) return r0;
   const int k = c->have_W ? c->k_eff : 0;
   if (k_eff) *k_eff = k;
   if (k == 0) return fail(RG_E_STATE, "no recycle space");

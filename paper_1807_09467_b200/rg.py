@@ -179,7 +179,11 @@ def rg_clear_snapshots(ctx):
     _check(_lib.rg_clear_snapshots(ctx))
 
 
-def rg_build_recycle(ctx, k, n_snapshots=64):
+def rg_build_recycle(ctx, k, n_snapshots=64, deferred=False):
+    """deferred=True: asynchronous build (k_eff, sigma NULL), returns (None, None)."""
+    if deferred:
+        _check(_lib.rg_build_recycle(ctx, int(k), None, None))
+        return None, None
     ke = ctypes.c_int32(0)
     sig = np.zeros(n_snapshots)
     _check(_lib.rg_build_recycle(ctx, int(k), ctypes.byref(ke), sig.ctypes.data))

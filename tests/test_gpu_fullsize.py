@@ -25,7 +25,9 @@ def test_full_size_sequence_properties(name, systems):
     st = torch.cuda.Stream(dev)
     seq = synth.HostSequence(cfg)
     with torch.cuda.stream(st):
-        run = bench.GpuRun(cfg, "deflate", cfg.k, dev, st, profile=False, sell=cfg.fmt == "sell")
+        # sync_build: the recycle build returns sigma (the bench's asynchronous build runs the same
+        # kernels; test_gpu_parity.py::test_deferred_build_matches_synchronous pins the two bitwise)
+        run = bench.GpuRun(cfg, "deflate", cfg.k, dev, st, profile=False, sell=cfg.fmt == "sell", sync_build=True)
         X = []
         for t in range(1, systems + 1):
             x_prev = run.x.cpu().numpy().copy()

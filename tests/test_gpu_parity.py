@@ -445,3 +445,42 @@ def test_persistent_multi_cta_wide_pattern(variant, rng):
     for rep, xg in outs:
         assert rep["converged"] and abs(rep["iterations"] - ref["iterations"]) <= 2
         assert np.linalg.norm(xg - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+
+
+# ------------------------------------------------------------------------- asynchronous recycle build
+@pytest.mark.parametrize("variant", ["deflate", "augment"])
+def test_deferred_build_matches_synchronous(variant, rng):
+    """rg_build_recycle with k_eff = sigma = NULL (asynchronous, finished inside the next rg_solve)
+    gives bit-identical solves to the synchronous call, also when a snapshot is pushed between the
+    build and its solve (the build reads the window in stream order)."""
+    cfg = synth.CONFIGS["C1"]
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    A1 = seq.matrix(1, u)
+    ctxs = [make_ctx(A1, max_m=cfg.m, s=cfg.s, k=cfg.k) for _ in range(2)]
+    xs = [torch.zeros(cfg.n, dtype=torch.float64, device=DEV) for _ in range(2)]
+    extra = t(rng.standard_normal(cfg.n))
+    for step in range(1, 6):
+        A = seq.matrix(step, u)
+        b = t(seq.rhs(step, u))
+        reps = []
+        for i, (ctx, x) in enumerate(zip(ctxs, xs)):
+            ctx.update_matrix(t(A.val))
+            if step > 1:
+                if i == 0:
+                    ke, _ = ctx.build_recycle(cfg.k)
+                    assert ke >= 1
+                else:
+                    assert ctx.build_recycle(cfg.k, deferred=True) == (None, None)
+                if step == 3:
+                    ctx.push_snapshot(extra)
+            x.zero_()
+            reps.append(ctx.solve(b, x, m=cfg.m, variant=variant, tol=cfg.tol))
+        assert reps[0]["iterations"] == reps[1]["iterations"], reps
+        assert reps[0]["converged"] and reps[1]["converged"]
+        assert torch.equal(xs[0], xs[1])
+        u = xs[0].cpu().numpy()
+        for ctx in ctxs:
+            ctx.push_snapshot(t(u))
+    for ctx in ctxs:
+        ctx.close()
