@@ -18,6 +18,10 @@ constexpr int MAXCOL = 2 * MAXK + MAXM + 2;// columns of the basis buffer Z = [W
 constexpr int MAXRED = MAXCOL + 2;         // values one grid reduction can return
 
 // ---------------------------------------------------------------- launch geometry
+#ifndef SELL_CH
+#define SELL_CH 12  // SELL-32 entries of a row loaded together (one round for the 9-point rows of C3;
+                    // measured 8 -> 12: standalone SELL SpMV 4.28 -> 5.24 TB/s, C3 persistent -1.9 %)
+#endif
 constexpr int OT = 512;                    // threads per CTA of the vector kernels
 constexpr int NWARP = OT / 32;
 constexpr int NSM = 148;                   // B200 SMs

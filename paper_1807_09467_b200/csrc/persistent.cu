@@ -253,18 +253,18 @@ __device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const do
     const int64_t sl = row >> 5;
     const int w = __ldg(A.sw + sl);
     const int64_t base = __ldg(A.sp + sl) + (row & 31);
-    for (int c = 0; c < w; c += 8) {
-      int32_t cc[8];
-      double vv[8];
+    for (int c = 0; c < w; c += SELL_CH) {
+      int32_t cc[SELL_CH];
+      double vv[SELL_CH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < SELL_CH; ++u) {
         const bool ok = c + u < w;
         const int64_t e = base + (int64_t)(c + u) * 32;
         cc[u] = ok ? __ldcs(A.sci + e) : 0;
         vv[u] = ok ? __ldcs(A.sv + e) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < SELL_CH; ++u)
         if (c + u < w) s += vv[u] * x[cc[u]];
     }
   } else {

@@ -9,6 +9,11 @@
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
+#ifndef RG_SPMV_CAP
+#define RG_SPMV_CAP 2  // CTAs per SM of the grid-stride SpMV launches (STEP / PLAIN modes): one wave
+                       // (measured: 4 -> 2 per SM: SELL C3 4.03 -> 4.28 TB/s, CSR C4 5.40 -> 5.67)
+#endif
+
 namespace rg {
 namespace {
 
@@ -154,18 +159,18 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
     const int w = __ldg(A.sw + sl);
     const int64_t base = __ldg(A.sp + sl) + (row & 31);
     double s = 0.0;
-    for (int c = 0; c < w; c += 8) {  // 8 coalesced (column, value) pairs in flight, then gathers
-      int32_t cc[8];
-      double vv[8];
+    for (int c = 0; c < w; c += SELL_CH) {  // SELL_CH coalesced (column, value) pairs in flight, then gathers
+      int32_t cc[SELL_CH];
+      double vv[SELL_CH];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < SELL_CH; ++u) {
         const bool ok = c + u < w;
         const int64_t e = base + (int64_t)(c + u) * 32;
         cc[u] = ok ? __ldcs(A.sci + e) : 0;
         vv[u] = ok ? __ldcs(A.sv + e) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < SELL_CH; ++u)
         if (c + u < w) s += vv[u] * __ldg(x + cc[u]);
     }
     if (row < A.n) nrm += emit(io, row, s);
@@ -518,12 +523,12 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
     k_spmv_bsr<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(a);
   } else if (A.fmt == 1) {
     int64_t g = (A.nslices * 32 + OT - 1) / OT;
-    const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * 4;
+    const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * RG_SPMV_CAP;
     if (g > cap) g = cap;
     k_spmv_sell<<<(int)(g < 1 ? 1 : g), OT, 0, s>>>(a);
   } else {
     int64_t g = (A.n * A.lpr + OT - 1) / OT;
-    const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * 4;
+    const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * RG_SPMV_CAP;
     if (g > cap) g = cap;
     const int gi = (int)(g < 1 ? 1 : g);
     switch (A.lpr) {
