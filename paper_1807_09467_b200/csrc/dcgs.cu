@@ -269,11 +269,13 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
 // registers over all of the CTA's rows and the chunk ends with ONE block reduction; u and y are
 // re-read per chunk (L2 hits).  No per-sub-tile barrier and no shared-memory staging.
 template <int SCH, int RU>  // SCH columns per chunk, RU rows per thread per iteration (loads in flight)
-__global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, unsigned long long cond) {
+__global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, unsigned long long cond, int nvw) {
+  // per-warp partials in the layout of dpart: a chunk ends with warp shuffles only (no barrier), so
+  // warps drift freely from chunk to chunk; ONE cross-warp sum at the end (fixed warp order).
+  // (First version: a block reduction with two barriers per chunk.)
+  extern __shared__ double wsm[];  // [DT / 32][nvw]
   __shared__ double dpart[DK1RED];
   __shared__ double tot[DK1RED];
-  __shared__ double wred[DT / 32][2 * SCH];
-  __shared__ double bsh[33];
   if (!st->active) { prof_noop(st, K_DK1); return; }
   prof_begin(st, K_DK1);
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
@@ -288,6 +290,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, un
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nv = 2 * p + 2 + nqd, ncols = p + nqd;
   const bool obl = galerkin_variant(var);
+  double* wp = wsm + (size_t)wid * nvw;
   const int64_t ng = ld >> 5;
   const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
   const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
@@ -331,35 +334,31 @@ __global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, un
 #pragma unroll
     for (int kk = 0; kk < SCH; ++kk) {
       const double a = warp_sum(su[kk]), b = warp_sum(sy[kk]);
-      if (lane == 0) {
-        wred[wid][kk] = a;
-        wred[wid][SCH + kk] = b;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < 2 * SCH) {
-      const int kk = threadIdx.x % SCH;
-      const bool isy = threadIdx.x >= SCH;
-      double sacc = 0.0;
-      for (int w = 0; w < DT / 32; ++w) sacc += wred[w][threadIdx.x];
       const int c = c0 + kk;
-      if (kk < nc) {
+      if (lane == 0 && kk < nc) {
         if (c < p) {
-          dpart[isy ? p + c : c] = sacc;
+          wp[c] = a;
+          wp[p + c] = b;
         } else {
           const bool wy = obl && (c - p) < k;  // extras: W^T y, P^T u (galerkin) / Q^T u (augment)
-          if (isy == wy) dpart[2 * p + 2 + (c - p)] = sacc;
+          wp[2 * p + 2 + (c - p)] = wy ? b : a;
         }
       }
     }
-    __syncthreads();
     if (ncols == 0) break;
   }
-  const double t1 = block_sum(s_uu, bsh);
-  const double t2 = block_sum(s_uy, bsh);
-  if (threadIdx.x == 0) {
-    dpart[2 * p] = t1;
-    dpart[2 * p + 1] = t2;
+  {
+    const double t1 = warp_sum(s_uu), t2 = warp_sum(s_uy);
+    if (lane == 0) {
+      wp[2 * p] = t1;
+      wp[2 * p + 1] = t2;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nv; i += DT) {
+    double sacc = 0.0;
+    for (int w = 0; w < DT / 32; ++w) sacc += wsm[(size_t)w * nvw + i];
+    dpart[i] = sacc;
   }
   __syncthreads();
   dk1_finish(L, st, dpart, tot, nv, p, nqd, j, have_y, cond);
@@ -428,9 +427,17 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
     // streaming variant by default (C4: 3.90 -> 4.54 TB/s; (SCH, RU) = (4, 2) and (6, 2) measured
     // equal, (4, 4) spills); RG_DK1_TILES=1 selects the shared-memory sub-tile kernel
     static const int tiles = getenv("RG_DK1_TILES") ? 1 : 0;
-    if (!tiles)
-      k_dk1_stream<8, 1><<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
-    else
+    if (!tiles) {
+      const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
+      const size_t smem = sizeof(double) * (DT / 32) * (size_t)nvw;
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_dk1_stream<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * (DT / 32) * (size_t)DK1RED));
+        attr = true;
+      }
+      k_dk1_stream<8, 1><<<vec_grid(L.ld), DT, smem, s>>>(L, st, cond, nvw);
+    } else
       k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
     return cudaGetLastError();
   }
