@@ -414,7 +414,260 @@ __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
   if (st->profile && grid_last(L.counter) && threadIdx.x == 0) prof_end(st, K_DK2, 8.0 * (double)L.n * (p + k2 + 4));
 }
 
+// ---------------------------------------------------------------- TMA-streamed DK1 / DK2
+// The register-limited kernels above keep ~10 loads of 8 B in flight per thread (64 registers at
+// 2 CTAs/SM): ncu shows them long-scoreboard bound at 3.8 (DK1) / 4.6 (DK2) TB/s cold at C4.  Here a
+// producer warp streams the CTA's rows of the basis columns with cp.async.bulk (TMA, 1-D) into a
+// TS_STG-stage shared-memory ring (TS_CH columns x TS_R rows per stage, 32 KB), completing on
+// mbarriers, so ~128 KB per SM are in flight independently of registers; TS_R consumer threads own
+// one row each of the current row tile.  Same loop order and accumulation order as the streaming
+// kernels (DK1: column chunk outer, row tile inner; DK2: row tile outer, columns ascending).
+constexpr int TS_R = 512;              // consumer threads = rows per tile
+constexpr int TS_T = TS_R + 32;        // + producer warp
+constexpr int TS_CH = 8;               // columns per stage
+constexpr int TS_STG = 4;              // stages
+constexpr int TS_STAGE = TS_CH * TS_R; // doubles per stage
+
+__device__ __forceinline__ uint32_t ts_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ts_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(ts_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void ts_init(uint64_t* full, uint64_t* empty) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TS_STG; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ts_u32(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(ts_u32(&empty[i])), "r"(TS_R / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+// L2 policy of the streamed basis: evict-first when the basis does not fit L2 (as the __ldcs loads
+// of the register kernels: the SpMV's A / x and DK1's u, y re-reads keep their L2 lines), evict-
+// normal when it does (keep_l2: the next pass re-hits it)
+__device__ __forceinline__ uint64_t ts_policy(bool keep) {
+  uint64_t pol;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// producer: stage number t (global sequence) of `nc` column segments [col_c + base, +cnt rows)
+__device__ __forceinline__ void ts_issue(double* ring, uint64_t* full, uint64_t* empty, int t, const double* Z,
+                                         int64_t ld, const int* cols, int nc, int64_t base, int cnt, uint64_t pol) {
+  const int s = t % TS_STG;
+  if (t >= TS_STG) ts_wait(&empty[s], (uint32_t)((t / TS_STG - 1) & 1));
+  const uint32_t bytes = (uint32_t)(nc * cnt * 8);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ts_u32(&full[s])), "r"(bytes) : "memory");
+  for (int c = 0; c < nc; ++c)
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                 ::"r"(ts_u32(ring + (size_t)s * TS_STAGE + c * TS_R)), "l"(Z + (int64_t)cols[c] * ld + base),
+                 "r"((uint32_t)(cnt * 8)), "r"(ts_u32(&full[s])), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void ts_release(uint64_t* empty, int s) {
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ts_u32(&empty[s])) : "memory");
+}
+
+__global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, unsigned long long cond, int nvw) {
+  extern __shared__ __align__(128) double ring[];   // [TS_STG][TS_STAGE], then per-warp partials [TS_R / 32][nvw]
+  __shared__ __align__(8) uint64_t full[TS_STG], empty[TS_STG];
+  double* wsm = ring + (size_t)TS_STG * TS_STAGE;
+  __shared__ double dpart[DK1RED];
+  __shared__ double tot[DK1RED];
+  __shared__ int colidx[DK1RED];
+  if (!st->active) { prof_noop(st, K_DK1); return; }
+  prof_begin(st, K_DK1);
+  const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
+  const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
+  const int nqd = (var == RG_AUGMENT) ? k : (galerkin_variant(var) ? 2 * k : 0);
+  const bool have_y = j < st->m;
+  const int64_t ld = L.ld;
+  const double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;
+  const double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nv = 2 * p + 2 + nqd, ncols = p + nqd;
+  const bool obl = galerkin_variant(var);
+  for (int c = tid; c < ncols; c += TS_T)
+    colidx[c] = c < p ? lo + c : (obl ? ((c - p) < k ? c - p : proj_base(var, k) + (c - p - k)) : QB + (c - p));
+  ts_init(full, empty);
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  const int nchunk = (ncols + TS_CH - 1) / TS_CH;
+  if (wid == TS_R / 32) {  // ---- producer (lane 0): chunk outer, row tile inner
+    if (lane == 0) {
+      const uint64_t pol = ts_policy(L.keep_l2 != 0);
+      int t = 0;
+      for (int q = 0; q < nchunk; ++q)
+        for (int64_t base = r0; base < r1; base += TS_R, ++t)
+          ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
+                   (int)min((int64_t)TS_R, r1 - base), pol);
+    }
+  } else {  // ---- consumers: thread = row of the tile
+    double s_uu = 0.0, s_uy = 0.0;
+    int t = 0;
+    // u, y of the tile TS_PF tiles ahead are loaded now (L2 hits, off the per-tile critical path);
+    // the tile sequence repeats per chunk, so "ahead" wraps to the start of the CTA's rows
+    constexpr int TS_PF = 3;
+    double upf[TS_PF], ypf[TS_PF];
+    int64_t bnext = r0;  // base of the next tile to prefetch
+#pragma unroll
+    for (int i = 0; i < TS_PF; ++i) {
+      const int64_t rn = bnext + tid;
+      upf[i] = rn < r1 ? u[rn] : 0.0;
+      ypf[i] = (rn < r1 && have_y) ? y[rn] : 0.0;
+      bnext = bnext + TS_R < r1 ? bnext + TS_R : r0;
+    }
+    for (int q = 0; q < nchunk || q == 0; ++q) {
+      const int nc = min(TS_CH, ncols - q * TS_CH);
+      double su[TS_CH], sy[TS_CH];
+#pragma unroll
+      for (int c = 0; c < TS_CH; ++c) su[c] = sy[c] = 0.0;
+      for (int64_t base = r0; base < r1; base += TS_R) {
+        const int64_t r = base + tid;
+        const bool ok = r < r1;
+        const double ur = upf[0], yr = ypf[0];
+        {
+#pragma unroll
+          for (int i = 0; i + 1 < TS_PF; ++i) {
+            upf[i] = upf[i + 1];
+            ypf[i] = ypf[i + 1];
+          }
+          const int64_t rn = bnext + tid;
+          upf[TS_PF - 1] = rn < r1 ? u[rn] : 0.0;
+          ypf[TS_PF - 1] = (rn < r1 && have_y) ? y[rn] : 0.0;
+          bnext = bnext + TS_R < r1 ? bnext + TS_R : r0;
+        }
+        if (q == 0) {
+          s_uu += ur * ur;
+          s_uy += ur * yr;
+        }
+        if (nc <= 0) continue;
+        const int stg = t % TS_STG;
+        ts_wait(&full[stg], (uint32_t)((t / TS_STG) & 1));
+        const double* zs = ring + (size_t)stg * TS_STAGE + tid;
+#pragma unroll
+        for (int c = 0; c < TS_CH; ++c) {
+          const double z = (ok && c < nc) ? zs[c * TS_R] : 0.0;
+          su[c] += z * ur;
+          sy[c] += z * yr;
+        }
+        ts_release(empty, stg);
+        ++t;
+      }
+#pragma unroll
+      for (int c = 0; c < TS_CH; ++c) {
+        const double a = warp_sum(su[c]), b = warp_sum(sy[c]);
+        const int cc = q * TS_CH + c;
+        if (lane == 0 && c < nc) {
+          if (cc < p) {
+            wsm[wid * nvw + cc] = a;
+            wsm[wid * nvw + p + cc] = b;
+          } else {
+            const bool wy = obl && (cc - p) < k;  // extras: W^T y, P^T u (galerkin) / Q^T u (augment)
+            wsm[wid * nvw + 2 * p + 2 + (cc - p)] = wy ? b : a;
+          }
+        }
+      }
+    }
+    const double t1 = warp_sum(s_uu), t2 = warp_sum(s_uy);
+    if (lane == 0) {
+      wsm[wid * nvw + 2 * p] = t1;
+      wsm[wid * nvw + 2 * p + 1] = t2;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < nv; i += TS_T) {
+    double sacc = 0.0;
+    for (int w = 0; w < TS_R / 32; ++w) sacc += wsm[w * nvw + i];
+    dpart[i] = sacc;
+  }
+  __syncthreads();
+  dk1_finish(L, st, dpart, tot, nv, p, nqd, j, have_y, cond);
+}
+
+__global__ void __launch_bounds__(TS_T, 1) k_dk2_tma(Layout L, DevState* st) {
+  extern __shared__ __align__(128) double ring[];
+  __shared__ __align__(8) uint64_t full[TS_STG], empty[TS_STG];
+  __shared__ double cv[MAXCOL + MAXK], cn[MAXCOL + MAXK];
+  __shared__ int colidx[MAXCOL + MAXK];
+  if (!st->active) { prof_noop(st, K_DK2); return; }
+  prof_begin(st, K_DK2);
+  const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
+  const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
+  const int64_t ld = L.ld;
+  double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;      // in: u, out: v_j
+  double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;  // in: y, out: next u
+  const int tid = threadIdx.x, wid = tid >> 5;
+  const int k2 = galerkin_variant(var) ? k : 0;  // next u also gets -P t / nu (P = C or W)
+  const int pb2 = proj_base(var, k), ncols = p + k2;
+  for (int c = tid; c < ncols; c += TS_T) {
+    if (c < p) {
+      cv[c] = st->coefv[lo + c];
+      cn[c] = st->coef[lo + c];
+      colidx[c] = lo + c;
+    } else {
+      cv[c] = 0.0;
+      cn[c] = st->coef[pb2 + (c - p)];
+      colidx[c] = pb2 + (c - p);
+    }
+  }
+  const double inv = st->k2_inv_nu, fy = st->k2_y, fu = st->k2_u_next;
+  ts_init(full, empty);
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  const int nchunk = (ncols + TS_CH - 1) / TS_CH;
+  if (wid == TS_R / 32) {  // ---- producer: row tile outer, column chunk inner
+    if ((tid & 31) == 0) {
+      const uint64_t pol = ts_policy(L.keep_l2 != 0);
+      int t = 0;
+      for (int64_t base = r0; base < r1; base += TS_R)
+        for (int q = 0; q < nchunk; ++q, ++t)
+          ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
+                   (int)min((int64_t)TS_R, r1 - base), pol);
+    }
+  } else {
+    int t = 0;
+    for (int64_t base = r0; base < r1; base += TS_R) {
+      const int64_t r = base + tid;
+      const bool ok = r < r1;
+      const double ur = ok ? u[r] : 0.0, yr = ok ? y[r] : 0.0;
+      double sv = 0.0, sn = 0.0;
+      for (int q = 0; q < nchunk; ++q, ++t) {
+        const int stg = t % TS_STG, c0 = q * TS_CH, nc = min(TS_CH, ncols - c0);
+        ts_wait(&full[stg], (uint32_t)((t / TS_STG) & 1));
+        const double* zs = ring + (size_t)stg * TS_STAGE + tid;
+#pragma unroll
+        for (int c = 0; c < TS_CH; ++c) {
+          if (c < nc) {
+            const double z = ok ? zs[c * TS_R] : 0.0;
+            sv += cv[c0 + c] * z;
+            sn += cn[c0 + c] * z;
+          }
+        }
+        ts_release(empty, stg);
+      }
+      if (ok) {
+        u[r] = ur * inv + sv;
+        y[r] = yr * fy + ur * fu + sn;
+      }
+    }
+  }
+  if (st->profile && grid_last(L.counter) && threadIdx.x == 0) prof_end(st, K_DK2, 8.0 * (double)L.n * (p + k2 + 4));
+}
+
 }  // namespace
+
+// one CTA per SM (the TMA kernels), at most one per 512-row tile
+static int tma_grid(int64_t rows) {
+  int64_t g = (rows + TS_R - 1) / TS_R;
+  if (g > NSM) g = NSM;
+  return (int)(g < 1 ? 1 : g);
+}
 
 cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond) {
   static bool init = false;
@@ -427,6 +680,19 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
     // streaming variant by default (C4: 3.90 -> 4.54 TB/s; (SCH, RU) = (4, 2) and (6, 2) measured
     // equal, (4, 4) spills); RG_DK1_TILES=1 selects the shared-memory sub-tile kernel
     static const int tiles = getenv("RG_DK1_TILES") ? 1 : 0;
+    static const int tma = getenv("RG_NO_TMA_DCGS") || getenv("RG_NO_TMA_DK1") ? 0 : 1;
+    if (tma && !tiles) {
+      const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
+      const size_t smem = sizeof(double) * ((size_t)TS_STG * TS_STAGE + (size_t)(TS_R / 32) * nvw);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_dk1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(sizeof(double) * ((size_t)TS_STG * TS_STAGE + (size_t)(TS_R / 32) * DK1RED)));
+        attr = true;
+      }
+      k_dk1_tma<<<tma_grid(L.ld), TS_T, smem, s>>>(L, st, cond, nvw);
+      return cudaGetLastError();
+    }
     if (!tiles) {
       const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
       const size_t smem = sizeof(double) * (DT / 32) * (size_t)nvw;
@@ -439,6 +705,16 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
       k_dk1_stream<8, 1><<<vec_grid(L.ld), DT, smem, s>>>(L, st, cond, nvw);
     } else
       k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
+    return cudaGetLastError();
+  }
+  static const int tma = getenv("RG_NO_TMA_DCGS") || getenv("RG_NO_TMA_DK2") ? 0 : 1;
+  if (tma) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_dk2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * TS_STG * TS_STAGE));
+      attr = true;
+    }
+    k_dk2_tma<<<tma_grid(L.ld), TS_T, sizeof(double) * TS_STG * TS_STAGE, s>>>(L, st);
     return cudaGetLastError();
   }
   k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
