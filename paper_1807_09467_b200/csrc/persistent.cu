@@ -137,19 +137,19 @@ __device__ __forceinline__ bool greduce(const double* vals, int nv, double* part
                                         unsigned* bar, int* s_fail, DevState* st = nullptr) {
   if (gridDim.x == 1) {  // single CTA: the CTA's values are the totals
     __syncthreads();
-    for (int i = threadIdx.x; i < nv; i += PT) tot[i] = vals[i];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) tot[i] = vals[i];
     __syncthreads();
     return true;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, G = gridDim.x;
-  for (int i = threadIdx.x; i < nv; i += PT) partial[(size_t)blockIdx.x * MAXRED + i] = vals[i];
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) partial[(size_t)blockIdx.x * MAXRED + i] = vals[i];
   const unsigned long long ta = (st && st->profile && blockIdx.x == 0 && threadIdx.x == 0) ? gtimer() : 0ull;
   if (!gbar(bar, s_fail)) return false;
   if (ta) {  // profiling: time CTA 0 waits in the first barrier (skew + arrival) -> p_reduce_arrive
     st->kstat[K_PB6].ns += gtimer() - ta;
     st->kstat[K_PB6].launches++;
   }
-  for (int col = blockIdx.x + G * wid; col < nv; col += G * (PT / 32)) {
+  for (int col = blockIdx.x + G * wid; col < nv; col += G * (int)(blockDim.x / 32)) {
     double a = 0.0;
     for (int b0 = lane; b0 < G; b0 += 32 * 8) {  // 8 independent L2 loads in flight per lane
       double v[8];
@@ -162,7 +162,7 @@ __device__ __forceinline__ bool greduce(const double* vals, int nv, double* part
     if (lane == 0) tot_g[col] = a;
   }
   if (!gbar(bar, s_fail)) return false;
-  for (int i = threadIdx.x; i < nv; i += PT) tot[i] = __ldcg(tot_g + i);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) tot[i] = __ldcg(tot_g + i);
   __syncthreads();
   return true;
 }
@@ -218,7 +218,7 @@ __device__ __forceinline__ bool greduce_ll(const double* vals, int nv, unsigned 
   unsigned long long* part = ll + (size_t)buf * LL_GMAX * MAXRED * 2;
   unsigned long long* totw = ll + (size_t)2 * LL_GMAX * MAXRED * 2 + (size_t)buf * LL_R * MAXRED * 2;
   __syncthreads();  // vals complete
-  for (int i = tid; i < nv; i += PT) ll_st(part + ((size_t)b * MAXRED + i) * 2, vals[i], ep);
+  for (int i = tid; i < nv; i += blockDim.x) ll_st(part + ((size_t)b * MAXRED + i) * 2, vals[i], ep);
   const unsigned long long ta = (st && st->profile && b == 0 && tid == 0) ? gtimer() : 0ull;
   bool ok = true;
   for (int col = b; col < nv; col += G) {
@@ -232,7 +232,7 @@ __device__ __forceinline__ bool greduce_ll(const double* vals, int nv, unsigned 
     if (tid < LL_R) ll_st(totw + ((size_t)tid * MAXRED + col) * 2, a, ep);
   }
   const unsigned long long* mine = totw + (size_t)(b % LL_R) * MAXRED * 2;
-  for (int i = tid; i < nv; i += PT) {
+  for (int i = tid; i < nv; i += blockDim.x) {
     double v = 0.0;
     if (!ll_ld(mine + (size_t)i * 2, ep, v)) ok = false;
     tot[i] = v;
@@ -322,8 +322,11 @@ __device__ __forceinline__ void ptick(DevState* st, int kid, unsigned long long&
 // VK selects the code the instantiation contains: 0 plain / deflate, 1 oblique / orthogonal, 2 augment
 // (one kernel with every variant's code carried more live registers and spilled in the hot loops:
 // C2 deflate +1.7 %).
-template <int VK>
-__global__ void __launch_bounds__(PT, PCTA) k_solve_persistent(PArgs pa) {
+// PTT: threads per CTA — RG_PT (512, 2 CTAs/SM) for multi-CTA solves, 1024 for single-CTA (tiny)
+// solves, where one CTA holds the whole problem (C1: 0.80 -> 0.74 ms/system measured)
+template <int VK, int PTT>
+__global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) {
+  constexpr int PT = PTT;  // shadows the namespace-scope default inside this kernel
   extern __shared__ double sm[];
   const Layout& L = pa.L;
   const MatDev& A = pa.A;
@@ -1257,9 +1260,9 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
 
 }  // namespace
 
-size_t persistent_smem(int m, int k, bool aug) {
+size_t persistent_smem(int m, int k, bool aug, int pt = PT) {
   return sizeof(double) * ((size_t)m * (m + 2) + (size_t)m * (m + 1) + (size_t)(m + 1) * (k > 0 ? k : 1) + 2 * PM +
-                           (PM + 2) + 3 * PCOL + 2 * PT + 2 * MAXRED + (PM + 2) + 2 * PK + PM + 2 +
+                           (PM + 2) + 3 * PCOL + 2 * (size_t)pt + 2 * MAXRED + (PM + 2) + 2 * PK + PM + 2 +
                            (aug ? 2 * (size_t)(m + 2) * (m + 2) : 0));
 }
 
@@ -1270,17 +1273,25 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   if (m > PM || k > PK || A.fmt == 2) return cudaErrorNotSupported;
   const bool aug = variant == RG_AUGMENT && k > 0;
   const int vk = aug ? 2 : ((galerkin_variant(variant) && k > 0) ? 1 : 0);
-  const void* fn = vk == 2 ? (const void*)k_solve_persistent<2>
-                           : (vk == 1 ? (const void*)k_solve_persistent<1> : (const void*)k_solve_persistent<0>);
-  const size_t smem0 = persistent_smem(m, k, aug);
-  // CSR pattern cache: what keeps PCTA CTAs per SM resident (228 KB per SM, 1 KB per CTA reserved,
+  // tiny systems (<= 8 rows per thread of one 512-thread CTA) run on ONE CTA: no grid barriers at
+  // all, and that CTA gets 1024 threads
+  static const bool no1024 = getenv("RG_NO_PT1024") != nullptr;
+  const bool single = L.ld <= 8 * PT;
+  const int pt = (single && !no1024) ? 1024 : PT, pcta = 1024 / pt;
+  const int vi = vk + (pt == 1024 ? 3 : 0);
+  static const void* fns[6] = {(const void*)k_solve_persistent<0, PT>, (const void*)k_solve_persistent<1, PT>,
+                               (const void*)k_solve_persistent<2, PT>, (const void*)k_solve_persistent<0, 1024>,
+                               (const void*)k_solve_persistent<1, 1024>, (const void*)k_solve_persistent<2, 1024>};
+  const void* fn = fns[vi];
+  const size_t smem0 = persistent_smem(m, k, aug, pt);
+  // CSR pattern cache: what keeps pcta CTAs per SM resident (228 KB per SM, 1 KB per CTA reserved,
   // ~1 KB static), sized for this CTA count's rows and ~1.5x its share of the entries
   int rcap = 0, ccap = 0;
   if (A.fmt == 0 && !getenv("RG_NO_SMEM_CSR")) {
-    const int64_t G0 = std::min<int64_t>((int64_t)NSM * PCTA, std::max<int64_t>(1, (L.ld + PT - 1) / PT));
+    const int64_t G0 = single ? 1 : std::min<int64_t>((int64_t)NSM * pcta, std::max<int64_t>(1, (L.ld + pt - 1) / pt));
     const int64_t rows = ((L.ld >> 5) / G0 + 2) * 32 + 1;
     const int64_t ents = A.nnz / G0 * 3 / 2 + 1024;
-    const int64_t budget = ((int64_t)228 * 1024 / PCTA - 2 * 1024 - (int64_t)smem0) / 4;
+    const int64_t budget = ((int64_t)228 * 1024 / pcta - 2 * 1024 - (int64_t)smem0) / 4;
     if (budget >= rows + ents) {
       rcap = (int)rows;
       ccap = (int)ents;
@@ -1289,28 +1300,26 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   const size_t smem = smem0 + sizeof(int32_t) * (size_t)(rcap + ccap);
   static int max_smem = -1;
   if (max_smem < 0) {
-    for (const void* f : {(const void*)k_solve_persistent<0>, (const void*)k_solve_persistent<1>,
-                          (const void*)k_solve_persistent<2>}) {
+    for (const void* f : fns) {
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     }
     max_smem = 200 * 1024;
   }
   if (smem > (size_t)max_smem) return cudaErrorNotSupported;
-  static size_t occ_smem[3] = {0, 0, 0};  // occupancy per instantiation and shared-memory size (queried once)
-  static int occ_last[3] = {0, 0, 0};
-  if (occ_smem[vk] != smem) {
-    occ_last[vk] = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last[vk], fn, PT, smem) != cudaSuccess) {
+  static size_t occ_smem[6] = {0, 0, 0, 0, 0, 0};  // occupancy per instantiation and shared-memory size
+  static int occ_last[6] = {0, 0, 0, 0, 0, 0};
+  if (occ_smem[vi] != smem) {
+    occ_last[vi] = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last[vi], fn, pt, smem) != cudaSuccess) {
       cudaGetLastError();
-      occ_last[vk] = 0;
+      occ_last[vi] = 0;
     }
-    occ_smem[vk] = smem;
+    occ_smem[vi] = smem;
   }
-  const int occ = occ_last[vk];
+  const int occ = occ_last[vi];
   if (occ < 1) return cudaErrorNotSupported;
-  // tiny systems (<= 8 rows per thread of one CTA) run on ONE CTA: no grid barriers at all
-  int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;
+  int64_t want = single ? 1 : (L.ld + pt - 1) / pt;
   static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : PCTA;
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
@@ -1326,7 +1335,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
     pa.pc_bytes = b2 + 8.0 * (double)L.n * 6.0;  // + perm, row pointers, 1/a_rr, in, out (fwd), out r/w (bwd)
   }
   void* args[] = {&pa};
-  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(PT), args, smem, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(pt), args, smem, s);
 }
 
 // One cooperative launch building C = A W, Q, R_C, R_C^{-1} (k_cbuild).  cudaErrorNotSupported when
