@@ -6,6 +6,7 @@
 // reading R-SVD), and W = Y V_2 Sigma^{-1}.  CholQR2 of C = A W uses the same Gram and X*M
 // kernels plus a one-CTA Cholesky.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -562,7 +563,8 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
     init = true;
   }
   const int half = (s + (s & 1)) / 2;  // one thread per 2x2 block of the rotation round (<= 1024)
-  const int nt = std::max(64, std::min(1024, (half * half + 31) / 32 * 32));
+  static const int nt_env = getenv("RG_JACOBI_NT") ? atoi(getenv("RG_JACOBI_NT")) : 0;
+  const int nt = nt_env > 0 ? nt_env : std::max(64, std::min(1024, (half * half + 31) / 32 * 32));
   k_jacobi<<<1, nt, smem, strm>>>(G, s, lam, V, sigma_out, st, s0 > 0 ? V0 : nullptr, s0);
   return cudaGetLastError();
 }
