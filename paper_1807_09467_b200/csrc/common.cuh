@@ -60,6 +60,7 @@ struct DevState {
   int spmv_count;
   int bzero;
   int dcgs;       // 1: delayed CGS2 (one reduction per Arnoldi step), 0: classical CGS2
+  int cfail;      // set by the C = A W build of this solve: singular CholQR2 factor / R_C / E
   double bnorm, beta, relres;
   double k2_inv_nu, k2_u_next, k2_y;  // DCGS2 update-pass scalars (v_j = u/nu + ..., u_next = ...)
   // least-squares state

@@ -327,14 +327,15 @@ rg_status build_c(rg_ctx* c, bool sync) {
   double* R2 = c->small + 3 * SMALL;
   double* R2i = c->small + 4 * SMALL;
   double* Q = c->Z + (int64_t)QB * ld;
-  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
+  int* flag = sync ? c->dflag : &c->st->cfail;  // solve: the header field (zeroed with the header)
+  if (sync) CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
   CK(launch_gram(Q, ld, c->n, k, G, c->partial, c->counter, c->st, s));
-  CK(launch_chol(G, k, R1, R1i, c->dflag, s));
+  CK(launch_chol(G, k, R1, R1i, flag, s));
   CK(launch_xm(Q, ld, c->n, k, R1i, k, k, nullptr, c->Y, ld, c->st, s));
   CK(launch_gram(c->Y, ld, c->n, k, G, c->partial, c->counter, c->st, s));
-  CK(launch_chol(G, k, R2, R2i, c->dflag, s));
+  CK(launch_chol(G, k, R2, R2i, flag, s));
   CK(launch_xm(c->Y, ld, c->n, k, R2i, k, k, nullptr, Q, ld, c->st, s));
-  CK(launch_rc_finish(R1, R1i, R2, R2i, k, c->st, c->dflag, s));
+  CK(launch_rc_finish(R1, R1i, R2, R2i, k, c->st, flag, s));
   if (!sync) {  // the caller reads dflag together with the solve header (one sync per solve)
     c->c_valid = true;
     return RG_OK;
@@ -379,9 +380,8 @@ rg_status build_c_oblique(rg_ctx* c) {
     CK(es);
   }
   double* G = c->small;
-  CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
   CK(launch_gram(c->Z, ld, c->n, 2 * k, G, c->partial, c->counter, c->st, s));
-  CK(launch_einv(G, k, c->st, c->dflag, s));
+  CK(launch_einv(G, k, c->st, &c->st->cfail, s));  // header field, zeroed with the solve's header
   c->c_valid = true;
   c->c_kind = 1;
   return RG_OK;
@@ -631,6 +631,10 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   ok(cudaMemsetAsync(c->counter, 0, sizeof(unsigned) * 4, c->stream));
   ok(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
   ok(cudaMemsetAsync(c->llw, 0, sizeof(unsigned long long) * ll_words(), c->stream));
+  // persistent-solve barrier words and neighbour epochs: zero at allocation and again right after
+  // every persistent solve (off the next solve's critical path)
+  ok(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, c->stream));
+  ok(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 16, c->stream));
   for (int i = 0; i < MAXCOL; ++i) c->hst->sc[i] = i < VB ? 1.0 : 0.0;
   ok(cudaMemcpyAsync(&c->st->sc[0], &c->hst->sc[0], sizeof(double) * MAXCOL, cudaMemcpyHostToDevice, c->stream));
   ok(cudaEventCreate(&c->e0));
@@ -832,8 +836,6 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (timing && !tev[0])
     for (auto& e : tev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(tev[0], s);
-  // C = A W is rebuilt when stale.  On the persistent path (deflate / augment, k <= 16) the solve
-  // kernel builds it itself (fuse_c); otherwise the build_c kernel chain runs first.
   const bool need_c = eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind);
   const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
   const double basis_pass0 = 8.0 * (double)c->n * (double)(k + m + 2);
@@ -841,11 +843,28 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   static const bool no_fuse = getenv("RG_NO_FUSE_C") != nullptr;
   bool fuse_c = need_c && !galerkin_variant(eff) && !no_fuse && c->use_persist && persist_size && dcgs_next &&
                 !(c->flags & RG_FLAG_NO_GRAPH);
+  // DCGS2 saves two reductions and one basis pass per Arnoldi step but spends one extra SpMV per
+  // cycle (the step after the stopping column).  When one SpMV moves more bytes than a whole pass
+  // over the basis (C5: 7.3 GB vs ~0.8 GB), classical CGS2 is cheaper (measured C5: see DESIGN.md).
+  const double basis_pass = 8.0 * (double)c->n * (double)(k + m + 2);
+  c->dcgs_now = c->use_dcgs && !(c->A.bytes > basis_pass && !getenv("RG_FORCE_DCGS"));
+  DevState* h = c->hst;
+  memset(h, 0, header_bytes());
+  h->variant = eff;
+  h->m = m;
+  h->k_eff = k;
+  h->max_iters = max_iters;
+  h->hist_cap = std::min(HIST_CAP, std::max(history_cap, 0));
+  h->profile = (c->flags & RG_FLAG_PROFILE) ? 1 : 0;
+  h->tol = tol;
+  h->jfinal = -1;
+  h->dcgs = c->dcgs_now ? 1 : 0;
+  CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));  // before the C build (cfail)
   if (need_c) {
-    CK(cudaMemsetAsync(c->dflag, 0, sizeof(int), s));
     if (fuse_c) {  // one cooperative kernel (persistent.cu k_cbuild) instead of build_c's ~10 launches
-      CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
-      const cudaError_t eb = launch_cbuild(c->L, c->A, c->st, c->tot_g, c->gbar, c->llw, k, c->dflag, s);
+      // (gbar is clean between solves; it uses it only without the flag-carrying reductions)
+      const cudaError_t eb = launch_cbuild(c->L, c->A, c->st, c->tot_g, c->gbar, c->llw, k, &c->st->cfail, s);
+      if (eb == cudaSuccess && getenv("RG_NO_LLRED")) CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
       if (eb == cudaSuccess) {
         c->c_valid = true;
       } else if (eb == cudaErrorNotSupported || eb == cudaErrorCooperativeLaunchTooLarge) {
@@ -861,45 +880,46 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     check_c = true;
   }
   c->cur_var = eff;
-  // DCGS2 saves two reductions and one basis pass per Arnoldi step but spends one extra SpMV per
-  // cycle (the step after the stopping column).  When one SpMV moves more bytes than a whole pass
-  // over the basis (C5: 7.3 GB vs ~0.8 GB), classical CGS2 is cheaper (measured C5: see DESIGN.md).
-  const double basis_pass = 8.0 * (double)c->n * (double)(k + m + 2);
-  c->dcgs_now = c->use_dcgs && !(c->A.bytes > basis_pass && !getenv("RG_FORCE_DCGS"));
-  if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
-  if (x0) {
-    if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+  c->L.prec = c->prec_kind ? 1 : 0;
+  // Measured on B200 (DESIGN.md §5): the single cooperative kernel wins while kernel-boundary
+  // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
+  // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
+  const bool try_persist = c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH);
+  // Persistent path with DEVICE buffers and n = n_pad (no padding rows): the kernel reads b and
+  // iterates on x in the caller's buffers (no copy of b, none of x back); otherwise the library's.
+  static const bool no_alias = getenv("RG_NO_ALIAS") != nullptr;
+  bool alias = try_persist && mem == RG_DEVICE && c->n == c->npad && !no_alias;
+  if (alias) {
+    if (x0 && x0 != x_out) CK(cudaMemcpyAsync(x_out, x0, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+    else if (!x0) CK(cudaMemsetAsync(x_out, 0, sizeof(double) * c->n, s));
   } else {
-    CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->npad, s));
+    if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+    if (x0) {
+      if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+    } else {
+      CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->npad, s));
+    }
   }
-  DevState* h = c->hst;
-  memset(h, 0, header_bytes());
-  h->variant = eff;
-  h->m = m;
-  h->k_eff = k;
-  h->max_iters = max_iters;
-  h->hist_cap = std::min(HIST_CAP, std::max(history_cap, 0));
-  h->profile = (c->flags & RG_FLAG_PROFILE) ? 1 : 0;
-  h->tol = tol;
-  h->jfinal = -1;
-  h->dcgs = c->dcgs_now ? 1 : 0;
-  CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));
   c->L.augment = eff == RG_AUGMENT;
   if (timing) cudaEventRecord(tev[1], s);
   CK(cudaEventRecord(c->e0, s));
   bool done_persist = false;
-  // Measured on B200 (DESIGN.md §5): the single cooperative kernel wins while kernel-boundary
-  // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
-  // reductions cost more than the graph path's last-CTA epilogues (+11%), so it is used up to 1.6M.
-  c->L.prec = c->prec_kind ? 1 : 0;
-  if (c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH)) {
-    CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
-    CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 16, s));
-    cudaError_t ep = launch_persistent(c->L, c->A, c->st, c->tot_g, c->gbar, c->pflags, c->llw, m, k, eff,
+  if (try_persist) {  // (barrier words and neighbour epochs are zero: reset after every persistent solve)
+    Layout Lp = c->L;
+    if (alias) {
+      Lp.b = b;
+      Lp.x = x_out;
+    }
+    cudaError_t ep = launch_persistent(Lp, c->A, c->st, c->tot_g, c->gbar, c->pflags, c->llw, m, k, eff,
                                        c->L.prec ? &c->P : nullptr, s);
     if (ep == cudaSuccess) done_persist = true;
     else if (ep == cudaErrorNotSupported || ep == cudaErrorCooperativeLaunchTooLarge) cudaGetLastError();
     else CK(ep);
+  }
+  if (!done_persist && alias) {  // the graph path works on the library's buffers
+    CK(cudaMemcpyAsync(c->b, b, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(c->x, x_out, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
+    alias = false;
   }
   if (!done_persist) {
     CK(launch_orth(c->L, c->st, OP_NORMB, s));
@@ -910,9 +930,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   // one synchronisation per solve: header, C=AW singularity flag, x and the history together
   int bad = 0;
   if (timing) cudaEventRecord(tev[2], s);
-  CK(cudaMemcpyAsync(h, c->st, header_bytes(), cudaMemcpyDeviceToHost, s));
-  if (check_c) CK(cudaMemcpyAsync(c->hflag, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(x_out, c->x, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(h, c->st, header_bytes(), cudaMemcpyDeviceToHost, s));  // incl. the C-build flag
+  if (!alias)
+    CK(cudaMemcpyAsync(x_out, c->x, sizeof(double) * c->n, mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
   const int hcap = std::min(history_cap, HIST_CAP);
   if (history && hcap > 0) CK(cudaMemcpyAsync(c->hhist, c->hist, sizeof(double) * hcap, cudaMemcpyDeviceToHost, s));
   if (timing) cudaEventRecord(tev[3], s);
@@ -925,7 +945,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     fprintf(stderr, "rg_solve device us: setup (C = A W, QR, copies) %.1f, solve %.1f, copy-out %.1f\n", a * 1e3,
             b2 * 1e3, d * 1e3);
   }
-  if (check_c) bad = c->hflag[0];
+  if (check_c) bad = h->cfail;
   if (done_persist && getenv("RG_SKEW")) {  // experiment: per-CTA step start / dots done / reduction done / SM
     std::vector<unsigned> ts((size_t)NSM * 8);
     cudaMemcpy(ts.data(), c->pflags + NSM * 2, sizeof(unsigned) * NSM * 8, cudaMemcpyDeviceToHost);
@@ -935,6 +955,10 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     for (int b2 = 0; b2 < NSM * 2; ++b2)
       fprintf(stderr, "skewcsv %d,%u,%.3f,%.3f,%.3f\n", b2, ts[3 * NSM * 2 + b2], (int)(ts[NSM * 2 + b2] - mn) * 1e-3,
               (int)(ts[b2] - mn) * 1e-3, (int)(ts[2 * NSM * 2 + b2] - mn) * 1e-3);
+  }
+  if (done_persist) {  // clean barrier words / epochs for the next persistent launch (runs while the host returns)
+    CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
+    CK(cudaMemsetAsync(c->pflags, 0, sizeof(unsigned) * NSM * 16, s));
   }
   if (bad) {
     c->have_W = false;
