@@ -146,6 +146,36 @@ def test_b_zero_and_converged_x0(rng):
     assert rep["converged"] and rep["iterations"] == 0
 
 
+@pytest.mark.parametrize("n", [1024, 1000])   # n = n_pad (caller buffers used in place) / padded
+def test_initial_guess_and_buffer_modes_agree(n, rng):
+    """The persistent solve reads b and iterates x in the caller's device buffers when n = n_pad;
+    every way of passing x0 (none, a separate device buffer, in place in x_out, host buffers) gives
+    the same iterates, and the result is the oracle's."""
+    hm = random_csr(n, rng, per_row=(2, 6))
+    ctx = make_ctx(hm)
+    b = rng.standard_normal(n)
+    x0 = 0.1 * rng.standard_normal(n)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=20, x0=x0, tol=1e-8)
+    outs = []
+    xa = torch.zeros(n, dtype=torch.float64, device=DEV)              # separate x0 buffer
+    outs.append((ctx.solve(t(b), xa, x0=t(x0), m=20), xa.cpu().numpy()))
+    xb = t(x0)                                                        # in place: x0 is x_out
+    outs.append((ctx.solve(t(b), xb, x0=xb, m=20), xb.cpu().numpy()))
+    xc = np.zeros(n)                                                  # host buffers
+    outs.append((ctx.solve(b, xc, x0=x0, m=20), xc))
+    for rep, x in outs:
+        assert rep["converged"]
+        assert rep["iterations"] == outs[0][0]["iterations"]
+        assert np.array_equal(x, outs[0][1])                          # bitwise: same kernels, same inputs
+        assert np.linalg.norm(x - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+        assert abs(rep["iterations"] - ref["iterations"]) <= 2
+    xd = torch.full((n,), 7.0, dtype=torch.float64, device=DEV)       # x0 = None: zero start, x_out overwritten
+    rep = ctx.solve(t(b), xd, m=20)
+    ref0 = oracle.solve(oracle.Matrix.from_host(hm), b, m=20, tol=1e-8)
+    assert rep["converged"] and abs(rep["iterations"] - ref0["iterations"]) <= 2
+    assert np.linalg.norm(xd.cpu().numpy() - ref0["x"]) <= 1e-7 * np.linalg.norm(ref0["x"])
+
+
 def test_max_iters_cap_reports_not_converged(rng):
     hm = random_csr(500, rng, diag=1.0)
     ctx = make_ctx(hm)
