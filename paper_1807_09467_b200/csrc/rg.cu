@@ -841,8 +841,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   const double basis_pass0 = 8.0 * (double)c->n * (double)(k + m + 2);
   const bool dcgs_next = c->use_dcgs && !(c->A.bytes > basis_pass0 && !getenv("RG_FORCE_DCGS"));
   static const bool no_fuse = getenv("RG_NO_FUSE_C") != nullptr;
-  bool fuse_c = need_c && !galerkin_variant(eff) && !no_fuse && c->use_persist && persist_size && dcgs_next &&
-                !(c->flags & RG_FLAG_NO_GRAPH);
+  // (independent of the solve path: the graph path reads the same Q columns and R_C^{-1})
+  bool fuse_c = need_c && !galerkin_variant(eff) && !no_fuse;
   // DCGS2 saves two reductions and one basis pass per Arnoldi step but spends one extra SpMV per
   // cycle (the step after the stopping column).  When one SpMV moves more bytes than a whole pass
   // over the basis (C5: 7.3 GB vs ~0.8 GB), classical CGS2 is cheaper (measured C5: see DESIGN.md).
