@@ -176,6 +176,21 @@ def test_initial_guess_and_buffer_modes_agree(n, rng):
     assert np.linalg.norm(xd.cpu().numpy() - ref0["x"]) <= 1e-7 * np.linalg.norm(ref0["x"])
 
 
+def test_persistent_refusal_falls_back_with_caller_buffers(rng):
+    """n = n_pad with device buffers but m > 64: the persistent kernel refuses the launch after the
+    caller's b / x were chosen as its buffers; the graph path then gets the library's copies."""
+    n, m = 4096, 100
+    hm = random_csr(n, rng, per_row=(2, 6), diag=2.0)
+    ctx = make_ctx(hm, max_m=m)
+    b = rng.standard_normal(n)
+    x0 = 0.1 * rng.standard_normal(n)
+    x = t(x0)                                                         # in place
+    rep = ctx.solve(t(b), x, x0=x, m=m, tol=1e-9)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=m, x0=x0, tol=1e-9)
+    assert rep["converged"] and abs(rep["iterations"] - ref["iterations"]) <= 2
+    assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+
+
 def test_max_iters_cap_reports_not_converged(rng):
     hm = random_csr(500, rng, diag=1.0)
     ctx = make_ctx(hm)
