@@ -19,9 +19,16 @@ rg: $(PKG)/lib/librg.so
 synth: synth/libsynth.so synth/libsynth_cuda.so
 oracle: oracle/liboracle.so
 
-$(PKG)/lib/librg.so: $(RG_SRC) $(RG_HDR)
+RG_OBJ    := $(patsubst $(PKG)/csrc/%.cu,build/rg/%.o,$(RG_SRC))
+
+# one object per translation unit (make -j compiles them in parallel), then one shared library
+build/rg/%.o: $(PKG)/csrc/%.cu $(RG_HDR)
+	@mkdir -p build/rg
+	$(NVCC) $(NVFLAGS) -c -o $@ $<
+
+$(PKG)/lib/librg.so: $(RG_OBJ)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(RG_SRC) -lcuda
+	$(NVCC) $(ARCH) -shared -o $@ $(RG_OBJ) -lcuda
 
 synth/libsynth.so: synth/synth.c synth/synth_common.h
 	$(CC) $(CFLAGS) -shared -o $@ synth/synth.c -lm
@@ -34,5 +41,6 @@ oracle/liboracle.so: oracle/oracle.c
 
 clean:
 	rm -f $(PKG)/lib/librg.so synth/*.so oracle/*.so
+	rm -rf build/rg
 
 .PHONY: all rg synth oracle clean
