@@ -31,7 +31,7 @@ constexpr int VEC_CTAS_PER_SM = 2;         // -> 296 CTAs: 32 resident warps / S
 enum KernelId {
   K_SPMV_STEP = 0, K_SPMV_RES, K_SPMV_PLAIN, K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN,
   K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_DK1, K_DK2,
-  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_SSOR, K_PB6, K_COND, K_SSORK, K_PB7, K_CBUILD, K_COUNT
+  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_SSOR, K_PB6, K_COND, K_SSORK, K_PB7, K_CBUILD, K_RES_Y, K_COUNT
 };
 
 struct KStatDev {

@@ -29,7 +29,7 @@ struct MatDev {
 // the total as the entry "host_launched".
 void note_host_launches(int n);
 
-enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2, SM_STEP_PC = 3 };
+enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2, SM_STEP_PC = 3, SM_RES_Y = 4 };
 
 // w = A v_j (STEP), r = b - A x (RES; epi != 0 runs the cycle-start epilogue on ||r||^2),
 // y = A x (PLAIN), w = A pz (STEP_PC: pz = M^{-1} v_j from launch_ssor, same gating as STEP).
@@ -38,8 +38,10 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
 
 // Y[:, 0:k] = A W[:, 0:k] (columns with leading dimension ld) with ONE read of A (a4: C = A W).
 // Returns cudaErrorNotSupported when no SpMM kernel covers the format (caller loops SpMVs).
+// xe != nullptr (BSR-64 TMA path, k + 1 <= 64 only; else cudaErrorInvalidValue): ye = A xe in the
+// same pass — the solve-start product fused with C = A W (then SM_RES_Y finishes the residual).
 cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld, int k, DevState* st, unsigned* counter,
-                        cudaStream_t s);
+                        cudaStream_t s, const double* xe = nullptr, double* ye = nullptr);
 
 enum OrthOp {
   OP_D1 = 0, OP_UD2, OP_UN, OP_CS_DQ, OP_CS_UN, OP_XW, OP_XUPD, OP_NORMB,

@@ -113,6 +113,7 @@ struct rg_ctx {
   bool have_W = false;
   int v1prev_s = 0;         // size of the stored first-pass eigenvectors (Jacobi warm start), 0 = none
   bool c_valid = false;
+  bool res_fused = false;  // this solve's C = A W SpMM also computes A x0 into V column 0 (SM_RES_Y start)
   int c_kind = 0;           // what c_valid refers to: 0 Q / R_C (augment, deflate), 1 C / E^{-1} (oblique)
   bool use_dcgs = true;
   bool dcgs_now = true;     // this solve uses DCGS2 (the oblique variant runs classical CGS2)
@@ -313,9 +314,12 @@ rg_status build_c(rg_ctx* c, bool sync) {
   const int QB = c->L.VB - k;
   const int64_t ld = c->npad;
   cudaStream_t s = c->stream;
-  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported : launch_spmm(c->A, c->Z, c->Z + (int64_t)QB * ld, ld, k, c->st, c->counter, s);
+  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported
+                                        : launch_spmm(c->A, c->Z, c->Z + (int64_t)QB * ld, ld, k, c->st, c->counter, s,
+                                                      c->res_fused ? c->x : nullptr, c->Z + (int64_t)c->L.VB * ld);
   if (es == cudaErrorNotSupported) {
     cudaGetLastError();
+    c->res_fused = false;
     for (int l = 0; l < k; ++l)
       CK(launch_spmv(c->A, c->L, c->st, SM_PLAIN, c->Z + (int64_t)l * ld, c->Z + (int64_t)(QB + l) * ld, 0, s));
   } else {
@@ -371,9 +375,12 @@ rg_status build_c_oblique(rg_ctx* c) {
   const int64_t ld = c->npad;
   cudaStream_t s = c->stream;
   double* C = c->Z + (int64_t)k * ld;
-  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported : launch_spmm(c->A, c->Z, C, ld, k, c->st, c->counter, s);
+  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported
+                                        : launch_spmm(c->A, c->Z, C, ld, k, c->st, c->counter, s,
+                                                      c->res_fused ? c->x : nullptr, c->Z + (int64_t)c->L.VB * ld);
   if (es == cudaErrorNotSupported) {
     cudaGetLastError();
+    c->res_fused = false;
     for (int l = 0; l < k; ++l)
       CK(launch_spmv(c->A, c->L, c->st, SM_PLAIN, c->Z + (int64_t)l * ld, C + (int64_t)l * ld, 0, s));
   } else {
@@ -388,8 +395,10 @@ rg_status build_c_oblique(rg_ctx* c) {
 }
 
 // ---- the kernel sequences of one solve
-cudaError_t cycle_start(rg_ctx* c, int variant) {
-  cudaError_t e = launch_spmv(c->A, c->L, c->st, SM_RES, nullptr, nullptr, variant == RG_PLAIN ? 1 : 0, c->stream);
+// from_y: A x is already in V column 0 (fused into the C = A W SpMM), only r = b - A x remains
+cudaError_t cycle_start(rg_ctx* c, int variant, bool from_y = false) {
+  cudaError_t e = launch_spmv(c->A, c->L, c->st, from_y ? SM_RES_Y : SM_RES, nullptr, nullptr,
+                              variant == RG_PLAIN ? 1 : 0, c->stream);
   if (e != cudaSuccess || variant == RG_PLAIN) return e;
   if (galerkin_variant(variant)) {  // Galerkin start x += W t, r -= C t, t = E^{-1} W^T r
     if ((e = launch_orth(c->L, c->st, OP_OB_CSD, c->stream)) != cudaSuccess) return e;
@@ -860,6 +869,20 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   h->jfinal = -1;
   h->dcgs = c->dcgs_now ? 1 : 0;
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));  // before the C build (cfail)
+  // BSR-64 solves on the graph path (C5): the start residual's product A x0 rides along as one
+  // extra column of the C = A W SpMM — one read of A (7.3 GB at C5) instead of two per system.
+  static const bool no_fuse_res = getenv("RG_NO_FUSE_RES") != nullptr;
+  c->res_fused = need_c && !no_fuse_res && c->A.fmt == 2 && c->A.b == 64 && c->A.tma && k + 1 <= 64 &&
+                 !(c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH));
+  const bool early_in = c->res_fused;  // b and x0 in the library's buffers before the SpMM reads x0
+  if (early_in) {
+    if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+    if (x0) {
+      if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
+    } else {
+      CK(cudaMemsetAsync(c->x, 0, sizeof(double) * c->npad, s));
+    }
+  }
   if (need_c) {
     if (fuse_c) {  // one cooperative kernel (persistent.cu k_cbuild) instead of build_c's ~10 launches
       // (gbar is clean between solves; it uses it only without the flag-carrying reductions)
@@ -892,7 +915,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if (alias) {
     if (x0 && x0 != x_out) CK(cudaMemcpyAsync(x_out, x0, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
     else if (!x0) CK(cudaMemsetAsync(x_out, 0, sizeof(double) * c->n, s));
-  } else {
+  } else if (!early_in) {
     if ((rs = copy_in(c->b, b, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
     if (x0) {
       if ((rs = copy_in(c->x, x0, sizeof(double) * c->n, mem, s)) != RG_OK) return rs;
@@ -923,7 +946,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   }
   if (!done_persist) {
     CK(launch_orth(c->L, c->st, OP_NORMB, s));
-    CK(cycle_start(c, eff));
+    const bool from_y = c->res_fused;
+    c->res_fused = false;
+    CK(cycle_start(c, eff, from_y));
     if ((rs = run_solve(c, eff, m)) != RG_OK) return rs;
   }
   CK(cudaEventRecord(c->e1, s));
@@ -1198,7 +1223,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
                                        "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
-                                       "ssor_sweep_kernels", "p_spmv", "cbuild"};
+                                       "ssor_sweep_kernels", "p_spmv", "cbuild", "res_from_ax"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));

@@ -6,6 +6,8 @@
 //   SM_STEP  w = A v_j into V column j+1 (x = un-normalised column j, scaled on output)
 //   SM_RES   r = b - A x into V column 0, ||r||^2 grid-reduced (cycle start)
 //   SM_PLAIN y = A x (rg_apply, C = A W)
+//   SM_RES_Y r = b - y into V column 0 where y = A x already sits there (the solve-start product
+//            fused into the C = A W SpMM as its extra column: one read of A for both), ||r||^2
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
@@ -50,8 +52,8 @@ __device__ __forceinline__ bool setup(const SpmvArgs& a, Io& io, int& kid) {
     io.y = L.Z + (int64_t)(L.VB + j + 1) * L.ld;
     // DCGS2: y = A u on the raw vector; STEP_PC: the SSOR sweep already applied the column scale
     io.xs = (st->dcgs || a.mode == SM_STEP_PC) ? 1.0 : st->sc[L.VB + j];
-  } else if (a.mode == SM_RES) {
-    kid = K_SPMV_RES;
+  } else if (a.mode == SM_RES || a.mode == SM_RES_Y) {
+    kid = a.mode == SM_RES ? K_SPMV_RES : K_RES_Y;
     if (st->done) { prof_noop(st, kid); return false; }
     io.x = L.x;
     io.y = L.Z + (int64_t)L.VB * L.ld;
@@ -76,7 +78,7 @@ __device__ __forceinline__ void finish(const SpmvArgs& a, const Io& io, int kid,
     __syncthreads();
     if (!grid_reduce(vals, 1, a.L.partial, a.L.counter, tot, tot)) return;
     if (a.res_epi) epi_cycle_start(st, a.L, tot[0]);
-    if (threadIdx.x == 0) prof_end(st, kid, a.A.bytes + 8.0 * a.L.n);
+    if (threadIdx.x == 0) prof_end(st, kid, a.mode == SM_RES_Y ? 24.0 * a.L.n : a.A.bytes + 8.0 * a.L.n);
     return;
   }
   if (st && st->profile) {
@@ -302,6 +304,17 @@ __global__ void __launch_bounds__(BT, 1) k_spmv_bsr_tma(SpmvArgs a) {
   finish(a, io, kid, nrm);
 }
 
+// ---------------------------------------------------------------- r = b - y, y = A x already in V column 0
+__global__ void __launch_bounds__(OT) k_res_y(SpmvArgs a) {
+  Io io;
+  int kid;
+  if (!setup(a, io, kid)) return;
+  double nrm = 0.0;
+  for (int64_t r = (int64_t)blockIdx.x * OT + threadIdx.x; r < a.A.n; r += (int64_t)gridDim.x * OT)
+    nrm += emit(io, r, io.y[r]);
+  finish(a, io, kid, nrm);
+}
+
 // ---------------------------------------------------------------- SpMM  Y = A W  (C = A W, a4)
 // BSR-64: one TMA-streamed read of A for all k columns; the 64x64 block (shared memory) times the
 // 64 x k panel of W runs on the FP64 tensor cores (DMMA m8n8k4): warp w owns output rows
@@ -340,8 +353,11 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
     }
 }
 
+// xe != nullptr: one extra input column (panel column k) whose product goes to ye (y = A x0 of the
+// solve start, fused with C = A W: one read of A instead of two).
 __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* __restrict__ W, double* Y,
-                                                        int64_t ld, int k, DevState* pst, unsigned* counter) {
+                                                        int64_t ld, int k, DevState* pst, unsigned* counter,
+                                                        const double* __restrict__ xe, double* ye) {
   if (pst) prof_begin(pst, K_SPMV_PLAIN);
   extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
@@ -354,6 +370,8 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const int kw = k;                  // columns of W / Y
+  if (xe) k += 1;                    // + the extra column
   const int ng = (k + 7) / 8;
   if (wid == BT_CONS / 32) {
     if (lane == 0) {
@@ -388,7 +406,8 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
 #pragma unroll
     for (int u = 0; u < PPT; ++u) {
       const int e = tid + u * BT_CONS;
-      pre[u] = e < nval ? __ldg(W + (int64_t)(e >> 6) * ld + wr + (e & 63)) : 0.0;
+      const int col = e >> 6;
+      pre[u] = e >= nval ? 0.0 : col < kw ? __ldg(W + (int64_t)col * ld + wr + (e & 63)) : __ldg(xe + wr + (e & 63));
     }
   };
   auto store_panel = [&](int buf) {
@@ -444,8 +463,10 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
       if (g < ng) {
         const int col = g * 8 + (lane & 3) * 2;
         const int64_t row = I * 64 + rrow;
-        if (col < k) Y[(int64_t)col * ld + row] = acc[g][0];
-        if (col + 1 < k) Y[(int64_t)(col + 1) * ld + row] = acc[g][1];
+        if (col < kw) Y[(int64_t)col * ld + row] = acc[g][0];
+        else if (col == kw && xe) ye[row] = acc[g][0];
+        if (col + 1 < kw) Y[(int64_t)(col + 1) * ld + row] = acc[g][1];
+        else if (col + 1 == kw && xe) ye[row] = acc[g][1];
       }
     }
     const int64_t In = I + gridDim.x;
@@ -506,6 +527,12 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
                         double* y, int res_epi, cudaStream_t s) {
   SpmvArgs a{A, L, st, mode, x, y, res_epi};
   const int cap_red = NSM * VEC_CTAS_PER_SM;  // reducing launches: bounded partials
+  if (mode == SM_RES_Y) {
+    int64_t g = (A.n + OT - 1) / OT;
+    if (g > cap_red) g = cap_red;
+    k_res_y<<<(int)(g < 1 ? 1 : g), OT, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   if (A.fmt == 2 && A.b == 64 && A.tma) {
     static bool init = false;
     if (!init) {
@@ -544,8 +571,9 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
 }
 
 cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld, int k, DevState* st, unsigned* counter,
-                        cudaStream_t s) {
+                        cudaStream_t s, const double* xe, double* ye) {
   if (k <= 0) return cudaSuccess;
+  if (xe && !(A.fmt == 2 && A.b == 64 && A.tma && k + 1 <= 64)) return cudaErrorInvalidValue;  // callers check
   if (A.fmt == 2 && A.b == 64 && A.tma && k <= 64) {
     static bool init = false;
     if (!init) {
@@ -553,7 +581,7 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
       init = true;
     }
     int64_t g = A.nb < NSM ? A.nb : NSM;
-    k_spmm_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, BNS * BSTAGE + 2 * 64 * 68 * 8, s>>>(A, W, Y, ld, k, st, counter);
+    k_spmm_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, BNS * BSTAGE + 2 * 64 * 68 * 8, s>>>(A, W, Y, ld, k, st, counter, xe, ye);
     return cudaGetLastError();
   }
   if (A.fmt == 2) return cudaErrorNotSupported;  // caller falls back to per-column SpMV

@@ -80,6 +80,43 @@ def test_c5_reduced_bsr(variant):
     run(synth.CONFIGS["C5"].reduced(3), variant, 5)
 
 
+@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
+def test_c5_warm_start_fused_start_residual(variant):
+    """BSR-64 graph path with a NONZERO initial guess x0 = x_{t-1}: the solve-start product A x0
+    rides along as an extra column of the C = A W SpMM (SM_RES_Y start) — every recycled solve
+    must take that path (kernel statistics) and still match the oracle started from the same x0."""
+    from paper_1807_09467_b200 import Context, rg as rgb
+    cfg = synth.CONFIGS["C5"].reduced(3)
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    A1 = seq.matrix(1, u)
+    ctx = Context(cfg.n, t(A1.row_ptr), t(A1.col_idx), t(A1.val), fmt="bsr", block=A1.block, max_m=cfg.m,
+                  max_snapshots=cfg.s, max_k=cfg.k, flags=rgb.RG_FLAG_PROFILE)
+    X, fused = [], 0
+    for step in range(1, 5):
+        A = seq.matrix(step, u)
+        b = seq.rhs(step, u)
+        ctx.update_matrix(t(A.val))
+        W = None
+        if X:
+            ke, _ = ctx.build_recycle(cfg.k)
+            W, _, ko = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), cfg.k)
+            assert ke == ko
+            fused += 1
+        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, x0=t(u), m=cfg.m, variant=variant, tol=cfg.tol)
+        ref = oracle.solve(oracle.Matrix.from_host(A), b, x0=u, m=cfg.m, variant=variant, W=W, tol=cfg.tol)
+        assert rep["converged"] and ref["converged"]
+        assert abs(rep["iterations"] - ref["iterations"]) <= 2, (step, rep["iterations"], ref["iterations"])
+        assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+        u = ref["x"]
+        X.append(u)
+        ctx.push_snapshot(t(u))
+    st = ctx.kernel_stats()
+    assert st["res_from_ax"]["launches"] == fused, st["res_from_ax"]
+    ctx.close()
+
+
 @pytest.mark.parametrize("variant", ["oblique", "orthogonal"])
 def test_c3_reduced_sell_galerkin(variant):
     run(synth.CONFIGS["C3"].reduced(96), variant, 5)
