@@ -80,11 +80,13 @@ def test_c5_reduced_bsr(variant):
     run(synth.CONFIGS["C5"].reduced(3), variant, 5)
 
 
-@pytest.mark.parametrize("variant", ["augment", "deflate", "oblique"])
-def test_c5_warm_start_fused_start_residual(variant):
+@pytest.mark.parametrize("variant,host", [("augment", False), ("deflate", False), ("oblique", False),
+                                          ("deflate", True)])
+def test_c5_warm_start_fused_start_residual(variant, host):
     """BSR-64 graph path with a NONZERO initial guess x0 = x_{t-1}: the solve-start product A x0
     rides along as an extra column of the C = A W SpMM (SM_RES_Y start) — every recycled solve
-    must take that path (kernel statistics) and still match the oracle started from the same x0."""
+    must take that path (kernel statistics) and still match the oracle started from the same x0.
+    host=True: b, x0 and x_out are HOST arrays (x0 is copied in before the SpMM reads it)."""
     from paper_1807_09467_b200 import Context, rg as rgb
     cfg = synth.CONFIGS["C5"].reduced(3)
     seq = synth.HostSequence(cfg)
@@ -103,12 +105,19 @@ def test_c5_warm_start_fused_start_residual(variant):
             W, _, ko = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), cfg.k)
             assert ke == ko
             fused += 1
-        x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
-        rep = ctx.solve(t(b), x, x0=t(u), m=cfg.m, variant=variant, tol=cfg.tol)
+        if host:
+            x = np.zeros(cfg.n)
+            rep = ctx.solve(np.ascontiguousarray(b), x, x0=np.ascontiguousarray(u), m=cfg.m, variant=variant,
+                            tol=cfg.tol)
+            xg = x
+        else:
+            x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+            rep = ctx.solve(t(b), x, x0=t(u), m=cfg.m, variant=variant, tol=cfg.tol)
+            xg = x.cpu().numpy()
         ref = oracle.solve(oracle.Matrix.from_host(A), b, x0=u, m=cfg.m, variant=variant, W=W, tol=cfg.tol)
         assert rep["converged"] and ref["converged"]
         assert abs(rep["iterations"] - ref["iterations"]) <= 2, (step, rep["iterations"], ref["iterations"])
-        assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+        assert np.linalg.norm(xg - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
         u = ref["x"]
         X.append(u)
         ctx.push_snapshot(t(u))
