@@ -93,3 +93,21 @@ def test_c5_blocks_and_perturbation():
     assert abs(np.mean(np.diag(diag_blk)) - 100) < 1.0
     b = seq.rhs(1, None)
     assert abs(b.mean()) < 0.1 and abs(b.std() - 1) < 0.1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nval,off", [(1, 0), (7, 0), (7, 1), (100003, 0), (100003, 1), (2 * 148 * 16 * 256 * 4 + 5, 0)])
+def test_c5_perturb_device_matches_host(nval, off):
+    """The device perturbation (16-byte vectorised, 4 pairs in flight; scalar path when the buffer is
+    not 16-byte aligned; odd tail) is bit-identical to the host C loop (R10: A_t = A_{t-1} o (1+0.01 xi))."""
+    import ctypes
+    torch = pytest.importorskip("torch")
+    L, C = synth.lib(), synth.culib()
+    rng = np.random.default_rng(nval)
+    v = rng.standard_normal(nval + off)
+    ref = v[off:].copy()
+    L.sy_c5_perturb(nval, 1234, 3, ref.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    d = torch.from_numpy(v).cuda()
+    assert C.syd_c5_perturb(nval, 1234, 3, ctypes.c_void_p(d.data_ptr() + 8 * off), None) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(d.cpu().numpy()[off:], ref)
