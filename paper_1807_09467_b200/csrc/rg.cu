@@ -897,7 +897,10 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
         CK(eb);
       }
     }
-    if (!fuse_c && (rs = (galerkin_variant(eff) ? build_c_oblique(c) : build_c(c, false))) != RG_OK) return rs;
+    if (!fuse_c && (rs = (galerkin_variant(eff) ? build_c_oblique(c) : build_c(c, false))) != RG_OK) {
+      c->res_fused = false;
+      return rs;
+    }
     c->c_kind = want_kind;
     c_spmv = k;
     check_c = true;
