@@ -3,7 +3,7 @@
 #   libsynth*.so      seeded input generators (host C + device CUDA, bit-identical)
 #   liboracle.so      CPU oracle (test infrastructure only)
 NVCC      ?= /usr/local/cuda/bin/nvcc
-CC        ?= gcc
+CC        := gcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
              --expt-relaxed-constexpr -Iinclude
@@ -37,7 +37,7 @@ synth/libsynth_cuda.so: synth/synth_cuda.cu synth/synth_common.h
 	$(NVCC) $(ARCH) -O3 -lineinfo -fmad=false -Xcompiler -fPIC -shared -o $@ synth/synth_cuda.cu
 
 oracle/liboracle.so: oracle/oracle.c
-	$(CC) $(CFLAGS) -shared -o $@ oracle/oracle.c -lm
+	$(CC) $(CFLAGS) -fopenmp -shared -o $@ oracle/oracle.c -lm
 
 clean:
 	rm -f $(PKG)/lib/librg.so synth/*.so oracle/*.so

@@ -1,6 +1,7 @@
 """CPU oracle — TEST INFRASTRUCTURE ONLY.
 
-Thin ctypes/numpy wrapper over ``oracle/liboracle.so`` (plain C99, fp64, single thread; see
+Thin ctypes/numpy wrapper over ``oracle/liboracle.so`` (plain C99, fp64, deterministic OpenMP threads
+over a fixed 256-chunk partition, so results do not depend on the thread count; see
 ``oracle.c`` for the definitions it follows and the PAPER.md passages it cites).  Only
 ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` / ``--impl reference``
 legs may import this package.  The product library (``paper_1807_09467_b200``) never does.
@@ -8,6 +9,10 @@ legs may import this package.  The product library (``paper_1807_09467_b200``) n
 Parity status of each function:
   spmv / spmv_row     pinned: identity, diagonal, dense brute force (tests/test_oracle_spmv.py)
   solve (plain)       pinned: I, 2I, dense LU, restart = n termination, Arnoldi/monotonicity
+  solve_basis         pinned: Arnoldi relation A V = V_{J+1} H (plain, augment) and the GCRO relation
+                      A V = U_C B + V_{J+1} H (deflate) with A V formed by scipy.sparse; V^T V = I,
+                      U_C^T V = 0 (tests/test_oracle_basis.py)
+  threads             1 thread == N threads bitwise (solve, svd, spmv; tests/test_oracle_basis.py)
   solve (aug/defl)    pinned: brute-force dense least squares over the explicit space, b = A W c
                       special case, k = 0 reduces to plain, Table-1 row-6 projector properties
   solve (oblique)     pinned: brute-force dense least squares over the explicit monomial Krylov
@@ -79,6 +84,14 @@ def lib():
         L.or_lsproj.argtypes = [ctypes.POINTER(_Mat), _f64p, ctypes.c_int, _f64p, ctypes.c_int]
         L.or_obproj.restype = ctypes.c_int
         L.or_obproj.argtypes = [ctypes.POINTER(_Mat), _f64p, ctypes.c_int, _f64p, ctypes.c_int]
+        L.or_solve_basis.restype = ctypes.c_int
+        L.or_solve_basis.argtypes = [ctypes.POINTER(_Mat), _f64p, _f64p, ctypes.c_int, ctypes.c_int, _f64p,
+                                     ctypes.c_int, ctypes.c_double, ctypes.c_int, _f64p, ctypes.POINTER(_Rep),
+                                     _f64p, _f64p, _f64p, ctypes.POINTER(ctypes.c_int)]
+        L.or_set_threads.restype = None
+        L.or_set_threads.argtypes = [ctypes.c_int]
+        L.or_get_threads.restype = ctypes.c_int
+        L.or_get_threads.argtypes = []
         L.or_svd.restype = ctypes.c_int
         L.or_svd.argtypes = [ctypes.c_int64, ctypes.c_int, _f64p, ctypes.c_int64, _f64p, _f64p,
                              ctypes.POINTER(ctypes.c_int)]
@@ -88,6 +101,15 @@ def lib():
 
 def _f(a):
     return a.ctypes.data_as(_f64p)
+
+
+def set_threads(t: int):
+    """Threads the oracle may use (results do not depend on it: fixed 256-chunk partition)."""
+    lib().or_set_threads(int(t))
+
+
+def threads() -> int:
+    return int(lib().or_get_threads())
 
 
 class Matrix:
@@ -190,6 +212,45 @@ def solve(A: Matrix, b, x0=None, m=30, variant="plain", W=None, tol=1e-8, max_it
         raise MemoryError("oracle: allocation failed")
     return dict(x=x, iterations=rep.iterations, cycles=rep.cycles, converged=bool(rep.converged),
                 rel_residual=rep.rel_residual, history=hist[:rep.hist_len].copy(), k_used=rep.k_used)
+
+
+def solve_basis(A: Matrix, b, x0=None, m=30, variant="plain", W=None, tol=1e-8, max_iters=20000):
+    """As solve (plain / augment / deflate, no preconditioner), also returning the LAST restart
+    cycle's Krylov basis: V (n x J, orthonormal v_0..v_{J-1}), H (J+1 x J upper Hessenberg: the
+    Arnoldi coefficients) and, for deflate, B (k x J: U_C^T A v_j against the orthonormal basis of
+    A W), so that A V = V_{J+1} H (plain, augment) / A V = U_C B + V_{J+1} H (deflate), where
+    v_J is the un-returned next vector (its coefficient is H[J, J-1])."""
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    if v not in (PLAIN, AUGMENT, DEFLATE):
+        raise ValueError("solve_basis: plain, augment or deflate")
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.empty(A.n)
+    k, Wf = 0, None
+    if W is not None and v != PLAIN:
+        W = np.asarray(W, dtype=np.float64).reshape(A.n, -1)
+        k = W.shape[1]
+        Wf = np.asfortranarray(W)
+    V = np.zeros((A.n, m), order="F")
+    H = np.zeros((m + 1, m), order="F")
+    B = np.zeros((max(k, 1), m), order="F")
+    rep = _Rep()
+    steps = ctypes.c_int(0)
+    x0p = None
+    if x0 is not None:
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        x0p = _f(x0)
+    st = lib().or_solve_basis(ctypes.byref(A._m), _f(b), x0p, int(m), v,
+                              Wf.ctypes.data_as(_f64p) if k > 0 else None, k, float(tol), int(max_iters), _f(x),
+                              ctypes.byref(rep), V.ctypes.data_as(_f64p), H.ctypes.data_as(_f64p),
+                              B.ctypes.data_as(_f64p), ctypes.byref(steps))
+    if st == 1:
+        raise np.linalg.LinAlgError("oracle: A W is (numerically) rank deficient")
+    if st != 0:
+        raise MemoryError("oracle: allocation failed")
+    J = steps.value
+    return dict(x=x, iterations=rep.iterations, cycles=rep.cycles, converged=bool(rep.converged),
+                rel_residual=rep.rel_residual, steps=J, V=np.ascontiguousarray(V[:, :J]),
+                H=np.ascontiguousarray(H[:J + 1, :J]), B=np.ascontiguousarray(B[:k, :J]))
 
 
 def lsproj(A: Matrix, W, Z):

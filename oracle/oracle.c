@@ -35,8 +35,16 @@
  *   - or_svd:   thin SVD by one-sided (Hestenes) Jacobi directly on X, long-double dot products;
  *               sorted non-increasing; rank = #{sigma > 1e-12 sigma_1} (PAPER.md:524-537, 552-553,
  *               Algorithm 1; Schmidt-Eckart-Young eq. opt_svd).
+ *
+ * Threading: every length-n loop is split into the SAME fixed partition of
+ * OR_CHUNKS = 256 contiguous chunks whatever the thread count; a reduction sums each chunk
+ * sequentially and then adds the 256 chunk sums in chunk order.  So every result is bitwise
+ * identical for 1 or N threads (tested); OpenMP only decides which thread runs which chunk.
+ * Loops shorter than OR_PAR_MIN run the same chunks on the calling thread.  Thread count:
+ * or_set_threads (default: OpenMP's, i.e. all online cores or OMP_NUM_THREADS).
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -61,27 +69,16 @@ typedef struct {
 } or_report;
 
 /* ------------------------------------------------------------------------------------------ */
-void or_spmv(const or_mat* A, const double* x, double* y) {
-  if (A->fmt == 0) {
-    for (int64_t i = 0; i < A->n; ++i) {
-      double s = 0.0;
-      for (int32_t p = A->rp[i]; p < A->rp[i + 1]; ++p) s += A->v[p] * x[A->ci[p]];
-      y[i] = s;
-    }
-    return;
-  }
-  const int64_t b = A->b, nb = A->n / b;
-  for (int64_t I = 0; I < nb; ++I)
-    for (int64_t r = 0; r < b; ++r) {
-      double s = 0.0;
-      for (int32_t p = A->rp[I]; p < A->rp[I + 1]; ++p)
-        for (int64_t c = 0; c < b; ++c) s += A->v[(int64_t)p * b * b + c * b + r] * x[(int64_t)A->ci[p] * b + c];
-      y[I * b + r] = s;
-    }
-}
+#define OR_CHUNKS 256
+#define OR_PAR_MIN 65536
+/* first index of chunk c of [0, n): a fixed partition, independent of the thread count */
+static int64_t chunk_lo(int64_t n, int c) { return n * c / OR_CHUNKS; }
 
-/* a single row of A x (used by tests to check sampled rows of huge products) */
-double or_spmv_row(const or_mat* A, int64_t row, const double* x) {
+void or_set_threads(int t) { if (t > 0) omp_set_num_threads(t); }
+int or_get_threads(void) { return omp_get_max_threads(); }
+
+/* one scalar row of A x, summed in stored order */
+static double spmv_row(const or_mat* A, int64_t row, const double* x) {
   double s = 0.0;
   if (A->fmt == 0) {
     for (int32_t p = A->rp[row]; p < A->rp[row + 1]; ++p) s += A->v[p] * x[A->ci[p]];
@@ -93,14 +90,56 @@ double or_spmv_row(const or_mat* A, int64_t row, const double* x) {
   return s;
 }
 
+/* y = A x: every row is an independent sum in stored order, so the row split cannot change it */
+void or_spmv(const or_mat* A, const double* x, double* y) {
+  const int64_t n = A->n;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+  for (int64_t i = 0; i < n; ++i) y[i] = spmv_row(A, i, x);
+}
+
+/* a single row of A x (used by tests to check sampled rows of huge products) */
+double or_spmv_row(const or_mat* A, int64_t row, const double* x) { return spmv_row(A, row, x); }
+
+/* a^T b: chunk sums in index order, then the OR_CHUNKS sums in chunk order */
 static double dot(int64_t n, const double* a, const double* b) {
+  double part[OR_CHUNKS];
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+  for (int c = 0; c < OR_CHUNKS; ++c) {
+    double s = 0.0;
+    for (int64_t i = chunk_lo(n, c); i < chunk_lo(n, c + 1); ++i) s += a[i] * b[i];
+    part[c] = s;
+  }
   double s = 0.0;
-  for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
+  for (int c = 0; c < OR_CHUNKS; ++c) s += part[c];
   return s;
 }
 static double nrm2(int64_t n, const double* a) { return sqrt(dot(n, a, a)); }
+/* y += al x */
 static void axpy(int64_t n, double al, const double* x, double* y) {
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
   for (int64_t i = 0; i < n; ++i) y[i] += al * x[i];
+}
+/* y = x / d */
+static void divide(int64_t n, const double* x, double d, double* y) {
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+  for (int64_t i = 0; i < n; ++i) y[i] = x[i] / d;
+}
+/* sum_i a_i b_i (and optionally a_i a_i, b_i b_i) in long double, chunked like dot() */
+static void dot3_ld(int64_t n, const double* a, const double* b, long double* aa, long double* bb, long double* ab) {
+  long double pa[OR_CHUNKS], pb[OR_CHUNKS], pg[OR_CHUNKS];
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+  for (int c = 0; c < OR_CHUNKS; ++c) {
+    long double sa = 0.0L, sb = 0.0L, sg = 0.0L;
+    for (int64_t i = chunk_lo(n, c); i < chunk_lo(n, c + 1); ++i) {
+      sa += (long double)a[i] * a[i];
+      sb += (long double)b[i] * b[i];
+      sg += (long double)a[i] * b[i];
+    }
+    pa[c] = sa; pb[c] = sb; pg[c] = sg;
+  }
+  long double sa = 0.0L, sb = 0.0L, sg = 0.0L;
+  for (int c = 0; c < OR_CHUNKS; ++c) { sa += pa[c]; sb += pb[c]; sg += pg[c]; }
+  *aa = sa; *bb = sb; *ab = sg;
 }
 
 /* Modified Gram-Schmidt applied twice: z <- (I - U U^T) z against the q orthonormal columns
@@ -128,7 +167,9 @@ static void backsolve(int q, const double* R, int ld, const double* e, double* c
 
 static void residual(const or_mat* A, const double* b, const double* x, double* r) {
   or_spmv(A, x, r);
-  for (int64_t i = 0; i < A->n; ++i) r[i] = b[i] - r[i];
+  const int64_t n = A->n;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
+  for (int64_t i = 0; i < n; ++i) r[i] = b[i] - r[i];
 }
 
 /* SSOR preconditioner in a row order: order[idx] = row processed idx-th (a permutation of 0..n-1). */
@@ -196,26 +237,53 @@ static int add_krylov_part(const or_mat* A, const or_prec* pc, const double* V, 
 static int solve_oblique(const or_mat* A, const double* b, const double* x0, int m, int row2, int orth,
                          const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
                          double* hist, int hist_cap, const or_prec* pc);
+/* The Krylov basis of the LAST restart cycle of a solve, for the basis invariants (SURVEY.md §8(c)
+ * "Arnoldi relation A V_m = V_{m+1} H_m", "V orthonormal", GCRO relation "A V_m = Q B_m + V_{m+1} H_m"
+ * ).  With J Arnoldi steps in that cycle:
+ *   V  n x J        v_0 .. v_{J-1} (column-major, leading dimension n)
+ *   H  (m+1) x m    column-major, leading dimension m+1: H[i + j(m+1)] = h_{ij}, i <= j+1 < J+1
+ *                   (the MGS2 coefficients of A v_j against v_0..v_j, and h_{j+1,j} = ||w||)
+ *   B  k x m        deflate only: B[l + j k] = u_l^T A v_j against the orthonormal basis U_C of A W
+ *                   (the coefficients of the projection P, P = I - U_C U_C^T)
+ *   steps           J */
+typedef struct {
+  double* V;
+  double* H;
+  double* B;
+  int steps;
+} or_basis;
+
 static int solve_impl(const or_mat* A, const double* b, const double* x0, int m, int variant,
                       const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
-                      double* hist, int hist_cap, const or_prec* pc);
+                      double* hist, int hist_cap, const or_prec* pc, or_basis* bx);
 
 int or_solve(const or_mat* A, const double* b, const double* x0, int m, int variant,
              const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
              double* hist, int hist_cap) {
-  return solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, NULL);
+  return solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, NULL, NULL);
+}
+
+/* or_solve that also returns the last cycle's Krylov basis (or_basis above; plain, augment,
+ * deflate; V n x m, H (m+1) x m, B k x m caller-allocated, B may be NULL).  *steps = J. */
+int or_solve_basis(const or_mat* A, const double* b, const double* x0, int m, int variant,
+                   const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
+                   double* V, double* H, double* B, int* steps) {
+  or_basis bx = {V, H, B, 0};
+  int st = solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, NULL, 0, NULL, &bx);
+  *steps = bx.steps;
+  return st;
 }
 
 /* or_solve with a right SSOR(omega) preconditioner in the row order `order` (NULL: none). */
 int or_solve_pc(const or_mat* A, const double* b, const double* x0, int m, int variant,
                 const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
                 double* hist, int hist_cap, const int32_t* order, double omega) {
-  if (!order) return solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, NULL);
+  if (!order) return solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, NULL, NULL);
   or_prec pc = {order, omega, malloc(sizeof(int32_t) * A->n), malloc(sizeof(double) * A->n)};
   int st = 2;
   if (pc.pos && pc.tmp) {
     for (int64_t i = 0; i < A->n; ++i) pc.pos[order[i]] = (int32_t)i;
-    st = solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, &pc);
+    st = solve_impl(A, b, x0, m, variant, W, k, tol, max_iters, x, rep, hist, hist_cap, &pc, NULL);
   }
   free(pc.pos); free(pc.tmp);
   return st;
@@ -233,7 +301,7 @@ int or_ssor(const or_mat* A, const int32_t* order, double omega, const double* z
 
 static int solve_impl(const or_mat* A, const double* b, const double* x0, int m, int variant,
                       const double* W, int k, double tol, int max_iters, double* x, or_report* rep,
-                      double* hist, int hist_cap, const or_prec* pc) {
+                      double* hist, int hist_cap, const or_prec* pc, or_basis* bx) {
   if (variant >= 3 && variant <= 6 && W != NULL && k > 0)
     return solve_oblique(A, b, x0, m, variant == 4 || variant == 6, variant >= 5, W, k, tol, max_iters, x, rep,
                          hist, hist_cap, pc);
@@ -271,7 +339,7 @@ static int solve_impl(const or_mat* A, const double* b, const double* x0, int m,
     if (!(zn > 1e-12 * cn)) { rep->status = 1; goto out; }
     for (int i = 0; i < l; ++i) RZ[(int64_t)l * (qmax + 1) + i] = coef[i];
     RZ[(int64_t)l * (qmax + 1) + l] = zn;
-    for (int64_t i = 0; i < n; ++i) UZ[(int64_t)l * n + i] = z[i] / zn;
+    divide(n, z, zn, UZ + (int64_t)l * n);
   }
   /* start: x <- x + W R_C^{-1} U_C^T r(x)  (min over x + span W) */
   if (kk > 0) {
@@ -306,7 +374,7 @@ static int solve_impl(const or_mat* A, const double* b, const double* x0, int m,
     }
     double v0n = nrm2(n, w);
     if (!(v0n > 0.0)) break;
-    for (int64_t i = 0; i < n; ++i) V[i] = w[i] / v0n;
+    divide(n, w, v0n, V);
 
     int q = kk;   /* current image-basis size */
     for (int j = 0; j < m; ++j) {
@@ -320,22 +388,34 @@ static int solve_impl(const or_mat* A, const double* b, const double* x0, int m,
       if (!image_breakdown) {
         for (int i = 0; i < q; ++i) RZ[(int64_t)q * (qmax + 1) + i] = coef[i];
         RZ[(int64_t)q * (qmax + 1) + q] = zn;
-        for (int64_t i = 0; i < n; ++i) UZ[(int64_t)q * n + i] = z[i] / zn;
+        divide(n, z, zn, UZ + (int64_t)q * n);
         e[q] = dot(n, UZ + (int64_t)q * n, rho);
         axpy(n, -e[q], UZ + (int64_t)q * n, rho);
         ++q;
       }
       double res = nrm2(n, rho);
       /* next Krylov vector: Arnoldi (MGS2) on A (plain/augment) or on P A (deflate) */
-      if (variant == 2 && kk > 0) mgs2(n, kk, UZ, w, coef);
+      if (variant == 2 && kk > 0) {
+        mgs2(n, kk, UZ, w, coef);
+        if (bx && bx->B)
+          for (int l = 0; l < kk; ++l) bx->B[l + (int64_t)j * kk] = coef[l];
+      }
       double hn = mgs2(n, j + 1, V, w, coef);
+      if (bx) {
+        for (int i = 0; i <= j; ++i) bx->H[i + (int64_t)j * (m + 1)] = coef[i];
+        bx->H[j + 1 + (int64_t)j * (m + 1)] = hn;
+      }
       rep->iterations++;
       if (hist && rep->hist_len < hist_cap) hist[rep->hist_len++] = res / bnorm;
       int stop = (res / bnorm <= tol) || image_breakdown || !(hn > 1e-14 * beta) || j == m - 1 ||
                  rep->iterations >= max_iters;
       if (!stop) {
-        for (int64_t i = 0; i < n; ++i) V[(int64_t)(j + 1) * n + i] = w[i] / hn;
+        divide(n, w, hn, V + (int64_t)(j + 1) * n);
         continue;
+      }
+      if (bx) {  /* this cycle's basis v_0 .. v_j (a later cycle overwrites it) */
+        memcpy(bx->V, V, sizeof(double) * n * (j + 1));
+        bx->steps = j + 1;
       }
       /* coefficients over the search basis [W, v_0, ..., v_{q-kk-1}] */
       backsolve(q, RZ, qmax + 1, e, c);
@@ -364,7 +444,7 @@ int or_lsproj(const or_mat* A, const double* W, int k, double* Z, int nz) {
     double cn = nrm2(n, z);
     double zn = mgs2(n, l, UC, z, coef);
     if (!(zn > 1e-12 * cn)) { st = 1; break; }
-    for (int64_t i = 0; i < n; ++i) z[i] /= zn;
+    divide(n, z, zn, z);
   }
   if (!st)
     for (int c = 0; c < nz; ++c) mgs2(n, k, UC, Z + (int64_t)c * n, coef);
@@ -518,7 +598,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
     memcpy(w, row2 ? r : rho, sizeof(double) * n);   /* Krylov initial vector */
     double v0n = nrm2(n, w);
     if (!(v0n > 0.0)) break;
-    for (int64_t i = 0; i < n; ++i) V[i] = w[i] / v0n;
+    divide(n, w, v0n, V);
     int q = 0;
     for (int j = 0; j < m; ++j) {
       if (op_apply(A, pc, V + (int64_t)j * n, w)) { rep->status = 3; goto out; }  /* w = M_D A (M^{-1}) v_j */
@@ -530,7 +610,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
       if (!image_breakdown) {
         for (int i = 0; i < q; ++i) RZ[(int64_t)q * (m + 1) + i] = coef[i];
         RZ[(int64_t)q * (m + 1) + q] = zn;
-        for (int64_t i = 0; i < n; ++i) UZ[(int64_t)q * n + i] = z[i] / zn;
+        divide(n, z, zn, UZ + (int64_t)q * n);
         e[q] = dot(n, UZ + (int64_t)q * n, rho);
         axpy(n, -e[q], UZ + (int64_t)q * n, rho);
         ++q;
@@ -542,7 +622,7 @@ static int solve_oblique(const or_mat* A, const double* b, const double* x0, int
       int stop = (res / bnorm <= tol) || image_breakdown || !(hn > 1e-14 * beta) || j == m - 1 ||
                  rep->iterations >= max_iters;
       if (!stop) {
-        for (int64_t i = 0; i < n; ++i) V[(int64_t)(j + 1) * n + i] = w[i] / hn;
+        divide(n, w, hn, V + (int64_t)(j + 1) * n);
         continue;
       }
       backsolve(q, RZ, m + 1, e, c);
@@ -583,17 +663,14 @@ int or_svd(int64_t n, int s, const double* X, int64_t ldx, double* U, double* si
       for (int q = p + 1; q < s; ++q) {
         double* up = U + (int64_t)p * n;
         double* uq = U + (int64_t)q * n;
-        long double a = 0.0L, bb = 0.0L, g = 0.0L;
-        for (int64_t i = 0; i < n; ++i) {
-          a += (long double)up[i] * up[i];
-          bb += (long double)uq[i] * uq[i];
-          g += (long double)up[i] * uq[i];
-        }
+        long double a, bb, g;
+        dot3_ld(n, up, uq, &a, &bb, &g);
         if (g == 0.0L) continue;
         if (fabsl(g) <= 1e-15L * sqrtl(a * bb)) continue;
         long double zeta = (bb - a) / (2.0L * g);
         long double t = (zeta >= 0 ? 1.0L : -1.0L) / (fabsl(zeta) + sqrtl(1.0L + zeta * zeta));
         long double cs = 1.0L / sqrtl(1.0L + t * t), sn = cs * t;
+#pragma omp parallel for schedule(static) if (n >= OR_PAR_MIN)
         for (int64_t i = 0; i < n; ++i) {
           long double xp = up[i], xq = uq[i];
           up[i] = (double)(cs * xp - sn * xq);
@@ -607,8 +684,8 @@ int or_svd(int64_t n, int s, const double* X, int64_t ldx, double* U, double* si
   int* perm = malloc(sizeof(int) * s);
   double* nr = malloc(sizeof(double) * s);
   for (int j = 0; j < s; ++j) {
-    long double t = 0.0L;
-    for (int64_t i = 0; i < n; ++i) t += (long double)U[(int64_t)j * n + i] * U[(int64_t)j * n + i];
+    long double t, t2, t3;
+    dot3_ld(n, U + (int64_t)j * n, U + (int64_t)j * n, &t, &t2, &t3);
     nr[j] = (double)sqrtl(t);
     perm[j] = j;
   }
@@ -623,8 +700,8 @@ int or_svd(int64_t n, int s, const double* X, int64_t ldx, double* U, double* si
   for (int a = 0; a < s; ++a) {
     double sg = nr[perm[a]];
     sigma[a] = sg;
-    for (int64_t i = 0; i < n; ++i)
-      U[(int64_t)a * n + i] = sg > 0.0 ? tmpU[(int64_t)perm[a] * n + i] / sg : 0.0;
+    if (sg > 0.0) divide(n, tmpU + (int64_t)perm[a] * n, sg, U + (int64_t)a * n);
+    else memset(U + (int64_t)a * n, 0, sizeof(double) * n);
   }
   int rk = 0;
   for (int a = 0; a < s; ++a)
