@@ -203,7 +203,7 @@ class ClockSampler:
 class GpuRun:
     """One replica: the library context plus the device-side sequence generator."""
 
-    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None, sync_build=False):
+    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None, sync_build=False, flags=0):
         import torch
 
         import synth
@@ -217,7 +217,7 @@ class GpuRun:
         self.x = torch.zeros(cfg.n, dtype=torch.float64, device=device)
         self.x.copy_(u0)
         self.gen.fill(1, self.x)
-        flags = rg.RG_FLAG_PROFILE if profile else 0
+        flags = flags | (rg.RG_FLAG_PROFILE if profile else 0)
         self.ctx = Context(cfg.n, self.gen.row_ptr, self.gen.col_idx, self.gen.val,
                            fmt="bsr" if cfg.kind == "bsr" else "csr", block=cfg.B if cfg.kind == "bsr" else 1,
                            sell_C=32 if sell else 0, max_m=cfg.m, max_snapshots=cfg.s,

@@ -115,6 +115,10 @@ typedef struct {
                               delayed CGS2 (1 reduction per step); same iterates in exact arithmetic */
 #define RG_FLAG_NO_PERSIST 8 /* never use the single cooperative-kernel solve (any variant, CSR/SELL,
                                 m <= 64, k <= 64, n_pad <= 1.6M); always use the CUDA-graph path */
+#define RG_FLAG_KEEP_BASIS 16 /* keep the Krylov basis V, the Hessenberg matrix H-bar and (deflate) the GCRO
+                                 matrix B of the last finished restart cycle of every solve, for
+                                 rg_export(RG_EXPORT_V / _H / _B): one more n x (max_m + 1) device buffer and
+                                 a copy of V at every cycle end (inspection and tests only) */
 
 /* Solve report (fields follow SPEC.md's SolveReport).
  *   iterations   Arnoldi steps summed over restart cycles (residual and C = AW products are
@@ -214,15 +218,29 @@ RG_API rg_status rg_apply_preconditioner(rg_ctx* ctx, const double* x, double* y
 /* y = A x with the context's current matrix (x, y length n in `mem`). */
 RG_API rg_status rg_apply(rg_ctx* ctx, const double* x, double* y, rg_mem mem);
 
-/* Copy out internal recycle quantities (for inspection and tests):
+/* Copy out internal quantities (for inspection and tests):
  *   RG_EXPORT_W   W   (n x k_eff, column-major, leading dimension n)
  *   RG_EXPORT_Q   Q   (n x k_eff) orthonormal basis of A W       (after a recycled solve)
  *   RG_EXPORT_RC  R_C (k_eff x k_eff, column-major, upper triangular, A W = Q R_C)
- * `out` must hold the stated number of doubles; returns RG_E_STATE if the item is unavailable. */
+ *   *count receives k_eff for these three.
+ * Krylov basis of the LAST finished restart cycle of the last rg_solve (context created with
+ * RG_FLAG_KEEP_BASIS; variants plain / augment / deflate; "orthogonal basis of the
+ * Krylov space", :169 the Arnoldi relation behind the iterate, :332 the GCRO relation).  With J
+ * Arnoldi steps in that cycle (*count receives J):
+ *   RG_EXPORT_V   V = [v_0 .. v_{J-1}]   (n x J, column-major, orthonormal)
+ *   RG_EXPORT_H   H-bar                  ((J+1) x J, column-major, upper Hessenberg)
+ *   RG_EXPORT_B   B = Q^T A V            (k_eff x J, column-major; deflate only)
+ *   so that A V = V_{J+1} H-bar (plain, augment: Arnoldi on A) and A V = Q B + V_{J+1} H-bar (deflate:
+ *   Arnoldi on P A, P = I - Q Q^T), v_J being the next (not exported) basis vector.
+ * out == NULL only reports *count.  `out` must hold the stated number of doubles; returns
+ * RG_E_STATE if the item is unavailable (not built, no finished cycle, flag not set). */
 #define RG_EXPORT_W 0
 #define RG_EXPORT_Q 1
 #define RG_EXPORT_RC 2
-RG_API rg_status rg_export(rg_ctx* ctx, int32_t which, double* out, rg_mem mem, int32_t* k_eff);
+#define RG_EXPORT_V 3
+#define RG_EXPORT_H 4
+#define RG_EXPORT_B 5
+RG_API rg_status rg_export(rg_ctx* ctx, int32_t which, double* out, rg_mem mem, int32_t* count);
 
 /* Per-kernel device-time statistics recorded while RG_FLAG_PROFILE is set. */
 typedef struct {

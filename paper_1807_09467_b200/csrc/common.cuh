@@ -61,6 +61,7 @@ struct DevState {
   int bzero;
   int dcgs;       // 1: delayed CGS2 (one reduction per Arnoldi step), 0: classical CGS2
   int cfail;      // set by the C = A W build of this solve: singular CholQR2 factor / R_C / E
+  int kb_steps;   // RG_FLAG_KEEP_BASIS: Arnoldi steps J of the last finished cycle kept for rg_export
   double bnorm, beta, relres;
   double k2_inv_nu, k2_u_next, k2_y;  // DCGS2 update-pass scalars (v_j = u/nu + ..., u_next = ...)
   // least-squares state
@@ -103,6 +104,7 @@ struct Layout {
   int prec;        // right preconditioner active (precond.cu): cycle end adds pz = M^{-1} (V y)
   double* pz;      // preconditioner output (M^{-1} u of the Arnoldi step, M^{-1} V y at the cycle end)
   double* pt;      // cycle-end scratch: V y
+  double* keepV;   // RG_FLAG_KEEP_BASIS: n_pad x (max_m + 1) copy of the last finished cycle's V (else null)
 };
 
 // Galerkin-start variants (oblique, orthogonal): C = A W in columns [k, 2k), E^{-1} in the state.
@@ -254,6 +256,14 @@ __device__ __forceinline__ bool grid_last(unsigned* counter) {
   if (s_t != gridDim.x - 1) return false;
   if (threadIdx.x == 0) *counter = 0u;
   return true;
+}
+
+// Function attributes and occupancy results are per device: launchers cache them per ordinal.
+constexpr int MAXDEV = 64;
+inline int current_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXDEV) { cudaGetLastError(); d = 0; }
+  return d;
 }
 
 inline int vec_grid(int64_t rows) {

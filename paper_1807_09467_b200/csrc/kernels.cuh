@@ -56,6 +56,8 @@ enum OrthOp {
 cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond = 0);
 // DCGS2 Arnoldi step (dcgs.cu): phase 1 = dots + epilogue (sets the WHILE condition), 2 = update
 cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond = 0);
+// RG_FLAG_KEEP_BASIS: copy the finished cycle's V into L.keepV at the cycle end (before the x update)
+cudaError_t launch_keep_basis(const Layout& L, DevState* st, cudaStream_t s);
 // WHILE-node condition from the state: which 0 -> active, 1 -> !done
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s);
 

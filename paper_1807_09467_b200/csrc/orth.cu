@@ -319,7 +319,27 @@ __global__ void __launch_bounds__(CT, 2) k_cgs(Layout L, DevState* st, unsigned 
   if (threadIdx.x == 0) prof_end(st, kid, 8.0 * (double)L.n * (p + (UPD ? 2.0 : 1.0)));
 }
 
+// RG_FLAG_KEEP_BASIS, cycle end: v_0 .. v_jfinal (normalised: v_i = sc_i * raw_i) into L.keepV, the
+// step count into st->kb_steps.  H-bar and B of the cycle stay in st->Hraw / st->Bm (epi_ls).
+__global__ void __launch_bounds__(OT) k_keep_basis(Layout L, DevState* st) {
+  if (!st->have_xupd) return;
+  const int J = st->jfinal + 1;
+  const int64_t ld = L.ld;
+  for (int i = 0; i < J; ++i) {
+    const double s = st->sc[L.VB + i];
+    const double* src = L.Z + (int64_t)(L.VB + i) * ld;
+    double* dst = L.keepV + (int64_t)i * ld;
+    for (int64_t r = (int64_t)blockIdx.x * OT + threadIdx.x; r < ld; r += (int64_t)gridDim.x * OT) dst[r] = s * src[r];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->kb_steps = J;
+}
+
 }  // namespace
+
+cudaError_t launch_keep_basis(const Layout& L, DevState* st, cudaStream_t s) {
+  k_keep_basis<<<vec_grid(L.ld), OT, 0, s>>>(L, st);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cudaStream_t s) {
   k_cond<<<1, 32, 0, s>>>(const_cast<DevState*>(st), (cudaGraphConditionalHandle)h, which);

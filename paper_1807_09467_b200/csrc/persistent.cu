@@ -27,6 +27,7 @@ constexpr int PCTA = 1024 / PT;  // resident CTAs per SM
 constexpr int PM = 64;        // max restart length on this path
 constexpr int PK = 64;        // max recycle dimension on this path
 constexpr int PCOL = PK + PM + 2;
+constexpr int NPFN = 10;      // k_solve_persistent instantiations (launch_persistent's table)
 constexpr int CBK = 16;       // max recycle dimension of the one-kernel operator build (k (k+1) / 2 <= MAXRED)
 
 struct PArgs {
@@ -324,7 +325,9 @@ __device__ __forceinline__ void ptick(DevState* st, int kid, unsigned long long&
 // C2 deflate +1.7 %).
 // PTT: threads per CTA — RG_PT (512, 2 CTAs/SM) for multi-CTA solves, 1024 for single-CTA (tiny)
 // solves, where one CTA holds the whole problem (C1: 0.80 -> 0.74 ms/system measured)
-template <int VK, int PTT>
+// KEEP: RG_FLAG_KEEP_BASIS (plain / deflate / augment only) — the cycle end also keeps the finished
+// cycle's basis for rg_export; a separate instantiation so the default kernels are untouched.
+template <int VK, int PTT, bool KEEP = false>
 __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) {
   constexpr int PT = PTT;  // shadows the namespace-scope default inside this kernel
   extern __shared__ double sm[];
@@ -914,6 +917,18 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
       ptick(st, K_PB5, tph);
     }
     // ================= cycle end: y = R^{-1} g, x += V y - W R_C^{-1} B y (own rows)
+    if constexpr (KEEP) {  // RG_FLAG_KEEP_BASIS: this cycle's V (own rows), H-bar and B (CTA 0) for rg_export
+      if (jf >= 0) {
+        for (int i = 0; i <= jf; ++i)
+          for (int64_t r = r0 + tid; r < r1; r += PT) L.keepV[(int64_t)i * ld + r] = Z[(int64_t)(VB + i) * ld + r];
+        if (cta0) {
+          for (int e = tid; e < (jf + 1) * (m + 2); e += PT) st->Hraw[e / (m + 2)][e % (m + 2)] = e % (m + 2) <= e / (m + 2) + 1 ? Hs[e] : 0.0;
+          if (!aug)
+            for (int e = tid; e < (jf + 1) * k; e += PT) st->Bm[e / k][e % k] = Bs[e];
+          if (tid == 0) st->kb_steps = jf + 1;
+        }
+      }
+    }
     if (jf >= 0) {
       if (tid == 0) {
         for (int i = jf; i >= 0; --i) {
@@ -1278,11 +1293,16 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   static const bool no1024 = getenv("RG_NO_PT1024") != nullptr;
   const bool single = L.ld <= 8 * PT;
   const int pt = (single && !no1024) ? 1024 : PT, pcta = 1024 / pt;
-  const int vi = vk + (pt == 1024 ? 3 : 0);
-  static const void* fns[6] = {(const void*)k_solve_persistent<0, PT>, (const void*)k_solve_persistent<1, PT>,
-                               (const void*)k_solve_persistent<2, PT>, (const void*)k_solve_persistent<0, 1024>,
-                               (const void*)k_solve_persistent<1, 1024>, (const void*)k_solve_persistent<2, 1024>};
+  if (L.keepV && vk == 1) return cudaErrorNotSupported;  // no basis export for oblique / orthogonal here
+  const int vi = L.keepV ? 6 + (vk == 2 ? 1 : 0) + (pt == 1024 ? 2 : 0) : vk + (pt == 1024 ? 3 : 0);
+  static const void* fns[NPFN] = {
+      (const void*)k_solve_persistent<0, PT>,         (const void*)k_solve_persistent<1, PT>,
+      (const void*)k_solve_persistent<2, PT>,         (const void*)k_solve_persistent<0, 1024>,
+      (const void*)k_solve_persistent<1, 1024>,       (const void*)k_solve_persistent<2, 1024>,
+      (const void*)k_solve_persistent<0, PT, true>,   (const void*)k_solve_persistent<2, PT, true>,
+      (const void*)k_solve_persistent<0, 1024, true>, (const void*)k_solve_persistent<2, 1024, true>};
   const void* fn = fns[vi];
+  const int dev = current_device();
   const size_t smem0 = persistent_smem(m, k, aug, pt);
   // CSR pattern cache: what keeps pcta CTAs per SM resident (228 KB per SM, 1 KB per CTA reserved,
   // ~1 KB static), sized for this CTA count's rows and ~1.5x its share of the entries
@@ -1298,26 +1318,28 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
     }
   }
   const size_t smem = smem0 + sizeof(int32_t) * (size_t)(rcap + ccap);
-  static int max_smem = -1;
-  if (max_smem < 0) {
+  // function attributes and occupancy are per device: cached per device ordinal
+  static bool attr_set[MAXDEV] = {};
+  constexpr size_t max_smem = 200 * 1024;
+  if (!attr_set[dev]) {
     for (const void* f : fns) {
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_smem);
       cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     }
-    max_smem = 200 * 1024;
+    attr_set[dev] = true;
   }
-  if (smem > (size_t)max_smem) return cudaErrorNotSupported;
-  static size_t occ_smem[6] = {0, 0, 0, 0, 0, 0};  // occupancy per instantiation and shared-memory size
-  static int occ_last[6] = {0, 0, 0, 0, 0, 0};
-  if (occ_smem[vi] != smem) {
-    occ_last[vi] = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last[vi], fn, pt, smem) != cudaSuccess) {
+  if (smem > max_smem) return cudaErrorNotSupported;
+  static size_t occ_smem[MAXDEV][NPFN] = {};  // occupancy per device, instantiation and shared-memory size
+  static int occ_last[MAXDEV][NPFN] = {};
+  if (occ_smem[dev][vi] != smem) {
+    occ_last[dev][vi] = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_last[dev][vi], fn, pt, smem) != cudaSuccess) {
       cudaGetLastError();
-      occ_last[vi] = 0;
+      occ_last[dev][vi] = 0;
     }
-    occ_smem[vi] = smem;
+    occ_smem[dev][vi] = smem;
   }
-  const int occ = occ_last[vi];
+  const int occ = occ_last[dev][vi];
   if (occ < 1) return cudaErrorNotSupported;
   int64_t want = single ? 1 : (L.ld + pt - 1) / pt;
   static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : PCTA;
@@ -1346,17 +1368,21 @@ cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double
   const int nch = (k + 7) / 8;
   const void* fn = nch == 1 ? (const void*)k_cbuild<8> : (const void*)k_cbuild<16>;
   const size_t smem = sizeof(double) * ((size_t)8 * nch * PT + 4 * CBK * CBK + 2 * MAXRED);
-  static int occ[3] = {-1, -1, -1};
-  if (occ[nch] < 0) {
+  static int occ_dev[MAXDEV][3] = {};  // 0: not yet queried on that device, else occupancy + 1
+  int& oc = occ_dev[current_device()][nch];
+  if (oc == 0) {
+    int o = 0;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[nch], fn, PT, smem) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, PT, smem) != cudaSuccess) {
       cudaGetLastError();
-      occ[nch] = 0;
+      o = 0;
     }
+    oc = o + 1;
   }
-  if (occ[nch] < 1) return cudaErrorNotSupported;
+  const int occ = oc - 1;
+  if (occ < 1) return cudaErrorNotSupported;
   const int64_t want = L.ld <= 8 * PT ? 1 : (L.ld + PT - 1) / PT;
-  const int64_t cap = (int64_t)NSM * (occ[nch] >= PCTA ? PCTA : occ[nch]);
+  const int64_t cap = (int64_t)NSM * (occ >= PCTA ? PCTA : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
   PArgs pa{};
   pa.L = L;

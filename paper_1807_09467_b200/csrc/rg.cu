@@ -125,6 +125,8 @@ struct rg_ctx {
   double* pz = nullptr;
   double* pt = nullptr;
   bool use_persist = true;  // one cooperative kernel per solve where supported (persistent.cu)
+  double* keepV = nullptr;  // RG_FLAG_KEEP_BASIS: last finished cycle's V (n_pad x (max_m + 1))
+  int kb_var = 0, kb_k = 0; // variant / k_eff of the solve whose basis keepV holds
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -417,6 +419,7 @@ cudaError_t cycle_end(rg_ctx* c) {
     if ((e = launch_orth(c->L, c->st, OP_VY, c->stream)) != cudaSuccess) return e;
     if ((e = launch_ssor(c->P, c->L, c->st, c->pt, c->pz, 2, c->stream)) != cudaSuccess) return e;
   }
+  if (c->keepV && (e = launch_keep_basis(c->L, c->st, c->stream)) != cudaSuccess) return e;
   return launch_orth(c->L, c->st, OP_XUPD, c->stream);
 }
 
@@ -557,7 +560,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
   cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar); cudaFree(c->pflags); cudaFree(c->llw);
   drop_preconditioner(c);
-  cudaFree(c->pz); cudaFree(c->pt);
+  cudaFree(c->pz); cudaFree(c->pt); cudaFree(c->keepV);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->hhist) cudaFreeHost(c->hhist);
   if (c->hflag) cudaFreeHost(c->hflag);
@@ -615,7 +618,8 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
       (s = dalloc(&c->tot_g, (size_t)MAXRED, "totals")) != RG_OK || (s = dalloc(&c->gbar, (size_t)BAR_WORDS, "barrier")) != RG_OK ||
       (s = dalloc(&c->pflags, (size_t)NSM * 16, "sync flags")) != RG_OK ||
       (s = dalloc(&c->llw, ll_words(), "reduction words")) != RG_OK ||
-      (s = dalloc(&c->st, 1, "state")) != RG_OK) {
+      (s = dalloc(&c->st, 1, "state")) != RG_OK ||
+      ((c->flags & RG_FLAG_KEEP_BASIS) && (s = dalloc(&c->keepV, np * (c->max_m + 1), "kept basis")) != RG_OK)) {
     rg_destroy(c);
     return s;
   }
@@ -664,6 +668,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   c->L.hist = c->hist;
   c->L.partial = c->partial;
   c->L.counter = c->counter;
+  c->L.keepV = c->keepV;
   c->L.cgs_ok = (c->max_k + c->max_m + 1) <= 128 && !getenv("RG_NO_CGS");
   c->L.keep_l2 = (double)c->npad * 8.0 * (2 * c->max_k + c->max_m + 1) <= 160e6;  // ~L2-sized (126 MB)
 
@@ -906,6 +911,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     check_c = true;
   }
   c->cur_var = eff;
+  c->kb_var = eff;
+  c->kb_k = k;
   c->L.prec = c->prec_kind ? 1 : 0;
   // Measured on B200: the single cooperative kernel wins while kernel-boundary
   // latency dominates (C1 -32%, C2 -16%, C3 -9% per system); at n = 2M rows (C4) its two-barrier
@@ -1197,8 +1204,35 @@ RG_API rg_status rg_apply_preconditioner(rg_ctx* c, const double* x, double* y, 
 }
 
 RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, int32_t* k_eff) {
-  if (!c || !out) return fail(RG_E_INVAL, "NULL argument");
+  if (!c) return fail(RG_E_INVAL, "NULL argument");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
+  if (which == RG_EXPORT_V || which == RG_EXPORT_H || which == RG_EXPORT_B) {
+    if (!c->keepV) return fail(RG_E_STATE, "basis export needs a context created with RG_FLAG_KEEP_BASIS");
+    if (galerkin_variant(c->kb_var)) return fail(RG_E_STATE, "basis export covers plain / augment / deflate solves");
+    int J = 0;
+    CK(cudaMemcpyAsync(&c->hst->kb_steps, &c->st->kb_steps, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    J = c->hst->kb_steps;
+    if (J < 1) return fail(RG_E_STATE, "no finished restart cycle to export");
+    const int kb = c->kb_var == RG_DEFLATE ? c->kb_k : 0;
+    if (which == RG_EXPORT_B && kb == 0) return fail(RG_E_STATE, "B exists for deflate solves with k_eff > 0 only");
+    if (k_eff) *k_eff = J;
+    if (!out) return RG_OK;
+    const cudaMemcpyKind kind = mem == RG_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (which == RG_EXPORT_V) {
+      CK(cudaMemcpy2DAsync(out, sizeof(double) * c->n, c->keepV, sizeof(double) * c->npad, sizeof(double) * c->n, J,
+                           kind, c->stream));
+    } else if (which == RG_EXPORT_H) {  // state column j holds rows 0..j+1 of H-bar column j
+      CK(cudaMemcpy2DAsync(out, sizeof(double) * (J + 1), &c->st->Hraw[0][0], sizeof(double) * (MAXM + 2),
+                           sizeof(double) * (J + 1), J, kind, c->stream));
+    } else {
+      CK(cudaMemcpy2DAsync(out, sizeof(double) * kb, &c->st->Bm[0][0], sizeof(double) * MAXK, sizeof(double) * kb, J,
+                           kind, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return RG_OK;
+  }
+  if (!out) return fail(RG_E_INVAL, "NULL argument");
   if (rg_status r0 = resolve_build(c)) return r0;
   const int k = c->have_W ? c->k_eff : 0;
   if (k_eff) *k_eff = k;

@@ -19,8 +19,8 @@ RG_OK, RG_E_INVAL, RG_E_NOMEM, RG_E_CUDA, RG_E_STATE, RG_E_SINGULAR, RG_E_NUMERI
 RG_CSR, RG_BSR = 0, 1
 RG_PLAIN, RG_AUGMENT, RG_DEFLATE, RG_OBLIQUE, RG_ORTHOGONAL = 0, 1, 2, 3, 4
 RG_HOST, RG_DEVICE = 0, 1
-RG_FLAG_NO_GRAPH, RG_FLAG_PROFILE, RG_FLAG_CGS2, RG_FLAG_NO_PERSIST = 1, 2, 4, 8
-RG_EXPORT_W, RG_EXPORT_Q, RG_EXPORT_RC = 0, 1, 2
+RG_FLAG_NO_GRAPH, RG_FLAG_PROFILE, RG_FLAG_CGS2, RG_FLAG_NO_PERSIST, RG_FLAG_KEEP_BASIS = 1, 2, 4, 8, 16
+RG_EXPORT_W, RG_EXPORT_Q, RG_EXPORT_RC, RG_EXPORT_V, RG_EXPORT_H, RG_EXPORT_B = 0, 1, 2, 3, 4, 5
 RG_MODES_LARGEST, RG_MODES_SMALLEST = 0, 1
 RG_PREC_NONE, RG_PREC_SSOR = 0, 1
 PRECS = {None: RG_PREC_NONE, "none": RG_PREC_NONE, "ssor": RG_PREC_SSOR}
@@ -105,22 +105,50 @@ def _check(st):
         raise RgError(st, _lib.rg_last_error().decode())
 
 
-def _ptr(a):
-    """(pointer, mem) of a numpy array or torch tensor (None -> (None, None))."""
+_CTX_N = {}  # context handle -> n (argument checks only)
+
+_DT_NAMES = {np.float64: ("float64", "torch.float64"), np.int32: ("int32", "torch.int32")}
+
+
+def _ptr(a, dtype=np.float64, min_len=None, name="array"):
+    """(pointer, mem) of a numpy array or torch tensor (None -> (None, None)).
+
+    Checks what the C ABI cannot: element type (float64 values, int32 indices), contiguity and,
+    when min_len is given, that at least min_len elements are there (the library reads or writes
+    that many through the raw pointer)."""
     if a is None:
         return None, None
+    np_name, torch_name = _DT_NAMES[dtype]
     if isinstance(a, np.ndarray):
+        if a.dtype != np.dtype(dtype):
+            raise TypeError(f"{name}: dtype {a.dtype}, expected {np_name}")
         if not a.flags.c_contiguous:
-            raise ValueError("arrays must be contiguous")
+            raise ValueError(f"{name}: arrays must be contiguous")
+        if min_len is not None and a.size < min_len:
+            raise ValueError(f"{name}: {a.size} elements, at least {min_len} needed")
         return a.ctypes.data, RG_HOST
     # torch tensor
+    if str(a.dtype) != torch_name:
+        raise TypeError(f"{name}: dtype {a.dtype}, expected {torch_name}")
     if not a.is_contiguous():
-        raise ValueError("tensors must be contiguous")
+        raise ValueError(f"{name}: tensors must be contiguous")
+    if min_len is not None and a.numel() < min_len:
+        raise ValueError(f"{name}: {a.numel()} elements, at least {min_len} needed")
     return a.data_ptr(), (RG_DEVICE if a.is_cuda else RG_HOST)
 
 
+def _n(ctx):
+    return _CTX_N.get(ctx.value if hasattr(ctx, "value") else ctx)
+
+
+def _mem(a):
+    if isinstance(a, np.ndarray):
+        return RG_HOST
+    return RG_DEVICE if a.is_cuda else RG_HOST
+
+
 def _mem_of(*arrays):
-    mems = {m for _, m in (_ptr(a) for a in arrays if a is not None)}
+    mems = {_mem(a) for a in arrays if a is not None}
     if len(mems) > 1:
         raise ValueError("all arrays of one call must live in the same memory (host or device)")
     return mems.pop() if mems else RG_HOST
@@ -135,11 +163,13 @@ def make_matrix(n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, keep=Non
         keep.extend(arrs)
     if fmt == "bsr":
         nnz = int(col_idx.shape[0]) if col_idx is not None else int(val.shape[0]) // (block * block)
+        nrows, vlen = int(n) // int(block), nnz * int(block) * int(block)
     else:
         nnz = int(val.shape[0])
-    rp, _ = _ptr(row_ptr)
-    ci, _ = _ptr(col_idx)
-    v, _ = _ptr(val)
+        nrows, vlen = int(n), nnz
+    rp, _ = _ptr(row_ptr, np.int32, nrows + 1, "row_ptr")
+    ci, _ = _ptr(col_idx, np.int32, nnz, "col_idx")
+    v, _ = _ptr(val, np.float64, vlen, "val")
     return rg_matrix(RG_BSR if fmt == "bsr" else RG_CSR, int(n), nnz, int(block), rp, ci, v, mem, int(sell_C), 1)
 
 
@@ -147,6 +177,7 @@ def rg_create(n, A: rg_matrix, max_m=64, max_snapshots=32, max_k=32, stream=None
     ctx = ctypes.c_void_p()
     opt = rg_options(int(max_m), int(max_snapshots), int(max_k), stream, int(flags))
     _check(_lib.rg_create(ctypes.byref(ctx), int(n), ctypes.byref(A), ctypes.byref(opt)))
+    _CTX_N[ctx.value] = int(n)
     return ctx
 
 
@@ -171,7 +202,7 @@ def rg_update_values_inplace(ctx, n, nnz, fmt="csr", block=1, sell_C=0):
 
 
 def rg_push_snapshot(ctx, x):
-    p, mem = _ptr(x)
+    p, mem = _ptr(x, np.float64, _n(ctx), "x")
     _check(_lib.rg_push_snapshot(ctx, p, mem))
 
 
@@ -201,9 +232,10 @@ def rg_build_recycle_modes(ctx, k, modes="largest", n_snapshots=64):
 def rg_solve(ctx, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=20000, history_cap=0):
     v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
     mem = _mem_of(b, x_out, x0)
-    pb, _ = _ptr(b)
-    px, _ = _ptr(x_out)
-    p0, _ = _ptr(x0)
+    n = _n(ctx)
+    pb, _ = _ptr(b, np.float64, n, "b")
+    px, _ = _ptr(x_out, np.float64, n, "x_out")
+    p0, _ = _ptr(x0, np.float64, n, "x0")
     hist = np.zeros(max(history_cap, 1))
     rep = rg_report()
     _check(_lib.rg_solve(ctx, pb, p0, int(m), v, float(tol), int(max_iters), px, mem,
@@ -215,27 +247,31 @@ def rg_solve(ctx, b, x_out, x0=None, m=30, variant="plain", tol=1e-8, max_iters=
 
 def rg_apply(ctx, x, y):
     mem = _mem_of(x, y)
-    _check(_lib.rg_apply(ctx, _ptr(x)[0], _ptr(y)[0], mem))
+    n = _n(ctx)
+    _check(_lib.rg_apply(ctx, _ptr(x, np.float64, n, "x")[0], _ptr(y, np.float64, n, "y")[0], mem))
 
 
 def rg_set_preconditioner(ctx, kind="ssor", omega=1.0, colors=None):
     """colors: None (library greedy colouring) or an int32 array / tensor of length n."""
     kd = PRECS[kind] if (kind is None or isinstance(kind, str)) else int(kind)
     nc = ctypes.c_int32(0)
-    p, mem = _ptr(colors)
+    p, mem = _ptr(colors, np.int32, _n(ctx), "colors")
     _check(_lib.rg_set_preconditioner(ctx, kd, float(omega), p, RG_HOST if mem is None else mem, ctypes.byref(nc)))
     return nc.value
 
 
 def rg_apply_preconditioner(ctx, x, y):
     mem = _mem_of(x, y)
-    _check(_lib.rg_apply_preconditioner(ctx, _ptr(x)[0], _ptr(y)[0], mem))
+    n = _n(ctx)
+    _check(_lib.rg_apply_preconditioner(ctx, _ptr(x, np.float64, n, "x")[0], _ptr(y, np.float64, n, "y")[0], mem))
 
 
 def rg_export(ctx, which, out):
+    """Copy an internal item into `out` (None: only return the count: k_eff for W / Q / R_C, the
+    number of Arnoldi steps J for V / H / B).  The caller sizes `out` (include/rg.h)."""
     ke = ctypes.c_int32(0)
-    p, mem = _ptr(out)
-    _check(_lib.rg_export(ctx, int(which), p, mem, ctypes.byref(ke)))
+    p, mem = _ptr(out, np.float64, None, "out")
+    _check(_lib.rg_export(ctx, int(which), p, RG_HOST if mem is None else mem, ctypes.byref(ke)))
     return ke.value
 
 
@@ -253,6 +289,7 @@ def rg_reset_kernel_stats(ctx):
 
 
 def rg_destroy(ctx):
+    _CTX_N.pop(ctx.value if hasattr(ctx, "value") else ctx, None)
     _lib.rg_destroy(ctx)
 
 

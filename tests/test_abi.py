@@ -56,7 +56,8 @@ def test_create_rejects_invalid_arguments_without_device():
     with pytest.raises(rg.RgError) as e:
         rg.rg_create(2, good, max_k=65)
     assert e.value.status == rg.RG_E_INVAL
-    bad = rg.make_matrix(3, rp, ci, v)      # n_rows mismatch
+    # n_rows mismatch (descriptor built by hand: make_matrix itself refuses the short row_ptr)
+    bad = rg.rg_matrix(rg.RG_CSR, 3, 2, 1, rp.ctypes.data, ci.ctypes.data, v.ctypes.data, rg.RG_HOST, 0, 1)
     with pytest.raises(rg.RgError) as e:
         rg.rg_create(2, bad)
     assert e.value.status == rg.RG_E_INVAL
@@ -78,3 +79,30 @@ def test_oracle_library_is_separate():
     olib = os.path.join(ROOT, "oracle", "liboracle.so")
     dep = subprocess.run(["ldd", olib], capture_output=True, text=True).stdout
     assert "cuda" not in dep
+
+
+def test_binding_checks_dtype_and_length():
+    """The binding refuses buffers the C ABI would read or write past (float32 / short
+    vectors, int64 index arrays)."""
+    from paper_1807_09467_b200 import rg
+    rp = np.array([0, 1, 2], np.int32)
+    ci = np.array([0, 1], np.int32)
+    v = np.array([1.0, 1.0])
+    with pytest.raises(ValueError):
+        rg.make_matrix(3, rp, ci, v)                      # row_ptr shorter than n + 1
+    with pytest.raises(TypeError):
+        rg.make_matrix(2, rp.astype(np.int64), ci, v)     # int64 indices
+    with pytest.raises(TypeError):
+        rg.make_matrix(2, rp, ci, v.astype(np.float32))   # float32 values
+    with pytest.raises(ValueError):
+        rg.make_matrix(2, rp, ci[:1], v)                  # col_idx shorter than nnz
+    rg._CTX_N[12345] = 10
+    try:
+        with pytest.raises(TypeError):
+            rg.rg_solve(12345, np.zeros(10, np.float32), np.zeros(10))
+        with pytest.raises(ValueError):
+            rg.rg_solve(12345, np.zeros(10), np.zeros(9))
+        with pytest.raises(ValueError):
+            rg.rg_push_snapshot(12345, np.zeros(9))
+    finally:
+        rg._CTX_N.pop(12345)
