@@ -31,7 +31,7 @@ $(PKG)/lib/librg.so: $(RG_OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(RG_OBJ) -lcuda
 
 synth/libsynth.so: synth/synth.c synth/synth_common.h
-	$(CC) $(CFLAGS) -shared -o $@ synth/synth.c -lm
+	$(CC) $(CFLAGS) -fopenmp -shared -o $@ synth/synth.c -lm
 
 synth/libsynth_cuda.so: synth/synth_cuda.cu synth/synth_common.h
 	$(NVCC) $(ARCH) -O3 -lineinfo -fmad=false -Xcompiler -fPIC -shared -o $@ synth/synth_cuda.cu

@@ -230,10 +230,14 @@ class GpuRun:
         self.vals_ptr, _ = self.ctx.values_ptr()
         self.nnz = int(self.gen.col_idx.numel())
 
-    def step(self):
-        """One system t of the sequence, entirely on the device (inputs resident in HBM)."""
+    def step(self, x_prev=None, push=None, history_cap=0):
+        """One system t of the sequence, entirely on the device (inputs resident in HBM).
+        Teacher forcing (tests): x_prev (device) replaces x_{t-1} before A_t, b_t are generated, and
+        push (device) is the snapshot pushed instead of the solver's x_t."""
         cfg = self.cfg
         self.t += 1
+        if x_prev is not None:
+            self.x.copy_(x_prev)
         if cfg.kind == "9pt":                          # C3: A is the same for the whole sequence
             self.gen.fill(self.t, self.x)              # (b_t only)
         else:                                          # A_t, b_t from x_{t-1}, written straight into
@@ -244,10 +248,10 @@ class GpuRun:
                 self.k_eff, self.sigma = self.ctx.build_recycle(self.k)
             else:                                      # a3, asynchronous (a4 happens inside the solve)
                 self.ctx.build_recycle(self.k, deferred=True)
-        rep = self.ctx.solve(self.gen.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol)
+        rep = self.ctx.solve(self.gen.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol, history_cap=history_cap)
         if not rep["converged"]:
             raise RuntimeError(f"system {self.t} did not converge: {rep}")
-        self.ctx.push_snapshot(self.x)                 # a2
+        self.ctx.push_snapshot(self.x if push is None else push)   # a2
         self.nsnap += 1
         self.iters.append(rep["iterations"])
         return rep

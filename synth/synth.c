@@ -113,6 +113,7 @@ int64_t sy_c5_pattern(int E, int32_t* row_ptr, int32_t* col_idx, int8_t* kind) {
 /* C5 base values of the nnzb blocks (B x B, column-major inside a block). */
 void sy_c5_values(int64_t nnzb, int B, uint64_t seed, const int8_t* kind, double s_up, double s_dn,
                   double* val) {
+#pragma omp parallel for schedule(static)
   for (int64_t b = 0; b < nnzb; ++b)
     for (int c = 0; c < B; ++c)
       for (int r = 0; r < B; ++r)
@@ -121,16 +122,19 @@ void sy_c5_values(int64_t nnzb, int B, uint64_t seed, const int8_t* kind, double
 
 /* A_t = A_{t-1} o (1 + 0.01 xi_t), entry-wise. */
 void sy_c5_perturb(int64_t nval, uint64_t seed, int t, double* val) {
+#pragma omp parallel for schedule(static)
   for (int64_t e = 0; e < nval; ++e) val[e] = val[e] * sy_c5_factor(seed, t, e);
 }
 
 /* seeded N(0,1)-like vector (C5 right-hand side). */
 void sy_normal_vec(int64_t n, uint64_t seed, uint64_t stream, double* out) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) out[i] = sy_normal12(seed, stream, (uint64_t)i);
 }
 
 /* b = u/dt + f (implicit Euler right-hand side, PAPER.md:592-598 with the configs' forcing). */
 void sy_rhs(int64_t n, const double* u, double dt, double f, double* b) {
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) b[i] = u[i] / dt + f;
 }
 

@@ -111,3 +111,27 @@ def test_c5_perturb_device_matches_host(nval, off):
     assert C.syd_c5_perturb(nval, 1234, 3, ctypes.c_void_p(d.data_ptr() + 8 * off), None) == 0
     torch.cuda.synchronize()
     assert np.array_equal(d.cpu().numpy()[off:], ref)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,t", [("C1", 3), ("C2", 2), ("C4", 5), ("C5", 3)])
+def test_device_stencil_and_rhs_match_host_full_size(name, t):
+    """The device generator bench.py times (syd_fill5_values / syd_fill7_values / syd_rhs /
+    syd_c5_values + perturbation / syd_normal_vec) writes bit-identical A_t and b_t to the host
+    generator the oracle consumes, at the configs' FULL sizes (C2: velocity u_{t-1}(1,1) per node;
+    C1 / C4: time-dependent constant velocity; C5: base blocks and the cumulative 1 % perturbation)."""
+    torch = pytest.importorskip("torch")
+    cfg = CONFIGS[name]
+    seq = HostSequence(cfg)
+    rng = np.random.default_rng(7)
+    u = seq.initial() + 0.05 * rng.standard_normal(cfg.n)   # any x_{t-1}, signs of both kinds
+    gen = synth.DeviceSequence(cfg, "cuda")
+    ud = torch.from_numpy(u).cuda()
+    gen.fill(1, ud)
+    gen.fill(t, ud)
+    torch.cuda.synchronize()
+    A = seq.matrix(t, u)
+    assert np.array_equal(gen.row_ptr.cpu().numpy(), A.row_ptr)
+    assert np.array_equal(gen.col_idx.cpu().numpy(), A.col_idx)
+    assert np.array_equal(gen.val.cpu().numpy(), A.val)
+    assert np.array_equal(gen.b.cpu().numpy(), seq.rhs(t, u))
