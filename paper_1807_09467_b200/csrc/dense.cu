@@ -144,8 +144,15 @@ constexpr int JLD = MAXS + 1;
 // start is valid for Jacobi.  With the previous system's eigenvectors (the window changed by one
 // column) the sweep count at the 1e-14 stop is unchanged (7 at s = 20), but most pairs fall below
 // the rotation threshold early and are skipped: measured -40 us per build at C2.
+// rel != 0 (the SVD's second pass, R7): stop only when no pair has |a_pq| > 1e-15 sqrt(a_pp a_qq)
+// and rotate only such pairs — the criterion of one-sided Jacobi.  The Gram matrix of the second pass
+// is scaled diagonally dominant (nearly orthogonal columns of graded norms), so this converges in a few
+// sweeps to eigenvalues with HIGH RELATIVE accuracy; the absolute stop off(A)_F <= 1e-14 ||A||_F (pass 1)
+// would stop at sweep 0 and leave the small singular values at the ~sqrt(eps) sigma_1 level of one Gram
+// pass (measured C4 window: 4e-9 sigma_1 errors; relative stop: <= 1e-15 sigma_1).
 __global__ void __launch_bounds__(1024) k_jacobi(const double* G, int s, double* lam, double* V,
-                                                double* sigma_out, DevState* st, const double* V0, int s0) {
+                                                double* sigma_out, DevState* st, const double* V0, int s0,
+                                                int rel) {
   extern __shared__ double jsm[];
   double* A_ = jsm;                    // JLD x JLD, A(r, c) = A_[r * JLD + c]
   double* V_ = jsm + JLD * JLD;
@@ -154,6 +161,8 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* G, int s, double*
   __shared__ int perm[MAXS + 1];
   __shared__ double jred[33], jcs[MAXS / 2 + 1], jsn[MAXS / 2 + 1];
   __shared__ unsigned short jpair[MAXS * MAXS / 2];  // round-robin pairing: (p | q << 8) per (round, i)
+  __shared__ int s_rot;                                // rel: rotations in the current sweep
+  __shared__ int s_rr[MAXS];                           // per round of the sweep: some pair rotates
   const int tid = threadIdx.x, bd = blockDim.x;
   if (st) prof_begin(st, K_JACOBI);
   const int ne = s + (s & 1);  // even size (pad with a decoupled zero row/column)
@@ -201,23 +210,37 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* G, int s, double*
   double* An = B_;
   int sweep = 0;
   for (; sweep < 40; ++sweep) {
-    double off = 0.0, fro = 0.0;
-    for (int e = tid; e < ne * ne; e += bd) {
-      const int r = e / ne, c = e % ne;
-      const double v2 = Ac[(r) * JLD + (c)] * Ac[(r) * JLD + (c)];
-      fro += v2;
-      if (r != c) off += v2;
+    if (rel) {
+      if (ne < 2) break;
+      if (sweep > 0 && s_rot == 0) break;  // no pair above the relative threshold in the last sweep
+      __syncthreads();                      // everyone has read s_rot
+      if (tid == 0) s_rot = 0;
+      __syncthreads();
+    } else {
+      double off = 0.0, fro = 0.0;
+      for (int e = tid; e < ne * ne; e += bd) {
+        const int r = e / ne, c = e % ne;
+        const double v2 = Ac[(r) * JLD + (c)] * Ac[(r) * JLD + (c)];
+        fro += v2;
+        if (r != c) off += v2;
+      }
+      off = block_sum(off, jred);
+      fro = block_sum(fro, jred);
+      if (!(off > 1e-28 * fro) || ne < 2) break;  // off(A)_F <= 1e-14 ||A||_F
     }
-    off = block_sum(off, jred);
-    fro = block_sum(fro, jred);
-    if (!(off > 1e-28 * fro) || ne < 2) break;  // off(A)_F <= 1e-14 ||A||_F
+    for (int r = tid; r < ne; r += bd) s_rr[r] = 0;
+    __syncthreads();
     for (int round = 0; round < ne - 1; ++round) {
       const unsigned short* pr = jpair + round * half;
       if (tid < half) {
         const int p = pr[tid] & 0xff, q = pr[tid] >> 8;
         const double apq = Ac[(p) * JLD + (q)], app = Ac[(p) * JLD + (p)], aqq = Ac[(q) * JLD + (q)];
         double c = 1.0, sv = 0.0;
-        if (fabs(apq) > 1e-300 && apq * apq > 1e-36 * fabs(app * aqq)) {
+        const bool go = rel ? (fabs(apq) > 1e-300 && apq * apq > 1e-30 * fabs(app * aqq))
+                            : (fabs(apq) > 1e-300 && apq * apq > 1e-36 * fabs(app * aqq));
+        if (go) {
+          s_rr[round] = 1;
+          if (rel) s_rot = 1;
           // t = tan(theta) = sign(th) / (|th| + sqrt(1 + th^2)), th = (aqq - app) / (2 apq), written as
           // t = b' / d with a = aqq - app, b = 2 apq, b' = b sign(a), d = |a| + sqrt(a^2 + b^2); then
           // c = 1 / sqrt(1 + t^2) = d w and s = t c = b' w with w = 1 / sqrt(d^2 + b^2): one sqrt and
@@ -232,6 +255,7 @@ __global__ void __launch_bounds__(1024) k_jacobi(const double* G, int s, double*
         jsn[tid] = sv;
       }
       __syncthreads();
+      if (!s_rr[round]) continue;  // no pair rotates: the update would be an exact identity (c = 1, s = 0)
       for (int e = tid; e < half * half; e += bd) {
         const int i = e / half, i2 = e - i * half;
         const int p = pr[i] & 0xff, q = pr[i] >> 8, p2 = pr[i2] & 0xff, q2 = pr[i2] >> 8;
@@ -555,7 +579,7 @@ cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G
 }
 
 cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double* sigma_out,
-                          DevState* st, cudaStream_t strm, const double* V0, int s0) {
+                          DevState* st, cudaStream_t strm, const double* V0, int s0, int rel) {
   const size_t smem = sizeof(double) * 3 * JLD * JLD;
   static bool init = false;
   if (!init) {
@@ -565,7 +589,7 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
   const int half = (s + (s & 1)) / 2;  // one thread per 2x2 block of the rotation round (<= 1024)
   static const int nt_env = getenv("RG_JACOBI_NT") ? atoi(getenv("RG_JACOBI_NT")) : 0;
   const int nt = nt_env > 0 ? nt_env : std::max(64, std::min(1024, (half * half + 31) / 32 * 32));
-  k_jacobi<<<1, nt, smem, strm>>>(G, s, lam, V, sigma_out, st, s0 > 0 ? V0 : nullptr, s0);
+  k_jacobi<<<1, nt, smem, strm>>>(G, s, lam, V, sigma_out, st, s0 > 0 ? V0 : nullptr, s0, rel);
   return cudaGetLastError();
 }
 

@@ -122,8 +122,10 @@ cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G
 // Symmetric eigen-decomposition of G (s x s) by parallel cyclic Jacobi in one CTA:
 // lam (s, non-increasing), V (s x s column-major eigenvectors).  sigma_out (nullable) = sqrt(max(lam,0)).
 // V0 (nullable, s0 x s0): warm-start eigenvectors (e.g. the previous build's), s0 <= s.
+// rel != 0: relative (one-sided-Jacobi) stopping / rotation criterion |a_pq| <= 1e-15 sqrt(a_pp a_qq):
+// high relative accuracy of small eigenvalues of a scaled diagonally dominant G (the SVD's pass 2).
 cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double* sigma_out,
-                          DevState* st, cudaStream_t strm, const double* V0 = nullptr, int s0 = 0);
+                          DevState* st, cudaStream_t strm, const double* V0 = nullptr, int s0 = 0, int rel = 0);
 // Y[:, c] = colscale[c] * sum_a X[:, a] M[a, c]  (M s x q column-major, leading dim ldm; colscale nullable).
 cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const double* M, int ldm, int q,
                       const double* colscale, double* Y, int64_t ldy, DevState* st, cudaStream_t strm);

@@ -793,7 +793,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   CK(launch_xm(c->X, ld, c->n, s, V1, s, s, nullptr, c->Y, ld, c->st, st));
   // pass 2: Y^T Y (nearly diagonal, column-scaled) -> V2, sigma
   CK(launch_gram(c->Y, ld, c->n, s, G, c->partial, c->counter, c->st, st));
-  CK(launch_jacobi(G, s, lam, V2, sig, c->st, st));
+  CK(launch_jacobi(G, s, lam, V2, sig, c->st, st, nullptr, 0, 1));
   const auto t1 = now();
   double* hs = c->hsig;  // pinned
   CK(cudaMemcpyAsync(hs, sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
