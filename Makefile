@@ -7,6 +7,10 @@ CC        := gcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
              --expt-relaxed-constexpr -Iinclude
+# EXPERIMENTS=1: honour the A/B environment knobs of csrc/knobs.cuh (compiled out by default)
+ifeq ($(EXPERIMENTS),1)
+NVFLAGS   += -DRG_EXPERIMENTS
+endif
 CFLAGS    := -O2 -fPIC -std=c99 -ffp-contract=off -Wall -Wno-unused-function
 
 PKG       := paper_1807_09467_b200

@@ -313,11 +313,24 @@ def flush_l2(buf):
     buf.add_(1.0)   # 256 MiB write > 126 MB L2
 
 
-def oracle_time(cfg, variant, k, systems, budget_s=30.0, precond=None):
-    """The oracle (plain C, 1 thread) on the first `systems` systems of its own sequence
-    (precond = omega: right SSOR in the greedy multicolour order of tests/coloring.py)."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_time(cfg, variant, k, systems, budget_s=30.0, precond=None, first=1):
+    """The oracle (plain C fp64, deterministic OpenMP threads on all online cores) on its own
+    sequence: systems 1..first-1 are solved untimed (they fill the snapshot window), then systems
+    first..systems are timed until `budget_s` is spent (at least one).  precond = omega: right SSOR
+    in the greedy multicolour order of tests/coloring.py.  Returns (times, iterations, threads)."""
     import oracle
     import synth
+    oracle.set_threads(os.cpu_count() or 1)
     seq = synth.HostSequence(cfg)
     u = seq.initial()
     pc = None
@@ -337,13 +350,14 @@ def oracle_time(cfg, variant, k, systems, budget_s=30.0, precond=None):
         if variant != "plain" and X:
             W, _, _ = oracle.recycle_basis(np.stack(X[-cfg.s:], 1), k)
         r = oracle.solve(A, b, m=cfg.m, variant=variant, W=W, tol=cfg.tol, precond=pc)
-        times.append(time.perf_counter() - t0)
-        its.append(r["iterations"])
+        if t >= first:
+            times.append(time.perf_counter() - t0)
+            its.append(r["iterations"])
         u = r["x"]
         X.append(u)
-        if sum(times) > budget_s:
+        if times and sum(times) > budget_s:
             break
-    return times, its
+    return times, its, oracle.threads()
 
 
 def run_ours(args, cfg):
@@ -459,11 +473,15 @@ def run_ours(args, cfg):
                    if not kname.startswith("p_") and kname != "ssor") + gen_launches
     cpu = None
     if not args.no_cpu_baseline and ws == 1:
-        times, its = oracle_time(cfg, args.variant, k, args.cpu_systems, budget_s=args.cpu_budget,
-                                 precond=args.omega if args.precond == "ssor" else None)
-        cpu = {"value": sum(times) / len(times), "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{cfg.name} systems 1..{len(times)} of the oracle's own sequence ({args.variant}, "
-                         f"iterations {its}), plain C fp64 single thread"}
+        first = args.warmup + 1                      # the first timed system of this run
+        times, its, nth = oracle_time(cfg, args.variant, k, args.warmup + args.steps, budget_s=args.cpu_budget,
+                                      precond=args.omega if args.precond == "ssor" else None, first=first)
+        cpu = {"value": sum(times) / len(times), "unit": UNIT, "cores": nth, "kind": "oracle",
+               "cpu_model": cpu_model(), "online_cores": os.cpu_count(),
+               "sample": f"{cfg.name} systems {first}..{first + len(times) - 1} of the oracle's own sequence "
+                         f"({args.variant}, iterations {its}; the timed region's first systems, bounded to "
+                         f"~{args.cpu_budget:.0f} s; systems 1..{first - 1} solved untimed to fill the window), "
+                         f"plain C fp64, deterministic OpenMP threads"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_max / args.steps * 1e3, "higher_is_better": False, "scaling": "weak",
@@ -498,17 +516,18 @@ def run_reference(args, cfg):
         return
     k = args.k or cfg.k
     n_sys = args.warmup + args.steps
-    times, its = oracle_time(cfg, args.variant, k, n_sys, budget_s=1e9,
-                             precond=args.omega if args.precond == "ssor" else None)
-    timed = times[args.warmup:]
+    timed, its, nth = oracle_time(cfg, args.variant, k, n_sys, budget_s=1e9,
+                                  precond=args.omega if args.precond == "ssor" else None, first=args.warmup + 1)
     v = sum(timed) / len(timed)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, synth/)",
             "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.cid - 1}]", "variant": args.variant,
                        "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "iterations": its},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{cfg.name} systems {args.warmup + 1}..{n_sys} of the oracle's sequence"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nth, "kind": "oracle", "cpu_model": cpu_model(),
+                             "online_cores": os.cpu_count(),
+                             "sample": f"{cfg.name} systems {args.warmup + 1}..{n_sys} of the oracle's own sequence "
+                                       f"(1..{args.warmup} untimed), deterministic OpenMP threads"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -521,7 +540,7 @@ def main(argv=None):
                          "(C2: 47 of 50) for our arm, 3 for --impl reference")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--variant", default="deflate", choices=["plain", "augment", "deflate", "oblique", "orthogonal"])
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--precond", default="none", choices=["none", "ssor"],
@@ -535,7 +554,6 @@ def main(argv=None):
                     help="skip the plain GMRES(m) sequence timed beside the recycled one")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-systems", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
@@ -543,7 +561,7 @@ def main(argv=None):
     import synth
     cfg = synth.CONFIGS[args.config]
     if args.steps is None:
-        args.steps = 3 if args.impl == "reference" else max(1, cfg.systems - args.warmup)
+        args.steps = max(1, cfg.systems - args.warmup)
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -114,7 +114,8 @@ typedef struct {
 #define RG_FLAG_CGS2 4     /* classical CGS2 (3 reductions per Arnoldi step) instead of the default
                               delayed CGS2 (1 reduction per step); same iterates in exact arithmetic */
 #define RG_FLAG_NO_PERSIST 8 /* never use the single cooperative-kernel solve (any variant, CSR/SELL,
-                                m <= 64, k <= 64, n_pad <= 1.6M); always use the CUDA-graph path */
+                                m <= 64, k <= 64, n_pad <= 1.6M rows: the measured crossover, DESIGN.md
+                                §5.2); always use the CUDA-graph path */
 #define RG_FLAG_KEEP_BASIS 16 /* keep the Krylov basis V, the Hessenberg matrix H-bar and (deflate) the GCRO
                                  matrix B of the last finished restart cycle of every solve, for
                                  rg_export(RG_EXPORT_V / _H / _B): one more n x (max_m + 1) device buffer and
@@ -136,11 +137,20 @@ typedef struct {
   double rel_residual, ms_total;
 } rg_report;
 
-/* Create a context for systems of dimension n with initial matrix A (validated and copied). */
+/* Create a context for the sequence A_t x_t = b_t, t = 1, 2, ... of systems of dimension n
+ * (eq. sequence_linear_systems: the systems arrive one at a time), with the first
+ * matrix A = A_1 (validated and copied into device memory the library owns; the caller keeps its
+ * arrays).  *ctx receives the context (NULL on failure).  Errors: RG_E_INVAL (n < 1 or >= 2^31, max_m
+ * outside 1..128, max_snapshots outside 1..64, max_k outside 0..min(64, max_snapshots), a malformed
+ * descriptor or pattern — no side effects), RG_E_CUDA (no device), RG_E_NOMEM. */
 RG_API rg_status rg_create(rg_ctx** ctx, int64_t n, const rg_matrix* A, const rg_options* opt);
 
-/* Replace A (same n and format).  Keeps the snapshot window and W; invalidates C = A W, its QR
- * factor Q and R_C, which are rebuilt by the next recycled solve. */
+/* Replace A by the next matrix A_t of the sequence ("the sequence of matrices and
+ * right-hand sides depend on the previous solution"; same n and format).  Keeps the snapshot window
+ * and W (Algorithm 1 carries them across systems); invalidates C = A W, its QR
+ * factor Q and R_C, which are rebuilt by the next recycled solve.  row_ptr = col_idx = NULL: values
+ * only (same pattern); otherwise the pattern is validated and replaced (RG_E_INVAL, no side
+ * effects, if malformed). */
 RG_API rg_status rg_update_matrix(rg_ctx* ctx, const rg_matrix* A);
 
 /* Device pointer and length (doubles) of the library-owned matrix values (CSR order, or BSR blocks
@@ -178,7 +188,10 @@ RG_API rg_status rg_build_recycle(rg_ctx* ctx, int32_t k, int32_t* k_eff, double
 #define RG_MODES_SMALLEST 1
 RG_API rg_status rg_build_recycle_modes(rg_ctx* ctx, int32_t k, int32_t modes, int32_t* k_eff, double* sigma);
 
-/* Solve A x = b with restarted GMRES(m), variant plain / augment / deflate.
+/* Solve A x = b with restarted GMRES(m) (PAPER.md:36-38 restarts, :133-135 minimal residual,
+ * :171-175 GMRES), accelerated by the recycle space through the variant's search space (rg_variant;
+ * augmentation PAPER.md:205-217, deflation :310/:332/:348, Table 1 rows :341-348), stopping on the
+ * true relative residual ("relative residual 1e-8").
  *   b, x0      length n in `mem`; x0 == NULL means x0 = 0
  *   m          restart length, 1..max_m
  *   tol        > 0; convergence is ||b - A x||_2 / ||b||_2 <= tol on the true residual
@@ -187,7 +200,9 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* ctx, int32_t k, int32_t modes, i
  *   history    nullable HOST array receiving up to history_cap relative-residual estimates
  *   rep        nullable report
  * A recycled variant with an empty recycle space runs plain GMRES (k_eff = 0).  b = 0 gives
- * x = 0, converged, 0 iterations.  Non-convergence is RG_OK with rep->converged = 0. */
+ * x = 0, converged, 0 iterations.  Non-convergence is RG_OK with rep->converged = 0.
+ * On RG_E_SINGULAR (the recycle operator A W or E is singular; the recycle space is then cleared) the
+ * contents of x_out are undefined: call again (it then runs plain GMRES, k_eff = 0). */
 RG_API rg_status rg_solve(rg_ctx* ctx, const double* b, const double* x0, int32_t m, rg_variant v,
                           double tol, int32_t max_iters, double* x_out, rg_mem mem, double* history,
                           int32_t history_cap, rg_report* rep);

@@ -25,6 +25,7 @@
 // reduction: M_D A v_j is never formed explicitly.
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include "knobs.cuh"
 
 #include <cstdlib>
 
@@ -679,8 +680,8 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
   if (phase == 1) {
     // streaming variant by default (C4: 3.90 -> 4.54 TB/s; (SCH, RU) = (4, 2) and (6, 2) measured
     // equal, (4, 4) spills); RG_DK1_TILES=1 selects the shared-memory sub-tile kernel
-    static const int tiles = getenv("RG_DK1_TILES") ? 1 : 0;
-    static const int tma = getenv("RG_NO_TMA_DCGS") || getenv("RG_NO_TMA_DK1") ? 0 : 1;
+    static const int tiles = knob("RG_DK1_TILES") ? 1 : 0;
+    static const int tma = knob("RG_NO_TMA_DCGS") || knob("RG_NO_TMA_DK1") ? 0 : 1;
     if (tma && !tiles) {
       const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
       const size_t smem = sizeof(double) * ((size_t)TS_STG * TS_STAGE + (size_t)(TS_R / 32) * nvw);
@@ -707,7 +708,7 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
       k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
     return cudaGetLastError();
   }
-  static const int tma = getenv("RG_NO_TMA_DCGS") || getenv("RG_NO_TMA_DK2") ? 0 : 1;
+  static const int tma = knob("RG_NO_TMA_DCGS") || knob("RG_NO_TMA_DK2") ? 0 : 1;
   if (tma) {
     static bool attr = false;
     if (!attr) {

@@ -10,6 +10,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "knobs.cuh"
 
 namespace rg {
 namespace {
@@ -587,7 +588,7 @@ cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double
     init = true;
   }
   const int half = (s + (s & 1)) / 2;  // one thread per 2x2 block of the rotation round (<= 1024)
-  static const int nt_env = getenv("RG_JACOBI_NT") ? atoi(getenv("RG_JACOBI_NT")) : 0;
+  static const int nt_env = knob_int("RG_JACOBI_NT", 0);
   const int nt = nt_env > 0 ? nt_env : std::max(64, std::min(1024, (half * half + 31) / 32 * 32));
   k_jacobi<<<1, nt, smem, strm>>>(G, s, lam, V, sigma_out, st, s0 > 0 ? V0 : nullptr, s0, rel);
   return cudaGetLastError();

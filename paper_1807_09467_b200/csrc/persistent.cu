@@ -12,6 +12,7 @@
 // coefficients exactly as dcgs.cu does it (V^T C replicated in shared memory).
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include "knobs.cuh"
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -386,6 +387,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
   double* __restrict__ x = L.x;
   const double* __restrict__ b = L.b;
   double bytes = 0.0;  // algorithmic bytes (CTA 0 accounts them)
+  int spmvs = 0;       // sparse products issued (CTA 0: rg_report.spmv_count)
   const bool keep = L.keep_l2 != 0;  // basis L2-sized: cached loads (the update pass re-hits them)
   // ---- this CTA's CSR pattern into shared memory when it fits (the SpMVs then read only values and x)
   bool sc = false;
@@ -529,7 +531,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
       __syncthreads();
       if (!gred(1, nullptr)) goto fail;
       beta = sqrt(tot[0]);
-      if (cta0) bytes += A.bytes + 8.0 * L.n;
+      if (cta0) { bytes += A.bytes + 8.0 * L.n; ++spmvs; }
     }
     if (k > 0) {  // LS projection onto span(W): a = Q^T r, x += W R_C^{-1} a, r -= Q a
                   // (oblique: Galerkin start a = W^T r, t = E^{-1} a, x += W t, r -= C t)
@@ -693,7 +695,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
         pa.flags[NSM * 2 + 2 * NSM * 2 + blockIdx.x] = (unsigned)(gtimer() & 0xffffffffu);
       }
       ptick(st, K_PB3, tph);
-      if (cta0) bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + nx + 2);
+      if (cta0) { bytes += (have_y ? A.bytes : 0.0) + 8.0 * L.n * (p + nx + 2); spmvs += have_y ? 1 : 0; }
       // ---- replicated epilogue: delayed second pass, column j-1, least squares
       const double* a = tot;
       const double* bb = tot + p;
@@ -1005,6 +1007,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
     st->relres = relres;
     st->iters = iters;
     st->cycles = cycles;
+    st->spmv_count += spmvs;
     st->hist_len = hist_len;
     st->converged = converged;
     st->status = status;
@@ -1267,6 +1270,7 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
         dmin = tot[i] < dmin ? tot[i] : dmin;
       }
       if (!ok || !(dmin > 1e-12 * dmax)) *cflag = 1;
+      st->spmv_count += k;  // C = A W (rg_report.spmv_count)
       if (pa.llred) st->red_epoch = ok ? rep : rep + 16u;  // past anything a CTA may have published
       prof_end(st, K_CBUILD, A.bytes + 8.0 * (double)L.n * 6.0 * k);
     }
@@ -1290,7 +1294,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   const int vk = aug ? 2 : ((galerkin_variant(variant) && k > 0) ? 1 : 0);
   // tiny systems (<= 8 rows per thread of one 512-thread CTA) run on ONE CTA: no grid barriers at
   // all, and that CTA gets 1024 threads
-  static const bool no1024 = getenv("RG_NO_PT1024") != nullptr;
+  static const bool no1024 = knob("RG_NO_PT1024");
   const bool single = L.ld <= 8 * PT;
   const int pt = (single && !no1024) ? 1024 : PT, pcta = 1024 / pt;
   if (L.keepV && vk == 1) return cudaErrorNotSupported;  // no basis export for oblique / orthogonal here
@@ -1307,7 +1311,7 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   // CSR pattern cache: what keeps pcta CTAs per SM resident (228 KB per SM, 1 KB per CTA reserved,
   // ~1 KB static), sized for this CTA count's rows and ~1.5x its share of the entries
   int rcap = 0, ccap = 0;
-  if (A.fmt == 0 && !getenv("RG_NO_SMEM_CSR")) {
+  if (A.fmt == 0 && !knob("RG_NO_SMEM_CSR")) {
     const int64_t G0 = single ? 1 : std::min<int64_t>((int64_t)NSM * pcta, std::max<int64_t>(1, (L.ld + pt - 1) / pt));
     const int64_t rows = ((L.ld >> 5) / G0 + 2) * 32 + 1;
     const int64_t ents = A.nnz / G0 * 3 / 2 + 1024;
@@ -1342,15 +1346,15 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
   const int occ = occ_last[dev][vi];
   if (occ < 1) return cudaErrorNotSupported;
   int64_t want = single ? 1 : (L.ld + pt - 1) / pt;
-  static const int per_sm = getenv("RG_PERSIST_CTAS_PER_SM") ? atoi(getenv("RG_PERSIST_CTAS_PER_SM")) : PCTA;
+  static const int per_sm = knob_int("RG_PERSIST_CTAS_PER_SM", PCTA);
   int64_t cap = (int64_t)NSM * (occ >= per_sm ? per_sm : occ);
   const int G = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
-  static const int nbsync = getenv("RG_NO_NBSYNC") ? 0 : 1;
+  static const int nbsync = knob("RG_NO_NBSYNC") ? 0 : 1;
   PArgs pa{L, A, st, tot_g, bar, m, variant == RG_PLAIN ? 0 : k,
            galerkin_variant(variant) && k > 0 ? (variant == RG_ORTHOGONAL ? 2 : 1) : 0, aug ? 1 : 0, flags, nbsync,
-           getenv("RG_SKEW") ? atoi(getenv("RG_SKEW")) : 0,
+           knob_int("RG_SKEW", 0),
            P ? 1 : 0, P ? *P : PrecDev(), L.pz, L.pt, 0.0, rcap, ccap, ll,
-           (ll && G > 1 && G <= LL_GMAX && G <= PT && !getenv("RG_NO_LLRED")) ? 1 : 0};
+           (ll && G > 1 && G <= LL_GMAX && G <= PT && !knob("RG_NO_LLRED")) ? 1 : 0};
   if (P) {
     double b2 = 0.0;
     for (int c = 0; c < P->ncolors; ++c) b2 += 12.0 * (double)(P->cL[c] + P->cU[c]);
@@ -1392,7 +1396,7 @@ cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double
   pa.bar = bar;
   pa.k = k;
   pa.ll = ll;
-  pa.llred = (ll && G > 1 && G <= LL_GMAX && G <= PT && !getenv("RG_NO_LLRED")) ? 1 : 0;
+  pa.llred = (ll && G > 1 && G <= LL_GMAX && G <= PT && !knob("RG_NO_LLRED")) ? 1 : 0;
   void* args[] = {&pa, &cflag};
   return cudaLaunchCooperativeKernel(fn, dim3(G), dim3(PT), args, smem, s);
 }

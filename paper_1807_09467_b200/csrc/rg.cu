@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "knobs.cuh"
 
 using namespace rg;
 
@@ -49,14 +50,22 @@ rg_status fail(rg_status s, const std::string& msg) {
 constexpr int HIST_CAP = 1 << 16;
 constexpr int SMALL = MAXS * MAXS;  // doubles per small-matrix slot
 
+// What a captured solve graph bakes in: the variant's kernel sequence, the preconditioner, and the
+// orthogonalisation (DCGS2 or classical CGS2 — chosen per solve from the byte model, so it can change
+// between solves of one context as k_eff grows).  m, k_eff, tol are read from the state.
 struct GraphKey {
-  int variant, m, prec;
+  int variant, dcgs, prec;
   bool operator<(const GraphKey& o) const {
     if (variant != o.variant) return variant < o.variant;
-    if (m != o.m) return m < o.m;
+    if (dcgs != o.dcgs) return dcgs < o.dcgs;
     return prec < o.prec;
   }
 };
+
+// Measured crossover (same box, alternating runs): the one-kernel persistent solve beats
+// the graph path up to ~1.6M padded rows (C3: 10.5 vs 11.5 ms); at C4's 2.1M its two-barrier reductions
+// lose to the graph path's last-CTA epilogues (15.9 vs 14.7 ms).
+constexpr int64_t PERSIST_MAX_ROWS = 1600000;
 
 }  // namespace
 
@@ -303,7 +312,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
   } else {
     M.b = c->block;
     M.nb = c->n / c->block;
-    M.tma = getenv("RG_NO_BSR_TMA") ? 0 : 1;
+    M.tma = knob("RG_NO_BSR_TMA") ? 0 : 1;
     M.bytes = 8.0 * c->v_len + 4.0 * c->nnz + 4.0 * (M.nb + 1) + 16.0 * c->n;
   }
   c->c_valid = false;
@@ -316,7 +325,7 @@ rg_status build_c(rg_ctx* c, bool sync) {
   const int QB = c->L.VB - k;
   const int64_t ld = c->npad;
   cudaStream_t s = c->stream;
-  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported
+  cudaError_t es = knob("RG_NO_SPMM") ? cudaErrorNotSupported
                                         : launch_spmm(c->A, c->Z, c->Z + (int64_t)QB * ld, ld, k, c->st, c->counter, s,
                                                       c->res_fused ? c->x : nullptr, c->Z + (int64_t)c->L.VB * ld);
   if (es == cudaErrorNotSupported) {
@@ -349,7 +358,7 @@ rg_status build_c(rg_ctx* c, bool sync) {
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, c->dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (getenv("RG_DEBUG")) {
+  if (knob("RG_DEBUG")) {
     std::vector<double> hb(5 * SMALL);
     cudaMemcpy(hb.data(), c->small, sizeof(double) * 5 * SMALL, cudaMemcpyDeviceToHost);
     for (int slot = 0; slot < 5; ++slot) {
@@ -377,7 +386,7 @@ rg_status build_c_oblique(rg_ctx* c) {
   const int64_t ld = c->npad;
   cudaStream_t s = c->stream;
   double* C = c->Z + (int64_t)k * ld;
-  cudaError_t es = getenv("RG_NO_SPMM") ? cudaErrorNotSupported
+  cudaError_t es = knob("RG_NO_SPMM") ? cudaErrorNotSupported
                                         : launch_spmm(c->A, c->Z, C, ld, k, c->st, c->counter, s,
                                                       c->res_fused ? c->x : nullptr, c->Z + (int64_t)c->L.VB * ld);
   if (es == cudaErrorNotSupported) {
@@ -524,7 +533,7 @@ rg_status run_solve(rg_ctx* c, int variant, int m) {
       CK(cycle_body(c, variant, m));
     }
   }
-  GraphKey key{variant, 0, c->L.prec};
+  GraphKey key{variant, c->dcgs_now ? 1 : 0, c->L.prec};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
     cudaGraphExec_t ge;
@@ -591,9 +600,9 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   rg_ctx* c = new rg_ctx();
   CK(cudaGetDevice(&c->dev));
   c->flags = opt->flags;
-  if (getenv("RG_NO_GRAPH")) c->flags |= RG_FLAG_NO_GRAPH;  // ncu cannot profile kernels inside conditional graphs
-  if (getenv("RG_CGS2") || (opt->flags & RG_FLAG_CGS2)) c->use_dcgs = false;
-  if (getenv("RG_NO_PERSIST") || (opt->flags & RG_FLAG_NO_PERSIST)) c->use_persist = false;
+  if (knob("RG_NO_GRAPH")) c->flags |= RG_FLAG_NO_GRAPH;  // ncu cannot profile kernels inside conditional graphs
+  if (knob("RG_CGS2") || (opt->flags & RG_FLAG_CGS2)) c->use_dcgs = false;
+  if (knob("RG_NO_PERSIST") || (opt->flags & RG_FLAG_NO_PERSIST)) c->use_persist = false;
   if (opt->cuda_stream) {
     c->stream = (cudaStream_t)opt->cuda_stream;
   } else {
@@ -669,7 +678,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   c->L.partial = c->partial;
   c->L.counter = c->counter;
   c->L.keepV = c->keepV;
-  c->L.cgs_ok = (c->max_k + c->max_m + 1) <= 128 && !getenv("RG_NO_CGS");
+  c->L.cgs_ok = (c->max_k + c->max_m + 1) <= 128 && !knob("RG_NO_CGS");
   c->L.keep_l2 = (double)c->npad * 8.0 * (2 * c->max_k + c->max_m + 1) <= 160e6;  // ~L2-sized (126 MB)
 
   if ((s = set_matrix(c, A, true)) != RG_OK) {
@@ -776,7 +785,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   const int s = c->s_count;
   const int64_t ld = c->npad;
   cudaStream_t st = c->stream;
-  static const bool timing = getenv("RG_TIMING") != nullptr;
+  static const bool timing = knob("RG_TIMING");
   auto now = [] { return std::chrono::steady_clock::now(); };
   const auto t0 = now();
   double* G = c->small;
@@ -797,7 +806,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   const auto t1 = now();
   double* hs = c->hsig;  // pinned
   CK(cudaMemcpyAsync(hs, sig, sizeof(double) * s, cudaMemcpyDeviceToHost, st));
-  if (!k_eff && !sigma && !getenv("RG_SYNC_BUILD")) {
+  if (!k_eff && !sigma && !knob("RG_SYNC_BUILD")) {
     // asynchronous: nothing to return now; the next call that needs W waits for sigma (finish_build)
     CK(cudaEventRecord(c->ebuild, st));
     c->pend = true;
@@ -810,7 +819,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
   }
   CK(cudaStreamSynchronize(st));
   const auto t2 = now();
-  if (getenv("RG_DEBUG")) {
+  if (knob("RG_DEBUG")) {
     double sw[2] = {0.0, 0.0};
     cudaMemcpy(sw, lam + s, 2 * sizeof(double), cudaMemcpyDeviceToHost);
     fprintf(stderr, "rg_build_recycle: s=%d, Jacobi sweeps %.0f (pass 1) %.0f (pass 2)\n", s, sw[0], sw[1]);
@@ -841,27 +850,24 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   if ((rs = resolve_build(c)) != RG_OK) return rs;
   const int eff = (v != RG_PLAIN && c->have_W && c->k_eff > 0) ? (int)v : (int)RG_PLAIN;
   const int k = eff == RG_PLAIN ? 0 : c->k_eff;
-  int c_spmv = 0;
   bool check_c = false;
   const int want_kind = galerkin_variant(eff) ? 1 : 0;
   // RG_TIMING: device-side phase split of one solve (events on the solve's stream)
-  static const bool timing = getenv("RG_TIMING") != nullptr;
+  static const bool timing = knob("RG_TIMING");
   static cudaEvent_t tev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   if (timing && !tev[0])
     for (auto& e : tev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(tev[0], s);
   const bool need_c = eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind);
-  const bool persist_size = c->npad <= 1600000 || getenv("RG_FORCE_PERSIST");
-  const double basis_pass0 = 8.0 * (double)c->n * (double)(k + m + 2);
-  const bool dcgs_next = c->use_dcgs && !(c->A.bytes > basis_pass0 && !getenv("RG_FORCE_DCGS"));
-  static const bool no_fuse = getenv("RG_NO_FUSE_C") != nullptr;
+  const bool persist_size = c->npad <= PERSIST_MAX_ROWS || knob("RG_FORCE_PERSIST");
+  static const bool no_fuse = knob("RG_NO_FUSE_C");
   // (independent of the solve path: the graph path reads the same Q columns and R_C^{-1})
   bool fuse_c = need_c && !galerkin_variant(eff) && !no_fuse;
   // DCGS2 saves two reductions and one basis pass per Arnoldi step but spends one extra SpMV per
   // cycle (the step after the stopping column).  When one SpMV moves more bytes than a whole pass
   // over the basis (C5: 7.3 GB vs ~0.8 GB), classical CGS2 is cheaper (measured C5: see DESIGN.md).
   const double basis_pass = 8.0 * (double)c->n * (double)(k + m + 2);
-  c->dcgs_now = c->use_dcgs && !(c->A.bytes > basis_pass && !getenv("RG_FORCE_DCGS"));
+  c->dcgs_now = c->use_dcgs && !(c->A.bytes > basis_pass && !knob("RG_FORCE_DCGS"));
   DevState* h = c->hst;
   memset(h, 0, header_bytes());
   h->variant = eff;
@@ -876,7 +882,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   CK(cudaMemcpyAsync(c->st, h, header_bytes(), cudaMemcpyHostToDevice, s));  // before the C build (cfail)
   // BSR-64 solves on the graph path (C5): the start residual's product A x0 rides along as one
   // extra column of the C = A W SpMM — one read of A (7.3 GB at C5) instead of two per system.
-  static const bool no_fuse_res = getenv("RG_NO_FUSE_RES") != nullptr;
+  static const bool no_fuse_res = knob("RG_NO_FUSE_RES");
   c->res_fused = need_c && !no_fuse_res && c->A.fmt == 2 && c->A.b == 64 && c->A.tma && k + 1 <= 64 &&
                  !(c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH));
   const bool early_in = c->res_fused;  // b and x0 in the library's buffers before the SpMM reads x0
@@ -892,7 +898,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     if (fuse_c) {  // one cooperative kernel (persistent.cu k_cbuild) instead of build_c's ~10 launches
       // (gbar is clean between solves; it uses it only without the flag-carrying reductions)
       const cudaError_t eb = launch_cbuild(c->L, c->A, c->st, c->tot_g, c->gbar, c->llw, k, &c->st->cfail, s);
-      if (eb == cudaSuccess && getenv("RG_NO_LLRED")) CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
+      if (eb == cudaSuccess && knob("RG_NO_LLRED")) CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
       if (eb == cudaSuccess) {
         c->c_valid = true;
       } else if (eb == cudaErrorNotSupported || eb == cudaErrorCooperativeLaunchTooLarge) {
@@ -907,7 +913,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
       return rs;
     }
     c->c_kind = want_kind;
-    c_spmv = k;
+
     check_c = true;
   }
   c->cur_var = eff;
@@ -920,7 +926,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   const bool try_persist = c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH);
   // Persistent path with DEVICE buffers and n = n_pad (no padding rows): the kernel reads b and
   // iterates on x in the caller's buffers (no copy of b, none of x back); otherwise the library's.
-  static const bool no_alias = getenv("RG_NO_ALIAS") != nullptr;
+  static const bool no_alias = knob("RG_NO_ALIAS");
   bool alias = try_persist && mem == RG_DEVICE && c->n == c->npad && !no_alias;
   if (alias) {
     if (x0 && x0 != x_out) CK(cudaMemcpyAsync(x_out, x0, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, s));
@@ -981,7 +987,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
             b2 * 1e3, d * 1e3);
   }
   if (check_c) bad = h->cfail;
-  if (done_persist && getenv("RG_SKEW")) {  // experiment: per-CTA step start / dots done / reduction done / SM
+  if (done_persist && knob("RG_SKEW")) {  // experiment: per-CTA step start / dots done / reduction done / SM
     std::vector<unsigned> ts((size_t)NSM * 8);
     cudaMemcpy(ts.data(), c->pflags + NSM * 2, sizeof(unsigned) * NSM * 8, cudaMemcpyDeviceToHost);
     unsigned mn = 0xffffffffu;
@@ -1019,7 +1025,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     rep->restarts = h->cycles > 0 ? h->cycles - 1 : 0;
     rep->converged = h->converged;
     rep->k_eff = k;
-    rep->spmv_count = h->bzero ? 0 : h->iters + h->cycles + 1 + c_spmv;
+    rep->spmv_count = h->spmv_count;  // counted on the device by every product the solve issued
     rep->history_len = hl;
     rep->rel_residual = h->bzero ? 0.0 : h->relres;
     rep->ms_total = ms;

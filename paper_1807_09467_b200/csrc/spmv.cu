@@ -64,6 +64,8 @@ __device__ __forceinline__ bool setup(const SpmvArgs& a, Io& io, int& kid) {
     io.x = a.x;
     io.y = a.y;
   }
+  // rg_report.spmv_count: every sparse product this solve issues, counted where it runs
+  if (st && kid != K_RES_Y && blockIdx.x == 0 && threadIdx.x == 0) st->spmv_count++;
   if (st) prof_begin(st, kid);
   return true;
 }
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
                                                         int64_t ld, int k, DevState* pst, unsigned* counter,
                                                         const double* __restrict__ xe, double* ye) {
   if (pst) prof_begin(pst, K_SPMV_PLAIN);
+  if (pst && blockIdx.x == 0 && threadIdx.x == 0) pst->spmv_count += k + (xe ? 1 : 0);
   extern __shared__ __align__(128) double ring[];
   __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
@@ -488,7 +491,8 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
 // CSR / SELL: thread per row, 16 columns of W per pass (k <= 64 -> at most 4 reads of A).
 template <int KC>
 __global__ void __launch_bounds__(256) k_spmm_rows(MatDev A, const double* __restrict__ W, double* Y, int64_t ld,
-                                                   int k0, int kc) {
+                                                   int k0, int kc, DevState* st) {
+  if (st && blockIdx.x == 0 && threadIdx.x == 0) st->spmv_count += kc;
   for (int64_t row = blockIdx.x * 256ll + threadIdx.x; row < A.n; row += (int64_t)gridDim.x * 256) {
     double acc[KC];
 #pragma unroll
@@ -588,7 +592,7 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
   int64_t g = (A.n + 255) / 256;
   if (g > NSM * 8) g = NSM * 8;
   for (int k0 = 0; k0 < k; k0 += 16) {
-    k_spmm_rows<16><<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(A, W, Y, ld, k0, k - k0 < 16 ? k - k0 : 16);
+    k_spmm_rows<16><<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(A, W, Y, ld, k0, k - k0 < 16 ? k - k0 : 16, st);
     note_host_launches(1);
   }
   return cudaGetLastError();

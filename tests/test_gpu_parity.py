@@ -529,3 +529,32 @@ def test_deferred_build_matches_synchronous(variant, rng):
             ctx.push_snapshot(t(u))
     for ctx in ctxs:
         ctx.close()
+
+
+@pytest.mark.parametrize("flags,exact", [(4 | 8, True), (8, False), (0, False)])   # CGS2 graph / DCGS2 graph / persistent
+@pytest.mark.parametrize("variant", ["plain", "deflate"])
+def test_spmv_count_is_counted(flags, exact, variant):
+    """rg_report.spmv_count is counted by the kernels that run the products (not a formula).  With
+    classical CGS2 every Arnoldi step is one SpMV and every cycle start one residual SpMV:
+    iterations + restarts + 2, plus k_eff for C = A W; DCGS2 may issue one extra product per cycle
+    (the step after the stopping column)."""
+    cfg = synth.CONFIGS["C1"]
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    hm = seq.matrix(1, u)
+    ctx = make_ctx(hm, max_m=cfg.m, s=cfg.s, k=cfg.k, flags=flags)
+    x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+    for i in range(4):
+        ctx.solve(t(seq.rhs(1, u) * (1 + 0.2 * i)), x, m=12, variant="plain", tol=1e-8)
+        ctx.push_snapshot(x)
+    k = 0
+    if variant == "deflate":
+        k, _ = ctx.build_recycle(3)
+    rep = ctx.solve(t(seq.rhs(1, u) * 1.7), x, m=12, variant=variant, tol=1e-8)
+    assert rep["converged"] and rep["restarts"] >= 1 and rep["k_eff"] == k
+    base = rep["iterations"] + rep["restarts"] + 2 + k
+    if exact:
+        assert rep["spmv_count"] == base, rep
+    else:
+        assert base <= rep["spmv_count"] <= base + rep["restarts"] + 1, rep
+    ctx.close()
