@@ -6,8 +6,11 @@ in HBM from x_{t-1} (a1), the values are handed to the library (rg_update_matrix
 space is rebuilt from the snapshot window (a3; C = A W and its QR are rebuilt inside the solve, a4),
 the system is solved with the recycled variant (a5-a10), and x_t is pushed as a snapshot (a2).
 
-Default workload: BASELINE.json configs[1] (C2, n = 262,144, GMRES(50), k = 10 from 20
-snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|augment|deflate|oblique|orthogonal.
+Default workload: BASELINE.json configs[4] (C5, n = 2,097,152, BSR-64 with 7.31 GB of values,
+GMRES(30), k = 20 from 40 snapshots), variant deflate: the largest single-GPU configuration.  When
+--warmup + --steps exceeds the config's sequence length (C5: 20 systems) the sequence continues with
+the same generator (C5: A_t = A_{t-1} o (1 + 0.01 xi_t), b fixed).  Other configs: --config C1..C4,
+--variant plain|augment|deflate|oblique|orthogonal.
 
   value      seconds per system (device time, CUDA events on the library's stream), whole job:
              max-over-ranks time / (systems solved by all ranks)
@@ -16,7 +19,8 @@ snapshots), variant deflate.  Other configs: --config C1..C5, --variant plain|au
   roofline   the dominant kernel's algorithmic bytes / its measured device time (%globaltimer
              stamps inside the kernels: launches live inside CUDA graphs, where host-side events
              cannot bracket single kernels), against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the oracle (plain C, 1 thread) on a bounded sample of the same workload
+  cpu_baseline  the oracle (plain C, deterministic OpenMP threads on all online cores) on the first
+             timed systems of the same workload, bounded to ~--cpu-budget seconds
 
 --impl reference runs the oracle (the reference arm for this tier) on the same config.
 Multi-GPU (torchrun): independent replicas, one sequence per rank, no collective on the data
@@ -374,8 +378,10 @@ def run_ours(args, cfg):
     flush = torch.zeros(32 * 1024 * 1024, dtype=torch.float64, device=device)
     with torch.cuda.stream(stream):
         sell = (cfg.fmt == "sell") if args.sell < 0 else bool(args.sell)
+        from paper_1807_09467_b200 import rg as _rg
         run = GpuRun(cfg, args.variant, k, device, stream, profile=not args.no_profile, sell=sell,
-                     precond=args.omega if args.precond == "ssor" else None)
+                     precond=args.omega if args.precond == "ssor" else None,
+                     flags=_rg.RG_FLAG_NO_GRAPH if args.no_graph else 0)
         for _ in range(args.warmup):
             run.step()
         torch.cuda.synchronize()
@@ -491,7 +497,9 @@ def run_ours(args, cfg):
                    "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "fmt": cfg.fmt,
                    "device_format": "SELL-32" if sell else ("BSR-64" if cfg.kind == "bsr" else "CSR"),
                    "tol": cfg.tol,
-                   "systems_timed": f"t={args.warmup + 1}..{args.warmup + args.steps}",
+                   "systems_timed": f"t={args.warmup + 1}..{args.warmup + args.steps}" + (
+                       f" (the config's sequence has {cfg.systems}; continued by the same generator)"
+                       if args.warmup + args.steps > cfg.systems else ""),
                    "iterations_timed": timed_iters,
                    "l2": "flushed (256 MiB write) between steps, outside the timed events",
                    "parallelism": f"replicas x{ws}"},
@@ -523,7 +531,10 @@ def run_reference(args, cfg):
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, synth/)",
             "config": {"workload": f"{cfg.name}: BASELINE.json configs[{cfg.cid - 1}]", "variant": args.variant,
-                       "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "iterations": its},
+                       "n": cfg.n, "m": cfg.m, "k": k, "s": cfg.s, "iterations": its,
+                       "systems_timed": f"t={args.warmup + 1}..{n_sys}" + (
+                           f" (the config's sequence has {cfg.systems}; continued by the same generator)"
+                           if n_sys > cfg.systems else "")},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": nth, "kind": "oracle", "cpu_model": cpu_model(),
                              "online_cores": os.cpu_count(),
                              "sample": f"{cfg.name} systems {args.warmup + 1}..{n_sys} of the oracle's own sequence "
@@ -549,6 +560,9 @@ def main(argv=None):
     ap.add_argument("--sell", type=int, default=-1, help="1: pack CSR to SELL-32 inside the library, "
                     "0: keep CSR, -1: config default")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="RG_FLAG_NO_GRAPH: launch the solve's kernels one by one (ncu cannot profile kernels "
+                         "inside conditional CUDA graphs); for profiler captures, not for timing")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-vs-plain", action="store_true",
                     help="skip the plain GMRES(m) sequence timed beside the recycled one")

@@ -16,6 +16,7 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference"
     assert line["unit"] == "s/system" and line["higher_is_better"] is False
     assert line["value"] > 0 and line["steps"] == 2 and line["warmup"] == 1
-    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] == 1
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "oracle" and cb["cores"] == os.cpu_count() == cb["online_cores"] and cb["cpu_model"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0
-    assert len(line["config"]["iterations"]) == 3
+    assert len(line["config"]["iterations"]) == 2      # the timed systems 2..3 (system 1 untimed)
