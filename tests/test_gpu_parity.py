@@ -550,7 +550,7 @@ def test_spmv_count_is_counted(flags, exact, variant):
     k = 0
     if variant == "deflate":
         k, _ = ctx.build_recycle(3)
-    rep = ctx.solve(t(seq.rhs(1, u) * 1.7), x, m=12, variant=variant, tol=1e-8)
+    rep = ctx.solve(t(seq.rhs(1, u) * 1.7), x, m=6, variant=variant, tol=1e-8)
     assert rep["converged"] and rep["restarts"] >= 1 and rep["k_eff"] == k
     base = rep["iterations"] + rep["restarts"] + 2 + k
     if exact:
