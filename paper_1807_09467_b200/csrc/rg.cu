@@ -453,15 +453,6 @@ cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
   return launch_orth(c->L, c->st, OP_UN, c->stream, cond);
 }
 
-cudaError_t cycle_body(rg_ctx* c, int variant, int m) {
-  cudaError_t e;
-  const int steps = m + (c->dcgs_now ? 1 : 0);  // DCGS2 finishes column j-1 in step j
-  for (int j = 0; j < steps; ++j)
-    if ((e = arnoldi_step(c, 0)) != cudaSuccess) return e;
-  if ((e = cycle_end(c)) != cudaSuccess) return e;
-  return cycle_start(c, variant);
-}
-
 #define CKG(call)                                                                      \
   do {                                                                                 \
     cudaError_t e_ = (call);                                                           \
@@ -525,12 +516,19 @@ rg_status build_solve_graph(rg_ctx* c, int variant, cudaGraphExec_t* out) {
 
 // Runs the rest of the solve after the first cycle start.
 rg_status run_solve(rg_ctx* c, int variant, int m) {
-  if (c->flags & RG_FLAG_NO_GRAPH) {  // host-driven loop (debugging): one sync per cycle
+  if (c->flags & RG_FLAG_NO_GRAPH) {
+    // host-driven loop (debugging, profiler captures): one sync per Arnoldi step, so every launched
+    // kernel does work (the graph's WHILE nodes decide the same on the device)
     for (;;) {
       CK(cudaMemcpyAsync(c->hst, c->st, offsetof(DevState, cs), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaStreamSynchronize(c->stream));
       if (c->hst->done) return RG_OK;
-      CK(cycle_body(c, variant, m));
+      if (c->hst->active) {
+        CK(arnoldi_step(c, 0));
+      } else {
+        CK(cycle_end(c));
+        CK(cycle_start(c, variant));
+      }
     }
   }
   GraphKey key{variant, c->dcgs_now ? 1 : 0, c->L.prec};
