@@ -21,7 +21,7 @@ struct MatDev {
   int64_t nslices = 0;
   int tma = 1;                  // BSR-64: stream blocks with TMA bulk copies
   double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
-  int64_t nnz = 0;              // CSR entries
+  int64_t nnz = 0;              // CSR entries / BSR stored blocks
 };
 
 // Kernels launched directly by the host without a device-side counter (recycle build, CholQR2,

@@ -313,6 +313,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
     M.b = c->block;
     M.nb = c->n / c->block;
     M.tma = knob("RG_NO_BSR_TMA") ? 0 : 1;
+    M.nnz = c->nnz;  // stored blocks
     M.bytes = 8.0 * c->v_len + 4.0 * c->nnz + 4.0 * (M.nb + 1) + 16.0 * c->n;
   }
   c->c_valid = false;

@@ -11,6 +11,8 @@
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
+#include <cuda.h>
+
 #ifndef RG_SPMV_CAP
 #define RG_SPMV_CAP 2  // CTAs per SM of the grid-stride SpMV launches (STEP / PLAIN modes): one wave
                        // (measured: 4 -> 2 per SM: SELL C3 4.03 -> 4.28 TB/s, CSR C4 5.40 -> 5.67)
@@ -321,14 +323,27 @@ __global__ void __launch_bounds__(OT) k_res_y(SpmvArgs a) {
 // BSR-64: one TMA-streamed read of A for all k columns; the 64x64 block (shared memory) times the
 // 64 x k panel of W runs on the FP64 tensor cores (DMMA m8n8k4): warp w owns output rows
 // 8w..8w+7 of the block row and every 8-column group.
+//
+// Landing layout: a block arrives through a 3-D tensor map {16 rows, 4 row quarters, columns} with
+// the 128-byte swizzle, i.e. 128-byte "lines" L = 4 c + r / 16 (c column, r row) whose 16-byte chunks
+// are permuted by chunk ^= L % 8.  The A fragment of a DMMA k-step (8 consecutive rows x 4 consecutive
+// columns) then covers all 32 banks twice: 2 wavefronts per load instead of the 4 of the dense
+// column-major landing (ncu r02: 171M bank conflicts in 321M shared wavefronts), which made the
+// shared-memory pipe, not the DMMA pipe, the limiter.
+// element (r, c) of a landed block -> double offset
+__device__ __forceinline__ int swz_off(int r, int c) {
+  const int L = 4 * c + (r >> 4);
+  return L * 16 + ((((r & 15) >> 1) ^ (L & 7)) << 1) + (r & 1);
+}
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
 // acc[g] += A_block(rows 8w.., :) * W_panel(:, 8g..8g+7), g < NG (WSP = panel stride)
+// blk + aoff: this lane's A element of k-step 0 in the swizzled landing (the k-step cc adds 64 cc)
 template <int NG>
-__device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int rrow, int lane) {
+__device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int aoff) {
   // CH independent accumulator chains per column group hide the DMMA latency when NG is small
   constexpr int CH = NG >= 4 ? 1 : (NG >= 2 ? 2 : 4);
   double ch[NG][CH][2];
@@ -341,7 +356,7 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
       const int cc = c0 + 4 * c;
-      const double av = blk[(cc + (lane & 3)) * 64 + rrow];    // A(rrow, cc + lane%4)
+      const double av = blk[aoff + cc * 64];                   // A(rrow, cc + lane%4), swizzled
 #pragma unroll
       for (int g = 0; g < NG; ++g) dmma884(ch[g][c][0], ch[g][c][1], av, wp[g * 8 * 68 + cc]);  // W(cc + lane%4, 8g + lane/4)
     }
@@ -357,12 +372,15 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
 
 // xe != nullptr: one extra input column (panel column k) whose product goes to ye (y = A x0 of the
 // solve start, fused with C = A W: one read of A instead of two).
-__global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* __restrict__ W, double* Y,
+__global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ CUtensorMap tmA, MatDev A,
+                                                        const double* __restrict__ W, double* Y,
                                                         int64_t ld, int k, DevState* pst, unsigned* counter,
                                                         const double* __restrict__ xe, double* ye) {
   if (pst) prof_begin(pst, K_SPMV_PLAIN);
   if (pst && blockIdx.x == 0 && threadIdx.x == 0) pst->spmv_count += k + (xe ? 1 : 0);
-  extern __shared__ __align__(128) double ring[];
+  extern __shared__ __align__(128) double smraw[];
+  // the 128-byte swizzle repeats every 1024 bytes: the ring starts on a 1024-byte boundary
+  double* ring = (double*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -385,8 +403,9 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
           const int s = t % BNS;
           if (t >= BNS) bar_wait(&empty[s], (uint32_t)((t / BNS - 1) & 1));
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                       ::"r"(su32(ring + (size_t)s * (BSTAGE / 8))), "l"(A.v + (int64_t)p * 4096), "r"(BSTAGE),
+          asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                       "[%0], [%1, {%2, %3, %4}], [%5];"
+                       ::"r"(su32(ring + (size_t)s * (BSTAGE / 8))), "l"(&tmA), "r"(0), "r"(0), "r"(p * 64),
                        "r"(su32(&full[s])) : "memory");
         }
       }
@@ -398,6 +417,7 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
   constexpr int WSP = 68;
   double* wpan = ring + (size_t)BNS * (BSTAGE / 8);          // 2 x 64 cols x WSP
   const int rrow = wid * 8 + (lane >> 2);                    // A fragment row inside the block
+  const int aoff = swz_off(rrow, lane & 3);                  // its k-step-0 element in the landing
   const int nval = 64 * k;                                   // panel values
   constexpr int PPT = (64 * 64 + BT_CONS - 1) / BT_CONS;     // panel values per thread (<= 16)
   // first block of this CTA
@@ -447,14 +467,14 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(MatDev A, const double* 
       const double* blk = ring + (size_t)st * (BSTAGE / 8);
       const double* wp = wpan + (size_t)(t & 1) * 64 * WSP + (lane >> 2) * WSP + (lane & 3);
       switch (ng) {  // exact trip count: predicated-off DMMAs still occupy the tensor pipe
-        case 1: block_mma<1>(acc, blk, wp, rrow, lane); break;
-        case 2: block_mma<2>(acc, blk, wp, rrow, lane); break;
-        case 3: block_mma<3>(acc, blk, wp, rrow, lane); break;
-        case 4: block_mma<4>(acc, blk, wp, rrow, lane); break;
-        case 5: block_mma<5>(acc, blk, wp, rrow, lane); break;
-        case 6: block_mma<6>(acc, blk, wp, rrow, lane); break;
-        case 7: block_mma<7>(acc, blk, wp, rrow, lane); break;
-        default: block_mma<8>(acc, blk, wp, rrow, lane); break;
+        case 1: block_mma<1>(acc, blk, wp, aoff); break;
+        case 2: block_mma<2>(acc, blk, wp, aoff); break;
+        case 3: block_mma<3>(acc, blk, wp, aoff); break;
+        case 4: block_mma<4>(acc, blk, wp, aoff); break;
+        case 5: block_mma<5>(acc, blk, wp, aoff); break;
+        case 6: block_mma<6>(acc, blk, wp, aoff); break;
+        case 7: block_mma<7>(acc, blk, wp, aoff); break;
+        default: block_mma<8>(acc, blk, wp, aoff); break;
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
@@ -579,13 +599,25 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
   if (k <= 0) return cudaSuccess;
   if (xe && !(A.fmt == 2 && A.b == 64 && A.tma && k + 1 <= 64)) return cudaErrorInvalidValue;  // callers check
   if (A.fmt == 2 && A.b == 64 && A.tma && k <= 64) {
-    static bool init = false;
-    if (!init) {
-      cudaFuncSetAttribute(k_spmm_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, BNS * BSTAGE + 2 * 64 * 68 * 8);
-      init = true;
+    // the values as a 3-D tensor {16 rows, 4 row quarters, nnzb * 64 columns} (strides 128 B, 512 B):
+    // one box {16, 4, 64} = one 32 KB block, landed with the 128-byte swizzle (see swz_off)
+    CUtensorMap tm;
+    const cuuint64_t dims[3] = {16, 4, (cuuint64_t)A.nnz * 64};
+    const cuuint64_t strides[2] = {16 * 8, 64 * 8};
+    const cuuint32_t box[3] = {16, 4, 64}, estr[3] = {1, 1, 1};
+    if (cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A.v, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+    constexpr int smem = BNS * BSTAGE + 2 * 64 * 68 * 8 + 1024;  // + alignment slack for the 1024-byte ring base
+    static bool attr_set[MAXDEV] = {};
+    const int dev = current_device();
+    if (!attr_set[dev]) {
+      cudaFuncSetAttribute(k_spmm_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr_set[dev] = true;
     }
     int64_t g = A.nb < NSM ? A.nb : NSM;
-    k_spmm_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, BNS * BSTAGE + 2 * 64 * 68 * 8, s>>>(A, W, Y, ld, k, st, counter, xe, ye);
+    k_spmm_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, smem, s>>>(tm, A, W, Y, ld, k, st, counter, xe, ye);
     return cudaGetLastError();
   }
   if (A.fmt == 2) return cudaErrorNotSupported;  // caller falls back to per-column SpMV
