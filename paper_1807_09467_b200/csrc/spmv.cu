@@ -324,26 +324,33 @@ __global__ void __launch_bounds__(OT) k_res_y(SpmvArgs a) {
 // 64 x k panel of W runs on the FP64 tensor cores (DMMA m8n8k4): warp w owns output rows
 // 8w..8w+7 of the block row and every 8-column group.
 //
-// Landing layout: a block arrives through a 3-D tensor map {16 rows, 4 row quarters, columns} with
-// the 128-byte swizzle, i.e. 128-byte "lines" L = 4 c + r / 16 (c column, r row) whose 16-byte chunks
-// are permuted by chunk ^= L % 8.  The A fragment of a DMMA k-step (8 consecutive rows x 4 consecutive
-// columns) then covers all 32 banks twice: 2 wavefronts per load instead of the 4 of the dense
-// column-major landing (ncu r02: 171M bank conflicts in 321M shared wavefronts), which made the
-// shared-memory pipe, not the DMMA pipe, the limiter.
+// Landing layout: a block arrives as four 8 KB row-quarter slices q (rows 16q..16q+15), each through a
+// 3-D tensor map {16 rows, 4 quarters, columns} with box {16, 1, 64} and the 128-byte swizzle: inside
+// slice q, line c (16 rows of column c, 128 B) has its 16-byte chunks permuted by chunk ^= c % 8.  The
+// DMMA k-step s takes the four columns kset(s) = c0 + {0, 2, 4, 6} (c0 = 8 (s/2) + s%2; the k order of a
+// sum is free): the XOR values of those columns differ in bits 1-2, so each half-warp's 16 A elements
+// (4 rows x 4 columns) fill 8 distinct chunks x both halves = one 128-byte wavefront, the ideal.  (Dense
+// column-major landing: 4 wavefronts per load, ncu r02: 171M bank conflicts in 321M shared wavefronts,
+// the shared-memory pipe and not the DMMA pipe was the limiter.)
 // element (r, c) of a landed block -> double offset
 __device__ __forceinline__ int swz_off(int r, int c) {
-  const int L = 4 * c + (r >> 4);
-  return L * 16 + ((((r & 15) >> 1) ^ (L & 7)) << 1) + (r & 1);
+  return (r >> 4) * 1024 + c * 16 + ((((r & 15) >> 1) ^ (c & 7)) << 1) + (r & 1);
 }
+// column of k-step s, lane j = lane % 4
+__device__ __forceinline__ int kcol(int s, int j) { return 8 * (s >> 1) + (s & 1) + 2 * j; }
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// acc[g] += A_block(rows 8w.., :) * W_panel(:, 8g..8g+7), g < NG (WSP = panel stride)
-// blk + aoff: this lane's A element of k-step 0 in the swizzled landing (the k-step cc adds 64 cc)
+// acc[g] += A_block(rows 8w.., :) * W_panel(:, 8g..8g+7), g < NG.  W panel stored k-major [kk][n] with
+// stride WSPK = 66 (== 2 mod 16: the B elements W(kcol(s, j), 8g + i) of a half-warp, i < 4, j < 4, land in
+// 16 distinct banks pairs).  ae / ao: this lane's A element of k-steps 0 / 1 (k-step s adds 128 (s / 2));
+// we / wo: its W element of k-steps 0 / 1 (+ 8 * WSPK (s / 2) + 8 g).
+constexpr int WSPK = 66;
 template <int NG>
-__device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int aoff) {
+__device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int ae, int ao,
+                                          int we, int wo) {
   // CH independent accumulator chains per column group hide the DMMA latency when NG is small
   constexpr int CH = NG >= 4 ? 1 : (NG >= 2 ? 2 : 4);
   double ch[NG][CH][2];
@@ -352,13 +359,14 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
 #pragma unroll
     for (int c = 0; c < CH; ++c) ch[g][c][0] = ch[g][c][1] = 0.0;
 #pragma unroll
-  for (int c0 = 0; c0 < 64; c0 += 4 * CH) {
+  for (int s0 = 0; s0 < 16; s0 += CH) {
 #pragma unroll
     for (int c = 0; c < CH; ++c) {
-      const int cc = c0 + 4 * c;
-      const double av = blk[aoff + cc * 64];                   // A(rrow, cc + lane%4), swizzled
+      const int s = s0 + c;
+      const double av = blk[((s & 1) ? ao : ae) + 128 * (s >> 1)];          // A(rrow, kcol(s, lane%4))
+      const int wb = ((s & 1) ? wo : we) + 8 * WSPK * (s >> 1);
 #pragma unroll
-      for (int g = 0; g < NG; ++g) dmma884(ch[g][c][0], ch[g][c][1], av, wp[g * 8 * 68 + cc]);  // W(cc + lane%4, 8g + lane/4)
+      for (int g = 0; g < NG; ++g) dmma884(ch[g][c][0], ch[g][c][1], av, wp[wb + 8 * g]);  // W(kcol, 8g + lane/4)
     }
   }
 #pragma unroll
@@ -379,8 +387,9 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
   if (pst) prof_begin(pst, K_SPMV_PLAIN);
   if (pst && blockIdx.x == 0 && threadIdx.x == 0) pst->spmv_count += k + (xe ? 1 : 0);
   extern __shared__ __align__(128) double smraw[];
-  // the 128-byte swizzle repeats every 1024 bytes: the ring starts on a 1024-byte boundary
-  double* ring = (double*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  // the 128-byte swizzle repeats every 1024 bytes: the ring starts on a 1024-byte boundary (pointer
+  // arithmetic on smraw keeps the shared address space: LDS, not generic loads)
+  double* ring = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u) / 8u;
   __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -403,10 +412,12 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
           const int s = t % BNS;
           if (t >= BNS) bar_wait(&empty[s], (uint32_t)((t / BNS - 1) & 1));
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
-          asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-                       "[%0], [%1, {%2, %3, %4}], [%5];"
-                       ::"r"(su32(ring + (size_t)s * (BSTAGE / 8))), "l"(&tmA), "r"(0), "r"(0), "r"(p * 64),
-                       "r"(su32(&full[s])) : "memory");
+#pragma unroll
+          for (int q = 0; q < 4; ++q)  // row quarter q -> slice q of the stage (8 KB, 1024-byte aligned)
+            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                         "[%0], [%1, {%2, %3, %4}], [%5];"
+                         ::"r"(su32(ring + (size_t)s * (BSTAGE / 8) + q * 1024)), "l"(&tmA), "r"(0), "r"(q), "r"(p * 64),
+                         "r"(su32(&full[s])) : "memory");
         }
       }
     }
@@ -414,10 +425,10 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
   }
   // consumers: W panel of block t in shared memory (double-buffered, stride WSP), the next panel
   // is prefetched into registers while block t's DMMAs run.
-  constexpr int WSP = 68;
-  double* wpan = ring + (size_t)BNS * (BSTAGE / 8);          // 2 x 64 cols x WSP
+  double* wpan = ring + (size_t)BNS * (BSTAGE / 8);          // 2 x 64 k-rows x WSPK
   const int rrow = wid * 8 + (lane >> 2);                    // A fragment row inside the block
-  const int aoff = swz_off(rrow, lane & 3);                  // its k-step-0 element in the landing
+  const int ae = swz_off(rrow, kcol(0, lane & 3)), ao = swz_off(rrow, kcol(1, lane & 3));
+  const int we = kcol(0, lane & 3) * WSPK + (lane >> 2), wo = kcol(1, lane & 3) * WSPK + (lane >> 2);
   const int nval = 64 * k;                                   // panel values
   constexpr int PPT = (64 * 64 + BT_CONS - 1) / BT_CONS;     // panel values per thread (<= 16)
   // first block of this CTA
@@ -437,7 +448,7 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
 #pragma unroll
     for (int u = 0; u < PPT; ++u) {
       const int e = tid + u * BT_CONS;
-      if (e < nval) wpan[(size_t)buf * 64 * WSP + (e >> 6) * WSP + (e & 63)] = pre[u];
+      if (e < nval) wpan[(size_t)buf * 64 * WSPK + (e & 63) * WSPK + (e >> 6)] = pre[u];   // [kk][n]
     }
   };
   if (I < A.nb && p < pend) {
@@ -465,16 +476,16 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
       const int st = t % BNS;
       bar_wait(&full[st], (uint32_t)((t / BNS) & 1));
       const double* blk = ring + (size_t)st * (BSTAGE / 8);
-      const double* wp = wpan + (size_t)(t & 1) * 64 * WSP + (lane >> 2) * WSP + (lane & 3);
+      const double* wp = wpan + (size_t)(t & 1) * 64 * WSPK;
       switch (ng) {  // exact trip count: predicated-off DMMAs still occupy the tensor pipe
-        case 1: block_mma<1>(acc, blk, wp, aoff); break;
-        case 2: block_mma<2>(acc, blk, wp, aoff); break;
-        case 3: block_mma<3>(acc, blk, wp, aoff); break;
-        case 4: block_mma<4>(acc, blk, wp, aoff); break;
-        case 5: block_mma<5>(acc, blk, wp, aoff); break;
-        case 6: block_mma<6>(acc, blk, wp, aoff); break;
-        case 7: block_mma<7>(acc, blk, wp, aoff); break;
-        default: block_mma<8>(acc, blk, wp, aoff); break;
+        case 1: block_mma<1>(acc, blk, wp, ae, ao, we, wo); break;
+        case 2: block_mma<2>(acc, blk, wp, ae, ao, we, wo); break;
+        case 3: block_mma<3>(acc, blk, wp, ae, ao, we, wo); break;
+        case 4: block_mma<4>(acc, blk, wp, ae, ao, we, wo); break;
+        case 5: block_mma<5>(acc, blk, wp, ae, ao, we, wo); break;
+        case 6: block_mma<6>(acc, blk, wp, ae, ao, we, wo); break;
+        case 7: block_mma<7>(acc, blk, wp, ae, ao, we, wo); break;
+        default: block_mma<8>(acc, blk, wp, ae, ao, we, wo); break;
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
@@ -600,16 +611,16 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
   if (xe && !(A.fmt == 2 && A.b == 64 && A.tma && k + 1 <= 64)) return cudaErrorInvalidValue;  // callers check
   if (A.fmt == 2 && A.b == 64 && A.tma && k <= 64) {
     // the values as a 3-D tensor {16 rows, 4 row quarters, nnzb * 64 columns} (strides 128 B, 512 B):
-    // one box {16, 4, 64} = one 32 KB block, landed with the 128-byte swizzle (see swz_off)
+    // box {16, 1, 64} = one row quarter of a block (8 KB), landed with the 128-byte swizzle (swz_off)
     CUtensorMap tm;
     const cuuint64_t dims[3] = {16, 4, (cuuint64_t)A.nnz * 64};
     const cuuint64_t strides[2] = {16 * 8, 64 * 8};
-    const cuuint32_t box[3] = {16, 4, 64}, estr[3] = {1, 1, 1};
+    const cuuint32_t box[3] = {16, 1, 64}, estr[3] = {1, 1, 1};  // one row quarter of a block (8 KB)
     if (cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A.v, dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-    constexpr int smem = BNS * BSTAGE + 2 * 64 * 68 * 8 + 1024;  // + alignment slack for the 1024-byte ring base
+    constexpr int smem = BNS * BSTAGE + 2 * 64 * WSPK * 8 + 1024;  // + alignment slack for the 1024-byte ring base
     static bool attr_set[MAXDEV] = {};
     const int dev = current_device();
     if (!attr_set[dev]) {
