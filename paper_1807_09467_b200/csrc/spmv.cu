@@ -344,11 +344,10 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 }
 
 // acc[g] += A_block(rows 8w.., :) * W_panel(:, 8g..8g+7), g < NG.  W panel stored k-major [kk][n] with
-// stride WSPK = 66 (== 2 mod 16: the B elements W(kcol(s, j), 8g + i) of a half-warp, i < 4, j < 4, land in
-// 16 distinct banks pairs).  ae / ao: this lane's A element of k-steps 0 / 1 (k-step s adds 128 (s / 2));
-// we / wo: its W element of k-steps 0 / 1 (+ 8 * WSPK (s / 2) + 8 g).
-constexpr int WSPK = 66;
-template <int NG>
+// stride WS == 2 mod 16 (the B elements W(kcol(s, j), 8g + i) of a half-warp, i < 4, j < 4, land in 16
+// distinct bank pairs).  ae / ao: this lane's A element of k-steps 0 / 1 (k-step s adds 128 (s / 2));
+// we / wo: its W element of k-steps 0 / 1 (+ 8 WS (s / 2) + 8 g).
+template <int NG, int WS>
 __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int ae, int ao,
                                           int we, int wo) {
   // CH independent accumulator chains per column group hide the DMMA latency when NG is small
@@ -364,7 +363,7 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
     for (int c = 0; c < CH; ++c) {
       const int s = s0 + c;
       const double av = blk[((s & 1) ? ao : ae) + 128 * (s >> 1)];          // A(rrow, kcol(s, lane%4))
-      const int wb = ((s & 1) ? wo : we) + 8 * WSPK * (s >> 1);
+      const int wb = ((s & 1) ? wo : we) + 8 * WS * (s >> 1);
 #pragma unroll
       for (int g = 0; g < NG; ++g) dmma884(ch[g][c][0], ch[g][c][1], av, wp[wb + 8 * g]);  // W(kcol, 8g + lane/4)
     }
@@ -380,6 +379,17 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
 
 // xe != nullptr: one extra input column (panel column k) whose product goes to ye (y = A x0 of the
 // solve start, fused with C = A W: one read of A instead of two).
+//
+// Pipeline: the producer warp streams, per block of the CTA's sequence, the 32 KB block (lane 0: four
+// tensor-map TMA copies, complete_tx) AND the block column's 64 x k panel of W (all 32 lanes:
+// cp.async 8-byte copies into the stage's k-major panel, completion tracked by the same mbarrier via
+// cp.async.mbarrier.arrive.noinc) into an NST-stage ring; the 8 consumer warps only wait on the
+// stage's full barrier, run the DMMAs out of shared memory and release the stage.  No global load
+// and no CTA-wide barrier on the consumer side.  (Previous version: consumers prefetched the next
+// panel through registers with a dependent column-index load and a named barrier per block; ncu r02
+// showed them stalled on that load chain and the barrier: 1.79 ms for one 7.3 GB read of A.)
+// WS: k-major panel stride (== 2 mod 16, >= the panel width k + [xe]); NST: stages.
+template <int NST, int WS>
 __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ CUtensorMap tmA, MatDev A,
                                                         const double* __restrict__ W, double* Y,
                                                         int64_t ld, int k, DevState* pst, unsigned* counter,
@@ -390,11 +400,14 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
   // the 128-byte swizzle repeats every 1024 bytes: the ring starts on a 1024-byte boundary (pointer
   // arithmetic on smraw keeps the shared address space: LDS, not generic loads)
   double* ring = smraw + ((1024u - (su32(smraw) & 1023u)) & 1023u) / 8u;
-  __shared__ __align__(8) uint64_t full[BNS], empty[BNS];
+  double* wpan = ring + (size_t)NST * (BSTAGE / 8);  // NST x [64 k-rows][WS]
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < NST * 64 * WS; e += BT) wpan[e] = 0.0;  // pad columns [k, 8 ng) stay zero
   if (tid == 0) {
-    for (int i = 0; i < BNS; ++i) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(1));
+    for (int i = 0; i < NST; ++i) {
+      // full: lane 0's expect_tx arrival + the 32 producer lanes' cp.async completions (+ TMA bytes)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&full[i])), "r"(33));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&empty[i])), "r"(BT_CONS / 32));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -404,13 +417,14 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
   if (xe) k += 1;                    // + the extra column
   const int ng = (k + 7) / 8;
   if (wid == BT_CONS / 32) {
-    if (lane == 0) {
-      int t = 0;
-      for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
-        const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
-        for (int32_t p = p0; p < p1; ++p, ++t) {
-          const int s = t % BNS;
-          if (t >= BNS) bar_wait(&empty[s], (uint32_t)((t / BNS - 1) & 1));
+    // ---- producer warp
+    int t = 0;
+    for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
+      const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
+      for (int32_t p = p0; p < p1; ++p, ++t) {
+        const int s = t % NST;
+        if (t >= NST) bar_wait(&empty[s], (uint32_t)((t / NST - 1) & 1));
+        if (lane == 0) {
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
 #pragma unroll
           for (int q = 0; q < 4; ++q)  // row quarter q -> slice q of the stage (8 KB, 1024-byte aligned)
@@ -419,78 +433,49 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
                          ::"r"(su32(ring + (size_t)s * (BSTAGE / 8) + q * 1024)), "l"(&tmA), "r"(0), "r"(q), "r"(p * 64),
                          "r"(su32(&full[s])) : "memory");
         }
+        const int64_t J64 = (int64_t)__ldg(A.ci + p) * 64;
+        const uint32_t pan = su32(wpan + (size_t)s * 64 * WS);
+        for (int e = lane; e < 64 * k; e += 32) {  // W(J64 + kk, n) -> panel[kk][n]; coalesced per column
+          const int kk = e & 63, n = e >> 6;
+          const double* src = n < kw ? W + (int64_t)n * ld + J64 + kk : xe + J64 + kk;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(pan + 8u * (uint32_t)(kk * WS + n)), "l"(src)
+                       : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s])) : "memory");
       }
     }
     return;
   }
-  // consumers: W panel of block t in shared memory (double-buffered, stride WSP), the next panel
-  // is prefetched into registers while block t's DMMAs run.
-  double* wpan = ring + (size_t)BNS * (BSTAGE / 8);          // 2 x 64 k-rows x WSPK
+  // ---- consumers
   const int rrow = wid * 8 + (lane >> 2);                    // A fragment row inside the block
   const int ae = swz_off(rrow, kcol(0, lane & 3)), ao = swz_off(rrow, kcol(1, lane & 3));
-  const int we = kcol(0, lane & 3) * WSPK + (lane >> 2), wo = kcol(1, lane & 3) * WSPK + (lane >> 2);
-  const int nval = 64 * k;                                   // panel values
-  constexpr int PPT = (64 * 64 + BT_CONS - 1) / BT_CONS;     // panel values per thread (<= 16)
-  // first block of this CTA
+  const int we = kcol(0, lane & 3) * WS + (lane >> 2), wo = kcol(1, lane & 3) * WS + (lane >> 2);
+  int t = 0;
   int64_t I = blockIdx.x;
   int32_t p = I < A.nb ? __ldg(A.rp + I) : 0, pend = I < A.nb ? __ldg(A.rp + I + 1) : 0;
-  double pre[PPT];
-  auto load_panel = [&](int32_t pp) {
-    const int64_t wr = (int64_t)__ldg(A.ci + pp) * 64;
-#pragma unroll
-    for (int u = 0; u < PPT; ++u) {
-      const int e = tid + u * BT_CONS;
-      const int col = e >> 6;
-      pre[u] = e >= nval ? 0.0 : col < kw ? __ldg(W + (int64_t)col * ld + wr + (e & 63)) : __ldg(xe + wr + (e & 63));
-    }
-  };
-  auto store_panel = [&](int buf) {
-#pragma unroll
-    for (int u = 0; u < PPT; ++u) {
-      const int e = tid + u * BT_CONS;
-      if (e < nval) wpan[(size_t)buf * 64 * WSPK + (e & 63) * WSPK + (e >> 6)] = pre[u];   // [kk][n]
-    }
-  };
-  if (I < A.nb && p < pend) {
-    load_panel(p);
-    store_panel(0);
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
-  int t = 0;
   for (; I < A.nb; I += gridDim.x) {
+    const int64_t In = I + gridDim.x;  // the next block row's range, loaded early
+    const int32_t pn = In < A.nb ? __ldg(A.rp + In) : 0, pendn = In < A.nb ? __ldg(A.rp + In + 1) : 0;
     double acc[8][2];
 #pragma unroll
     for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
     for (; p < pend; ++p, ++t) {
-      // next block in this CTA's sequence (same block row, or the first block of the next one)
-      int32_t pn = p + 1;
-      int64_t In = I;
-      int32_t pendn = pend;
-      if (pn >= pend) {
-        In = I + gridDim.x;
-        pn = In < A.nb ? __ldg(A.rp + In) : 0;
-        pendn = In < A.nb ? __ldg(A.rp + In + 1) : 0;
-      }
-      const bool has_next = In < A.nb && pn < pendn;
-      if (has_next) load_panel(pn);
-      const int st = t % BNS;
-      bar_wait(&full[st], (uint32_t)((t / BNS) & 1));
+      const int st = t % NST;
+      bar_wait(&full[st], (uint32_t)((t / NST) & 1));
       const double* blk = ring + (size_t)st * (BSTAGE / 8);
-      const double* wp = wpan + (size_t)(t & 1) * 64 * WSPK;
+      const double* wp = wpan + (size_t)st * 64 * WS;
       switch (ng) {  // exact trip count: predicated-off DMMAs still occupy the tensor pipe
-        case 1: block_mma<1>(acc, blk, wp, ae, ao, we, wo); break;
-        case 2: block_mma<2>(acc, blk, wp, ae, ao, we, wo); break;
-        case 3: block_mma<3>(acc, blk, wp, ae, ao, we, wo); break;
-        case 4: block_mma<4>(acc, blk, wp, ae, ao, we, wo); break;
-        case 5: block_mma<5>(acc, blk, wp, ae, ao, we, wo); break;
-        case 6: block_mma<6>(acc, blk, wp, ae, ao, we, wo); break;
-        case 7: block_mma<7>(acc, blk, wp, ae, ao, we, wo); break;
-        default: block_mma<8>(acc, blk, wp, ae, ao, we, wo); break;
+        case 1: block_mma<1, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        case 2: block_mma<2, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        case 3: block_mma<3, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        case 4: block_mma<4, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        case 5: block_mma<5, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        case 6: block_mma<6, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        case 7: block_mma<7, WS>(acc, blk, wp, ae, ao, we, wo); break;
+        default: block_mma<8, WS>(acc, blk, wp, ae, ao, we, wo); break;
       }
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
-      if (has_next) store_panel((t + 1) & 1);
-      asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
     }
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
@@ -503,9 +488,8 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
         else if (col + 1 == kw && xe) ye[row] = acc[g][1];
       }
     }
-    const int64_t In = I + gridDim.x;
-    p = In < A.nb ? __ldg(A.rp + In) : 0;
-    pend = In < A.nb ? __ldg(A.rp + In + 1) : 0;
+    p = pn;
+    pend = pendn;
   }
   if (pst && pst->profile) {
     asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
@@ -620,15 +604,21 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
-    constexpr int smem = BNS * BSTAGE + 2 * 64 * WSPK * 8 + 1024;  // + alignment slack for the 1024-byte ring base
+    // panel stride (== 2 mod 16, >= the panel width) and ring depth within ~200 KB of shared memory
+    const int width = k + (xe ? 1 : 0);
     static bool attr_set[MAXDEV] = {};
     const int dev = current_device();
+    auto smem_of = [](int nst, int ws) { return nst * BSTAGE + nst * 64 * ws * 8 + 1024; };  // + 1024-byte alignment slack
     if (!attr_set[dev]) {
-      cudaFuncSetAttribute(k_spmm_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(k_spmm_bsr_tma<4, 18>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(4, 18));
+      cudaFuncSetAttribute(k_spmm_bsr_tma<4, 34>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(4, 34));
+      cudaFuncSetAttribute(k_spmm_bsr_tma<3, 66>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_of(3, 66));
       attr_set[dev] = true;
     }
-    int64_t g = A.nb < NSM ? A.nb : NSM;
-    k_spmm_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, smem, s>>>(tm, A, W, Y, ld, k, st, counter, xe, ye);
+    const int g = (int)(A.nb < NSM ? (A.nb < 1 ? 1 : A.nb) : NSM);
+    if (width <= 18) k_spmm_bsr_tma<4, 18><<<g, BT, smem_of(4, 18), s>>>(tm, A, W, Y, ld, k, st, counter, xe, ye);
+    else if (width <= 34) k_spmm_bsr_tma<4, 34><<<g, BT, smem_of(4, 34), s>>>(tm, A, W, Y, ld, k, st, counter, xe, ye);
+    else k_spmm_bsr_tma<3, 66><<<g, BT, smem_of(3, 66), s>>>(tm, A, W, Y, ld, k, st, counter, xe, ye);
     return cudaGetLastError();
   }
   if (A.fmt == 2) return cudaErrorNotSupported;  // caller falls back to per-column SpMV
