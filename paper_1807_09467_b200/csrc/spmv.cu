@@ -417,32 +417,62 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
   if (xe) k += 1;                    // + the extra column
   const int ng = (k + 7) / 8;
   if (wid == BT_CONS / 32) {
-    // ---- producer warp
-    int t = 0;
-    for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
-      const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
-      for (int32_t p = p0; p < p1; ++p, ++t) {
-        const int s = t % NST;
-        if (t >= NST) bar_wait(&empty[s], (uint32_t)((t / NST - 1) & 1));
-        if (lane == 0) {
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
-#pragma unroll
-          for (int q = 0; q < 4; ++q)  // row quarter q -> slice q of the stage (8 KB, 1024-byte aligned)
-            asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-                         "[%0], [%1, {%2, %3, %4}], [%5];"
-                         ::"r"(su32(ring + (size_t)s * (BSTAGE / 8) + q * 1024)), "l"(&tmA), "r"(0), "r"(q), "r"(p * 64),
-                         "r"(su32(&full[s])) : "memory");
-        }
-        const int64_t J64 = (int64_t)__ldg(A.ci + p) * 64;
-        const uint32_t pan = su32(wpan + (size_t)s * 64 * WS);
-        for (int e = lane; e < 64 * k; e += 32) {  // W(J64 + kk, n) -> panel[kk][n]; coalesced per column
-          const int kk = e & 63, n = e >> 6;
-          const double* src = n < kw ? W + (int64_t)n * ld + J64 + kk : xe + J64 + kk;
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(pan + 8u * (uint32_t)(kk * WS + n)), "l"(src)
-                       : "memory");
-        }
-        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s])) : "memory");
+    // ---- producer warp.  The block sequence (block rows I = blockIdx, +gridDim, ...; blocks p of each)
+    // is walked one block AHEAD: the next block's column index (and the next block row's range) are
+    // loaded while the current block's copies are issued, so no dependent global load sits between
+    // two blocks' copies.  A streams through L2 with evict-first (read once); the W panels (re-read by
+    // the ~7 block rows that touch a block column) keep the normal policy.
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    int64_t I = blockIdx.x;
+    int32_t p = 0, pend = 0;
+    auto next_block = [&](int64_t& Ib, int32_t& pb, int32_t& pe) -> bool {  // successor in the sequence
+      ++pb;
+      while (pb >= pe) {
+        Ib += gridDim.x;
+        if (Ib >= A.nb) return false;
+        pb = __ldg(A.rp + Ib);
+        pe = __ldg(A.rp + Ib + 1);
       }
+      return true;
+    };
+    bool have = false;
+    if (I < A.nb) {
+      p = __ldg(A.rp + I) - 1;
+      pend = __ldg(A.rp + I + 1);
+      have = next_block(I, p, pend);
+    }
+    int32_t ci_cur = have ? __ldg(A.ci + p) : 0;
+    for (int t = 0; have; ++t) {
+      int64_t I2 = I;
+      int32_t p2 = p, pe2 = pend;
+      const bool have2 = next_block(I2, p2, pe2);
+      const int32_t ci_next = have2 ? __ldg(A.ci + p2) : 0;  // consumed next iteration
+      const int s = t % NST;
+      if (t >= NST) bar_wait(&empty[s], (uint32_t)((t / NST - 1) & 1));
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(BSTAGE) : "memory");
+#pragma unroll
+        for (int q = 0; q < 4; ++q)  // row quarter q -> slice q of the stage (8 KB, 1024-byte aligned)
+          asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+                       "[%0], [%1, {%2, %3, %4}], [%5], %6;"
+                       ::"r"(su32(ring + (size_t)s * (BSTAGE / 8) + q * 1024)), "l"(&tmA), "r"(0), "r"(q), "r"(p * 64),
+                       "r"(su32(&full[s])), "l"(pol) : "memory");
+      }
+      const int64_t J64 = (int64_t)ci_cur * 64;
+      const uint32_t pan = su32(wpan + (size_t)s * 64 * WS);
+      for (int e = lane; e < 64 * k; e += 32) {  // W(J64 + kk, n) -> panel[kk][n]; coalesced per column
+        const int kk = e & 63, n = e >> 6;
+        const double* src = n < kw ? W + (int64_t)n * ld + J64 + kk : xe + J64 + kk;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(pan + 8u * (uint32_t)(kk * WS + n)), "l"(src)
+                     : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s])) : "memory");
+      I = I2;
+      p = p2;
+      pend = pe2;
+      ci_cur = ci_next;
+      have = have2;
     }
     return;
   }
