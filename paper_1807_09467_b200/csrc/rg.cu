@@ -882,7 +882,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   // BSR-64 solves on the graph path (C5): the start residual's product A x0 rides along as one
   // extra column of the C = A W SpMM — one read of A (7.3 GB at C5) instead of two per system.
   static const bool no_fuse_res = knob("RG_NO_FUSE_RES");
-  c->res_fused = need_c && !no_fuse_res && c->A.fmt == 2 && c->A.b == 64 && c->A.tma && k + 1 <= 64 &&
+  // (x0 == NULL: A x0 = 0 needs no product at all — the first cycle start forms r = b directly, below)
+  c->res_fused = x0 && need_c && !no_fuse_res && c->A.fmt == 2 && c->A.b == 64 && c->A.tma && k + 1 <= 64 &&
                  !(c->use_persist && persist_size && c->dcgs_now && !(c->flags & RG_FLAG_NO_GRAPH));
   const bool early_in = c->res_fused;  // b and x0 in the library's buffers before the SpMM reads x0
   if (early_in) {
@@ -961,7 +962,13 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   }
   if (!done_persist) {
     CK(launch_orth(c->L, c->st, OP_NORMB, s));
-    const bool from_y = c->res_fused;
+    // start residual r = b - y with y = A x0 in V column 0: y from the fused SpMM, or y = 0 when
+    // x0 = 0 (no SpMV of a zero vector: one read of A saved per solve, 7.3 GB at C5)
+    bool from_y = c->res_fused;
+    if (!x0 && !from_y) {
+      CK(cudaMemsetAsync(c->Z + (int64_t)c->L.VB * c->npad, 0, sizeof(double) * c->npad, s));
+      from_y = true;
+    }
     c->res_fused = false;
     CK(cycle_start(c, eff, from_y));
     if ((rs = run_solve(c, eff, m)) != RG_OK) return rs;
