@@ -1,4 +1,6 @@
-# A/B of environment settings on the bench: tools/ab_env.sh "<bench args>" "ENV1" "ENV2" ... (ENV "-" = none)
+# A/B of bench settings: tools/ab.sh "<bench args>" "VAR=1" "-" ...  ("-": no extra environment).
+# The library's environment knobs (csrc/knobs.cuh) are compiled out of product builds: build the A/B
+# library first with `make rg EXPERIMENTS=1` (and rebuild with plain `make rg` afterwards).
 A="$1"; shift
 for rep in 1 2; do for e in "$@"; do
   ee=$e; [ "$e" = "-" ] && ee=""
