@@ -6,6 +6,7 @@
 // the host reads one 4-byte-class header per cycle to learn whether the solve has finished.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a profiler is attached
 
 #include <algorithm>
 #include <atomic>
@@ -70,6 +71,14 @@ constexpr int64_t PERSIST_MAX_ROWS = 1600000;
 }  // namespace
 
 void rg::note_host_launches(int n) { g_host_launches += n; }
+
+namespace {
+// NVTX range per C-ABI call (SURVEY §5 tracing): nsys / ncu --nvtx show rg_solve, rg_build_recycle, ...
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 struct rg_ctx {
   int dev = 0;
@@ -695,6 +704,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
 }
 
 RG_API rg_status rg_update_matrix(rg_ctx* c, const rg_matrix* A) {
+  NvtxRange nvtx_("rg_update_matrix");
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
   rg_status s = check_desc(A, c->n, false);
   if (s != RG_OK) return s;
@@ -712,6 +722,7 @@ RG_API rg_status rg_matrix_values(rg_ctx* c, double** values, int64_t* len) {
 }
 
 RG_API rg_status rg_push_snapshot(rg_ctx* c, const double* x, rg_mem mem) {
+  NvtxRange nvtx_("rg_push_snapshot");
   if (!c || !x) return fail(RG_E_INVAL, "NULL argument");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
   rg_status s = copy_in(c->X + (int64_t)c->s_head * c->npad, x, sizeof(double) * c->n, mem, c->stream);
@@ -776,6 +787,7 @@ RG_API rg_status rg_build_recycle(rg_ctx* c, int32_t k, int32_t* k_eff, double* 
 }
 
 RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int32_t* k_eff, double* sigma) {
+  NvtxRange nvtx_("rg_build_recycle_modes");
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
   if (modes != RG_MODES_LARGEST && modes != RG_MODES_SMALLEST) return fail(RG_E_INVAL, "unknown modes");
   if (k < 1 || k > c->max_k) return fail(RG_E_INVAL, "k must be in 1..max_k");
@@ -835,6 +847,7 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
 RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t m, rg_variant v, double tol,
                           int32_t max_iters, double* x_out, rg_mem mem, double* history, int32_t history_cap,
                           rg_report* rep) {
+  NvtxRange nvtx_("rg_solve");
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
   if (!b || !x_out) return fail(RG_E_INVAL, "b and x_out are required");
   if (m < 1 || m > c->max_m) return fail(RG_E_INVAL, "m must be in 1..max_m");
@@ -1042,6 +1055,7 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
 }
 
 RG_API rg_status rg_apply(rg_ctx* c, const double* x, double* y, rg_mem mem) {
+  NvtxRange nvtx_("rg_apply");
   if (!c || !x || !y) return fail(RG_E_INVAL, "NULL argument");
   if (mem != RG_HOST && mem != RG_DEVICE) return fail(RG_E_INVAL, "unknown memory kind");
   rg_status s = copy_in(c->t1, x, sizeof(double) * c->n, mem, c->stream);
