@@ -207,13 +207,15 @@ class ClockSampler:
 class GpuRun:
     """One replica: the library context plus the device-side sequence generator."""
 
-    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None, sync_build=False, flags=0):
+    def __init__(self, cfg, variant, k, device, stream, profile, sell, precond=None, sync_build=False, flags=0,
+                 warm=False):
         import torch
 
         import synth
         from paper_1807_09467_b200 import Context, rg
         self.torch, self.cfg, self.variant, self.k = torch, cfg, variant, k
         self.sync_build = sync_build   # True: rg_build_recycle returns k_eff, sigma (host sync)
+        self.warm = warm               # True: x0 = x_{t-1} (SURVEY A4's warm-started reference row)
         self.dev = device
         self.stream = stream
         self.gen = synth.DeviceSequence(cfg, device)
@@ -252,7 +254,8 @@ class GpuRun:
                 self.k_eff, self.sigma = self.ctx.build_recycle(self.k)
             else:                                      # a3, asynchronous (a4 happens inside the solve)
                 self.ctx.build_recycle(self.k, deferred=True)
-        rep = self.ctx.solve(self.gen.b, self.x, m=cfg.m, variant=self.variant, tol=cfg.tol, history_cap=history_cap)
+        rep = self.ctx.solve(self.gen.b, self.x, x0=self.x if self.warm else None, m=cfg.m, variant=self.variant,
+                             tol=cfg.tol, history_cap=history_cap)
         if not rep["converged"]:
             raise RuntimeError(f"system {self.t} did not converge: {rep}")
         self.ctx.push_snapshot(self.x if push is None else push)   # a2
@@ -438,11 +441,25 @@ def run_ours(args, cfg):
                                              between=lambda: flush_l2(flush), stream=stream)
             pits = prun.iters[args.warmup:]
             prun.ctx.close()
+            # warm-started plain GMRES(m): x0 = x_{t-1} (the paper compares initial guesses,
+            # PAPER.md:405-436, Table 2)
+            wrun = GpuRun(cfg, "plain", k, device, stream, profile=False, sell=sell,
+                          precond=args.omega if args.precond == "ssor" else None, warm=True)
+            for _ in range(args.warmup):
+                wrun.step()
+            torch.cuda.synchronize()
+            _, _, wt_max = timed_replicas(wrun.step, args.steps, 0, dist_on, device, "cuda",
+                                          between=lambda: flush_l2(flush), stream=stream)
+            wits = wrun.iters[args.warmup:]
+            wrun.ctx.close()
             vs_plain = {"variant": "plain", "value": pt_max / (args.steps * ws), "unit": UNIT,
                         "sequence_s": pt_max, "iterations_timed": pits,
                         "iterations_total": sum(pits), "recycled_iterations_total": sum(timed_iters),
                         "recycled_sequence_s": t_max,
                         "sequence_speedup": round(pt_max / t_max, 4),
+                        "warm_plain": {"value": wt_max / (args.steps * ws), "unit": UNIT, "sequence_s": wt_max,
+                                       "iterations_total": sum(wits), "sequence_speedup": round(wt_max / t_max, 4),
+                                       "scope": "plain GMRES(m) with x0 = x_{t-1} (SURVEY A4), same systems"},
                         "scope": "the same systems t of a free-running plain GMRES(m) sequence (its own "
                                  "x_{t-1} drives A_t, b_t), timed like the main line"}
 
