@@ -31,7 +31,8 @@ constexpr int VEC_CTAS_PER_SM = 2;         // -> 296 CTAs: 32 resident warps / S
 enum KernelId {
   K_SPMV_STEP = 0, K_SPMV_RES, K_SPMV_PLAIN, K_ORTH_D1, K_ORTH_UD2, K_ORTH_UN, K_CS_DQ, K_CS_UN,
   K_XW, K_XUPD, K_NORMB, K_GRAM, K_JACOBI, K_XM, K_CHOL, K_MISC, K_DK1, K_DK2,
-  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_SSOR, K_PB6, K_COND, K_SSORK, K_PB7, K_CBUILD, K_RES_Y, K_COUNT
+  K_PB1, K_PB2, K_PB3, K_PB4, K_PB5, K_OBD, K_OBU, K_SSOR, K_PB6, K_COND, K_SSORK, K_PB7, K_CBUILD, K_RES_Y, K_DLS,
+  K_COUNT
 };
 
 struct KStatDev {
@@ -82,6 +83,11 @@ struct DevState {
   double coefv[MAXCOL];            // DCGS2: v_j = u/nu + sum_c coefv_c P_c
   KStatDev kstat[K_COUNT];
   unsigned red_epoch;              // persistent solve: last flag value of its flag-carrying reductions
+  // graph-path DCGS2 split epilogue: DK1's last CTA leaves the least-squares step of column ls_j to
+  // k_dcgs_ls (which runs concurrently with DK2): its input [Q^T v (augment) | ||v||^2]; k2_skip: no
+  // update pass this step (j = m: no next column)
+  int ls_j, k2_skip;
+  double ls_in[MAXK + 2];
 };
 
 // Basis layout (constant per context).  Z is n_pad x MAXCOL... column-major with leading

@@ -41,7 +41,6 @@ constexpr int DK1RED = 2 * (MAXK + MAXM) + 2 + 2 * MAXK;
 // tot = [a (p) | b (p) | s | g | q (k, augment) or W^T y (k), C^T u (k) (oblique)],
 // P = columns [lo, VB + j).
 __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p) {
-  __shared__ double lst[MAXK + 2];
   __shared__ double Ha[MAXM + 2], Ba[MAXK], ob_t[MAXK], ob_ct[MAXM + 2];
   __shared__ double s_nu, s_d, s_aj;
   __shared__ int s_go;
@@ -72,31 +71,38 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   const double ab = s_d;
   const double nu = s_nu;
   if (j >= 1) {
-    // finish column j-1: second-pass coefficients a (V part -> H, Q part -> B via hcol)
+    // finish column j-1: second-pass coefficients a (V part -> H, Q part -> B via hcol), stored as
+    // H-bar column j-1 (rows 0..j, h_{j,j-1} = nu) and B column j-1; the least-squares step on that
+    // column (Givens, stop test, history) is left to k_dcgs_ls, which runs concurrently with DK2: it
+    // gates only the NEXT step, and nothing DK2 needs depends on it (split epilogue: the last-CTA
+    // tail of this kernel no longer holds the whole GPU for the serial Givens chain)
     for (int c = tid; c < p; c += bd) st->hcol[lo + c] += a[c];
-    if (var == RG_AUGMENT && k > 0) {  // Q^T v_j = (Q^T u - G_j^T a_V) / nu, handed to epi_ls as (.)*nu
+    __syncthreads();
+    for (int i = tid; i < j; i += bd) st->Hraw[j - 1][i] = st->hcol[VB + i];
+    if (var == RG_DEFLATE)
+      for (int l = tid; l < k; l += bd) st->Bm[j - 1][l] = st->hcol[QB + l];
+    if (var == RG_AUGMENT && k > 0) {  // Q^T v_j = (Q^T u - G_j^T a_V) / nu, handed to the LS step as (.)*nu
       for (int l = tid; l < k; l += bd) {
         double q = tot[2 * p + 2 + l];
         for (int i = 0; i < j; ++i) q -= st->Gm[i][l] * a[nq + i];
-        lst[l] = q;
+        st->ls_in[l] = q;
       }
     }
     if (tid == 0) {
-      lst[(var == RG_AUGMENT) ? k : 0] = nu * nu;
-      st->j = j - 1;
-    }
-    __syncthreads();
-    epi_ls(st, L, lst, (var == RG_AUGMENT) ? k : 0);
-    if (tid == 0) {
+      st->Hraw[j - 1][j] = nu;
+      st->ls_in[(var == RG_AUGMENT) ? k : 0] = nu * nu;
+      st->ls_j = j - 1;
       st->sc[VB + j] = 1.0;  // DK2 writes v_j normalised
-      s_go = st->active;
     }
-    __syncthreads();
-    if (!s_go) return;
-  } else {
-    if (tid == 0) s_go = 1;
-    __syncthreads();
+  } else if (tid == 0) {
+    st->ls_j = -1;
   }
+  if (tid == 0) {
+    s_go = j < st->m;        // j = m: no next column (DK2 would write past the basis)
+    st->k2_skip = !s_go;
+  }
+  __syncthreads();
+  if (!s_go) return;
   // ---- coefficients of DK2 and the first-pass coefficients of column j
   const double inv = nu > 0.0 ? 1.0 / nu : 0.0;
   const bool obl = galerkin_variant(var) && k > 0;  // oblique / orthogonal (P = C / W, T = E^{-1} / I)
@@ -179,10 +185,28 @@ __device__ __forceinline__ void dk1_finish(const Layout& L, DevState* st, double
   prof_tail(st, K_DK1);
   epi_dcgs(st, L, tot, p);
   if (threadIdx.x == 0) {
-    if (st->active) st->j = j + 1;  // next iteration (DK2 of this one uses st->j - 1)
-    if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
+    st->j = j + 1;  // next iteration (DK2 of this one uses st->j - 1); k_dcgs_ls decides whether it runs
+    (void)cond;     // the WHILE condition is set by k_dcgs_ls
     prof_end(st, K_DK1, 8.0 * (double)L.n * (p + nqd + (have_y ? 2 : 1)));
   }
+}
+
+// ---------------------------------------------------------------- the least-squares step (split epilogue)
+// Column st->ls_j of the cycle (finished by DK1): Givens / M = T H update, history, stop test, and at a
+// stop the cycle-end coefficients (epi_ls).  Runs on a side branch of the graph, concurrently with DK2;
+// the graph joins both before the next step, whose launch this kernel's WHILE condition gates.
+__global__ void __launch_bounds__(256) k_dcgs_ls(Layout L, DevState* st, unsigned long long cond) {
+  __shared__ double lst[MAXK + 2];
+  const int jx = st->ls_j;
+  if (jx >= 0) {
+    if (st->profile && threadIdx.x == 0) st->kstat[K_DLS].start = gtimer();
+    const int nd = st->variant == RG_AUGMENT ? st->k_eff : 0;
+    for (int i = threadIdx.x; i <= nd; i += blockDim.x) lst[i] = st->ls_in[i];
+    __syncthreads();
+    epi_ls(st, L, lst, nd, jx);
+    if (threadIdx.x == 0) prof_end(st, K_DLS, 0.0);
+  }
+  if (cond && threadIdx.x == 0) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------- DK1: dots of u and y with P
@@ -368,7 +392,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, un
 // ---------------------------------------------------------------- DK2: v_j and the next u
 __global__ void __launch_bounds__(DT, 2) k_dk2(Layout L, DevState* st) {
   __shared__ double cv[MAXCOL], cn[MAXCOL], cc2[MAXK];
-  if (!st->active) { prof_noop(st, K_DK2); return; }
+  if (st->k2_skip) { prof_noop(st, K_DK2); return; }  // (not st->active: k_dcgs_ls may be writing it)
   prof_begin(st, K_DK2);
   const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
@@ -595,7 +619,7 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk2_tma(Layout L, DevState* st) {
   __shared__ __align__(8) uint64_t full[TS_STG], empty[TS_STG];
   __shared__ double cv[MAXCOL + MAXK], cn[MAXCOL + MAXK];
   __shared__ int colidx[MAXCOL + MAXK];
-  if (!st->active) { prof_noop(st, K_DK2); return; }
+  if (st->k2_skip) { prof_noop(st, K_DK2); return; }  // (not st->active: k_dcgs_ls may be writing it)
   prof_begin(st, K_DK2);
   const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
@@ -706,6 +730,10 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
       k_dk1_stream<8, 1><<<vec_grid(L.ld), DT, smem, s>>>(L, st, cond, nvw);
     } else
       k_dk1<<<vec_grid(L.ld), DT, 0, s>>>(L, st, cond);
+    return cudaGetLastError();
+  }
+  if (phase == 3) {
+    k_dcgs_ls<<<1, 256, 0, s>>>(L, st, cond);
     return cudaGetLastError();
   }
   static const int tma = knob("RG_NO_TMA_DCGS") || knob("RG_NO_TMA_DK2") ? 0 : 1;

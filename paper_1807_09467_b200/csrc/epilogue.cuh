@@ -72,18 +72,22 @@ __device__ __forceinline__ void rcinv_apply(const DevState* st, int k, const dou
 // nd = k_eff), tot[nd] = ||w||^2 of the new (un-normalised) basis vector w = raw v_{j+1}.
 // Every global access is issued as a parallel batch (no serial chains of dependent loads);
 // the serial Givens recurrence runs in thread 0 from shared memory.
-__device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const double* tot, int nd) {
+// jx >= 0 (graph-path DCGS2 split epilogue, k_dcgs_ls): the column index is jx, its Hessenberg entries
+// h_0..h_jx come from Hraw[jx] (DK1's last CTA stored them with B), and the state DK1 owns is left alone
+// (the step index st->j, the column scales sc, Hraw / Bm).
+__device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const double* tot, int nd, int jx = -1) {
   __shared__ double h[MAXM + 2], mc[MAXM + 2], tv[MAXM + 2], csS[MAXM], snS[MAXM];
   __shared__ double ys[MAXM + 2], gs[MAXM + 2], us[MAXK], zs[MAXK], rd[MAXM + 2];
   __shared__ int s_stop, s_jf, s_tb;
   __shared__ double s_sc[8];
   __shared__ int s_ic[8];
   const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, nw = bd >> 5;
-  const int j = st->j, VB = L.VB, k = st->k_eff, var = st->variant;
+  const bool split = jx >= 0;
+  const int j = split ? jx : st->j, VB = L.VB, k = st->k_eff, var = st->variant;
   const int QB = VB - k;
   const double nrm = sqrt(tot[nd]);
   // ---- one parallel batch of loads: h column, rotations, scalars
-  for (int i = tid; i <= j; i += bd) h[i] = st->hcol[VB + i];
+  for (int i = tid; i <= j; i += bd) h[i] = split ? st->Hraw[j][i] : st->hcol[VB + i];
   for (int i = tid; i < j; i += bd) { csS[i] = st->cs[i]; snS[i] = st->sn[i]; }
   if (tid == 0) {
     h[j + 1] = nrm;
@@ -100,9 +104,11 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
     s_ic[4] = st->hist_cap;
   }
   __syncthreads();
-  for (int i = tid; i <= j + 1; i += bd) st->Hraw[j][i] = h[i];
-  if (var == RG_DEFLATE)
-    for (int l = tid; l < k; l += bd) st->Bm[j][l] = st->hcol[QB + l];
+  if (!split) {
+    for (int i = tid; i <= j + 1; i += bd) st->Hraw[j][i] = h[i];
+    if (var == RG_DEFLATE)
+      for (int l = tid; l < k; l += bd) st->Bm[j][l] = st->hcol[QB + l];
+  }
   if (var == RG_AUGMENT)
     for (int l = tid; l < k; l += bd) st->Gm[j + 1][l] = nrm > 0.0 ? tot[l] / nrm : 0.0;
   __syncthreads();
@@ -158,7 +164,7 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
     }
   }
   if (tid == 0) {
-    st->sc[VB + j + 1] = nrm > 0.0 ? 1.0 / nrm : 0.0;
+    if (!split) st->sc[VB + j + 1] = nrm > 0.0 ? 1.0 / nrm : 0.0;
     const double bnorm = s_sc[1], tol = s_sc[2], beta = s_sc[3];
     int iters = s_ic[1];
     int stop = 0, jf = j;
@@ -200,7 +206,7 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
       }
     }
     st->iters = iters;
-    if (!stop) st->j = j + 1;
+    if (!stop && !split) st->j = j + 1;
     s_stop = stop;
     s_jf = jf;
     if (stop) {

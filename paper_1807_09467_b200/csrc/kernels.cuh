@@ -54,7 +54,8 @@ enum OrthOp {
 };
 // cond != 0: cudaGraphConditionalHandle set to st->active by OP_UN's epilogue (graph WHILE node)
 cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond = 0);
-// DCGS2 Arnoldi step (dcgs.cu): phase 1 = dots + epilogue (sets the WHILE condition), 2 = update
+// DCGS2 Arnoldi step (dcgs.cu): phase 1 = dots + coefficient epilogue, 2 = update pass, 3 = the
+// least-squares step of the finished column (one CTA, concurrent with phase 2; sets the WHILE condition)
 cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond = 0);
 // RG_FLAG_KEEP_BASIS: copy the finished cycle's V into L.keepV at the cycle end (before the x update)
 cudaError_t launch_keep_basis(const Layout& L, DevState* st, cudaStream_t s);

@@ -84,6 +84,8 @@ struct rg_ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t side = nullptr;     // DCGS2 split epilogue: k_dcgs_ls runs here, concurrently with DK2
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int flags = 0;
   int64_t n = 0, npad = 0;
   int max_m = 0, max_s = 0, max_k = 0;
@@ -454,9 +456,16 @@ cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
     if ((e = launch_orth(c->L, c->st, OP_OB_SD, c->stream)) != cudaSuccess) return e;
     if ((e = launch_orth(c->L, c->st, OP_OB_SU, c->stream)) != cudaSuccess) return e;
   }
-  if (c->dcgs_now) {  // delayed CGS2: one reduction + one update pass
-    if ((e = launch_dcgs(c->L, c->st, 1, c->stream, cond)) != cudaSuccess) return e;
-    return launch_dcgs(c->L, c->st, 2, c->stream);
+  if (c->dcgs_now) {  // delayed CGS2: one reduction + one update pass; the least-squares step of the
+                      // finished column on a side branch, concurrent with the update pass (joined
+                      // before the next step, which its WHILE condition gates)
+    if ((e = launch_dcgs(c->L, c->st, 1, c->stream)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(c->ev_fork, c->stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(c->side, c->ev_fork, 0)) != cudaSuccess) return e;
+    if ((e = launch_dcgs(c->L, c->st, 3, c->side, cond)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(c->ev_join, c->side)) != cudaSuccess) return e;
+    if ((e = launch_dcgs(c->L, c->st, 2, c->stream)) != cudaSuccess) return e;
+    return cudaStreamWaitEvent(c->stream, c->ev_join, 0);
   }
   if ((e = launch_orth(c->L, c->st, OP_D1, c->stream)) != cudaSuccess) return e;
   if ((e = launch_orth(c->L, c->st, OP_UD2, c->stream)) != cudaSuccess) return e;
@@ -585,6 +594,9 @@ RG_API void rg_destroy(rg_ctx* c) {
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->ebuild) cudaEventDestroy(c->ebuild);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -670,6 +682,9 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   ok(cudaEventCreate(&c->e0));
   ok(cudaEventCreate(&c->e1));
   ok(cudaEventCreateWithFlags(&c->ebuild, cudaEventDisableTiming));
+  ok(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  ok(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  ok(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   ok(cudaStreamSynchronize(c->stream));
   if (e != cudaSuccess) {
     rg_destroy(c);
@@ -1286,7 +1301,7 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
                                        "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
                                        "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
                                        "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
-                                       "ssor_sweep_kernels", "p_spmv", "cbuild", "res_from_ax"};
+                                       "ssor_sweep_kernels", "p_spmv", "cbuild", "res_from_ax", "dcgs_ls"};
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));
