@@ -384,7 +384,8 @@ def run_ours(args, cfg):
         from paper_1807_09467_b200 import rg as _rg
         run = GpuRun(cfg, args.variant, k, device, stream, profile=not args.no_profile, sell=sell,
                      precond=args.omega if args.precond == "ssor" else None,
-                     flags=_rg.RG_FLAG_NO_GRAPH if args.no_graph else 0)
+                     flags=(_rg.RG_FLAG_NO_GRAPH if args.no_graph else 0) |
+                           (_rg.RG_FLAG_NO_PERSIST if args.no_persist else 0))
         for _ in range(args.warmup):
             run.step()
         torch.cuda.synchronize()
@@ -577,6 +578,8 @@ def main(argv=None):
     ap.add_argument("--sell", type=int, default=-1, help="1: pack CSR to SELL-32 inside the library, "
                     "0: keep CSR, -1: config default")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-persist", action="store_true",
+                    help="RG_FLAG_NO_PERSIST: the CUDA-graph path even where the persistent kernel would run")
     ap.add_argument("--no-graph", action="store_true",
                     help="RG_FLAG_NO_GRAPH: launch the solve's kernels one by one (ncu cannot profile kernels "
                          "inside conditional CUDA graphs); for profiler captures, not for timing")

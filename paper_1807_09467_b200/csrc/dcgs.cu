@@ -743,7 +743,10 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
       cudaFuncSetAttribute(k_dk2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * TS_STG * TS_STAGE));
       attr = true;
     }
-    k_dk2_tma<<<tma_grid(L.ld), TS_T, sizeof(double) * TS_STG * TS_STAGE, s>>>(L, st);
+    // one SM left to the concurrent least-squares kernel (k_dcgs_ls) so that no update-pass CTA shares
+    // an SM with it
+    const int g2 = tma_grid(L.ld) == NSM ? NSM - 1 : tma_grid(L.ld);
+    k_dk2_tma<<<g2, TS_T, sizeof(double) * TS_STG * TS_STAGE, s>>>(L, st);
     return cudaGetLastError();
   }
   k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
