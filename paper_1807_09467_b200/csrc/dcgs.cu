@@ -496,11 +496,6 @@ __device__ __forceinline__ void ts_release(uint64_t* empty, int s) {
   if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ts_u32(&empty[s])) : "memory");
 }
 
-// DK1 stages carry DK1_CH basis columns AND the tile's u and y (slots DK1_CH, DK1_CH + 1): the chunk-outer
-// loop re-reads u, y once per chunk, and through TMA those re-reads (L2 hits) are in flight with the
-// basis stream instead of stalling each consumer on a register prefetch (ncu r02, C4 cold: 17 % of the
-// warp samples waited on the u / y prefetch, 0.61 of the copy peak).
-constexpr int DK1_CH = TS_CH - 2;
 __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, unsigned long long cond, int nvw) {
   extern __shared__ __align__(128) double ring[];   // [TS_STG][TS_STAGE], then per-warp partials [TS_R / 32][nvw]
   __shared__ __align__(8) uint64_t full[TS_STG], empty[TS_STG];
@@ -515,6 +510,8 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
   const int nqd = (var == RG_AUGMENT) ? k : (galerkin_variant(var) ? 2 * k : 0);
   const bool have_y = j < st->m;
   const int64_t ld = L.ld;
+  const double* __restrict__ u = L.Z + (int64_t)(VB + j) * ld;
+  const double* __restrict__ y = L.Z + (int64_t)(VB + j + 1) * ld;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nv = 2 * p + 2 + nqd, ncols = p + nqd;
   const bool obl = galerkin_variant(var);
@@ -524,61 +521,72 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
   const int64_t ng = ld >> 5;
   const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
   const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
-  const int nchunk = max(1, (ncols + DK1_CH - 1) / DK1_CH);  // one pass even without columns (u.u, u.y)
+  const int nchunk = (ncols + TS_CH - 1) / TS_CH;
   if (wid == TS_R / 32) {  // ---- producer (lane 0): chunk outer, row tile inner
     if (lane == 0) {
       const uint64_t pol = ts_policy(L.keep_l2 != 0);
-      uint64_t keep;  // u and y are re-read by every chunk: normal L2 priority
-      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(keep));
       int t = 0;
       for (int q = 0; q < nchunk; ++q)
-        for (int64_t base = r0; base < r1; base += TS_R, ++t) {
-          const int nc = max(0, min(DK1_CH, ncols - q * DK1_CH)), cnt = (int)min((int64_t)TS_R, r1 - base);
-          const int s = t % TS_STG;
-          if (t >= TS_STG) ts_wait(&empty[s], (uint32_t)((t / TS_STG - 1) & 1));
-          const uint32_t bytes = (uint32_t)((nc + (have_y ? 2 : 1)) * cnt * 8);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ts_u32(&full[s])), "r"(bytes) : "memory");
-          for (int c = 0; c < nc + 2; ++c) {
-            if (c == nc + 1 && !have_y) break;
-            const int col = c < nc ? colidx[q * DK1_CH + c] : VB + j + (c - nc);  // basis, then u, y
-            const int slot = c < nc ? c : DK1_CH + (c - nc);
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                         ::"r"(ts_u32(ring + (size_t)s * TS_STAGE + slot * TS_R)), "l"(L.Z + (int64_t)col * ld + base),
-                         "r"((uint32_t)(cnt * 8)), "r"(ts_u32(&full[s])), "l"(c < nc ? pol : keep) : "memory");
-          }
-        }
+        for (int64_t base = r0; base < r1; base += TS_R, ++t)
+          ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
+                   (int)min((int64_t)TS_R, r1 - base), pol);
     }
   } else {  // ---- consumers: thread = row of the tile
     double s_uu = 0.0, s_uy = 0.0;
     int t = 0;
-    for (int q = 0; q < nchunk; ++q) {
-      const int nc = max(0, min(DK1_CH, ncols - q * DK1_CH));
-      double su[DK1_CH], sy[DK1_CH];
+    // u, y of the tile TS_PF tiles ahead are loaded now (L2 hits, off the per-tile critical path);
+    // the tile sequence repeats per chunk, so "ahead" wraps to the start of the CTA's rows
+    constexpr int TS_PF = 3;
+    double upf[TS_PF], ypf[TS_PF];
+    int64_t bnext = r0;  // base of the next tile to prefetch
 #pragma unroll
-      for (int c = 0; c < DK1_CH; ++c) su[c] = sy[c] = 0.0;
-      for (int64_t base = r0; base < r1; base += TS_R, ++t) {
-        const bool ok = base + tid < r1;
-        const int stg = t % TS_STG;
-        ts_wait(&full[stg], (uint32_t)((t / TS_STG) & 1));
-        const double* zs = ring + (size_t)stg * TS_STAGE + tid;
-        const double ur = ok ? zs[DK1_CH * TS_R] : 0.0;
-        const double yr = (ok && have_y) ? zs[(DK1_CH + 1) * TS_R] : 0.0;
+    for (int i = 0; i < TS_PF; ++i) {
+      const int64_t rn = bnext + tid;
+      upf[i] = rn < r1 ? u[rn] : 0.0;
+      ypf[i] = (rn < r1 && have_y) ? y[rn] : 0.0;
+      bnext = bnext + TS_R < r1 ? bnext + TS_R : r0;
+    }
+    for (int q = 0; q < nchunk || q == 0; ++q) {
+      const int nc = min(TS_CH, ncols - q * TS_CH);
+      double su[TS_CH], sy[TS_CH];
+#pragma unroll
+      for (int c = 0; c < TS_CH; ++c) su[c] = sy[c] = 0.0;
+      for (int64_t base = r0; base < r1; base += TS_R) {
+        const int64_t r = base + tid;
+        const bool ok = r < r1;
+        const double ur = upf[0], yr = ypf[0];
+        {
+#pragma unroll
+          for (int i = 0; i + 1 < TS_PF; ++i) {
+            upf[i] = upf[i + 1];
+            ypf[i] = ypf[i + 1];
+          }
+          const int64_t rn = bnext + tid;
+          upf[TS_PF - 1] = rn < r1 ? u[rn] : 0.0;
+          ypf[TS_PF - 1] = (rn < r1 && have_y) ? y[rn] : 0.0;
+          bnext = bnext + TS_R < r1 ? bnext + TS_R : r0;
+        }
         if (q == 0) {
           s_uu += ur * ur;
           s_uy += ur * yr;
         }
+        if (nc <= 0) continue;
+        const int stg = t % TS_STG;
+        ts_wait(&full[stg], (uint32_t)((t / TS_STG) & 1));
+        const double* zs = ring + (size_t)stg * TS_STAGE + tid;
 #pragma unroll
-        for (int c = 0; c < DK1_CH; ++c) {
+        for (int c = 0; c < TS_CH; ++c) {
           const double z = (ok && c < nc) ? zs[c * TS_R] : 0.0;
           su[c] += z * ur;
           sy[c] += z * yr;
         }
         ts_release(empty, stg);
+        ++t;
       }
 #pragma unroll
-      for (int c = 0; c < DK1_CH; ++c) {
+      for (int c = 0; c < TS_CH; ++c) {
         const double a = warp_sum(su[c]), b = warp_sum(sy[c]);
-        const int cc = q * DK1_CH + c;
+        const int cc = q * TS_CH + c;
         if (lane == 0 && c < nc) {
           if (cc < p) {
             wsm[wid * nvw + cc] = a;
