@@ -536,7 +536,10 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
     int t = 0;
     // u, y of the tile TS_PF tiles ahead are loaded now (L2 hits, off the per-tile critical path);
     // the tile sequence repeats per chunk, so "ahead" wraps to the start of the CTA's rows
-    constexpr int TS_PF = 3;
+#ifndef RG_DK1_PF
+#define RG_DK1_PF 3
+#endif
+    constexpr int TS_PF = RG_DK1_PF;
     double upf[TS_PF], ypf[TS_PF];
     int64_t bnext = r0;  // base of the next tile to prefetch
 #pragma unroll
