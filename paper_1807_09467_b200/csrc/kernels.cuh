@@ -76,8 +76,10 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
 // C = A W, CholQR2 -> Q (columns [VB - k, VB) of Z), R_C, R_C^{-1} (device state) in ONE cooperative
 // kernel; *cflag (zeroed by the caller) set on a singular factor.  CSR / SELL, k <= 16; otherwise
 // cudaErrorNotSupported (caller: build_c).  bar zeroed by the caller; ll as for launch_persistent.
+// cgiven: C = A W already in the Q columns (BSR, after launch_spmm): the kernel is the CholQR2 alone.
+// k <= 22.
 cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
-                          unsigned long long* ll, int k, int* cflag, cudaStream_t s);
+                          unsigned long long* ll, int k, int* cflag, cudaStream_t s, bool cgiven = false);
 
 // ---- multicolour SSOR(omega) preconditioner (precond.cu)
 constexpr int MAXCOLORS = 64;

@@ -29,7 +29,7 @@ constexpr int PM = 64;        // max restart length on this path
 constexpr int PK = 64;        // max recycle dimension on this path
 constexpr int PCOL = PK + PM + 2;
 constexpr int NPFN = 10;      // k_solve_persistent instantiations (launch_persistent's table)
-constexpr int CBK = 16;       // max recycle dimension of the one-kernel operator build (k (k+1) / 2 <= MAXRED)
+constexpr int CBK = 22;       // max recycle dimension of the one-kernel operator build (k (k+1) / 2 <= MAXRED)
 
 struct PArgs {
   Layout L;
@@ -1037,14 +1037,17 @@ fail:
 // kernel, not a prologue of k_solve_persistent: inside it the extra code perturbed the register
 // allocation of the Arnoldi loop (update pass 8.8 -> 11.7 us per step at C2).
 // Thread per row (all k <= KC columns in registers: every load of a row is in flight at once);
-// rows staged in PT-row tiles [KC][PT] for the Gram, which is register-blocked: warp w < nblk owns a
-// 4 x 4 block (a-block <= b-block) of the k x k Gram and accumulates it over all of the CTA's rows
-// (lanes over rows), reduced across lanes once per pass.
-template <int KC>
+// rows staged in PT-row tiles [KC][PT] for the Gram, which is register-blocked: warp w owns the 4 x 4
+// blocks w and w + 16 (a-block <= b-block) of the k x k Gram and accumulates them over all of the
+// CTA's rows (lanes over rows), reduced across lanes once per pass.
+// CGIVEN: C = A W is already in the Q columns (BSR: the TMA + DMMA SpMM ran first); the kernel then is
+// the CholQR2 alone (replaces 2 x (Gram, reduce, Cholesky, X R^{-1}) + R_C finish: 8 launches).
+template <int KC, bool CGIVEN = false>
 __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs pa, int* cflag) {
   constexpr int NB = KC / 4;                       // 4-column blocks
-  constexpr int NBLK = NB * (NB + 1) / 2;          // Gram blocks (a-block <= b-block), <= PT / 32
-  static_assert(NBLK <= PT / 32, "one warp per Gram block");
+  constexpr int NBLK = NB * (NB + 1) / 2;          // Gram blocks (a-block <= b-block)
+  constexpr int GPW = (NBLK + PT / 32 - 1) / (PT / 32);  // Gram blocks per warp
+  static_assert(GPW <= 2, "at most two Gram blocks per warp");
   extern __shared__ double sm[];
   double* tile = sm;                   // [KC][PT]
   double* R1 = tile + KC * PT;         // [col][row], k x k each
@@ -1074,42 +1077,52 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
     return pa.llred ? greduce_ll(dpart, nv, pa.ll, tot, rep, bsh, &s_fail, nullptr)
                     : greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, nullptr);
   };
-  // this warp's Gram block (ab, bb): rows 4 ab.., columns 4 bb..
-  int ab = 0, bb = 0;
-  {
-    int q = wid;
-    while (q >= NB - ab && ab < NB) { q -= NB - ab; ++ab; }
-    bb = ab + q;
+  // this warp's Gram blocks g (ab[g], bb[g]): rows 4 ab.., columns 4 bb..
+  int ab[GPW], bb[GPW];
+  bool gw[GPW];
+#pragma unroll
+  for (int g = 0; g < GPW; ++g) {
+    int q = wid + g * (PT / 32), a = 0;
+    while (q >= NB - a && a < NB) { q -= NB - a; ++a; }
+    ab[g] = a;
+    bb[g] = a + q;
+    gw[g] = wid + g * (PT / 32) < NBLK && 4 * ab[g] < k && 4 * bb[g] < k;
   }
-  const bool gw = wid < NBLK && 4 * ab < k && 4 * bb < k;
-  double gacc[16];
+  double gacc[GPW][16];
   auto gram_zero = [&]() {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) gacc[i] = 0.0;
+    for (int g = 0; g < GPW; ++g)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) gacc[g][i] = 0.0;
   };
   auto gram_tile = [&](int cnt) {  // accumulate the staged tile's rows (lanes over rows)
-    if (!gw) return;
-    for (int t = lane; t < cnt; t += 32) {
-      double xa[4], xb[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        xa[i] = tile[(4 * ab + i) * PT + t];
-        xb[i] = tile[(4 * bb + i) * PT + t];
+    for (int g = 0; g < GPW; ++g) {
+      if (!gw[g]) continue;
+      for (int t = lane; t < cnt; t += 32) {
+        double xa[4], xb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          xa[i] = tile[(4 * ab[g] + i) * PT + t];
+          xb[i] = tile[(4 * bb[g] + i) * PT + t];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) gacc[g][4 * i + j] += xa[i] * xb[j];
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) gacc[4 * i + j] += xa[i] * xb[j];
     }
   };
   auto gram_flush = [&]() {  // lane sums -> dpart (packed upper, index of (a, b), a <= b)
-    if (gw) {
+#pragma unroll
+    for (int g = 0; g < GPW; ++g) {
+      if (!gw[g]) continue;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const double v = warp_sum(gacc[4 * i + j]);
-          const int a2 = 4 * ab + i, b2 = 4 * bb + j;
+          const double v = warp_sum(gacc[g][4 * i + j]);
+          const int a2 = 4 * ab[g] + i, b2 = 4 * bb[g] + j;
           if (lane == 0 && a2 < k && b2 < k && a2 <= b2) dpart[a2 * k - a2 * (a2 - 1) / 2 + (b2 - a2)] = v;
         }
     }
@@ -1147,17 +1160,17 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
     }
     __syncthreads();
   };
-  // row r of the Q columns times an upper-triangular inverse, in place (this thread owns the row)
-  auto row_tri = [&](int64_t r, const double* Ri, double* out) {
-    double x[KC];
+  // row r of the Q columns times an upper-triangular inverse (this thread owns the row); computed in
+  // place in x, columns descending (column c needs x_0..x_c only: one KC-vector of registers)
+  auto row_tri = [&](int64_t r, const double* Ri, double* x) {
 #pragma unroll
     for (int l = 0; l < KC; ++l) x[l] = l < k ? Qc[(int64_t)l * ld + r] : 0.0;
 #pragma unroll
-    for (int c = 0; c < KC; ++c) {
+    for (int c = KC - 1; c >= 0; --c) {
       double acc = 0.0;
 #pragma unroll
       for (int l = 0; l <= c; ++l) acc += x[l] * Ri[c * k + l];
-      out[c] = acc;
+      x[c] = acc;
     }
   };
   for (int i = tid; i < MAXRED; i += PT) dpart[i] = 0.0;
@@ -1172,7 +1185,10 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
       double acc[KC];
 #pragma unroll
       for (int u = 0; u < KC; ++u) acc[u] = 0.0;
-      if (r < L.n) {
+      if (CGIVEN) {
+#pragma unroll
+        for (int u = 0; u < KC; ++u) acc[u] = u < k ? Qc[(int64_t)u * ld + r] : 0.0;
+      } else if (r < L.n) {
         // 8 (value, column) pairs in flight, then the W gathers of every column in flight
         int64_t e0, est;
         int ne;
@@ -1209,7 +1225,7 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
       }
 #pragma unroll
       for (int u = 0; u < KC; ++u) {
-        if (u < k) Qc[(int64_t)u * ld + r] = acc[u];
+        if (u < k && !CGIVEN) Qc[(int64_t)u * ld + r] = acc[u];
         tile[u * PT + tid] = acc[u];
       }
     }
@@ -1270,9 +1286,9 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
         dmin = tot[i] < dmin ? tot[i] : dmin;
       }
       if (!ok || !(dmin > 1e-12 * dmax)) *cflag = 1;
-      st->spmv_count += k;  // C = A W (rg_report.spmv_count)
+      if (!CGIVEN) st->spmv_count += k;  // C = A W (rg_report.spmv_count; the SpMM counts its own)
       if (pa.llred) st->red_epoch = ok ? rep : rep + 16u;  // past anything a CTA may have published
-      prof_end(st, K_CBUILD, A.bytes + 8.0 * (double)L.n * 6.0 * k);
+      prof_end(st, K_CBUILD, (CGIVEN ? 0.0 : A.bytes) + 8.0 * (double)L.n * (CGIVEN ? 5.0 : 6.0) * k);
     }
   }
 }
@@ -1367,13 +1383,19 @@ cudaError_t launch_persistent(const Layout& L, const MatDev& A, DevState* st, do
 // One cooperative launch building C = A W, Q, R_C, R_C^{-1} (k_cbuild).  cudaErrorNotSupported when
 // outside its scope (BSR, k > CBK, not co-resident): the caller runs build_c's kernel chain instead.
 cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double* tot_g, unsigned* bar,
-                          unsigned long long* ll, int k, int* cflag, cudaStream_t s) {
-  if (k < 1 || k > CBK || A.fmt == 2) return cudaErrorNotSupported;
-  const int nch = (k + 7) / 8;
-  const void* fn = nch == 1 ? (const void*)k_cbuild<8> : (const void*)k_cbuild<16>;
-  const size_t smem = sizeof(double) * ((size_t)8 * nch * PT + 4 * CBK * CBK + 2 * MAXRED);
-  static int occ_dev[MAXDEV][3] = {};  // 0: not yet queried on that device, else occupancy + 1
-  int& oc = occ_dev[current_device()][nch];
+                          unsigned long long* ll, int k, int* cflag, cudaStream_t s, bool cgiven) {
+  // CSR / SELL: C = A W computed here; BSR: only with C given (the TMA + DMMA SpMM ran first)
+  if (k < 1 || k > CBK || (A.fmt == 2 && !cgiven)) return cudaErrorNotSupported;
+  if (k > 16 && !cgiven) return cudaErrorNotSupported;  // the fused SpMV + 24-column rows spill: build_c
+  const int kc = k <= 8 ? 8 : (k <= 16 ? 16 : 24);
+  const int vi = (kc / 8 - 1) + (cgiven ? 3 : 0);
+  static const void* fns[6] = {(const void*)k_cbuild<8>, (const void*)k_cbuild<16>, (const void*)k_cbuild<16>,
+                               (const void*)k_cbuild<8, true>, (const void*)k_cbuild<16, true>,
+                               (const void*)k_cbuild<24, true>};
+  const void* fn = fns[vi];
+  const size_t smem = sizeof(double) * ((size_t)kc * PT + 4 * CBK * CBK + 2 * MAXRED);
+  static int occ_dev[MAXDEV][6] = {};  // 0: not yet queried on that device, else occupancy + 1
+  int& oc = occ_dev[current_device()][vi];
   if (oc == 0) {
     int o = 0;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -348,6 +348,19 @@ rg_status build_c(rg_ctx* c, bool sync) {
   } else {
     CK(es);
   }
+  if (!sync) {
+    // CholQR2 of the C just formed as ONE cooperative kernel (k_cbuild with C given: Gram, Cholesky and
+    // the two in-place triangular solves for all rows, Cholesky factors redundant per CTA) instead of
+    // the 8-launch chain below; k <= 22 (C5: k = 20)
+    const cudaError_t eb = launch_cbuild(c->L, c->A, c->st, c->tot_g, c->gbar, c->llw, k, &c->st->cfail, s, true);
+    if (eb == cudaSuccess) {
+      if (knob("RG_NO_LLRED")) CK(cudaMemsetAsync(c->gbar, 0, sizeof(unsigned) * BAR_WORDS, s));
+      c->c_valid = true;
+      return RG_OK;
+    }
+    if (eb != cudaErrorNotSupported && eb != cudaErrorCooperativeLaunchTooLarge) CK(eb);
+    cudaGetLastError();
+  }
   double* G = c->small;
   double* R1 = c->small + 1 * SMALL;
   double* R1i = c->small + 2 * SMALL;
