@@ -151,77 +151,6 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_csr(SpmvArgs a) {
   finish(a, io, kid, nrm);
 }
 
-// ---------------------------------------------------------------- CSR, warp-stream (short rows)
-// A warp takes 32 consecutive rows at a time: their entries are one contiguous range of the CSR arrays,
-// loaded in fully coalesced passes of 32 (8 passes = 256 entries in flight per warp, with the x gathers
-// behind them), the products staged in shared memory, and lane l sums row l's products in stored order
-// (the same order as the oracle's row sum).  The next chunk's row pointers are loaded while the current
-// chunk is processed.  Replaces thread-per-row for short rows (C4's 7-point rows): there every row
-// was three dependent loads (row pointer, entries, x) and ncu r02 showed the kernel long-scoreboard
-// bound (31 stall cycles per issue, 0.64 of the copy peak cold).
-constexpr int WS_PASS = 8;   // coalesced passes per batch (256 entries)
-__global__ void __launch_bounds__(OT, 2) k_spmv_csr_ws(SpmvArgs a) {
-  __shared__ double prod[OT / 32][WS_PASS * 32];
-  Io io;
-  int kid;
-  if (!setup(a, io, kid)) return;
-  const MatDev& A = a.A;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int32_t* __restrict__ rp = A.rp;
-  const int32_t* __restrict__ ci = A.ci;
-  const double* __restrict__ v = A.v;
-  const double* __restrict__ x = io.x;
-  double* pw = prod[wid];
-  double nrm = 0.0;
-  const int64_t nchunk = (A.n + 31) >> 5;
-  const int64_t step = (int64_t)gridDim.x * (OT / 32);
-  int64_t chunk = (int64_t)blockIdx.x * (OT / 32) + wid;
-  // row bounds of a chunk: lane l holds rp[row0 + l] (its row's start) and every lane rp[row0 + nr]
-  auto bounds = [&](int64_t ch, int32_t& beg, int32_t& endall) {
-    if (ch >= nchunk) { beg = endall = 0; return; }
-    const int64_t row0 = ch << 5;
-    const int nr = (int)min((int64_t)32, A.n - row0);
-    beg = lane < nr ? __ldg(rp + row0 + lane) : 0;
-    endall = __ldg(rp + row0 + nr);
-  };
-  int32_t beg, endall;
-  bounds(chunk, beg, endall);
-  for (; chunk < nchunk; chunk += step) {
-    int32_t nbeg, nend;
-    bounds(chunk + step, nbeg, nend);   // next chunk's row pointers: in flight during this chunk
-    const int64_t row0 = chunk << 5;
-    const int nr = (int)min((int64_t)32, A.n - row0);
-    int32_t end = __shfl_down_sync(0xffffffffu, beg, 1);
-    if (lane >= nr - 1) end = endall;
-    const int32_t e0 = __shfl_sync(0xffffffffu, beg, 0);
-    const int32_t total = endall - e0;
-    double s = 0.0;
-    for (int32_t b0 = 0; b0 < total; b0 += WS_PASS * 32) {
-      const int32_t nb = min(total - b0, WS_PASS * 32);
-      int32_t cc[WS_PASS];
-      double vv[WS_PASS];
-#pragma unroll
-      for (int u = 0; u < WS_PASS; ++u) {
-        const bool ok = u * 32 + lane < nb;
-        cc[u] = ok ? __ldcs(ci + e0 + b0 + u * 32 + lane) : 0;
-        vv[u] = ok ? __ldcs(v + e0 + b0 + u * 32 + lane) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < WS_PASS; ++u)
-        if (u * 32 + lane < nb) pw[u * 32 + lane] = vv[u] * __ldg(x + cc[u]);
-      __syncwarp();
-      const int32_t lo = max(beg - e0 - b0, 0), hi = min(end - e0 - b0, nb);
-      if (lane < nr)
-        for (int32_t q = lo; q < hi; ++q) s += pw[q];
-      __syncwarp();
-    }
-    if (lane < nr) nrm += emit(io, row0 + lane, s);
-    beg = nbeg;
-    endall = nend;
-  }
-  finish(a, io, kid, nrm);
-}
-
 // ---------------------------------------------------------------- SELL-32 (sigma = 1)
 __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
   Io io;
@@ -679,7 +608,7 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
     if (g > cap) g = cap;
     const int gi = (int)(g < 1 ? 1 : g);
     switch (A.lpr) {
-      case 1: k_spmv_csr_ws<<<gi, OT, 0, s>>>(a); break;   // short rows: warp-stream
+      case 1: k_spmv_csr<1><<<gi, OT, 0, s>>>(a); break;
       case 2: k_spmv_csr<2><<<gi, OT, 0, s>>>(a); break;
       case 4: k_spmv_csr<4><<<gi, OT, 0, s>>>(a); break;
       case 8: k_spmv_csr<8><<<gi, OT, 0, s>>>(a); break;
