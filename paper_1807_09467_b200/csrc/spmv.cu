@@ -151,6 +151,61 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_csr(SpmvArgs a) {
   finish(a, io, kid, nrm);
 }
 
+// ---------------------------------------------------------------- CSR, thread per row, software-pipelined
+// Short rows (<= 8 entries: 5- / 7-point stencils): the next row's row pointers and entries are loaded
+// while the current row's x gathers are in flight, so each thread keeps two rows' loads outstanding
+// instead of paying the three dependent latencies (row pointer, entries, x) of every row in sequence.
+// Rows longer than 8 entries are finished by a plain loop.
+__global__ void __launch_bounds__(OT, 2) k_spmv_csr_pipe(SpmvArgs a) {
+  Io io;
+  int kid;
+  if (!setup(a, io, kid)) return;
+  const MatDev& A = a.A;
+  const int32_t* __restrict__ rp = A.rp;
+  const int32_t* __restrict__ ci = A.ci;
+  const double* __restrict__ v = A.v;
+  const double* __restrict__ x = io.x;
+  const int64_t stride = (int64_t)gridDim.x * OT;
+  double nrm = 0.0;
+  int64_t row = (int64_t)blockIdx.x * OT + threadIdx.x;
+  int32_t p0 = 0, p1 = 0;
+  int32_t cc[8];
+  double vv[8];
+  auto load_row = [&](int64_t r, int32_t& q0, int32_t& q1, int32_t (&c)[8], double (&w)[8]) {
+    q0 = r < A.n ? __ldg(rp + r) : 0;
+    q1 = r < A.n ? __ldg(rp + r + 1) : 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = q0 + u < q1;
+      c[u] = ok ? __ldcs(ci + q0 + u) : 0;
+      w[u] = ok ? __ldcs(v + q0 + u) : 0.0;
+    }
+  };
+  load_row(row, p0, p1, cc, vv);
+  for (; row < A.n; row += stride) {
+    double xv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) xv[u] = p0 + u < p1 ? __ldg(x + cc[u]) : 0.0;  // this row's gathers
+    int32_t q0, q1, nc[8];
+    double nv[8];
+    load_row(row + stride, q0, q1, nc, nv);                                      // next row, in flight
+    double s = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u < p1) s += vv[u] * xv[u];
+    for (int32_t p = p0 + 8; p < p1; ++p) s += __ldcs(v + p) * __ldg(x + __ldcs(ci + p));  // long rows
+    nrm += emit(io, row, s);
+    p0 = q0;
+    p1 = q1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      cc[u] = nc[u];
+      vv[u] = nv[u];
+    }
+  }
+  finish(a, io, kid, nrm);
+}
+
 // ---------------------------------------------------------------- SELL-32 (sigma = 1)
 __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
   Io io;
@@ -608,7 +663,7 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
     if (g > cap) g = cap;
     const int gi = (int)(g < 1 ? 1 : g);
     switch (A.lpr) {
-      case 1: k_spmv_csr<1><<<gi, OT, 0, s>>>(a); break;
+      case 1: k_spmv_csr_pipe<<<gi, OT, 0, s>>>(a); break;
       case 2: k_spmv_csr<2><<<gi, OT, 0, s>>>(a); break;
       case 4: k_spmv_csr<4><<<gi, OT, 0, s>>>(a); break;
       case 8: k_spmv_csr<8><<<gi, OT, 0, s>>>(a); break;
