@@ -207,6 +207,9 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_csr_pipe(SpmvArgs a) {
 }
 
 // ---------------------------------------------------------------- SELL-32 (sigma = 1)
+// Thread per row; the first SELL_CH entries of the NEXT row (slice width / pointer, columns, values)
+// are loaded while this row's x gathers are in flight (software pipelining across the grid-stride rows,
+// as k_spmv_csr_pipe); entries beyond SELL_CH are finished by a plain loop.
 __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
   Io io;
   int kid;
@@ -215,26 +218,54 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
   double nrm = 0.0;
   const int64_t rows = A.nslices * 32;
   const double* __restrict__ x = io.x;
-  for (int64_t row = (int64_t)blockIdx.x * OT + threadIdx.x; row < rows; row += (int64_t)gridDim.x * OT) {
-    const int64_t sl = row >> 5;
-    const int w = __ldg(A.sw + sl);
-    const int64_t base = __ldg(A.sp + sl) + (row & 31);
+  const int64_t stride = (int64_t)gridDim.x * OT;
+  auto load_row = [&](int64_t r, int& w, int64_t& base, int32_t (&c)[SELL_CH], double (&vv)[SELL_CH]) {
+    w = 0;
+    base = 0;
+    if (r < rows) {
+      const int64_t sl = r >> 5;
+      w = __ldg(A.sw + sl);
+      base = __ldg(A.sp + sl) + (r & 31);
+    }
+#pragma unroll
+    for (int u = 0; u < SELL_CH; ++u) {
+      const bool ok = u < w;
+      const int64_t e = base + (int64_t)u * 32;
+      c[u] = ok ? __ldcs(A.sci + e) : 0;
+      vv[u] = ok ? __ldcs(A.sv + e) : 0.0;
+    }
+  };
+  int64_t row = (int64_t)blockIdx.x * OT + threadIdx.x;
+  int w;
+  int64_t base;
+  int32_t cc[SELL_CH];
+  double vv[SELL_CH];
+  load_row(row, w, base, cc, vv);
+  for (; row < rows; row += stride) {
+    double xv[SELL_CH];
+#pragma unroll
+    for (int u = 0; u < SELL_CH; ++u) xv[u] = u < w ? __ldg(x + cc[u]) : 0.0;   // this row's gathers
+    int wn;
+    int64_t bn;
+    int32_t cn[SELL_CH];
+    double vn[SELL_CH];
+    load_row(row + stride, wn, bn, cn, vn);                                        // next row, in flight
     double s = 0.0;
-    for (int c = 0; c < w; c += SELL_CH) {  // SELL_CH coalesced (column, value) pairs in flight, then gathers
-      int32_t cc[SELL_CH];
-      double vv[SELL_CH];
 #pragma unroll
-      for (int u = 0; u < SELL_CH; ++u) {
-        const bool ok = c + u < w;
-        const int64_t e = base + (int64_t)(c + u) * 32;
-        cc[u] = ok ? __ldcs(A.sci + e) : 0;
-        vv[u] = ok ? __ldcs(A.sv + e) : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < SELL_CH; ++u)
-        if (c + u < w) s += vv[u] * __ldg(x + cc[u]);
+    for (int u = 0; u < SELL_CH; ++u)
+      if (u < w) s += vv[u] * xv[u];
+    for (int c = SELL_CH; c < w; ++c) {                                            // long rows
+      const int64_t e = base + (int64_t)c * 32;
+      s += __ldcs(A.sv + e) * __ldg(x + __ldcs(A.sci + e));
     }
     if (row < A.n) nrm += emit(io, row, s);
+    w = wn;
+    base = bn;
+#pragma unroll
+    for (int u = 0; u < SELL_CH; ++u) {
+      cc[u] = cn[u];
+      vv[u] = vn[u];
+    }
   }
   finish(a, io, kid, nrm);
 }
