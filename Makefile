@@ -32,7 +32,7 @@ build/rg/%.o: $(PKG)/csrc/%.cu $(RG_HDR)
 
 $(PKG)/lib/librg.so: $(RG_OBJ)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -o $@ $(RG_OBJ) -lcuda
+	$(NVCC) $(ARCH) -shared -o $@ $(RG_OBJ)
 
 synth/libsynth.so: synth/synth.c synth/synth_common.h
 	$(CC) $(CFLAGS) -fopenmp -shared -o $@ synth/synth.c -lm

@@ -705,6 +705,25 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
   return cudaGetLastError();
 }
 
+// cuTensorMapEncodeTiled resolved through the runtime's driver entry point: librg.so does not link
+// libcuda (the library must load, and export its symbols, on a host without the driver)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+    tried = true;
+  }
+  return fn;
+}
+
 cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld, int k, DevState* st, unsigned* counter,
                         cudaStream_t s, const double* xe, double* ye) {
   if (k <= 0) return cudaSuccess;
@@ -716,7 +735,7 @@ cudaError_t launch_spmm(const MatDev& A, const double* W, double* Y, int64_t ld,
     const cuuint64_t dims[3] = {16, 4, (cuuint64_t)A.nnz * 64};
     const cuuint64_t strides[2] = {16 * 8, 64 * 8};
     const cuuint32_t box[3] = {16, 1, 64}, estr[3] = {1, 1, 1};  // one row quarter of a block (8 KB)
-    if (cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A.v, dims, strides, box, estr,
+    if (!encode_tiled() || encode_tiled()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A.v, dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
