@@ -10,7 +10,13 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisi
 # EXPERIMENTS=1: honour the A/B environment knobs of csrc/knobs.cuh (compiled out by default)
 ifeq ($(EXPERIMENTS),1)
 NVFLAGS   += -DRG_EXPERIMENTS
+OBJDIR    := build/rg_exp
+else
+OBJDIR    := build/rg
 endif
+# the library is relinked whenever the build variant changes (product <-> EXPERIMENTS)
+VARIANT   := $(if $(filter 1,$(EXPERIMENTS)),experiments,product)
+$(shell mkdir -p build; echo $(VARIANT) | cmp -s - build/variant || echo $(VARIANT) > build/variant)
 CFLAGS    := -O2 -fPIC -std=c99 -ffp-contract=off -Wall -Wno-unused-function
 
 PKG       := paper_1807_09467_b200
@@ -23,14 +29,14 @@ rg: $(PKG)/lib/librg.so
 synth: synth/libsynth.so synth/libsynth_cuda.so
 oracle: oracle/liboracle.so
 
-RG_OBJ    := $(patsubst $(PKG)/csrc/%.cu,build/rg/%.o,$(RG_SRC))
+RG_OBJ    := $(patsubst $(PKG)/csrc/%.cu,$(OBJDIR)/%.o,$(RG_SRC))
 
 # one object per translation unit (make -j compiles them in parallel), then one shared library
-build/rg/%.o: $(PKG)/csrc/%.cu $(RG_HDR)
-	@mkdir -p build/rg
+$(OBJDIR)/%.o: $(PKG)/csrc/%.cu $(RG_HDR)
+	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c -o $@ $<
 
-$(PKG)/lib/librg.so: $(RG_OBJ)
+$(PKG)/lib/librg.so: $(RG_OBJ) build/variant
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $(RG_OBJ)
 
@@ -45,6 +51,6 @@ oracle/liboracle.so: oracle/oracle.c
 
 clean:
 	rm -f $(PKG)/lib/librg.so synth/*.so oracle/*.so
-	rm -rf build/rg
+	rm -rf build/rg build/rg_exp build/variant
 
 .PHONY: all rg synth oracle clean

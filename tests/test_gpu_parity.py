@@ -560,3 +560,45 @@ def test_spmv_count_is_counted(flags, exact, variant):
     else:
         assert base <= rep["spmv_count"] <= base + rep["restarts"] + 2, rep
     ctx.close()
+
+
+def test_orthogonalisation_switch_inside_one_context(rng):
+    """The graph path picks DCGS2 or classical CGS2 per solve (one SpMV vs one basis pass,
+    8 n (k_eff + m + 2) bytes), and the solve graph is cached per choice (a graph
+    captured for one choice must never be replayed for the other).  One context, graph path, a
+    deflate sequence whose k_eff grows across the threshold and back down, and m changing between
+    solves: every solve against the oracle, and both orthogonalisations observed."""
+    from paper_1807_09467_b200 import rg as rgb
+    n = 3000
+    hm = random_csr(n, rng, per_row=(4, 6), diag=2.5)     # ~6 entries/row
+    M = oracle.Matrix.from_host(hm)
+    kmax = 8
+    basis = np.linalg.qr(rng.standard_normal((n, kmax)))[0]
+    ctx = make_ctx(hm, max_m=16, s=kmax, k=kmax, flags=rgb.RG_FLAG_NO_PERSIST | rgb.RG_FLAG_PROFILE)
+    seen = set()
+    # (k_eff, m): 8 n (k + m + 2) vs ~92 n bytes of A (+ x, y) -> CGS2 below, DCGS2 above
+    plan = [(1, 4), (3, 4), (8, 4), (2, 4), (0, 4), (0, 12), (8, 12), (1, 4), (6, 8)]
+    for k, m in plan:
+        ctx.clear_snapshots()
+        for i in range(k):
+            ctx.push_snapshot(t(basis[:, i] * (k - i)))
+        if k:
+            assert ctx.build_recycle(k)[0] == k
+        variant = "deflate" if k else "plain"
+        b = rng.standard_normal(n)
+        ctx.reset_kernel_stats()
+        x = torch.zeros(n, dtype=torch.float64, device=DEV)
+        rep = ctx.solve(t(b), x, m=m, variant=variant, tol=1e-9)
+        ks = ctx.kernel_stats()
+        dc = ks["dcgs_dots_ls"]["launches"] > 0
+        cg = ks["orth_upd_norm_ls"]["launches"] > 0
+        assert dc != cg, (k, m, ks["dcgs_dots_ls"], ks["orth_upd_norm_ls"])
+        seen.add("dcgs2" if dc else "cgs2")
+        a_bytes = 12 * len(hm.val) + 4 * (n + 1) + 16 * n   # the library's byte model of one SpMV
+        assert dc == (a_bytes <= 8 * n * (k + m + 2)), (k, m, dc)
+        ref = oracle.solve(M, b, m=m, variant=variant, W=basis[:, :k] if k else None, tol=1e-9)
+        assert rep["converged"] and ref["converged"], (k, m)
+        assert abs(rep["iterations"] - ref["iterations"]) <= 2, (k, m, rep["iterations"], ref["iterations"])
+        assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"]), (k, m)
+    assert seen == {"dcgs2", "cgs2"}
+    ctx.close()
