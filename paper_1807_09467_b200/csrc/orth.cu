@@ -17,6 +17,7 @@
 // OP_OB_CSU / OP_OB_SU w -= C t (+ ||w|| -> cycle-start epilogue at the cycle start).
 #include "epilogue.cuh"
 #include "kernels.cuh"
+#include "knobs.cuh"
 
 namespace rg {
 namespace {
@@ -319,6 +320,185 @@ __global__ void __launch_bounds__(CT, 2) k_cgs(Layout L, DevState* st, unsigned 
   if (threadIdx.x == 0) prof_end(st, kid, 8.0 * (double)L.n * (p + (UPD ? 2.0 : 1.0)));
 }
 
+// ------------------------------------------------------------------------------------------
+// TMA-staged CGS passes of the graph path (round 2): OP_D1 / OP_UD2 / OP_UN (not augment) and the
+// cycle-start OP_CS_DQ / OP_CS_UN.  The register kernels above keep <= 8 loads of 8 B in flight per
+// thread and measured 3.4-4.5 TB/s on C5's 2M-row basis.  Here a producer warp streams, per tile of
+// TR rows, the target w and every column of the pass ([Q|V] rows) with cp.async.bulk into a ring of
+// CG_NS whole-tile stages (completion on mbarriers), so ~190 KB per SM are in flight independently of
+// registers.  Consumer thread (r, g) (r < TR rows, g < G = 512/TR groups) owns columns g, g+G, ...:
+//   update: part_g[r] = sum over its columns of cf_c Z_rc; w_r' = w_r - sum_g part_g[r] (groups in order)
+//   dots:   d_c += Z_rc w_r' per thread over all tiles, then warp shuffles and the warps in order
+//   norm:   ||w'||^2 (group 0)
+// TR is picked per launch on the device from the pass width p: the largest power of two <= 512 with
+// CG_NS tiles of p + 1 columns in the ring and at most CG_CPT columns per thread.  Deterministic.
+constexpr int CG_NS = 3;
+constexpr int CG_CPT = 16;                        // dot accumulators per thread
+constexpr int CG_SMEM = 192 * 1024;               // ring bytes (dynamic shared memory)
+__device__ __forceinline__ uint32_t cg_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cg_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(cg_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void cg_bar_consumers() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+
+template <int MODE>  // 0 = dots (D1, CS_DQ), 1 = update + dots (UD2), 2 = update + norm (UN, CS_UN)
+__global__ void __launch_bounds__(544, 1) k_cgs_tma(Layout L, DevState* st, int op, unsigned long long cond) {
+  extern __shared__ __align__(128) double ring[];  // [CG_NS][p + 1][TR]; partials alias it at the end
+  __shared__ __align__(8) uint64_t full[CG_NS], empty[CG_NS];
+  __shared__ double cf[MAXCOL];
+  __shared__ double part[2][512];
+  __shared__ double dpart[MAXRED];
+  __shared__ double tot[MAXRED];
+  __shared__ double bsh[33];
+  constexpr bool UPD = MODE != 0, DOTS = MODE != 2, NRM = MODE == 2;
+  const int kid = op == OP_D1 ? K_ORTH_D1 : op == OP_UD2 ? K_ORTH_UD2 : op == OP_UN ? K_ORTH_UN
+                : op == OP_CS_DQ ? K_CS_DQ : K_CS_UN;
+  const bool cs = op == OP_CS_DQ || op == OP_CS_UN;
+  if (cs ? st->done != 0 : st->active == 0) { prof_noop(st, kid); return; }
+  prof_begin(st, kid);
+  const int j = st->j, k = st->k_eff, var = st->variant;
+  const int VB = L.VB, QB = VB - k;
+  const int64_t ld = L.ld;
+  // pass columns [c0, c0 + p) and the target column tc
+  int c0, p, tc;
+  if (cs) { c0 = QB; p = k; tc = VB; }
+  else { c0 = (var == RG_DEFLATE) ? QB : VB; tc = VB + j + 1; p = tc - c0; }
+  double* __restrict__ w = L.Z + (int64_t)tc * ld;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (UPD)
+    for (int c = tid; c < p; c += 544) cf[c] = st->coef[c0 + c] * st->sc[c0 + c];
+  // rows per tile
+  int TR = 512;
+  while (TR > 32 && ((size_t)CG_NS * (p + 1) * TR * 8 > (size_t)CG_SMEM || (p + (512 / TR) - 1) / (512 / TR) > CG_CPT)) TR >>= 1;
+  const int G = 512 / TR, SD = (p + 1) * TR;  // doubles per stage: p columns then w
+  if (tid == 0) {
+    for (int i = 0; i < CG_NS; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cg_u32(&full[i])), "r"(1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cg_u32(&empty[i])), "r"(16));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ng = ld >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
+  const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
+  const int ntile = (int)((r1 - r0 + TR - 1) / TR);
+  double dacc[CG_CPT];
+#pragma unroll
+  for (int i = 0; i < CG_CPT; ++i) dacc[i] = 0.0;
+  double nrm = 0.0;
+  const int r = tid % TR, g = tid / TR;
+  if (wid == 16) {  // ---- producer
+    if (lane == 0) {
+      uint64_t pol, keep;
+      if (L.keep_l2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+      else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
+      for (int t = 0; t < ntile; ++t) {
+        const int s = t % CG_NS;
+        if (t >= CG_NS) cg_wait(&empty[s], (uint32_t)((t / CG_NS - 1) & 1));
+        const int64_t base = r0 + (int64_t)t * TR;
+        const uint32_t cnt = (uint32_t)min((int64_t)TR, r1 - base);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cg_u32(&full[s])),
+                     "r"((uint32_t)(p + 1) * cnt * 8u) : "memory");
+        double* stg = ring + (size_t)s * SD;
+        for (int c = 0; c <= p; ++c) {
+          const double* src = c < p ? L.Z + (int64_t)(c0 + c) * ld + base : w + base;
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                       ::"r"(cg_u32(stg + (size_t)c * TR)), "l"(src), "r"(cnt * 8u), "r"(cg_u32(&full[s])),
+                       "l"(c < p ? pol : keep) : "memory");
+        }
+      }
+    }
+  } else {  // ---- consumers
+    for (int t = 0; t < ntile; ++t) {
+      const int s = t % CG_NS;
+      const int64_t base = r0 + (int64_t)t * TR;
+      const int cnt = (int)min((int64_t)TR, r1 - base);
+      const bool in = r < cnt;
+      cg_wait(&full[s], (uint32_t)((t / CG_NS) & 1));
+      const double* stg = ring + (size_t)s * SD;
+      const double wr = in ? stg[(size_t)p * TR + r] : 0.0;
+      double wn = wr;
+      if (UPD) {
+        double a0 = 0.0;
+#pragma unroll
+        for (int i = 0; i < CG_CPT; ++i) {
+          const int c = g + i * G;
+          if (c < p) a0 += cf[c] * (in ? stg[(size_t)c * TR + r] : 0.0);
+        }
+        if (G == 1) {
+          wn = wr - a0;
+        } else {
+          double* pp = part[t & 1];
+          pp[g * TR + r] = a0;
+          cg_bar_consumers();
+          double sum = 0.0;
+          for (int gg = 0; gg < G; ++gg) sum += pp[gg * TR + r];
+          wn = wr - sum;
+        }
+        if (g == 0 && in) {
+          w[base + r] = wn;
+          if (NRM) nrm += wn * wn;
+        }
+      }
+      if (DOTS) {
+#pragma unroll
+        for (int i = 0; i < CG_CPT; ++i) {
+          const int c = g + i * G;
+          if (c < p && in) dacc[i] += stg[(size_t)c * TR + r] * wn;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cg_u32(&empty[s])) : "memory");
+    }
+  }
+  __syncthreads();  // all stages consumed: the ring is free for the per-warp partials
+  double* wsm = ring;  // [16][p]
+  if (DOTS) {
+    if (wid < 16) {
+      // a warp = 32 consecutive rows of one group (TR >= 32): its columns are g + i G
+#pragma unroll
+      for (int i = 0; i < CG_CPT; ++i) {
+        const int c = g + i * G;
+        if (c < p) {
+          const double v = warp_sum(dacc[i]);
+          if (lane == 0) wsm[wid * p + c] = v;
+        }
+      }
+    }
+    __syncthreads();
+    const int wpg = TR / 32;  // warps per group
+    for (int c = tid; c < p; c += 544) {
+      const int gg = c % G;
+      double sum = 0.0;
+      for (int ww = 0; ww < wpg; ++ww) sum += wsm[(gg * wpg + ww) * p + c];
+      dpart[c] = sum;
+    }
+  }
+  if (NRM) {
+    const double tn = block_sum(nrm, bsh);  // (producer warp contributes 0)
+    if (tid == 0) dpart[0] = tn;
+  }
+  __syncthreads();
+  const int nv = DOTS ? p : 1;
+  if (!grid_reduce(dpart, nv, L.partial, L.counter, tot, tot)) return;
+  switch (op) {
+    case OP_D1: epi_pass(st, tot, c0, p, true); break;
+    case OP_UD2: epi_pass(st, tot, c0, p, false); break;
+    case OP_UN:
+      epi_ls(st, L, tot, 0);
+      if (cond && tid == 0) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, st->active ? 1u : 0u);
+      break;
+    case OP_CS_DQ: epi_cs_dq(st, L, tot); break;
+    default: epi_cycle_start(st, L, tot[0]); break;  // OP_CS_UN
+  }
+  if (tid == 0) prof_end(st, kid, 8.0 * (double)L.n * (p + (UPD ? 2.0 : 1.0)));
+}
+
 // RG_FLAG_KEEP_BASIS, cycle end: v_0 .. v_jfinal (normalised: v_i = sc_i * raw_i) into L.keepV, the
 // step count into st->kb_steps.  H-bar and B of the cycle stay in st->Hraw / st->Bm (epi_ls).
 __global__ void __launch_bounds__(OT) k_keep_basis(Layout L, DevState* st) {
@@ -354,6 +534,24 @@ cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, u
     cudaFuncSetAttribute(k_cgs<1>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_cgs<2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     init = true;
+  }
+  // TMA-staged passes (graph path; augment's OP_UN also needs Q^T w: generic path)
+  static const bool no_tma = knob("RG_NO_TMA_CGS");
+  const bool tma_op = op == OP_D1 || op == OP_UD2 || (op == OP_UN && !L.augment) || op == OP_CS_DQ || op == OP_CS_UN;
+  if (tma_op && !no_tma && L.ld >= (int64_t)NSM * 512) {
+    static bool attr[MAXDEV] = {};
+    const int dev = current_device();
+    if (!attr[dev]) {
+      cudaFuncSetAttribute(k_cgs_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, CG_SMEM);
+      cudaFuncSetAttribute(k_cgs_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, CG_SMEM);
+      cudaFuncSetAttribute(k_cgs_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CG_SMEM);
+      attr[dev] = true;
+    }
+    const int mode = (op == OP_D1 || op == OP_CS_DQ) ? 0 : op == OP_UD2 ? 1 : 2;
+    if (mode == 0) k_cgs_tma<0><<<NSM, 544, CG_SMEM, s>>>(L, st, op, cond);
+    else if (mode == 1) k_cgs_tma<1><<<NSM, 544, CG_SMEM, s>>>(L, st, op, cond);
+    else k_cgs_tma<2><<<NSM, 544, CG_SMEM, s>>>(L, st, op, cond);
+    return cudaGetLastError();
   }
   if (L.cgs_ok) {  // register-resident CGS kernels (augment's OP_UN also needs Q^T w: generic path)
     const int g = vec_grid(L.ld);

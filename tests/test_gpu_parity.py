@@ -602,3 +602,39 @@ def test_orthogonalisation_switch_inside_one_context(rng):
         assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"]), (k, m)
     assert seen == {"dcgs2", "cgs2"}
     ctx.close()
+
+
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate"])
+def test_cgs2_tma_passes_vs_oracle(variant, rng):
+    """Classical CGS2 on the graph path at a size where its passes run TMA-staged (n_pad >= 148 x 512
+    rows: k_cgs_tma for D1 / UD2 / UN and the cycle-start CS_DQ / CS_UN), against the oracle, with
+    restarts and the recycle space of a window of earlier solutions."""
+    from paper_1807_09467_b200 import rg as rgb
+    cfg = synth.CONFIGS["C2"].reduced(320)            # n = 102,400
+    seq = synth.HostSequence(cfg)
+    u = seq.initial()
+    hm = seq.matrix(1, u)
+    b = seq.rhs(1, u)
+    M = oracle.Matrix.from_host(hm)
+    k = 6
+    snaps = [oracle.solve(M, seq.rhs(1, u) + 0.1 * i * rng.standard_normal(cfg.n), m=cfg.m, tol=1e-6)["x"]
+             for i in range(k)]
+    m = 20                                             # restarts inside the solve
+    ctx = make_ctx(hm, max_m=m, s=k, k=k, flags=rgb.RG_FLAG_CGS2 | rgb.RG_FLAG_NO_PERSIST)
+    W = None
+    if variant != "plain":
+        for v in snaps:
+            ctx.push_snapshot(t(v))
+        ke, _ = ctx.build_recycle(k)
+        W, _, _ = oracle.recycle_basis(np.stack(snaps, 1), k)
+        assert ke == W.shape[1]
+    x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), x, m=m, variant=variant, tol=cfg.tol, history_cap=5000)
+    ref = oracle.solve(M, b, m=m, variant=variant, W=W, tol=cfg.tol)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["iterations"] - ref["iterations"]) <= 2, (rep["iterations"], ref["iterations"])
+    xg = x.cpu().numpy()
+    assert np.linalg.norm(xg - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+    r = b - oracle.spmv(M, xg)
+    assert np.linalg.norm(r) / np.linalg.norm(b) <= cfg.tol
+    ctx.close()
