@@ -29,6 +29,7 @@ constexpr int PM = 64;        // max restart length on this path
 constexpr int PK = 64;        // max recycle dimension on this path
 constexpr int PCOL = PK + PM + 2;
 constexpr int NPFN = 10;      // k_solve_persistent instantiations (launch_persistent's table)
+constexpr int CB_TSW = 36;   // k_cbuild per-warp tile column stride (32 rows + 4: DMMA fragment loads spread over banks)
 constexpr int CBK = 22;       // max recycle dimension of the one-kernel operator build (k (k+1) / 2 <= MAXRED)
 
 struct PArgs {
@@ -1042,15 +1043,23 @@ fail:
 // CTA's rows (lanes over rows), reduced across lanes once per pass.
 // CGIVEN: C = A W is already in the Q columns (BSR: the TMA + DMMA SpMM ran first); the kernel then is
 // the CholQR2 alone (replaces 2 x (Gram, reduce, Cholesky, X R^{-1}) + R_C finish: 8 launches).
+// FP64 tensor-core MMA (DMMA.8x8x4): C[8x8] += A[8x4] B[4x8]; fragments (PTX m8n8k4 .f64):
+// a: A(lane/4, lane%4), b: B(lane%4, lane/4), c{0,1}: C(lane/4, 2*(lane%4) + {0,1}).
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+}
 template <int KC, bool CGIVEN = false>
 __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs pa, int* cflag) {
-  constexpr int NB = KC / 4;                       // 4-column blocks
-  constexpr int NBLK = NB * (NB + 1) / 2;          // Gram blocks (a-block <= b-block)
-  constexpr int GPW = (NBLK + PT / 32 - 1) / (PT / 32);  // Gram blocks per warp
-  static_assert(GPW <= 2, "at most two Gram blocks per warp");
+  // Gram of the staged rows: warp w stages ITS 32 rows of a tile ([KC][CB_TSW] column-major, rows past
+  // the CTA's range zero) and accumulates the upper 8 x 8 block pairs (I <= J) of their Gram with FP64
+  // DMMA (m8n8k4: 8 k-steps over the 32 rows) in registers across all tiles: no CTA barrier per tile
+  // (the first version staged PT-row tiles for 4 x 4 register blocks owned by NB(NB+1)/2 warps: two
+  // __syncthreads per tile, the other warps idle — C4 k = 8: 462 us, barrier-stall bound).
+  constexpr int NBK = KC / 8, NPR = NBK * (NBK + 1) / 2, NWP = PT / 32;
   extern __shared__ double sm[];
-  double* tile = sm;                   // [KC][PT]
-  double* R1 = tile + KC * PT;         // [col][row], k x k each
+  double* tile = sm;                   // per warp [KC][CB_TSW]; after a pass: per-warp Gram partials
+  double* R1 = tile + KC * NWP * CB_TSW;  // [col][row], k x k each
   double* R1i = R1 + CBK * CBK;
   double* R2 = R1i + CBK * CBK;
   double* R2i = R2 + CBK * CBK;
@@ -1077,54 +1086,44 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
     return pa.llred ? greduce_ll(dpart, nv, pa.ll, tot, rep, bsh, &s_fail, nullptr)
                     : greduce(dpart, nv, L.partial, pa.tot_g, tot, pa.bar, &s_fail, nullptr);
   };
-  // this warp's Gram blocks g (ab[g], bb[g]): rows 4 ab.., columns 4 bb..
-  int ab[GPW], bb[GPW];
-  bool gw[GPW];
-#pragma unroll
-  for (int g = 0; g < GPW; ++g) {
-    int q = wid + g * (PT / 32), a = 0;
-    while (q >= NB - a && a < NB) { q -= NB - a; ++a; }
-    ab[g] = a;
-    bb[g] = a + q;
-    gw[g] = wid + g * (PT / 32) < NBLK && 4 * ab[g] < k && 4 * bb[g] < k;
-  }
-  double gacc[GPW][16];
+  double* wt = tile + wid * KC * CB_TSW;
+  double gacc[NPR][2];
   auto gram_zero = [&]() {
 #pragma unroll
-    for (int g = 0; g < GPW; ++g)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) gacc[g][i] = 0.0;
+    for (int q = 0; q < NPR; ++q) gacc[q][0] = gacc[q][1] = 0.0;
   };
-  auto gram_tile = [&](int cnt) {  // accumulate the staged tile's rows (lanes over rows)
+  auto gram_rows = [&]() {  // the warp's staged 32 rows
+    __syncwarp();
+    int q = 0;
 #pragma unroll
-    for (int g = 0; g < GPW; ++g) {
-      if (!gw[g]) continue;
-      for (int t = lane; t < cnt; t += 32) {
-        double xa[4], xb[4];
+    for (int I = 0; I < NBK; ++I)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          xa[i] = tile[(4 * ab[g] + i) * PT + t];
-          xb[i] = tile[(4 * bb[g] + i) * PT + t];
-        }
+      for (int J = I; J < NBK; ++J, ++q) {
+        const double* ta = wt + (8 * I + (lane >> 2)) * CB_TSW + (lane & 3);
+        const double* tb = wt + (8 * J + (lane >> 2)) * CB_TSW + (lane & 3);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) gacc[g][4 * i + j] += xa[i] * xb[j];
+        for (int kk = 0; kk < 8; ++kk) dmma_f64(gacc[q][0], gacc[q][1], ta[4 * kk], tb[4 * kk]);
       }
-    }
+    __syncwarp();
   };
-  auto gram_flush = [&]() {  // lane sums -> dpart (packed upper, index of (a, b), a <= b)
+  auto gram_flush = [&]() {  // per-warp blocks -> shared, warps summed in index order -> dpart (packed upper)
+    __syncthreads();  // every warp is done with its tile region (reused here)
+    int q = 0;
 #pragma unroll
-    for (int g = 0; g < GPW; ++g) {
-      if (!gw[g]) continue;
+    for (int I = 0; I < NBK; ++I)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double v = warp_sum(gacc[g][4 * i + j]);
-          const int a2 = 4 * ab[g] + i, b2 = 4 * bb[g] + j;
-          if (lane == 0 && a2 < k && b2 < k && a2 <= b2) dpart[a2 * k - a2 * (a2 - 1) / 2 + (b2 - a2)] = v;
-        }
+      for (int J = I; J < NBK; ++J, ++q) {
+        const int a2 = 8 * I + (lane >> 2), b2 = 8 * J + 2 * (lane & 3);
+        tile[(size_t)wid * KC * KC + a2 * KC + b2] = gacc[q][0];
+        tile[(size_t)wid * KC * KC + a2 * KC + b2 + 1] = gacc[q][1];
+      }
+    __syncthreads();
+    for (int e = tid; e < k * k; e += PT) {
+      const int a2 = e / k, b2 = e % k;
+      if (a2 > b2) continue;
+      double v = 0.0;
+      for (int w = 0; w < NWP; ++w) v += tile[(size_t)w * KC * KC + a2 * KC + b2];
+      dpart[a2 * k - a2 * (a2 - 1) / 2 + (b2 - a2)] = v;
     }
     __syncthreads();
   };
@@ -1162,9 +1161,11 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
   };
   // row r of the Q columns times an upper-triangular inverse (this thread owns the row); computed in
   // place in x, columns descending (column c needs x_0..x_c only: one KC-vector of registers)
-  auto row_tri = [&](int64_t r, const double* Ri, double* x) {
+  auto row_load = [&](int64_t r, double* x) {
 #pragma unroll
     for (int l = 0; l < KC; ++l) x[l] = l < k ? Qc[(int64_t)l * ld + r] : 0.0;
+  };
+  auto tri = [&](const double* Ri, double* x) {
 #pragma unroll
     for (int c = KC - 1; c >= 0; --c) {
       double acc = 0.0;
@@ -1173,6 +1174,9 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
       x[c] = acc;
     }
   };
+  // KC = 8: the next row's values are loaded while this row's triangular products run (16 loads in
+  // flight per thread in the streaming passes 2 and 3); wider rows would spill
+  constexpr bool PF = KC <= 8;
   for (int i = tid; i < MAXRED; i += PT) dpart[i] = 0.0;
   for (int i = tid; i < 4 * CBK * CBK; i += PT) R1[i] = 0.0;
   __syncthreads();
@@ -1226,44 +1230,67 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
 #pragma unroll
       for (int u = 0; u < KC; ++u) {
         if (u < k && !CGIVEN) Qc[(int64_t)u * ld + r] = acc[u];
-        tile[u * PT + tid] = acc[u];
+        wt[u * CB_TSW + lane] = acc[u];
       }
+    } else {
+#pragma unroll
+      for (int u = 0; u < KC; ++u) wt[u * CB_TSW + lane] = 0.0;
     }
-    __syncthreads();
-    gram_tile(cnt);
-    __syncthreads();
+    gram_rows();
   }
   gram_flush();
   bool ok = gred(P2);
   if (ok) chol(R1, R1i);
-  // pass 2: Q1 = C R1^{-1} in place, Gram of Q1
+  // pass 2: Gram of Q1 = C R1^{-1}, Q1 NOT stored (pass 3 recomputes it from C with the same arithmetic:
+  // one n x k write and its re-read less than storing Q1)
   gram_zero();
-  for (int64_t base = r0; ok && base < r1; base += PT) {
-    const int64_t r = base + tid;
-    const int cnt = (int)min((int64_t)PT, r1 - base);
-    if (tid < cnt) {
-      double y[KC];
-      row_tri(r, R1i, y);
+  {
+    double nx[KC];
+    if (ok && r0 + tid < r1) row_load(r0 + tid, nx);
+    for (int64_t base = r0; ok && base < r1; base += PT) {
+      const int64_t r = base + tid;
+      const int cnt = (int)min((int64_t)PT, r1 - base);
+      if (tid < cnt) {
+        double y[KC];
+        if (PF) {
 #pragma unroll
-      for (int u = 0; u < KC; ++u) {
-        if (u < k) Qc[(int64_t)u * ld + r] = y[u];
-        tile[u * PT + tid] = u < k ? y[u] : 0.0;
+          for (int u = 0; u < KC; ++u) y[u] = nx[u];
+          if (r + PT < r1) row_load(r + PT, nx);
+        } else {
+          row_load(r, y);
+        }
+        tri(R1i, y);
+#pragma unroll
+        for (int u = 0; u < KC; ++u) wt[u * CB_TSW + lane] = u < k ? y[u] : 0.0;
+      } else {
+#pragma unroll
+        for (int u = 0; u < KC; ++u) wt[u * CB_TSW + lane] = 0.0;
       }
+      gram_rows();
     }
-    __syncthreads();
-    gram_tile(cnt);
-    __syncthreads();
   }
   gram_flush();
   if (ok) ok = gred(P2);
   if (ok) chol(R2, R2i);
-  // pass 3: Q = Q1 R2^{-1} in place (no staging)
-  for (int64_t r = r0 + tid; ok && r < r1; r += PT) {
-    double y[KC];
-    row_tri(r, R2i, y);
+  // pass 3: Q = (C R1^{-1}) R2^{-1} in place (no staging)
+  {
+    double nx[KC];
+    if (ok && r0 + tid < r1) row_load(r0 + tid, nx);
+    for (int64_t r = r0 + tid; ok && r < r1; r += PT) {
+      double y[KC];
+      if (PF) {
 #pragma unroll
-    for (int u = 0; u < KC; ++u)
-      if (u < k) Qc[(int64_t)u * ld + r] = y[u];
+        for (int u = 0; u < KC; ++u) y[u] = nx[u];
+        if (r + PT < r1) row_load(r + PT, nx);
+      } else {
+        row_load(r, y);
+      }
+      tri(R1i, y);
+      tri(R2i, y);
+#pragma unroll
+      for (int u = 0; u < KC; ++u)
+        if (u < k) Qc[(int64_t)u * ld + r] = y[u];
+    }
   }
   if (cta0) {
     // R_C = R2 R1, R_C^{-1} = R1^{-1} R2^{-1} ([col][row]), and k_rc_finish's singularity test
@@ -1393,7 +1420,7 @@ cudaError_t launch_cbuild(const Layout& L, const MatDev& A, DevState* st, double
                                (const void*)k_cbuild<8, true>, (const void*)k_cbuild<16, true>,
                                (const void*)k_cbuild<24, true>};
   const void* fn = fns[vi];
-  const size_t smem = sizeof(double) * ((size_t)kc * PT + 4 * CBK * CBK + 2 * MAXRED);
+  const size_t smem = sizeof(double) * ((size_t)kc * (PT / 32) * CB_TSW + 4 * CBK * CBK + 2 * MAXRED);
   static int occ_dev[MAXDEV][6] = {};  // 0: not yet queried on that device, else occupancy + 1
   int& oc = occ_dev[current_device()][vi];
   if (oc == 0) {
