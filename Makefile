@@ -23,7 +23,7 @@ PKG       := paper_1807_09467_b200
 RG_SRC    := $(wildcard $(PKG)/csrc/*.cu)
 RG_HDR    := $(wildcard $(PKG)/csrc/*.cuh) include/rg.h
 
-all: oracle synth rg
+all: oracle synth rg rg-checked
 
 rg: $(PKG)/lib/librg.so
 synth: synth/libsynth.so synth/libsynth_cuda.so
@@ -40,6 +40,18 @@ $(PKG)/lib/librg.so: $(RG_OBJ) build/variant
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $(RG_OBJ)
 
+# CHECKED build (test infrastructure, never loaded by the product path): device-side bounds / invariant
+# checks (RG_CHK in csrc/common.cuh) compiled in; failures return RG_E_CHECK.  The stand-in for
+# compute-sanitizer, which the GPU pool refuses (profiles/r02_sanitizer/).
+RG_CHK_OBJ := $(patsubst $(PKG)/csrc/%.cu,build/rg_chk/%.o,$(RG_SRC))
+rg-checked: $(PKG)/lib/librg_checked.so
+build/rg_chk/%.o: $(PKG)/csrc/%.cu $(RG_HDR)
+	@mkdir -p build/rg_chk
+	$(NVCC) $(filter-out -DRG_EXPERIMENTS,$(NVFLAGS)) -DRG_CHECKED -c -o $@ $<
+$(PKG)/lib/librg_checked.so: $(RG_CHK_OBJ)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(RG_CHK_OBJ)
+
 synth/libsynth.so: synth/synth.c synth/synth_common.h
 	$(CC) $(CFLAGS) -fopenmp -shared -o $@ synth/synth.c -lm
 
@@ -50,7 +62,7 @@ oracle/liboracle.so: oracle/oracle.c
 	$(CC) $(CFLAGS) -fopenmp -shared -o $@ oracle/oracle.c -lm
 
 clean:
-	rm -f $(PKG)/lib/librg.so synth/*.so oracle/*.so
-	rm -rf build/rg build/rg_exp build/variant
+	rm -f $(PKG)/lib/librg.so $(PKG)/lib/librg_checked.so synth/*.so oracle/*.so
+	rm -rf build/rg build/rg_exp build/rg_chk build/variant
 
-.PHONY: all rg synth oracle clean
+.PHONY: all rg rg-checked synth oracle clean

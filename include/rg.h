@@ -53,7 +53,10 @@ typedef enum {
   RG_E_SINGULAR = 5, /* A W rank deficient: min|r_ii| <= 1e-12 max|r_ii| of R_C, or (oblique)
                         E = W^T A W singular: a pivot <= 1e-13 max|E_ab| (PAPER.md:562-564
                         "E_s may be singular"); the recycle space is cleared                   */
-  RG_E_NUMERIC = 6   /* NaN/Inf met during the solve                                           */
+  RG_E_NUMERIC = 6,  /* NaN/Inf met during the solve                                           */
+  RG_E_CHECK = 7     /* CHECKED builds only (make rg-checked -> lib/librg_checked.so, test
+                        infrastructure): a device-side bounds / invariant check failed; the
+                        message names the source file and line.  Product builds never return it */
 } rg_status;
 
 typedef enum { RG_CSR = 0, RG_BSR = 1 } rg_format;

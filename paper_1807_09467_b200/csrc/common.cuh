@@ -63,6 +63,7 @@ struct DevState {
   int dcgs;       // 1: delayed CGS2 (one reduction per Arnoldi step), 0: classical CGS2
   int cfail;      // set by the C = A W build of this solve: singular CholQR2 factor / R_C / E
   int kb_steps;   // RG_FLAG_KEEP_BASIS: Arnoldi steps J of the last finished cycle kept for rg_export
+  unsigned chk_count, chk_where;  // CHECKED builds: failed device checks, first (file id << 16 | line)
   double bnorm, beta, relres;
   double k2_inv_nu, k2_u_next, k2_y;  // DCGS2 update-pass scalars (v_j = u/nu + ..., u_next = ...)
   // least-squares state
@@ -98,6 +99,7 @@ struct Layout {
   int64_t ld;      // = n_pad (multiple of 64)
   int64_t n;       // true dimension
   int maxk;        // W / Q region width
+  int ncol;        // columns of Z (checked builds bound every column index by it)
   int VB;          // first V column = 2 * maxk
   double* x;       // iterate (n_pad)
   const double* b; // right-hand side (n_pad)
@@ -147,6 +149,40 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   __syncthreads();
   return sh[32];
 }
+
+// ---- CHECKED builds (make rg-checked, -DRG_CHECKED; test infrastructure): device-side bounds and
+// invariant checks on the hand-computed indexing — TMA copy ranges, basis column ranges, reduction
+// widths, least-squares state indices, sparse column indices, persistent-kernel row / neighbour
+// ranges.  A failing check is counted in the device state (first location kept) and execution
+// continues; the host returns RG_E_CHECK after the call.  Compiled out of the product.
+#ifndef RG_FILE_ID
+#define RG_FILE_ID 0
+#endif
+#ifdef RG_CHECKED
+__device__ __noinline__ inline void rg_chk_fail(DevState* st, unsigned where) {
+  if (!st) return;
+  atomicAdd(&st->chk_count, 1u);
+  atomicCAS(&st->chk_where, 0u, where);
+}
+#define RG_CHK(st, cond)                                                        \
+  do {                                                                          \
+    if (!(cond)) rg_chk_fail((st), ((unsigned)RG_FILE_ID << 16) | (unsigned)__LINE__); \
+  } while (0)
+#else
+#define RG_CHK(st, cond) \
+  do {                   \
+  } while (0)
+#endif
+
+// Programmatic dependent launch (PDL).  A kernel launched with cudaLaunchAttributeProgrammaticStream-
+// Serialization (launch_ex(..., pdl = true)) may be scheduled while its predecessor on the stream (or
+// graph edge) drains: it overlaps its launch ramp and any prologue that does not read the predecessor's
+// output with the predecessor's tail.  pdl_wait() blocks until the predecessor grid has completed and
+// its writes are visible (a no-op when the kernel was launched normally); pdl_trigger() lets the
+// dependent grid be scheduled once every CTA of this grid has executed it (or exited).  Only kernels
+// that call pdl_wait() before consuming anything a predecessor wrote are ever launched with pdl = true.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Kernel-entry profiling hook (block 0 stamps the start time).
 __device__ __forceinline__ void prof_begin(DevState* st, int kid) {

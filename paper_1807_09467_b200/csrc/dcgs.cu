@@ -23,6 +23,7 @@
 // (C^T u - (V_j^T C)^T a)/nu to the maintained V^T C (state Gm), and corrects the first-pass
 // coefficients by -(V_{j+1}^T C) t / nu; DK2 adds -C t / nu to the next u.  No extra pass or
 // reduction: M_D A v_j is never formed explicitly.
+#define RG_FILE_ID 1  // RG_CHK locations (checked builds)
 #include "epilogue.cuh"
 #include "kernels.cuh"
 #include "knobs.cuh"
@@ -48,6 +49,7 @@ __device__ void epi_dcgs(DevState* st, const Layout& L, const double* tot, int p
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB;
   const int nq = VB - lo;  // Q columns inside P (deflate)
+  RG_CHK(st, j >= 0 && j < MAXM && lo + p <= MAXCOL && (var != RG_DEFLATE || nq == k));
   const double* a = tot;
   const double* b = tot + p;
   const double ss = tot[2 * p], gg = tot[2 * p + 1];
@@ -198,6 +200,7 @@ __device__ __forceinline__ void dk1_finish(const Layout& L, DevState* st, double
 __global__ void __launch_bounds__(256) k_dcgs_ls(Layout L, DevState* st, unsigned long long cond) {
   __shared__ double lst[MAXK + 2];
   const int jx = st->ls_j;
+  RG_CHK(st, jx < MAXM && jx < st->m);
   if (jx >= 0) {
     if (st->profile && threadIdx.x == 0) st->kstat[K_DLS].start = gtimer();
     const int nd = st->variant == RG_AUGMENT ? st->k_eff : 0;
@@ -515,8 +518,12 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nv = 2 * p + 2 + nqd, ncols = p + nqd;
   const bool obl = galerkin_variant(var);
-  for (int c = tid; c < ncols; c += TS_T)
+  for (int c = tid; c < ncols; c += TS_T) {
     colidx[c] = c < p ? lo + c : (obl ? ((c - p) < k ? c - p : proj_base(var, k) + (c - p - k)) : QB + (c - p));
+    RG_CHK(st, colidx[c] >= 0 && colidx[c] < L.ncol && (c >= p || colidx[c] < VB + j));
+  }
+  RG_CHK(st, j >= 0 && j <= st->m && st->m <= MAXM && k >= 0 && k <= L.maxk && lo >= 0 && nv <= DK1RED && nv <= nvw &&
+                 ncols <= DK1RED && (!have_y || VB + j + 1 < L.ncol));
   ts_init(full, empty);
   const int64_t ng = ld >> 5;
   const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
@@ -532,6 +539,7 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
                    (int)min((int64_t)TS_R, r1 - base), pol);
     }
   } else {  // ---- consumers: thread = row of the tile
+    pdl_wait();  // u, y: written by the SpMV this launch may overlap (PDL); the basis stream above is not
     double s_uu = 0.0, s_uy = 0.0;
     int t = 0;
     // u, y of the tile TS_PF tiles ahead are loaded now (L2 hits, off the per-tile critical path);
@@ -607,6 +615,7 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
       wsm[wid * nvw + 2 * p + 1] = t2;
     }
   }
+  pdl_trigger();  // the update pass may be scheduled (it waits for this grid before reading anything)
   __syncthreads();
   for (int i = tid; i < nv; i += TS_T) {
     double sacc = 0.0;
@@ -622,6 +631,7 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk2_tma(Layout L, DevState* st) {
   __shared__ __align__(8) uint64_t full[TS_STG], empty[TS_STG];
   __shared__ double cv[MAXCOL + MAXK], cn[MAXCOL + MAXK];
   __shared__ int colidx[MAXCOL + MAXK];
+  pdl_wait();  // everything below reads DK1's epilogue output (launched with PDL behind DK1)
   if (st->k2_skip) { prof_noop(st, K_DK2); return; }  // (not st->active: k_dcgs_ls may be writing it)
   prof_begin(st, K_DK2);
   const int j = st->j - 1, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
@@ -643,6 +653,7 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk2_tma(Layout L, DevState* st) {
       colidx[c] = pb2 + (c - p);
     }
   }
+  RG_CHK(st, j >= 0 && j < st->m && VB + j + 1 < L.ncol && ncols <= MAXCOL + MAXK && lo >= 0 && pb2 + k2 <= L.ncol);
   const double inv = st->k2_inv_nu, fy = st->k2_y, fu = st->k2_u_next;
   ts_init(full, empty);
   const int64_t ng = ld >> 5;
@@ -697,6 +708,13 @@ static int tma_grid(int64_t rows) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// PDL between the kernels of an Arnoldi step (SpMV -> DK1 -> DK2): measured in a conditional WHILE body,
+// ~2.5 us per edge (tools/cutest/t_pdl.cu); RG_NO_PDL (EXPERIMENTS builds) for A/B
+static bool pdl_on() {
+  static const bool off = knob("RG_NO_PDL");
+  return !off;
+}
+
 cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond) {
   static bool init = false;
   if (!init) {
@@ -718,8 +736,7 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
                              (int)(sizeof(double) * ((size_t)TS_STG * TS_STAGE + (size_t)(TS_R / 32) * DK1RED)));
         attr = true;
       }
-      k_dk1_tma<<<tma_grid(L.ld), TS_T, smem, s>>>(L, st, cond, nvw);
-      return cudaGetLastError();
+      return launch_ex(k_dk1_tma, dim3(tma_grid(L.ld)), dim3(TS_T), smem, s, pdl_on(), L, st, cond, nvw);
     }
     if (!tiles) {
       const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
@@ -749,8 +766,7 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
     // one SM left to the concurrent least-squares kernel (k_dcgs_ls) so that no update-pass CTA shares
     // an SM with it
     const int g2 = tma_grid(L.ld) == NSM ? NSM - 1 : tma_grid(L.ld);
-    k_dk2_tma<<<g2, TS_T, sizeof(double) * TS_STG * TS_STAGE, s>>>(L, st);
-    return cudaGetLastError();
+    return launch_ex(k_dk2_tma, dim3(g2), dim3(TS_T), sizeof(double) * TS_STG * TS_STAGE, s, pdl_on(), L, st);
   }
   k_dk2<<<vec_grid(L.ld), DT, 0, s>>>(L, st);
   return cudaGetLastError();

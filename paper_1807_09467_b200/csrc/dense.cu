@@ -5,6 +5,7 @@
 // Gram/Jacobi pass on Y to restore the accuracy the squared conditioning costs (DESIGN.md
 // reading R-SVD), and W = Y V_2 Sigma^{-1}.  CholQR2 of C = A W uses the same Gram and X*M
 // kernels plus a one-CTA Cholesky.
+#define RG_FILE_ID 2  // RG_CHK locations (checked builds)
 #include <algorithm>
 #include <cstdlib>
 
@@ -60,6 +61,7 @@ __global__ void __launch_bounds__(GT) k_gram_mma(const double* __restrict__ Y, i
   extern __shared__ double ring[];     // NST x s8 x TS
   if (st) prof_begin(st, K_GRAM);
   const int s8 = (s + 7) & ~7, nb = s8 / 8, np = nb * (nb + 1) / 2;
+  RG_CHK(st, s >= 1 && s8 <= S8MAX);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int MAXQ = (S8MAX / 8) * (S8MAX / 8 + 1) / 2 / 8 + 1;  // pairs per warp (<= 5)
   double acc[MAXQ][2];

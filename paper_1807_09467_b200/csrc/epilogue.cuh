@@ -85,6 +85,7 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
   const bool split = jx >= 0;
   const int j = split ? jx : st->j, VB = L.VB, k = st->k_eff, var = st->variant;
   const int QB = VB - k;
+  RG_CHK(st, j >= 0 && j < MAXM && j < st->m && k <= MAXK && nd <= MAXK && st->hist_cap <= (1 << 16));
   const double nrm = sqrt(tot[nd]);
   // ---- one parallel batch of loads: h column, rotations, scalars
   for (int i = tid; i <= j; i += bd) h[i] = split ? st->Hraw[j][i] : st->hcol[VB + i];

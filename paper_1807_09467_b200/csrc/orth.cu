@@ -15,6 +15,7 @@
 // OP_NORMB: ||b||.
 // Oblique variant (M_D = I - C E^{-1} W^T): OP_OB_CSD / OP_OB_SD t = E^{-1} W^T w,
 // OP_OB_CSU / OP_OB_SU w -= C t (+ ||w|| -> cycle-start epilogue at the cycle start).
+#define RG_FILE_ID 3  // RG_CHK locations (checked builds)
 #include "epilogue.cuh"
 #include "kernels.cuh"
 #include "knobs.cuh"
@@ -93,6 +94,8 @@ __global__ void __launch_bounds__(OT, 2) k_orth(OrthArgs a) {
     case OP_OB_SU: w = L.Z + (int64_t)(VB + j + 1) * ld; u0 = proj_base(var, k); u1 = u0 + k; break;
     default: w = const_cast<double*>(L.b); nrmflag = true; break;  // OP_NORMB (read only)
   }
+  RG_CHK(st, u0 >= 0 && u1 <= L.ncol && u2 >= 0 && u3 <= L.ncol && d0 >= 0 && d1 <= L.ncol && d1 - d0 < MAXRED &&
+                 u1 <= MAXCOL && u3 <= MAXCOL);
   const bool upd = (u1 > u0) || (u3 > u2) || (op == OP_XUPD && L.prec) || op == OP_VY;
   const bool dots = d1 > d0;
   const int nd = d1 - d0;
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(544, 1) k_cgs_tma(Layout L, DevState* st, int 
   __shared__ double tot[MAXRED];
   __shared__ double bsh[33];
   constexpr bool UPD = MODE != 0, DOTS = MODE != 2, NRM = MODE == 2;
+  pdl_wait();  // launched with PDL behind the previous kernel of the Arnoldi step: everything below reads its output
   const int kid = op == OP_D1 ? K_ORTH_D1 : op == OP_UD2 ? K_ORTH_UD2 : op == OP_UN ? K_ORTH_UN
                 : op == OP_CS_DQ ? K_CS_DQ : K_CS_UN;
   const bool cs = op == OP_CS_DQ || op == OP_CS_UN;
@@ -374,6 +378,8 @@ __global__ void __launch_bounds__(544, 1) k_cgs_tma(Layout L, DevState* st, int 
   int TR = 512;
   while (TR > 32 && ((size_t)CG_NS * (p + 1) * TR * 8 > (size_t)CG_SMEM || (p + (512 / TR) - 1) / (512 / TR) > CG_CPT)) TR >>= 1;
   const int G = 512 / TR, SD = (p + 1) * TR;  // doubles per stage: p columns then w
+  RG_CHK(st, c0 >= 0 && p >= 0 && c0 + p <= tc && tc < L.ncol && p < MAXRED && p <= MAXCOL &&
+                 (size_t)CG_NS * SD * 8 <= (size_t)CG_SMEM && (p + G - 1) / G <= CG_CPT && 16 * p <= CG_NS * SD);
   if (tid == 0) {
     for (int i = 0; i < CG_NS; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(cg_u32(&full[i])), "r"(1));
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(544, 1) k_cgs_tma(Layout L, DevState* st, int 
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(cg_u32(&empty[s])) : "memory");
     }
   }
+  pdl_trigger();
   __syncthreads();  // all stages consumed: the ring is free for the per-warp partials
   double* wsm = ring;  // [16][p]
   if (DOTS) {
@@ -548,10 +555,13 @@ cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, u
       attr[dev] = true;
     }
     const int mode = (op == OP_D1 || op == OP_CS_DQ) ? 0 : op == OP_UD2 ? 1 : 2;
-    if (mode == 0) k_cgs_tma<0><<<NSM, 544, CG_SMEM, s>>>(L, st, op, cond);
-    else if (mode == 1) k_cgs_tma<1><<<NSM, 544, CG_SMEM, s>>>(L, st, op, cond);
-    else k_cgs_tma<2><<<NSM, 544, CG_SMEM, s>>>(L, st, op, cond);
-    return cudaGetLastError();
+    // PDL inside the Arnoldi step (behind the SpMV / the previous pass); the cycle-start passes follow
+    // kernels that do not trigger early
+    static const bool no_pdl = knob("RG_NO_PDL");
+    const bool pdl = !no_pdl && (op == OP_D1 || op == OP_UD2 || op == OP_UN);
+    if (mode == 0) return launch_ex(k_cgs_tma<0>, dim3(NSM), dim3(544), CG_SMEM, s, pdl, L, st, op, cond);
+    if (mode == 1) return launch_ex(k_cgs_tma<1>, dim3(NSM), dim3(544), CG_SMEM, s, pdl, L, st, op, cond);
+    return launch_ex(k_cgs_tma<2>, dim3(NSM), dim3(544), CG_SMEM, s, pdl, L, st, op, cond);
   }
   if (L.cgs_ok) {  // register-resident CGS kernels (augment's OP_UN also needs Q^T w: generic path)
     const int g = vec_grid(L.ld);

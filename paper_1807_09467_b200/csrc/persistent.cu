@@ -10,6 +10,7 @@
 // CTA 0 alone writes the solve report (iterations, history, status) to the device state.
 // Oblique (obl): P = V only; the Galerkin cycle start and the M_D projection folded into the DCGS2
 // coefficients exactly as dcgs.cu does it (V^T C replicated in shared memory).
+#define RG_FILE_ID 4  // RG_CHK locations (checked builds)
 #include "epilogue.cuh"
 #include "kernels.cuh"
 #include "knobs.cuh"
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
       const int G = gridDim.x;
       s_clo = s_chi < 0 ? (int)blockIdx.x : row_owner(s_clo, ng, G);
       s_chi = s_chi < 0 ? (int)blockIdx.x : row_owner(s_chi, ng, G);
+      RG_CHK(st, s_clo >= 0 && s_clo <= s_chi && s_chi < G && s_clo <= (int)blockIdx.x && (int)blockIdx.x <= s_chi);
     }
     __syncthreads();
   }
@@ -599,6 +601,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
     int jf = -1;
     for (int j = 0; j <= m; ++j) {
       const int p = nq + j;
+      RG_CHK(st, m <= MAXM && VB + j < L.ncol && (j == m || VB + j + 1 < L.ncol) && p <= MAXCOL && nq <= MAXK);
       double* __restrict__ u = Z + (int64_t)(VB + j) * ld;
       double* __restrict__ y = Z + (int64_t)(VB + j + 1) * ld;
       const bool have_y = j < m;
@@ -1071,6 +1074,7 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
   const MatDev& A = pa.A;
   DevState* st = pa.st;
   const int k = pa.k, QB = L.VB - k, P2 = k * (k + 1) / 2;
+  RG_CHK(pa.st, k >= 1 && k <= KC && k <= CBK && QB >= k && P2 <= MAXRED);
   const int64_t ld = L.ld;
   double* Qc = L.Z + (int64_t)QB * ld;
   const double* __restrict__ Wc = L.Z;

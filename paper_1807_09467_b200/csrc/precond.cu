@@ -11,6 +11,7 @@
 // one launch per colour and direction; the backward sweep of the last colour is the identity.
 // It is applied as a RIGHT preconditioner: the Arnoldi SpMV becomes y = A M^{-1} u and the cycle
 // end adds M^{-1} (V y) — GMRES keeps minimising the TRUE residual.
+#define RG_FILE_ID 5  // RG_CHK locations (checked builds)
 #include "kernels.cuh"
 
 #include <algorithm>

@@ -4,6 +4,7 @@
 // arithmetic step of the method runs on the device.  A restart cycle (m Arnoldi steps, the
 // cycle-end update and the next cycle start) is captured once as a CUDA graph and replayed;
 // the host reads one 4-byte-class header per cycle to learn whether the solve has finished.
+#define RG_FILE_ID 6  // RG_CHK locations (checked builds)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a profiler is attached
@@ -707,6 +708,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   c->L.ld = c->npad;
   c->L.n = n;
   c->L.maxk = c->max_k;
+  c->L.ncol = c->ncol;
   c->L.VB = VB;
   c->L.x = c->x;
   c->L.b = c->b;
@@ -776,6 +778,26 @@ RG_API rg_status rg_clear_snapshots(rg_ctx* c) {
 }
 
 // Second half of a recycle build, once sigma is on the host: rank, k_eff, W = Y V2 Sigma^{-1}.
+#ifdef RG_CHECKED
+// CHECKED builds: device check failures (RG_CHK) recorded since the last read, by the kernels of any call
+static rg_status chk_report(unsigned count, unsigned where) {
+  static const char* files[] = {"?", "dcgs.cu", "dense.cu", "orth.cu", "persistent.cu", "precond.cu", "rg.cu", "spmv.cu"};
+  const unsigned f = where >> 16;
+  char buf[192];
+  snprintf(buf, sizeof buf, "device check failed at %s:%u (or a header it includes), %u failure(s)",
+           f < 8 ? files[f] : "?", where & 0xffffu, count);
+  return fail(RG_E_CHECK, buf);
+}
+static rg_status chk_pending(rg_ctx* c) {
+  unsigned v[2] = {0u, 0u};
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return RG_OK;  // a CUDA error is reported by the call
+  cudaMemcpy(v, &c->st->chk_count, sizeof v, cudaMemcpyDeviceToHost);
+  if (!v[0]) return RG_OK;
+  cudaMemset(&c->st->chk_count, 0, sizeof v);
+  return chk_report(v[0], v[1]);
+}
+#endif
+
 rg_status finish_build(rg_ctx* c, int k, int modes, int s, int32_t* k_eff, double* sigma) {
   const int64_t ld = c->npad;
   cudaStream_t st = c->stream;
@@ -864,6 +886,10 @@ RG_API rg_status rg_build_recycle_modes(rg_ctx* c, int32_t k, int32_t modes, int
     fprintf(stderr, "rg_build_recycle: s=%d, Jacobi sweeps %.0f (pass 1) %.0f (pass 2)\n", s, sw[0], sw[1]);
   }
   const rg_status rs = finish_build(c, k, modes, s, k_eff, sigma);
+#ifdef RG_CHECKED
+  if (rs == RG_OK)
+    if (rg_status cs = chk_pending(c)) return cs;
+#endif
   if (timing) {
     const auto t3 = now();
     auto us = [](auto a2, auto b2) { return std::chrono::duration<double, std::micro>(b2 - a2).count(); };
@@ -908,6 +934,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
   // over the basis (C5: 7.3 GB vs ~0.8 GB), classical CGS2 is cheaper (measured C5: see DESIGN.md).
   const double basis_pass = 8.0 * (double)c->n * (double)(k + m + 2);
   c->dcgs_now = c->use_dcgs && !(c->A.bytes > basis_pass && !knob("RG_FORCE_DCGS"));
+#ifdef RG_CHECKED
+  if (rg_status cs = chk_pending(c)) return cs;  // failures of earlier calls (the header upload clears them)
+#endif
   DevState* h = c->hst;
   memset(h, 0, header_bytes());
   h->variant = eff;
@@ -1077,6 +1106,9 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     rep->rel_residual = h->bzero ? 0.0 : h->relres;
     rep->ms_total = ms;
   }
+#ifdef RG_CHECKED
+  if (h->chk_count) return chk_report(h->chk_count, h->chk_where);
+#endif
   if (h->status == RG_E_NUMERIC) return fail(RG_E_NUMERIC, "NaN/Inf met during the solve");
   if (h->status == RG_E_CUDA) return fail(RG_E_CUDA, "persistent solve: grid barrier timed out");
   return RG_OK;

@@ -8,6 +8,7 @@
 //   SM_PLAIN y = A x (rg_apply, C = A W)
 //   SM_RES_Y r = b - y into V column 0 where y = A x already sits there (the solve-start product
 //            fused into the C = A W SpMM as its extra column: one read of A for both), ||r||^2
+#define RG_FILE_ID 7  // RG_CHK locations (checked builds)
 #include "epilogue.cuh"
 #include "kernels.cuh"
 
@@ -41,6 +42,7 @@ struct Io {
 
 // Returns false if this launch is a no-op (decided uniformly from the device state).
 __device__ __forceinline__ bool setup(const SpmvArgs& a, Io& io, int& kid) {
+  pdl_trigger();  // the Arnoldi step's next kernel (PDL) may be scheduled as SpMV CTAs retire
   DevState* st = a.st;
   const Layout& L = a.L;
   io.res = false;
@@ -135,8 +137,10 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_csr(SpmvArgs a) {
             vv[u] = ok ? __ldcs(v + p + u) : 0.0;
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < 8; ++u) {
+            RG_CHK(a.st, !(p + u < p1) || (cc[u] >= 0 && cc[u] < A.n));
             if (p + u < p1) s += vv[u] * __ldg(x + cc[u]);
+          }
         }
       } else {
         for (int32_t p = p0 + lane; p < p1; p += LPR) s += __ldcs(v + p) * __ldg(x + __ldcs(ci + p));
@@ -191,8 +195,11 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_csr_pipe(SpmvArgs a) {
     load_row(row + stride, q0, q1, nc, nv);                                      // next row, in flight
     double s = 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 8; ++u) {
+      RG_CHK(a.st, !(p0 + u < p1) || (cc[u] >= 0 && cc[u] < A.n));
       if (p0 + u < p1) s += vv[u] * xv[u];
+    }
+    RG_CHK(a.st, p0 <= p1);
     for (int32_t p = p0 + 8; p < p1; ++p) s += __ldcs(v + p) * __ldg(x + __ldcs(ci + p));  // long rows
     nrm += emit(io, row, s);
     p0 = q0;
@@ -252,8 +259,10 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
     load_row(row + stride, wn, bn, cn, vn);                                        // next row, in flight
     double s = 0.0;
 #pragma unroll
-    for (int u = 0; u < SELL_CH; ++u)
+    for (int u = 0; u < SELL_CH; ++u) {
+      RG_CHK(a.st, !(u < w) || (cc[u] >= 0 && cc[u] < A.n));
       if (u < w) s += vv[u] * xv[u];
+    }
     for (int c = SELL_CH; c < w; ++c) {                                            // long rows
       const int64_t e = base + (int64_t)c * 32;
       s += __ldcs(A.sv + e) * __ldg(x + __ldcs(A.sci + e));
@@ -352,6 +361,7 @@ __global__ void __launch_bounds__(BT, 1) k_spmv_bsr_tma(SpmvArgs a) {
       int t = 0;
       for (int64_t I = blockIdx.x; I < A.nb; I += gridDim.x) {
         const int32_t p0 = __ldg(A.rp + I), p1 = __ldg(A.rp + I + 1);
+        RG_CHK(a.st, p0 >= 0 && p0 <= p1 && p1 <= A.nnz);
         for (int32_t p = p0; p < p1; ++p, ++t) {
           const int s = t % BNS;
           if (t >= BNS) bar_wait(&empty[s], (uint32_t)((t / BNS - 1) & 1));
@@ -371,6 +381,7 @@ __global__ void __launch_bounds__(BT, 1) k_spmv_bsr_tma(SpmvArgs a) {
       double s0 = 0.0, s1 = 0.0;
       for (int32_t p = p0; p < p1; ++p, ++t) {
         const int st = t % BNS;
+        RG_CHK(a.st, __ldg(A.ci + p) >= 0 && __ldg(A.ci + p) < A.nb);
         const double* __restrict__ xb = io.x + (int64_t)__ldg(A.ci + p) * 64 + q * 16;
         double xv[16];
 #pragma unroll

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RG_LIB_PATH") or os.path.join(_HERE, "lib", "librg.so")  # override: A/B experiments
 
-RG_OK, RG_E_INVAL, RG_E_NOMEM, RG_E_CUDA, RG_E_STATE, RG_E_SINGULAR, RG_E_NUMERIC = range(7)
+RG_OK, RG_E_INVAL, RG_E_NOMEM, RG_E_CUDA, RG_E_STATE, RG_E_SINGULAR, RG_E_NUMERIC, RG_E_CHECK = range(8)
 RG_CSR, RG_BSR = 0, 1
 RG_PLAIN, RG_AUGMENT, RG_DEFLATE, RG_OBLIQUE, RG_ORTHOGONAL = 0, 1, 2, 3, 4
 RG_HOST, RG_DEVICE = 0, 1
@@ -28,7 +28,7 @@ MODES = {"largest": RG_MODES_LARGEST, "smallest": RG_MODES_SMALLEST}
 VARIANTS = {"plain": RG_PLAIN, "augment": RG_AUGMENT, "deflate": RG_DEFLATE, "oblique": RG_OBLIQUE,
             "orthogonal": RG_ORTHOGONAL}
 STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E_STATE",
-          5: "RG_E_SINGULAR", 6: "RG_E_NUMERIC"}
+          5: "RG_E_SINGULAR", 6: "RG_E_NUMERIC", 7: "RG_E_CHECK"}
 
 # Symbols declared in include/rg.h (tests check the .so exports exactly these).
 SYMBOLS = ("rg_create", "rg_update_matrix", "rg_matrix_values", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle", "rg_build_recycle_modes",
