@@ -64,10 +64,12 @@ struct GraphKey {
   }
 };
 
-// Measured crossover (same box, alternating runs): the one-kernel persistent solve beats
-// the graph path up to ~1.6M padded rows (C3: 10.5 vs 11.5 ms); at C4's 2.1M its two-barrier reductions
-// lose to the graph path's last-CTA epilogues (15.9 vs 14.7 ms).
-constexpr int64_t PERSIST_MAX_ROWS = 1600000;
+// Measured crossover (same box, alternating runs, tools/crossover.py; round 2, after the
+// graph path's TMA DCGS2 passes, split epilogue and PDL): C3-type 9-point SELL sequences, deflate —
+// 409,600 rows persistent/graph 2.59/3.12 ms, 589,824 rows 4.09/4.43, 802,816 rows 6.52/6.30,
+// 1,048,576 rows (C3) 8.37/7.92; augment at 589,824 3.95/4.26 and at 1,048,576 8.47/8.08; C2 (262,144)
+// 2.25/3.39.  (Round 1: the persistent solve won up to ~1.6M rows.)
+constexpr int64_t PERSIST_MAX_ROWS = 700000;
 
 }  // namespace
 

@@ -122,7 +122,8 @@ def test_c2_full(c2_prefill, variant):
 def test_c3_full_sell():
     cfg = synth.CONFIGS["C3"]
     seq, X = _oracle_prefill(cfg, cfg.s)
-    rows = _teacher_forced(cfg, seq, X, cfg.s, 3, "deflate", "persistent")
+    # 1,048,576 rows: above the persistent-solve crossover (rg.cu PERSIST_MAX_ROWS, measured): graph + TMA DCGS2
+    rows = _teacher_forced(cfg, seq, X, cfg.s, 3, "deflate", "graph_dcgs")
     assert all(r[1] == cfg.k for r in rows)
 
 
