@@ -244,16 +244,19 @@ class GpuRun:
         self.t += 1
         if x_prev is not None:
             self.x.copy_(x_prev)
-        if cfg.kind == "9pt":                          # C3: A is the same for the whole sequence
-            self.gen.fill(self.t, self.x)              # (b_t only)
-        else:                                          # A_t, b_t from x_{t-1}, written straight into
-            self.gen.fill(self.t, self.x, val_ptr=self.vals_ptr)   # the solver's value buffer (a1)
-            self.ctx.update_values_inplace(self.nnz)
+        # a3 first: W depends only on the snapshot window, not on A_t, so the asynchronous build is issued
+        # before the generator and its completion (which the solve waits for on the host) overlaps the
+        # generation of A_t instead of leaving a bubble before the solve (tools/trace.py: ~0.1 ms/system)
         if self.variant != "plain" and self.nsnap > 0:
             if self.sync_build:
                 self.k_eff, self.sigma = self.ctx.build_recycle(self.k)
             else:                                      # a3, asynchronous (a4 happens inside the solve)
                 self.ctx.build_recycle(self.k, deferred=True)
+        if cfg.kind == "9pt":                          # C3: A is the same for the whole sequence
+            self.gen.fill(self.t, self.x)              # (b_t only)
+        else:                                          # A_t, b_t from x_{t-1}, written straight into
+            self.gen.fill(self.t, self.x, val_ptr=self.vals_ptr)   # the solver's value buffer (a1)
+            self.ctx.update_values_inplace(self.nnz)
         rep = self.ctx.solve(self.gen.b, self.x, x0=self.x if self.warm else None, m=cfg.m, variant=self.variant,
                              tol=cfg.tol, history_cap=history_cap)
         if not rep["converged"]:

@@ -271,6 +271,19 @@ typedef struct {
   double bytes;         /* summed algorithmic bytes (DESIGN.md byte model) */
 } rg_kstat;
 RG_API rg_status rg_kernel_stats(rg_ctx* ctx, rg_kstat* out, int32_t cap, int32_t* count);
+/* Device timeline of the library's kernels (SURVEY.md §5 tracing; no nsys on the target boxes).  While
+ * RG_FLAG_PROFILE is set (at rg_create), every kernel that keeps statistics appends events to a device
+ * ring of 65,536 entries: its start (block 0's first instruction, %globaltimer ns), its end (the last
+ * CTA's exit path) or a no-op launch.  rg_kernel_trace copies up to `cap` events in device order into
+ * `out` (host memory, owned by the caller) and sets *count to the number recorded since the last
+ * rg_reset_kernel_stats (which also clears the trace; events past the ring capacity are dropped and
+ * counted).  `name` matches rg_kstat's.  RG_E_STATE if the context was created without RG_FLAG_PROFILE. */
+typedef struct {
+  int64_t t_ns;   /* %globaltimer                                  */
+  int32_t kind;   /* 0 start, 1 end, 2 no-op launch                 */
+  char name[20];
+} rg_trace_event;
+RG_API rg_status rg_kernel_trace(rg_ctx* ctx, rg_trace_event* out, int32_t cap, int32_t* count);
 RG_API rg_status rg_reset_kernel_stats(rg_ctx* ctx);
 
 RG_API void rg_destroy(rg_ctx* ctx);

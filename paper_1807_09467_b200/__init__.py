@@ -75,6 +75,9 @@ class Context:
     def kernel_stats(self):
         return rg.rg_kernel_stats(self.ctx)
 
+    def kernel_trace(self, cap=65536):
+        return rg.rg_kernel_trace(self.ctx, cap)
+
     def reset_kernel_stats(self):
         rg.rg_reset_kernel_stats(self.ctx)
 

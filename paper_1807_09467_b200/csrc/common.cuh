@@ -89,7 +89,11 @@ struct DevState {
   // update pass this step (j = m: no next column)
   int ls_j, k2_skip;
   double ls_in[MAXK + 2];
+  // RG_FLAG_PROFILE: device timeline ring (rg_kernel_trace): 2 words per event {t_ns, kid | kind << 16}
+  unsigned long long* trace;
+  unsigned trace_cap, trace_len;
 };
+constexpr unsigned TRACE_CAP = 1u << 16;
 
 // Basis layout (constant per context).  Z is n_pad x MAXCOL... column-major with leading
 // dimension ld; columns [0, maxk) hold W, [VB - k_eff, VB) hold Q, [VB, VB + m + 1) hold V.
@@ -185,11 +189,26 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // Kernel-entry profiling hook (block 0 stamps the start time).
+__device__ __forceinline__ void trace_ev(DevState* st, int kid, unsigned kind, unsigned long long t) {
+  if (!st->trace) return;
+  const unsigned i = atomicAdd(&st->trace_len, 1u);
+  if (i < st->trace_cap) {
+    st->trace[2 * (size_t)i] = t;
+    st->trace[2 * (size_t)i + 1] = (unsigned long long)kid | ((unsigned long long)kind << 16);
+  }
+}
 __device__ __forceinline__ void prof_begin(DevState* st, int kid) {
-  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) st->kstat[kid].start = gtimer();
+  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    st->kstat[kid].start = t;
+    trace_ev(st, kid, 0u, t);
+  }
 }
 __device__ __forceinline__ void prof_noop(DevState* st, int kid) {
-  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) st->kstat[kid].noop++;
+  if (st->profile && blockIdx.x == 0 && threadIdx.x == 0) {
+    st->kstat[kid].noop++;
+    trace_ev(st, kid, 2u, gtimer());
+  }
 }
 // Called by thread 0 of the last CTA when it has won the grid-reduction ticket.
 __device__ __forceinline__ void prof_tail(DevState* st, int kid) {
@@ -205,6 +224,7 @@ __device__ __forceinline__ void prof_end(DevState* st, int kid, double bytes) {
     k.ns += t - k.start;
     k.launches++;
     k.bytes += bytes;
+    trace_ev(st, kid, 1u, t);
   }
 }
 

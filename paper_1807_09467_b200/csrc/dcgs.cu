@@ -193,6 +193,16 @@ __device__ __forceinline__ void dk1_finish(const Layout& L, DevState* st, double
   }
 }
 
+// DK1 of a step after the cycle stopped (unrolled Arnoldi bodies run up to RG_UNROLL-1 such steps):
+// nothing to reduce; the step's update pass and least-squares kernel must not act either
+__device__ __forceinline__ void dk1_noop(DevState* st) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->k2_skip = 1;
+    st->ls_j = -1;
+  }
+  prof_noop(st, K_DK1);
+}
+
 // ---------------------------------------------------------------- the least-squares step (split epilogue)
 // Column st->ls_j of the cycle (finished by DK1): Givens / M = T H update, history, stop test, and at a
 // stop the cycle-end coefficients (epi_ls).  Runs on a side branch of the graph, concurrently with DK2;
@@ -202,7 +212,10 @@ __global__ void __launch_bounds__(256) k_dcgs_ls(Layout L, DevState* st, unsigne
   const int jx = st->ls_j;
   RG_CHK(st, jx < MAXM && jx < st->m);
   if (jx >= 0) {
-    if (st->profile && threadIdx.x == 0) st->kstat[K_DLS].start = gtimer();
+    if (st->profile && threadIdx.x == 0) {
+      st->kstat[K_DLS].start = gtimer();
+      trace_ev(st, K_DLS, 0u, st->kstat[K_DLS].start);
+    }
     const int nd = st->variant == RG_AUGMENT ? st->k_eff : 0;
     for (int i = threadIdx.x; i <= nd; i += blockDim.x) lst[i] = st->ls_in[i];
     __syncthreads();
@@ -221,7 +234,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1(Layout L, DevState* st, unsigned 
   __shared__ double dpart[DK1RED];
   __shared__ double tot[DK1RED];
   __shared__ double bsh[33];
-  if (!st->active) { prof_noop(st, K_DK1); return; }
+  if (!st->active) { dk1_noop(st); return; }
   prof_begin(st, K_DK1);
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
@@ -304,7 +317,7 @@ __global__ void __launch_bounds__(DT, 2) k_dk1_stream(Layout L, DevState* st, un
   extern __shared__ double wsm[];  // [DT / 32][nvw]
   __shared__ double dpart[DK1RED];
   __shared__ double tot[DK1RED];
-  if (!st->active) { prof_noop(st, K_DK1); return; }
+  if (!st->active) { dk1_noop(st); return; }
   prof_begin(st, K_DK1);
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;
@@ -506,7 +519,7 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
   __shared__ double dpart[DK1RED];
   __shared__ double tot[DK1RED];
   __shared__ int colidx[DK1RED];
-  if (!st->active) { prof_noop(st, K_DK1); return; }
+  if (!st->active) { dk1_noop(st); return; }
   prof_begin(st, K_DK1);
   const int j = st->j, k = st->k_eff, var = st->variant, VB = L.VB, QB = VB - k;
   const int lo = (var == RG_DEFLATE) ? QB : VB, hi = VB + j, p = hi - lo;

@@ -51,8 +51,9 @@ enum SpmvMode { SM_STEP = 0, SM_RES = 1, SM_PLAIN = 2, SM_STEP_PC = 3, SM_RES_Y 
 
 // w = A v_j (STEP), r = b - A x (RES; epi != 0 runs the cycle-start epilogue on ||r||^2),
 // y = A x (PLAIN), w = A pz (STEP_PC: pz = M^{-1} v_j from launch_ssor, same gating as STEP).
+// pdl: launched with programmatic dependent launch (the kernels wait for their predecessor first)
 cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode, const double* x,
-                        double* y, int res_epi, cudaStream_t s);
+                        double* y, int res_epi, cudaStream_t s, bool pdl = false);
 
 // Y[:, 0:k] = A W[:, 0:k] (columns with leading dimension ld) with ONE read of A (a4: C = A W).
 // Returns cudaErrorNotSupported when no SpMM kernel covers the format (caller loops SpMVs).

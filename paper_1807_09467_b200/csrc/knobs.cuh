@@ -18,6 +18,7 @@
 //   RG_SYNC_BUILD                                  rg_build_recycle always synchronous
 //   RG_TIMING / RG_DEBUG                           host-side phase timings / Jacobi sweep counts (stderr)
 //   RG_NO_PDL / RG_NO_TMA_CGS                       no programmatic dependent launch / register CGS2 passes
+//   RG_UNROLL=n                                    Arnoldi steps per WHILE-loop body (default 4 DCGS2, 2 CGS2)
 //   RG_NO_GRAPH / RG_CGS2 / RG_NO_PERSIST          same as the RG_FLAG_* bits of include/rg.h
 #pragma once
 #include <cstdlib>

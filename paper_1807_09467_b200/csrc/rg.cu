@@ -149,6 +149,7 @@ struct rg_ctx {
   double* pt = nullptr;
   bool use_persist = true;  // one cooperative kernel per solve where supported (persistent.cu)
   double* keepV = nullptr;  // RG_FLAG_KEEP_BASIS: last finished cycle's V (n_pad x (max_m + 1))
+  unsigned long long* trace = nullptr;  // RG_FLAG_PROFILE: device kernel timeline (2 words per event)
   int kb_var = 0, kb_k = 0; // variant / k_eff of the solve whose basis keepV holds
   // graphs
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -460,8 +461,12 @@ cudaError_t cycle_end(rg_ctx* c) {
   return launch_orth(c->L, c->st, OP_XUPD, c->stream);
 }
 
-cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond) {
+// chained: not the first step of the captured body.  (Measured: launching the SpMV of a chained step with
+// PDL behind the previous update pass removes most of the edge's gap but slows C4 by 1.5 %, C3 gains
+// 0.4 %; A/B in profiles/r02/ab_unroll.txt.  Kept as a plain edge.)
+cudaError_t arnoldi_step(rg_ctx* c, unsigned long long cond, bool chained) {
   cudaError_t e;
+  (void)chained;
   if (c->L.prec) {  // y = A M^{-1} u
     if ((e = launch_ssor(c->P, c->L, c->st, nullptr, c->pz, 1, c->stream)) != cudaSuccess) return e;
     if ((e = launch_spmv(c->A, c->L, c->st, SM_STEP_PC, nullptr, nullptr, 0, c->stream)) != cudaSuccess) return e;
@@ -533,7 +538,14 @@ rg_status build_solve_graph(rg_ctx* c, int variant, cudaGraphExec_t* out) {
   CKG(cudaGraphAddNode(&inner, bodyO, &pre, 1, &ip));
   cudaGraph_t bodyI = ip.conditional.phGraph_out[0];
   CKG(cudaStreamBeginCaptureToGraph(c->stream, bodyI, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  e1 = arnoldi_step(c, (unsigned long long)hin);
+  // U Arnoldi steps per WHILE iteration: an iteration boundary (body end -> condition -> next body launch)
+  // measured ~7.3 us on the device timeline (tools/trace.py, C3 / C4) against ~3-4 us for a plain edge
+  // inside the body; steps after the cycle stopped are no-op launches (every kernel gates on st->active;
+  // a no-op DK1 also disables its step's update pass and least-squares kernel)
+  static const int unroll_knob = knob_int("RG_UNROLL", 0);
+  const int U = unroll_knob > 0 ? unroll_knob : (c->dcgs_now ? 4 : 2);
+  e1 = cudaSuccess;
+  for (int u = 0; u < U && e1 == cudaSuccess; ++u) e1 = arnoldi_step(c, (unsigned long long)hin, u > 0);
   CKG(cudaStreamEndCapture(c->stream, &tmp));
   CKG(e1);
   CKG(cudaStreamBeginCaptureToGraph(c->stream, bodyO, &inner, nullptr, 1, cudaStreamCaptureModeThreadLocal));
@@ -559,7 +571,7 @@ rg_status run_solve(rg_ctx* c, int variant, int m) {
       CK(cudaStreamSynchronize(c->stream));
       if (c->hst->done) return RG_OK;
       if (c->hst->active) {
-        CK(arnoldi_step(c, 0));
+        CK(arnoldi_step(c, 0, false));
       } else {
         CK(cycle_end(c));
         CK(cycle_start(c, variant));
@@ -602,7 +614,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   cudaFree(c->t1); cudaFree(c->t2); cudaFree(c->hist); cudaFree(c->partial); cudaFree(c->counter);
   cudaFree(c->small); cudaFree(c->dflag); cudaFree(c->st); cudaFree(c->tot_g); cudaFree(c->gbar); cudaFree(c->pflags); cudaFree(c->llw);
   drop_preconditioner(c);
-  cudaFree(c->pz); cudaFree(c->pt); cudaFree(c->keepV);
+  cudaFree(c->pz); cudaFree(c->pt); cudaFree(c->keepV); cudaFree(c->trace);
   if (c->hst) cudaFreeHost(c->hst);
   if (c->hhist) cudaFreeHost(c->hhist);
   if (c->hflag) cudaFreeHost(c->hflag);
@@ -664,7 +676,8 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
       (s = dalloc(&c->pflags, (size_t)NSM * 16, "sync flags")) != RG_OK ||
       (s = dalloc(&c->llw, ll_words(), "reduction words")) != RG_OK ||
       (s = dalloc(&c->st, 1, "state")) != RG_OK ||
-      ((c->flags & RG_FLAG_KEEP_BASIS) && (s = dalloc(&c->keepV, np * (c->max_m + 1), "kept basis")) != RG_OK)) {
+      ((c->flags & RG_FLAG_KEEP_BASIS) && (s = dalloc(&c->keepV, np * (c->max_m + 1), "kept basis")) != RG_OK) ||
+      ((c->flags & RG_FLAG_PROFILE) && (s = dalloc(&c->trace, (size_t)2 * TRACE_CAP, "kernel trace")) != RG_OK)) {
     rg_destroy(c);
     return s;
   }
@@ -688,6 +701,12 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   ok(cudaMemsetAsync(c->t2, 0, sizeof(double) * np, c->stream));
   ok(cudaMemsetAsync(c->counter, 0, sizeof(unsigned) * 4, c->stream));
   ok(cudaMemsetAsync(c->st, 0, sizeof(DevState), c->stream));
+  if (c->trace) {  // outside the per-solve header: set once
+    c->hst->trace = c->trace;
+    c->hst->trace_cap = TRACE_CAP;
+    ok(cudaMemcpyAsync(&c->st->trace, &c->hst->trace, sizeof(c->hst->trace) + 2 * sizeof(unsigned),
+                       cudaMemcpyHostToDevice, c->stream));
+  }
   ok(cudaMemsetAsync(c->llw, 0, sizeof(unsigned long long) * ll_words(), c->stream));
   // persistent-solve barrier words and neighbour epochs: zero at allocation and again right after
   // every persistent solve (off the next solve's critical path)
@@ -1342,13 +1361,15 @@ RG_API rg_status rg_export(rg_ctx* c, int32_t which, double* out, rg_mem mem, in
   return RG_OK;
 }
 
+static const char* const kernel_names[K_COUNT] = {"spmv_step", "spmv_res", "spmv_plain", "orth_dots1", "orth_upd_dots2",
+                                              "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
+                                              "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
+                                              "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
+                                              "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
+                                              "ssor_sweep_kernels", "p_spmv", "cbuild", "res_from_ax", "dcgs_ls"};
+
 RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t* count) {
-  static const char* names[K_COUNT] = {"spmv_step", "spmv_res", "spmv_plain", "orth_dots1", "orth_upd_dots2",
-                                       "orth_upd_norm_ls", "cs_dots_q", "cs_upd_norm", "x_upd_w", "x_upd_cycle",
-                                       "norm_b", "gram", "jacobi", "xm", "chol", "persistent_solve", "dcgs_dots_ls",
-                                       "dcgs_update", "p_barrier", "p_spmv_dots", "p_reduce", "p_epilogue",
-                                       "p_update", "ob_dots", "ob_update", "ssor", "p_reduce_arrive", "cond",
-                                       "ssor_sweep_kernels", "p_spmv", "cbuild", "res_from_ax", "dcgs_ls"};
+  const char* const* names = kernel_names;
   if (!c || !count) return fail(RG_E_INVAL, "NULL argument");
   KStatDev ks[K_COUNT];
   CK(cudaMemcpyAsync(ks, &c->st->kstat[0], sizeof(ks), cudaMemcpyDeviceToHost, c->stream));
@@ -1375,9 +1396,33 @@ RG_API rg_status rg_kernel_stats(rg_ctx* c, rg_kstat* out, int32_t cap, int32_t*
   return RG_OK;
 }
 
+RG_API rg_status rg_kernel_trace(rg_ctx* c, rg_trace_event* out, int32_t cap, int32_t* count) {
+  NvtxRange nvtx_("rg_kernel_trace");
+  if (!c || !count || (cap > 0 && !out)) return fail(RG_E_INVAL, "NULL argument");
+  if (!c->trace) return fail(RG_E_STATE, "the kernel trace needs a context created with RG_FLAG_PROFILE");
+  unsigned len = 0;
+  CK(cudaMemcpyAsync(&len, &c->st->trace_len, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  *count = (int32_t)std::min<unsigned>(len, (unsigned)INT32_MAX);
+  const int n = (int)std::min<int64_t>({(int64_t)len, (int64_t)TRACE_CAP, (int64_t)std::max(cap, 0)});
+  if (n <= 0) return RG_OK;
+  std::vector<unsigned long long> buf((size_t)2 * n);
+  CK(cudaMemcpy(buf.data(), c->trace, sizeof(unsigned long long) * 2 * n, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n; ++i) {
+    rg_trace_event& e = out[i];
+    memset(&e, 0, sizeof(e));
+    e.t_ns = (int64_t)buf[2 * i];
+    const int kid = (int)(buf[2 * i + 1] & 0xffffu);
+    e.kind = (int32_t)(buf[2 * i + 1] >> 16);
+    strncpy(e.name, kid < K_COUNT ? kernel_names[kid] : "?", sizeof(e.name) - 1);
+  }
+  return RG_OK;
+}
+
 RG_API rg_status rg_reset_kernel_stats(rg_ctx* c) {
   if (!c) return fail(RG_E_INVAL, "ctx is NULL");
   CK(cudaMemsetAsync(&c->st->kstat[0], 0, sizeof(KStatDev) * K_COUNT, c->stream));
+  CK(cudaMemsetAsync(&c->st->trace_len, 0, sizeof(unsigned), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   g_host_launches = 0;
   return RG_OK;

@@ -670,7 +670,7 @@ __global__ void __launch_bounds__(256) k_spmm_rows(MatDev A, const double* __res
 }  // namespace
 
 cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode, const double* x,
-                        double* y, int res_epi, cudaStream_t s) {
+                        double* y, int res_epi, cudaStream_t s, bool pdl) {
   SpmvArgs a{A, L, st, mode, x, y, res_epi};
   const int cap_red = NSM * VEC_CTAS_PER_SM;  // reducing launches: bounded partials
   if (mode == SM_RES_Y) {
@@ -686,31 +686,30 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
       init = true;
     }
     int64_t g = A.nb < NSM ? A.nb : NSM;
-    k_spmv_bsr_tma<<<(int)(g < 1 ? 1 : g), BT, BNS * BSTAGE, s>>>(a);
-    return cudaGetLastError();
+    return launch_ex(k_spmv_bsr_tma, dim3((int)(g < 1 ? 1 : g)), dim3(BT), BNS * BSTAGE, s, pdl, a);
   }
   if (A.fmt == 2) {
     int64_t g = (A.nb + 3) / 4;
     const int64_t cap = (int64_t)NSM * 8;  // partials buffer holds NSM*8 rows: RES may use them all
     if (g > cap) g = cap;
-    k_spmv_bsr<<<(int)(g < 1 ? 1 : g), 256, 0, s>>>(a);
+    return launch_ex(k_spmv_bsr, dim3((int)(g < 1 ? 1 : g)), dim3(256), 0, s, pdl, a);
   } else if (A.fmt == 1) {
     int64_t g = (A.nslices * 32 + OT - 1) / OT;
     const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * RG_SPMV_CAP;
     if (g > cap) g = cap;
-    k_spmv_sell<<<(int)(g < 1 ? 1 : g), OT, 0, s>>>(a);
+    return launch_ex(k_spmv_sell, dim3((int)(g < 1 ? 1 : g)), dim3(OT), 0, s, pdl, a);
   } else {
     int64_t g = (A.n * A.lpr + OT - 1) / OT;
     const int64_t cap = mode == SM_RES ? cap_red : (int64_t)NSM * RG_SPMV_CAP;
     if (g > cap) g = cap;
     const int gi = (int)(g < 1 ? 1 : g);
     switch (A.lpr) {
-      case 1: k_spmv_csr_pipe<<<gi, OT, 0, s>>>(a); break;
-      case 2: k_spmv_csr<2><<<gi, OT, 0, s>>>(a); break;
-      case 4: k_spmv_csr<4><<<gi, OT, 0, s>>>(a); break;
-      case 8: k_spmv_csr<8><<<gi, OT, 0, s>>>(a); break;
-      case 16: k_spmv_csr<16><<<gi, OT, 0, s>>>(a); break;
-      default: k_spmv_csr<32><<<gi, OT, 0, s>>>(a); break;
+      case 1: return launch_ex(k_spmv_csr_pipe, dim3(gi), dim3(OT), 0, s, pdl, a);
+      case 2: return launch_ex(k_spmv_csr<2>, dim3(gi), dim3(OT), 0, s, pdl, a);
+      case 4: return launch_ex(k_spmv_csr<4>, dim3(gi), dim3(OT), 0, s, pdl, a);
+      case 8: return launch_ex(k_spmv_csr<8>, dim3(gi), dim3(OT), 0, s, pdl, a);
+      case 16: return launch_ex(k_spmv_csr<16>, dim3(gi), dim3(OT), 0, s, pdl, a);
+      default: return launch_ex(k_spmv_csr<32>, dim3(gi), dim3(OT), 0, s, pdl, a);
     }
   }
   return cudaGetLastError();

@@ -33,7 +33,7 @@ STATUS = {0: "RG_OK", 1: "RG_E_INVAL", 2: "RG_E_NOMEM", 3: "RG_E_CUDA", 4: "RG_E
 # Symbols declared in include/rg.h (tests check the .so exports exactly these).
 SYMBOLS = ("rg_create", "rg_update_matrix", "rg_matrix_values", "rg_push_snapshot", "rg_clear_snapshots", "rg_build_recycle", "rg_build_recycle_modes",
            "rg_solve", "rg_apply", "rg_set_preconditioner", "rg_apply_preconditioner", "rg_export",
-           "rg_kernel_stats", "rg_reset_kernel_stats", "rg_destroy", "rg_last_error")
+           "rg_kernel_stats", "rg_kernel_trace", "rg_reset_kernel_stats", "rg_destroy", "rg_last_error")
 
 
 class RgError(RuntimeError):
@@ -68,6 +68,10 @@ class rg_kstat(ctypes.Structure):
                 ("total_ms", ctypes.c_double), ("tail_ms", ctypes.c_double), ("bytes", ctypes.c_double)]
 
 
+class rg_trace_event(ctypes.Structure):
+    _fields_ = [("t_ns", ctypes.c_int64), ("kind", ctypes.c_int32), ("name", ctypes.c_char * 20)]
+
+
 def load(path: str = LIB_PATH):
     if not os.path.exists(path):
         raise ImportError(f"{path} is missing: build it with __graft_entry__.build() (no CPU fallback exists)")
@@ -87,6 +91,7 @@ def load(path: str = LIB_PATH):
     L.rg_apply_preconditioner.argtypes = [vp, vp, vp, ctypes.c_int]
     L.rg_export.argtypes = [vp, i32, vp, ctypes.c_int, ctypes.POINTER(i32)]
     L.rg_kernel_stats.argtypes = [vp, ctypes.POINTER(rg_kstat), i32, ctypes.POINTER(i32)]
+    L.rg_kernel_trace.argtypes = [vp, ctypes.POINTER(rg_trace_event), i32, ctypes.POINTER(i32)]
     L.rg_reset_kernel_stats.argtypes = [vp]
     L.rg_destroy.argtypes = [vp]
     L.rg_destroy.restype = None
@@ -282,6 +287,16 @@ def rg_kernel_stats(ctx):
     return {buf[i].name.decode(): dict(launches=buf[i].launches, noop=buf[i].noop_launches,
                                        ms=buf[i].total_ms, tail_ms=buf[i].tail_ms, bytes=buf[i].bytes)
             for i in range(cnt.value)}
+
+
+def rg_kernel_trace(ctx, cap=65536):
+    """Device kernel timeline since the last reset: list of (t_ns, kind, name), kind 0 start / 1 end /
+    2 no-op (contexts created with RG_FLAG_PROFILE); plus the number of events recorded."""
+    buf = (rg_trace_event * cap)()
+    cnt = ctypes.c_int32(0)
+    _check(_lib.rg_kernel_trace(ctx, buf, cap, ctypes.byref(cnt)))
+    n = min(cnt.value, cap)
+    return [(buf[i].t_ns, buf[i].kind, buf[i].name.decode()) for i in range(n)], cnt.value
 
 
 def rg_reset_kernel_stats(ctx):

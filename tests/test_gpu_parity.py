@@ -638,3 +638,30 @@ def test_cgs2_tma_passes_vs_oracle(variant, rng):
     r = b - oracle.spmv(M, xg)
     assert np.linalg.norm(r) / np.linalg.norm(b) <= cfg.tol
     ctx.close()
+
+
+def test_kernel_trace_timeline(rng):
+    """rg_kernel_trace (RG_FLAG_PROFILE): every kernel start has a matching end or is a no-op, times are
+    ordered, and the trace is cleared by rg_reset_kernel_stats; refused without the flag."""
+    from paper_1807_09467_b200 import rg as rgb
+    hm = random_csr(5000, rng, per_row=(2, 8), diag=2.5)
+    b = rng.standard_normal(5000)
+    for flags in (rgb.RG_FLAG_PROFILE, rgb.RG_FLAG_PROFILE | rgb.RG_FLAG_NO_PERSIST):
+        ctx = make_ctx(hm, max_m=20, s=4, k=4, flags=flags)
+        x = torch.zeros(5000, dtype=torch.float64, device=DEV)
+        ctx.solve(t(b), x, m=20, variant="plain", tol=1e-9)
+        ev, cnt = ctx.kernel_trace()
+        assert cnt == len(ev) > 0
+        starts = [e for e in ev if e[1] == 0]
+        ends = [e for e in ev if e[1] == 1]
+        assert len(starts) == len(ends)
+        for s0 in starts:
+            assert any(e[2] == s0[2] and e[0] >= s0[0] for e in ends)
+        ctx.reset_kernel_stats()
+        assert ctx.kernel_trace()[1] == 0
+        ctx.close()
+    ctx = make_ctx(hm, max_m=20, s=4, k=4)
+    with pytest.raises(rgb.RgError) as e:
+        ctx.kernel_trace()
+    assert e.value.status == rgb.RG_E_STATE
+    ctx.close()
