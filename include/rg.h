@@ -85,8 +85,12 @@ typedef enum { RG_HOST = 0, RG_DEVICE = 1 } rg_mem;
  *         (val[p*b*b + c*b + r] = block_p(r, c)).
  *   In rg_update_matrix, row_ptr == col_idx == NULL keeps the current pattern and replaces the
  *   values only (the fast path for sequences with a fixed sparsity pattern).
- *   sell_C = 32 packs a CSR matrix into SELL-32-sigma internally (sell_sigma = 1: no row
- *   sorting; other sigma values are rejected in this version); sell_C = 0 keeps CSR. */
+ *   sell_C = 32 packs a CSR matrix into SELL-32-sigma internally: inside every window of
+ *   sell_sigma consecutive rows the rows are ordered by decreasing length (stable), then cut into
+ *   slices of 32 rows padded to the slice's longest row (Kreutzer et al.'s SELL-C-sigma; the
+ *   permutation is internal: x, y, b and every vector of the API keep the caller's row order).
+ *   sell_sigma = 1 (or 0): no sorting; otherwise a multiple of 32 (RG_E_INVAL if not).  A
+ *   sorted SELL matrix (sigma > 1) always runs the graph path.  sell_C = 0 keeps CSR. */
 typedef struct {
   rg_format fmt;
   int64_t n_rows;

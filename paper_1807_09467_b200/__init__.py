@@ -17,16 +17,17 @@ class Context:
     """One rg_ctx: a sequence solver for systems of dimension n (marshalling only)."""
 
     def __init__(self, n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, max_m=64,
-                 max_snapshots=32, max_k=32, stream=None, flags=0):
+                 max_snapshots=32, max_k=32, stream=None, flags=0, sell_sigma=1):
         keep = []
         self.n, self.fmt, self.block, self.sell_C = int(n), fmt, int(block), int(sell_C)
-        A = rg.make_matrix(n, row_ptr, col_idx, val, fmt, block, sell_C, keep)
+        self.sell_sigma = int(sell_sigma)
+        A = rg.make_matrix(n, row_ptr, col_idx, val, fmt, block, sell_C, keep, self.sell_sigma)
         self.max_snapshots = max_snapshots
         self.ctx = rg.rg_create(n, A, max_m, max_snapshots, max_k, stream, flags)
 
     def update_matrix(self, val, row_ptr=None, col_idx=None):
         keep = []
-        A = rg.make_matrix(self.n, row_ptr, col_idx, val, self.fmt, self.block, self.sell_C, keep)
+        A = rg.make_matrix(self.n, row_ptr, col_idx, val, self.fmt, self.block, self.sell_C, keep, self.sell_sigma)
         rg.rg_update_matrix(self.ctx, A)
 
     def values_ptr(self):
@@ -35,7 +36,7 @@ class Context:
 
     def update_values_inplace(self, nnz):
         """The values behind values_ptr() were rewritten on the context's stream."""
-        rg.rg_update_values_inplace(self.ctx, self.n, nnz, self.fmt, self.block, self.sell_C)
+        rg.rg_update_values_inplace(self.ctx, self.n, nnz, self.fmt, self.block, self.sell_C, self.sell_sigma)
 
     def push_snapshot(self, x):
         rg.rg_push_snapshot(self.ctx, x)

@@ -507,28 +507,38 @@ __global__ void k_rc_finish(const double* R1, const double* R1i, const double* R
   }
 }
 
-__global__ void k_sell_widths(const int32_t* rp, int64_t n, int32_t* sw) {
+// SELL position i holds matrix row perm[i] (identity when perm is null: sigma = 1)
+__global__ void k_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, const int32_t* perm) {
   const int64_t ns = (n + 31) / 32;
   for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < ns; sl += (int64_t)gridDim.x * blockDim.x) {
     int w = 0;
     for (int r = 0; r < 32; ++r) {
-      const int64_t row = sl * 32 + r;
-      if (row < n) { const int l = rp[row + 1] - rp[row]; w = l > w ? l : w; }
+      const int64_t pos = sl * 32 + r;
+      if (pos < n) {
+        const int64_t row = perm ? perm[pos] : pos;
+        const int l = rp[row + 1] - rp[row];
+        w = l > w ? l : w;
+      }
     }
     sw[sl] = w;
   }
 }
 
 __global__ void k_sell_pack(const int32_t* rp, const int32_t* ci, const double* v, int64_t n,
-                            const int64_t* sp, const int32_t* sw, int32_t* sci, double* sv, int pattern) {
+                            const int64_t* sp, const int32_t* sw, int32_t* sci, double* sv, int pattern,
+                            const int32_t* perm) {
   const int64_t ns = (n + 31) / 32;
-  for (int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; row < ns * 32;
-       row += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t sl = row >> 5;
+  for (int64_t pos = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pos < ns * 32;
+       pos += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = pos >> 5;
     const int w = sw[sl];
-    const int64_t base = sp[sl] + (row & 31);
+    const int64_t base = sp[sl] + (pos & 31);
     int len = 0, p0 = 0;
-    if (row < n) { p0 = rp[row]; len = rp[row + 1] - p0; }
+    if (pos < n) {
+      const int64_t row = perm ? perm[pos] : pos;
+      p0 = rp[row];
+      len = rp[row + 1] - p0;
+    }
     for (int c = 0; c < w; ++c) {
       const int64_t e = base + (int64_t)c * 32;
       if (c < len) {
@@ -646,17 +656,17 @@ cudaError_t launch_rc_finish(const double* R1, const double* R1i, const double* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaStream_t strm) {
+cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaStream_t strm, const int32_t* perm) {
   note_host_launches(1);
-  k_sell_widths<<<NSM * 4, 256, 0, strm>>>(rp, n, sw);
+  k_sell_widths<<<NSM * 4, 256, 0, strm>>>(rp, n, sw, perm);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sell_pack(const int32_t* rp, const int32_t* ci, const double* v, int64_t n,
                              const int64_t* sp, const int32_t* sw, int32_t* sci, double* sv,
-                             int pattern, cudaStream_t strm) {
+                             int pattern, cudaStream_t strm, const int32_t* perm) {
   note_host_launches(1);
-  k_sell_pack<<<NSM * 8, 256, 0, strm>>>(rp, ci, v, n, sp, sw, sci, sv, pattern);
+  k_sell_pack<<<NSM * 8, 256, 0, strm>>>(rp, ci, v, n, sp, sw, sci, sv, pattern, perm);
   return cudaGetLastError();
 }
 

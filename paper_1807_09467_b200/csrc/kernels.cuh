@@ -36,6 +36,8 @@ struct MatDev {
   const int32_t* sw = nullptr;  // SELL slice widths
   const int32_t* sci = nullptr; // SELL columns (column-major inside a slice)
   const double* sv = nullptr;   // SELL values
+  const int32_t* sperm = nullptr;   // SELL-32-sigma (sigma > 1): SELL position -> matrix row (null: identity)
+  const int32_t* siperm = nullptr;  //                          matrix row -> SELL position
   int64_t nslices = 0;
   int tma = 1;                  // BSR-64: stream blocks with TMA bulk copies
   double bytes = 0.0;           // algorithmic bytes of one product (DESIGN.md byte model)
@@ -161,8 +163,8 @@ cudaError_t launch_rc_finish(const double* R1, const double* R1i, const double* 
 // SELL packing of a CSR matrix (values, and columns when pattern != 0)
 cudaError_t launch_sell_pack(const int32_t* rp, const int32_t* ci, const double* v, int64_t n,
                              const int64_t* sp, const int32_t* sw, int32_t* sci, double* sv,
-                             int pattern, cudaStream_t strm);
-cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaStream_t strm);
+                             int pattern, cudaStream_t strm, const int32_t* perm = nullptr);
+cudaError_t launch_sell_widths(const int32_t* rp, int64_t n, int32_t* sw, cudaStream_t strm, const int32_t* perm = nullptr);
 // CSR / BSR pattern validation on the device; bad[0] != 0 on failure.
 cudaError_t launch_validate(const int32_t* rp, const int32_t* ci, int64_t nrows, int64_t ncols,
                             int64_t nnz, int* bad, cudaStream_t strm);

@@ -254,9 +254,10 @@ __device__ __forceinline__ bool greduce_ll(const double* vals, int nv, unsigned 
 __device__ __forceinline__ double row_dot(const MatDev& A, int64_t row, const double* __restrict__ x) {
   double s = 0.0;
   if (A.fmt == 1) {
-    const int64_t sl = row >> 5;
+    const int64_t pos = A.siperm ? (int64_t)__ldg(A.siperm + row) : row;  // (sorted SELL runs the graph path)
+    const int64_t sl = pos >> 5;
     const int w = __ldg(A.sw + sl);
-    const int64_t base = __ldg(A.sp + sl) + (row & 31);
+    const int64_t base = __ldg(A.sp + sl) + (pos & 31);
     for (int c = 0; c < w; c += SELL_CH) {
       int32_t cc[SELL_CH];
       double vv[SELL_CH];
@@ -434,7 +435,8 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
       const int G = gridDim.x;
       s_clo = s_chi < 0 ? (int)blockIdx.x : row_owner(s_clo, ng, G);
       s_chi = s_chi < 0 ? (int)blockIdx.x : row_owner(s_chi, ng, G);
-      RG_CHK(st, s_clo >= 0 && s_clo <= s_chi && s_chi < G && s_clo <= (int)blockIdx.x && (int)blockIdx.x <= s_chi);
+      RG_CHK(st, s_clo >= 0 && s_clo <= s_chi && s_chi < G && s_clo <= (int)blockIdx.x && (int)blockIdx.x <= s_chi &&
+                     A.sperm == nullptr);
     }
     __syncthreads();
   }
@@ -1201,9 +1203,10 @@ __global__ void __launch_bounds__(PT, 1) k_cbuild(const __grid_constant__ PArgs 
         int64_t e0, est;
         int ne;
         if (A.fmt == 1) {
-          const int64_t sl = r >> 5;
+          const int64_t pos = A.siperm ? (int64_t)__ldg(A.siperm + r) : r;  // row -> SELL position (sigma > 1)
+          const int64_t sl = pos >> 5;
           ne = __ldg(A.sw + sl);
-          e0 = __ldg(A.sp + sl) + (r & 31);
+          e0 = __ldg(A.sp + sl) + (pos & 31);
           est = 32;
         } else {
           e0 = __ldg(A.rp + r);

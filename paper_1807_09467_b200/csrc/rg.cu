@@ -102,6 +102,9 @@ struct rg_ctx {
   double* v = nullptr;
   int64_t v_len = 0;
   int64_t nslices = 0, sell_len = 0;
+  int32_t sell_sigma = 1;
+  int32_t* sperm = nullptr;   // SELL-32-sigma: SELL position -> row, and its inverse (sigma > 1 only)
+  int32_t* siperm = nullptr;
   int64_t* sp = nullptr;
   int32_t* sw = nullptr;
   int32_t* sci = nullptr;
@@ -180,8 +183,9 @@ void drop_preconditioner(rg_ctx* c) {
 
 void free_matrix(rg_ctx* c) {
   cudaFree(c->rp); cudaFree(c->ci); cudaFree(c->v);
-  cudaFree(c->sp); cudaFree(c->sw); cudaFree(c->sci); cudaFree(c->sv);
+  cudaFree(c->sp); cudaFree(c->sw); cudaFree(c->sci); cudaFree(c->sv); cudaFree(c->sperm); cudaFree(c->siperm);
   c->rp = c->ci = nullptr; c->v = nullptr; c->sp = nullptr; c->sw = c->sci = nullptr; c->sv = nullptr;
+  c->sperm = c->siperm = nullptr;
 }
 
 bool is_dev_ptr(const void* p) {
@@ -224,7 +228,8 @@ rg_status check_desc(const rg_matrix* A, int64_t n, bool pattern_required) {
     if (A->sell_C) return fail(RG_E_INVAL, "SELL packing applies to CSR only");
   }
   if (A->sell_C != 0 && A->sell_C != 32) return fail(RG_E_INVAL, "sell_C must be 0 or 32");
-  if (A->sell_C == 32 && A->sell_sigma > 1) return fail(RG_E_INVAL, "sell_sigma > 1 is not supported");
+  if (A->sell_C == 32 && A->sell_sigma > 1 && A->sell_sigma % 32) return fail(RG_E_INVAL, "sell_sigma must be 1 or a multiple of 32");
+  if (A->sell_sigma < 0) return fail(RG_E_INVAL, "sell_sigma must be >= 0");
   const bool has_rp = A->row_ptr != nullptr, has_ci = A->col_idx != nullptr;
   if (has_rp != has_ci) return fail(RG_E_INVAL, "row_ptr and col_idx must both be given or both be NULL");
   if (pattern_required && !has_rp) return fail(RG_E_INVAL, "row_ptr/col_idx required");
@@ -280,13 +285,33 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
     if ((s = copy_in(c->rp, A->row_ptr, sizeof(int32_t) * (nrows + 1), A->mem, c->stream)) != RG_OK) return s;
     if ((s = copy_in(c->ci, A->col_idx, sizeof(int32_t) * A->nnz, A->mem, c->stream)) != RG_OK) return s;
     if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
-    if (newfmt == 1) {  // SELL-32 packing
+    if (newfmt == 1) {  // SELL-32-sigma packing
       c->nslices = (c->n + 31) / 32;
-      cudaFree(c->sp); cudaFree(c->sw); cudaFree(c->sci); cudaFree(c->sv);
-      c->sp = nullptr; c->sw = nullptr; c->sci = nullptr; c->sv = nullptr;
+      cudaFree(c->sp); cudaFree(c->sw); cudaFree(c->sci); cudaFree(c->sv); cudaFree(c->sperm); cudaFree(c->siperm);
+      c->sp = nullptr; c->sw = nullptr; c->sci = nullptr; c->sv = nullptr; c->sperm = c->siperm = nullptr;
+      c->sell_sigma = A->sell_sigma > 1 ? A->sell_sigma : 1;
+      if (c->sell_sigma > 1) {
+        // rows ordered by decreasing length inside each window of sigma rows (stable: equal lengths keep
+        // their order), from the validated row pointers (one host pass per pattern change)
+        std::vector<int32_t> rph(c->n + 1), perm(c->n), iperm(c->n);
+        CK(cudaMemcpyAsync(rph.data(), c->rp, sizeof(int32_t) * (c->n + 1), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < c->n; ++i) perm[i] = (int32_t)i;
+        for (int64_t w0 = 0; w0 < c->n; w0 += c->sell_sigma) {
+          const int64_t w1 = std::min<int64_t>(c->n, w0 + c->sell_sigma);
+          std::stable_sort(perm.begin() + w0, perm.begin() + w1,
+                           [&](int32_t a, int32_t b2) { return rph[a + 1] - rph[a] > rph[b2 + 1] - rph[b2]; });
+        }
+        for (int64_t i = 0; i < c->n; ++i) iperm[perm[i]] = (int32_t)i;
+        CK(cudaMalloc(&c->sperm, sizeof(int32_t) * std::max<int64_t>(c->n, 1)));
+        CK(cudaMalloc(&c->siperm, sizeof(int32_t) * std::max<int64_t>(c->n, 1)));
+        CK(cudaMemcpyAsync(c->sperm, perm.data(), sizeof(int32_t) * c->n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->siperm, iperm.data(), sizeof(int32_t) * c->n, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // (the host vectors go out of scope)
+      }
       CK(cudaMalloc(&c->sw, sizeof(int32_t) * c->nslices));
       CK(cudaMalloc(&c->sp, sizeof(int64_t) * (c->nslices + 1)));
-      CK(launch_sell_widths(c->rp, c->n, c->sw, c->stream));
+      CK(launch_sell_widths(c->rp, c->n, c->sw, c->stream, c->sperm));
       std::vector<int32_t> w(c->nslices);
       std::vector<int64_t> sp(c->nslices + 1);
       CK(cudaMemcpyAsync(w.data(), c->sw, sizeof(int32_t) * c->nslices, cudaMemcpyDeviceToHost, c->stream));
@@ -297,7 +322,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
       CK(cudaMemcpyAsync(c->sp, sp.data(), sizeof(int64_t) * (c->nslices + 1), cudaMemcpyHostToDevice, c->stream));
       CK(cudaMalloc(&c->sci, sizeof(int32_t) * std::max<int64_t>(c->sell_len, 1)));
       CK(cudaMalloc(&c->sv, sizeof(double) * std::max<int64_t>(c->sell_len, 1)));
-      CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 1, c->stream));
+      CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 1, c->stream, c->sperm));
       CK(cudaStreamSynchronize(c->stream));
       clear_graphs(c);
     }
@@ -307,7 +332,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
       if (A->mem == RG_DEVICE && !is_dev_ptr(A->val)) return fail(RG_E_INVAL, "mem = RG_DEVICE but val is not device memory");
       if ((s = copy_in(c->v, A->val, sizeof(double) * vlen, A->mem, c->stream)) != RG_OK) return s;
     }
-    if (c->fmt == 1) CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 0, c->stream));
+    if (c->fmt == 1) CK(launch_sell_pack(c->rp, c->ci, c->v, c->n, c->sp, c->sw, c->sci, c->sv, 0, c->stream, c->sperm));
     if (c->prec_kind) CK(launch_ssor_values(c->P, c->v, c->n, c->stream));  // SSOR copies follow the values
   }
   // device descriptor and byte model
@@ -323,6 +348,7 @@ rg_status set_matrix(rg_ctx* c, const rg_matrix* A, bool first) {
     M.nnz = c->nnz;
   } else if (c->fmt == 1) {
     M.sp = c->sp; M.sw = c->sw; M.sci = c->sci; M.sv = c->sv; M.nslices = c->nslices;
+    M.sperm = c->sperm; M.siperm = c->siperm;
     M.bytes = 12.0 * c->sell_len + 12.0 * c->nslices + 16.0 * c->n;
   } else {
     M.b = c->block;
@@ -946,7 +972,8 @@ RG_API rg_status rg_solve(rg_ctx* c, const double* b, const double* x0, int32_t 
     for (auto& e : tev) cudaEventCreate(&e);
   if (timing) cudaEventRecord(tev[0], s);
   const bool need_c = eff != RG_PLAIN && (!c->c_valid || c->c_kind != want_kind);
-  const bool persist_size = c->npad <= PERSIST_MAX_ROWS || knob("RG_FORCE_PERSIST");
+  // (a sorted SELL-32-sigma matrix permutes rows across the persistent kernel's CTA row ranges: graph path)
+  const bool persist_size = (c->npad <= PERSIST_MAX_ROWS || knob("RG_FORCE_PERSIST")) && !(c->fmt == 1 && c->sperm);
   static const bool no_fuse = knob("RG_NO_FUSE_C");
   // (independent of the solve path: the graph path reads the same Q columns and R_C^{-1})
   bool fuse_c = need_c && !galerkin_variant(eff) && !no_fuse;

@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(OT, 2) k_spmv_sell(SpmvArgs a) {
       const int64_t e = base + (int64_t)c * 32;
       s += __ldcs(A.sv + e) * __ldg(x + __ldcs(A.sci + e));
     }
-    if (row < A.n) nrm += emit(io, row, s);
+    if (row < A.n) nrm += emit(io, A.sperm ? (int64_t)__ldg(A.sperm + row) : row, s);  // SELL position -> row
     w = wn;
     base = bn;
 #pragma unroll
@@ -640,9 +640,10 @@ __global__ void __launch_bounds__(256) k_spmm_rows(MatDev A, const double* __res
 #pragma unroll
     for (int l = 0; l < KC; ++l) acc[l] = 0.0;
     if (A.fmt == 1) {
-      const int64_t sl = row >> 5;
+      const int64_t pos = A.siperm ? (int64_t)__ldg(A.siperm + row) : row;  // row -> SELL position
+      const int64_t sl = pos >> 5;
       const int w = __ldg(A.sw + sl);
-      const int64_t base = __ldg(A.sp + sl) + (row & 31);
+      const int64_t base = __ldg(A.sp + sl) + (pos & 31);
       for (int c = 0; c < w; ++c) {
         const int64_t e = base + (int64_t)c * 32;
         const double v = __ldcs(A.sv + e);

@@ -159,7 +159,7 @@ def _mem_of(*arrays):
     return mems.pop() if mems else RG_HOST
 
 
-def make_matrix(n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, keep=None):
+def make_matrix(n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, keep=None, sell_sigma=1):
     """Build an rg_matrix descriptor.  row_ptr/col_idx None -> values-only update.  Arrays must
     stay alive during the call (`keep` collects references)."""
     arrs = [a for a in (row_ptr, col_idx, val) if a is not None]
@@ -175,7 +175,8 @@ def make_matrix(n, row_ptr, col_idx, val, fmt="csr", block=1, sell_C=0, keep=Non
     rp, _ = _ptr(row_ptr, np.int32, nrows + 1, "row_ptr")
     ci, _ = _ptr(col_idx, np.int32, nnz, "col_idx")
     v, _ = _ptr(val, np.float64, vlen, "val")
-    return rg_matrix(RG_BSR if fmt == "bsr" else RG_CSR, int(n), nnz, int(block), rp, ci, v, mem, int(sell_C), 1)
+    return rg_matrix(RG_BSR if fmt == "bsr" else RG_CSR, int(n), nnz, int(block), rp, ci, v, mem, int(sell_C),
+                     int(sell_sigma))
 
 
 def rg_create(n, A: rg_matrix, max_m=64, max_snapshots=32, max_k=32, stream=None, flags=0):
@@ -198,11 +199,11 @@ def rg_matrix_values(ctx):
     return p.value, n.value
 
 
-def rg_update_values_inplace(ctx, n, nnz, fmt="csr", block=1, sell_C=0):
+def rg_update_values_inplace(ctx, n, nnz, fmt="csr", block=1, sell_C=0, sell_sigma=1):
     """rg_update_matrix with val == rg_matrix_values() (values already written in place)."""
     ptr, _ = rg_matrix_values(ctx)
     A = rg_matrix(RG_BSR if fmt == "bsr" else RG_CSR, int(n), int(nnz), int(block), None, None, ptr, RG_DEVICE,
-                  int(sell_C), 1)
+                  int(sell_C), int(sell_sigma))
     _check(_lib.rg_update_matrix(ctx, ctypes.byref(A)))
 
 

@@ -1,6 +1,6 @@
 """Randomised GPU-vs-oracle parity over the option space (seeded, reproducible): matrix size and
 sparsity (ragged rows, n from 1 to 20,000, so single- and multi-CTA persistent solves occur), restart
-length, recycle dimension, variant, SELL packing, SSOR, nonzero x0, and the execution path (persistent,
+length, recycle dimension, variant, SELL packing (sigma 1 / 32 / 256), SSOR, nonzero x0, and the execution path (persistent,
 CUDA graph, classical CGS2).
 Bar as in test_gpu_parity: x within 1e-7 relative, iterations within +-2, true residual <= tol."""
 import numpy as np
@@ -48,8 +48,10 @@ def test_fuzz_case(case):
     x0 = rng.standard_normal(n) * 0.1 if rng.integers(0, 2) else None
     from paper_1807_09467_b200 import rg as rgb
     flags = int(rng.choice([0, 0, rgb.RG_FLAG_NO_PERSIST, rgb.RG_FLAG_CGS2]))  # persistent / graph / classical CGS2
+    # SELL-32-sigma row sorting (own generator: the main draw sequence of the cases stays as it was)
+    sigma = int(np.random.default_rng(7700 + case).choice([1, 32, 256])) if sell else 1
     ctx = Context(n, t(hm.row_ptr), t(hm.col_idx), t(hm.val), sell_C=32 if sell else 0, max_m=max(m, 2),
-                  max_snapshots=max(k, 1), max_k=max(k, 1), flags=flags)
+                  max_snapshots=max(k, 1), max_k=max(k, 1), flags=flags, sell_sigma=sigma)
     W = None
     if k:
         W = np.linalg.qr(rng.standard_normal((n, k)))[0]
@@ -65,7 +67,7 @@ def test_fuzz_case(case):
     rep = ctx.solve(t(b), x, x0=None if x0 is None else t(x0), m=m, variant=variant, tol=1e-9, max_iters=5000)
     ref = oracle.solve(oracle.Matrix.from_host(hm), b, x0=x0, m=m, variant=variant, W=W, tol=1e-9,
                        max_iters=5000, precond=None if order is None else (order, omega))
-    desc = dict(n=n, m=m, k=k, variant=variant, sell=sell, pc=pc, x0=x0 is not None, flags=flags,
+    desc = dict(n=n, m=m, k=k, variant=variant, sell=sell, sigma=sigma, pc=pc, x0=x0 is not None, flags=flags,
                 its=(rep["iterations"], ref["iterations"]))
     assert rep["converged"] == ref["converged"], desc
     if ref["converged"]:

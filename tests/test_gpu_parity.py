@@ -665,3 +665,61 @@ def test_kernel_trace_timeline(rng):
         ctx.kernel_trace()
     assert e.value.status == rgb.RG_E_STATE
     ctx.close()
+
+
+# ------------------------------------------------------------------------------------- SELL-32-sigma
+def _sell_ctx(hm, sigma, **kw):
+    from paper_1807_09467_b200 import Context
+    return Context(hm.n, t(hm.row_ptr), t(hm.col_idx), t(hm.val), sell_C=32, sell_sigma=sigma, **kw)
+
+
+@pytest.mark.parametrize("sigma", [32, 256, 4096])
+@pytest.mark.parametrize("n", [31, 1000, 4097, 70001])
+def test_sell_sigma_spmv(sigma, n, rng):
+    """SELL-32-sigma with row sorting inside sigma-windows (ragged rows 0..40 entries, so the order
+    really changes): y = A x against the oracle at 1e-13, in the caller's row order; a values-only
+    update is repacked through the same permutation."""
+    hm = random_csr(n, rng, per_row=(0, 40) if n > 100 else (0, 5))
+    ctx = _sell_ctx(hm, sigma)
+    x = rng.standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device=DEV)
+    ctx.apply(t(x), y)
+    spmv_check(hm, x, y.cpu().numpy())
+    hm2 = synth.HostMatrix("csr", n, hm.row_ptr, hm.col_idx, rng.standard_normal(len(hm.val)))
+    ctx.update_matrix(t(hm2.val))
+    ctx.apply(t(x), y)
+    spmv_check(hm2, x, y.cpu().numpy())
+    ctx.close()
+
+
+def test_sell_sigma_rejected_values(rng):
+    from paper_1807_09467_b200 import rg as rgb
+    hm = random_csr(200, rng)
+    for bad in (3, 48, -1):
+        with pytest.raises(rgb.RgError) as e:
+            _sell_ctx(hm, bad)
+        assert e.value.status == rgb.RG_E_INVAL
+
+
+@pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique"])
+def test_sell_sigma_solve_vs_oracle(variant, rng):
+    """Solves with a sorted SELL-32-sigma matrix (graph path: the permutation crosses the persistent
+    kernel's row ranges), including C = A W through the operator build, against the oracle."""
+    from paper_1807_09467_b200 import rg as rgb
+    n, m, k = 20000, 25, 6
+    hm = random_csr(n, rng, per_row=(0, 24), diag=3.0)
+    W = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    b = rng.standard_normal(n)
+    ctx = _sell_ctx(hm, 512, max_m=m, max_snapshots=k, max_k=k, flags=rgb.RG_FLAG_PROFILE)
+    for i in range(k):
+        ctx.push_snapshot(t(W[:, i] * (k - i)))
+    assert ctx.build_recycle(k)[0] == k
+    x = torch.zeros(n, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), x, m=m, variant=variant, tol=1e-9)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=m, variant=variant, W=W if variant != "plain" else None,
+                       tol=1e-9)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["iterations"] - ref["iterations"]) <= 2
+    assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-7 * np.linalg.norm(ref["x"])
+    assert ctx.kernel_stats()["persistent_solve"]["launches"] == 0
+    ctx.close()
