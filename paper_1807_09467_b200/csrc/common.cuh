@@ -327,6 +327,16 @@ inline int current_device() {
   if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= MAXDEV) { cudaGetLastError(); d = 0; }
   return d;
 }
+// once per device: `static PerDevice once; if (once.first()) cudaFuncSetAttribute(...)`
+struct PerDevice {
+  bool done[MAXDEV];
+  bool first() {
+    const int d = current_device();
+    if (done[d]) return false;
+    done[d] = true;
+    return true;
+  }
+};
 
 inline int vec_grid(int64_t rows) {
   int64_t g = (rows + OT - 1) / OT;

@@ -729,11 +729,10 @@ static bool pdl_on() {
 }
 
 cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s, unsigned long long cond) {
-  static bool init = false;
-  if (!init) {
+  static PerDevice init_once;
+  if (init_once.first()) {
     cudaFuncSetAttribute(k_dk1, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_dk2, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    init = true;
   }
   if (phase == 1) {
     // streaming variant by default (C4: 3.90 -> 4.54 TB/s; (SCH, RU) = (4, 2) and (6, 2) measured
@@ -743,22 +742,20 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
     if (tma && !tiles) {
       const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
       const size_t smem = sizeof(double) * ((size_t)TS_STG * TS_STAGE + (size_t)(TS_R / 32) * nvw);
-      static bool attr = false;
-      if (!attr) {
+      static PerDevice attr_once;
+      if (attr_once.first()) {
         cudaFuncSetAttribute(k_dk1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double) * ((size_t)TS_STG * TS_STAGE + (size_t)(TS_R / 32) * DK1RED)));
-        attr = true;
       }
       return launch_ex(k_dk1_tma, dim3(tma_grid(L.ld)), dim3(TS_T), smem, s, pdl_on(), L, st, cond, nvw);
     }
     if (!tiles) {
       const int nvw = 2 * (L.maxk + MAXM) + 2 + 2 * L.maxk;  // >= nv of any step of this context
       const size_t smem = sizeof(double) * (DT / 32) * (size_t)nvw;
-      static bool attr = false;
-      if (!attr) {
+      static PerDevice attr_once;
+      if (attr_once.first()) {
         cudaFuncSetAttribute(k_dk1_stream<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(sizeof(double) * (DT / 32) * (size_t)DK1RED));
-        attr = true;
       }
       k_dk1_stream<8, 1><<<vec_grid(L.ld), DT, smem, s>>>(L, st, cond, nvw);
     } else
@@ -771,10 +768,9 @@ cudaError_t launch_dcgs(const Layout& L, DevState* st, int phase, cudaStream_t s
   }
   static const int tma = knob("RG_NO_TMA_DCGS") || knob("RG_NO_TMA_DK2") ? 0 : 1;
   if (tma) {
-    static bool attr = false;
-    if (!attr) {
+    static PerDevice attr_once;
+    if (attr_once.first()) {
       cudaFuncSetAttribute(k_dk2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * TS_STG * TS_STAGE));
-      attr = true;
     }
     // one SM left to the concurrent least-squares kernel (k_dcgs_ls) so that no update-pass CTA shares
     // an SM with it

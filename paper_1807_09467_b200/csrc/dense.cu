@@ -577,10 +577,9 @@ cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G
   note_host_launches(1);
   const int s8 = (s + 7) & ~7;
   const size_t smem = sizeof(double) * NST * s8 * TS;
-  static bool init = false;
-  if (!init) {
+  static PerDevice init_once;
+  if (init_once.first()) {
     cudaFuncSetAttribute(k_gram_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(double) * NST * S8MAX * TS));
-    init = true;
   }
   int64_t g = (n + GTR - 1) / GTR;
   if (g > GRAM_CTAS) g = GRAM_CTAS;
@@ -594,10 +593,9 @@ cudaError_t launch_gram(const double* Y, int64_t ld, int64_t n, int s, double* G
 cudaError_t launch_jacobi(const double* G, int s, double* lam, double* V, double* sigma_out,
                           DevState* st, cudaStream_t strm, const double* V0, int s0, int rel) {
   const size_t smem = sizeof(double) * 3 * JLD * JLD;
-  static bool init = false;
-  if (!init) {
+  static PerDevice init_once;
+  if (init_once.first()) {
     cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    init = true;
   }
   const int half = (s + (s & 1)) / 2;  // one thread per 2x2 block of the rotation round (<= 1024)
   static const int nt_env = knob_int("RG_JACOBI_NT", 0);
@@ -611,14 +609,13 @@ cudaError_t launch_xm(const double* X, int64_t ldx, int64_t n, int s, const doub
   note_host_launches(1);
   const int s8 = (s + 7) & ~7;
   const size_t smem = sizeof(double) * (s8 * XMS + XTR * XMS + NST * s8 * TS);
-  static bool init = false;
-  if (!init) {
+  static PerDevice init_once;
+  if (init_once.first()) {
     cudaFuncSetAttribute(k_xm, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(sizeof(double) * (S8MAX * XMS + XTR * XMS + NST * S8MAX * TS)));
-    init = true;
   }
-  static int occ_s8[S8MAX / 8 + 1] = {0};  // occupancy per panel width (queried once each)
-  int& occ = occ_s8[s8 / 8];
+  static int occ_s8[MAXDEV][S8MAX / 8 + 1] = {};  // occupancy per device and panel width (queried once each)
+  int& occ = occ_s8[current_device()][s8 / 8];
   if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_xm, XT, smem) != cudaSuccess) {
     cudaGetLastError();
     occ = 1;

@@ -534,13 +534,12 @@ cudaError_t launch_cond(const DevState* st, unsigned long long h, int which, cud
 }
 
 cudaError_t launch_orth(const Layout& L, DevState* st, int op, cudaStream_t s, unsigned long long cond) {
-  static bool init = false;
-  if (!init) {  // two 512-thread CTAs per SM need more than the default shared-memory carveout
+  static PerDevice init_once;
+  if (init_once.first()) {  // two 512-thread CTAs per SM need more than the default shared-memory carveout
     cudaFuncSetAttribute(k_orth, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_cgs<0>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_cgs<1>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_cgs<2>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    init = true;
   }
   // TMA-staged passes (graph path; augment's OP_UN also needs Q^T w: generic path)
   static const bool no_tma = knob("RG_NO_TMA_CGS");

@@ -681,10 +681,9 @@ cudaError_t launch_spmv(const MatDev& A, const Layout& L, DevState* st, int mode
     return cudaGetLastError();
   }
   if (A.fmt == 2 && A.b == 64 && A.tma) {
-    static bool init = false;
-    if (!init) {
+    static PerDevice init_once;
+    if (init_once.first()) {
       cudaFuncSetAttribute(k_spmv_bsr_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, BNS * BSTAGE);
-      init = true;
     }
     int64_t g = A.nb < NSM ? A.nb : NSM;
     return launch_ex(k_spmv_bsr_tma, dim3((int)(g < 1 ? 1 : g)), dim3(BT), BNS * BSTAGE, s, pdl, a);
