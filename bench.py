@@ -235,6 +235,13 @@ class GpuRun:
         self.nsnap = 0
         self.vals_ptr, _ = self.ctx.values_ptr()
         self.nnz = int(self.gen.col_idx.numel())
+        self.phase_ev = None           # a list: step() appends its 5 phase-boundary events (run_ours)
+
+    def _mark(self, evs):
+        if evs is not None:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(self.stream)
+            evs.append(e)
 
     def step(self, x_prev=None, push=None, history_cap=0):
         """One system t of the sequence, entirely on the device (inputs resident in HBM).
@@ -244,6 +251,8 @@ class GpuRun:
         self.t += 1
         if x_prev is not None:
             self.x.copy_(x_prev)
+        evs = [] if self.phase_ev is not None else None
+        self._mark(evs)
         # a3 first: W depends only on the snapshot window, not on A_t, so the asynchronous build is issued
         # before the generator and its completion (which the solve waits for on the host) overlaps the
         # generation of A_t instead of leaving a bubble before the solve (tools/trace.py: ~0.1 ms/system)
@@ -252,16 +261,22 @@ class GpuRun:
                 self.k_eff, self.sigma = self.ctx.build_recycle(self.k)
             else:                                      # a3, asynchronous (a4 happens inside the solve)
                 self.ctx.build_recycle(self.k, deferred=True)
+        self._mark(evs)
         if cfg.kind == "9pt":                          # C3: A is the same for the whole sequence
             self.gen.fill(self.t, self.x)              # (b_t only)
         else:                                          # A_t, b_t from x_{t-1}, written straight into
             self.gen.fill(self.t, self.x, val_ptr=self.vals_ptr)   # the solver's value buffer (a1)
             self.ctx.update_values_inplace(self.nnz)
+        self._mark(evs)
         rep = self.ctx.solve(self.gen.b, self.x, x0=self.x if self.warm else None, m=cfg.m, variant=self.variant,
                              tol=cfg.tol, history_cap=history_cap)
         if not rep["converged"]:
             raise RuntimeError(f"system {self.t} did not converge: {rep}")
+        self._mark(evs)
         self.ctx.push_snapshot(self.x if push is None else push)   # a2
+        self._mark(evs)
+        if evs is not None:
+            self.phase_ev.append(evs)
         self.nsnap += 1
         self.iters.append(rep["iterations"])
         return rep
@@ -394,11 +409,18 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         run.ctx.reset_kernel_stats()
         gen0 = run.gen.launches
+        run.phase_ev = []
         with ClockSampler(local) as clk:
             per, t_local, t_max = timed_replicas(run.step, args.steps, 0, dist_on, device, "cuda",
                                                  between=lambda: flush_l2(flush), stream=stream)
         kstats = run.ctx.kernel_stats()
         gen_launches = run.gen.launches - gen0
+        # per-system setup / generation / solve times, from events on the library's stream at
+        # the phase boundaries of every timed step (the solve includes a4, C = A W, which needs A_t)
+        names = ["recycle_build_a3", "generation_and_a1", "solve_a4_to_a10", "snapshot_push_a2"]
+        phases = {nm: sum(ev[i].elapsed_time(ev[i + 1]) for ev in run.phase_ev) / len(run.phase_ev)
+                  for i, nm in enumerate(names)}
+        run.phase_ev = None
         value = t_max / (args.steps * ws)
         timed_iters = run.iters[args.warmup:]
 
@@ -526,6 +548,11 @@ def run_ours(args, cfg):
                    "parallelism": f"replicas x{ws}"},
         "per_step_s": [round(p, 6) for p in per],
         "sequence_s": t_max,
+        "phases_ms_per_step": {**{nm: round(v, 4) for nm, v in phases.items()},
+                               "scope": "rank 0, device events on the library's stream at the phase boundaries "
+                                        "of each timed step; generation = the synthetic source writing A_t, b_t "
+                                        "(in place into the library's value buffer), not a library kernel; "
+                                        "`value` includes all four"},
         "vs_plain": vs_plain,
         "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
         "clocks": clk.summary(),

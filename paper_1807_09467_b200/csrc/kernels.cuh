@@ -120,6 +120,7 @@ struct PrecDev {
   double* Uv = nullptr;
   const int32_t* Umap = nullptr;
   double* dinv = nullptr;         // [n] over idx
+  double* dinvr = nullptr;        // [n] over the matrix row (the fused colour-0/1 forward sweep gathers it)
   const int32_t* dmap = nullptr;  // position of a_rr (over idx)
   int64_t nL = 0, nU = 0;
   int ncolors = 0;

@@ -23,30 +23,50 @@ constexpr int ST = 256;
 
 struct SsorArgs {
   PrecDev P;
-  int64_t c0, c1;        // this colour's range in perm
+  int64_t c0, c1;        // this launch's range in perm
   int backward;
+  int fuse0;             // forward launch over colours 0 AND 1: colour-0 values formed on the fly
   const double* in;      // forward input (nullptr: the Arnoldi vector u of the device state)
   double* out;           // w (forward) / t (backward, in place)
   int gate;              // 0 always, 1 Arnoldi step (st->active ...), 2 cycle end (st->have_xupd)
   int first;             // first sweep of an application (profiling start)
+  int last;              // last sweep of an application (closes the K_SSOR interval)
+  int nsweeps;           // kernel launches of the application
   Layout L;
   DevState* st;
   double bytes;
 };
 
+// One sweep = one launch, thread per row of the colour(s).  Round 2: (1) the forward sweeps of colours
+// 0 and 1 are ONE launch: a colour-0 row has no lower-coloured coupling, so its forward value is the
+// diagonal scale w_j = w(2-w) z_j / a_jj, which a colour-1 row forms on the fly from z and the row-
+// indexed 1/a_jj (dinvr) instead of reading it back — the same operations in the same order, so the
+// result is bitwise what the two-launch sequence gave; (2) every sweep after the first is launched with
+// PDL and loads its row's matrix entries (constant data) before griddepcontrol.wait, so the launch ramp
+// and the entry loads overlap the previous sweep's tail; (3) the last sweep closes the profiling
+// interval (there was a 1-thread kernel for that).  2-colour patterns (5- / 7-point): 4 launches -> 2.
 __global__ void __launch_bounds__(ST) k_ssor(SsorArgs a) {
+  pdl_trigger();
   DevState* st = a.st;
   double xs = 1.0;
   const double* in = a.in;
+  bool noop = false;
+  // (device state read before pdl_wait: written before the application's first sweep, which is a
+  // normal launch)
   if (a.gate == 1) {
     const int j = st->j;
-    if (!st->active || (st->dcgs && j >= st->m)) { prof_noop(st, K_SSOR); return; }
-    if (!a.backward) {
+    noop = !st->active || (st->dcgs && j >= st->m);
+    if (!noop && !a.backward) {
       in = a.L.Z + (int64_t)(a.L.VB + j) * a.L.ld;
       xs = st->dcgs ? 1.0 : st->sc[a.L.VB + j];  // CGS2 path: V stored un-normalised
     }
   } else if (a.gate == 2) {
-    if (!st->have_xupd) { prof_noop(st, K_SSOR); return; }
+    noop = !st->have_xupd;
+  }
+  if (noop) {
+    if (a.last && st->profile && blockIdx.x == 0 && threadIdx.x == 0) st->kstat[K_SSORK].launches += a.nsweeps;
+    prof_noop(st, K_SSOR);
+    return;
   }
   if (a.first && blockIdx.x == 0 && threadIdx.x == 0) prof_begin(st, K_SSOR);
   const PrecDev& P = a.P;
@@ -57,47 +77,70 @@ __global__ void __launch_bounds__(ST) k_ssor(SsorArgs a) {
     const int32_t* __restrict__ ci = a.backward ? P.Uci : P.Lci;
     const double* __restrict__ vv = a.backward ? P.Uv : P.Lv;
     const int32_t p0 = __ldg(rp + idx), p1 = __ldg(rp + idx + 1);
+    RG_CHK(st, r >= 0 && r < a.L.n && p0 <= p1 && p1 <= (a.backward ? P.nU : P.nL));
+    const double om = P.omega, di = __ldg(P.dinv + idx);
+    const double cf = xs * om * (2.0 - om);
+    int32_t cc[8];
+    double va[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = p0 + u < p1;
+      cc[u] = ok ? __ldcs(ci + p0 + u) : r;
+      va[u] = ok ? __ldcs(vv + p0 + u) : 0.0;
+    }
+    pdl_wait();  // out[] of the earlier sweeps
     double s = 0.0;
-    for (int32_t p = p0; p < p1; p += 8) {
-      int32_t cc[8];
-      double va[8];
+    for (int32_t p = p0;;) {
+      if (a.fuse0) {
+        double zz[8], dd[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          zz[u] = in[cc[u]];
+          dd[u] = __ldg(P.dinvr + cc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (p + u < p1) s += va[u] * ((cf * zz[u]) * dd[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (p + u < p1) s += va[u] * a.out[cc[u]];
+      }
+      p += 8;
+      if (p >= p1) break;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const bool ok = p + u < p1;
         cc[u] = ok ? __ldcs(ci + p + u) : r;
         va[u] = ok ? __ldcs(vv + p + u) : 0.0;
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (p + u < p1) s += va[u] * a.out[cc[u]];
     }
-    const double om = P.omega, di = __ldg(P.dinv + idx);
     if (!a.backward) {
-      a.out[r] = (xs * om * (2.0 - om) * in[r] - om * s) * di;
+      a.out[r] = (cf * in[r] - om * s) * di;
     } else {
       a.out[r] = a.out[r] - om * s * di;
     }
   }
-  if (st->profile && grid_last(a.L.counter) && threadIdx.x == 0) st->kstat[K_SSOR].bytes += a.bytes;
-}
-
-// closes the K_SSOR timing interval after the last sweep of one application
-__global__ void k_ssor_done(DevState* st, int gate, int nsweeps) {
-  if (!st->profile) return;
-  st->kstat[K_SSORK].launches += nsweeps + 1;  // kernel launches of this application (incl. this one)
-  if (gate == 1 && (!st->active || (st->dcgs && st->j >= st->m))) return;
-  if (gate == 2 && !st->have_xupd) return;
-  KStatDev& k = st->kstat[K_SSOR];
-  const unsigned long long t = gtimer();
-  k.ns += t - k.start;
-  k.launches++;
+  if (st->profile && grid_last(a.L.counter) && threadIdx.x == 0) {
+    KStatDev& k = st->kstat[K_SSOR];
+    k.bytes += a.bytes;
+    if (a.last) {  // closes the K_SSOR timing interval of one application
+      st->kstat[K_SSORK].launches += a.nsweeps;
+      k.ns += gtimer() - k.start;
+      k.launches++;
+    }
+  }
 }
 
 __global__ void k_ssor_values(PrecDev P, const double* __restrict__ v, int64_t n) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.nL; i += stride) P.Lv[i] = v[P.Lmap[i]];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.nU; i += stride) P.Uv[i] = v[P.Umap[i]];
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) P.dinv[i] = 1.0 / v[P.dmap[i]];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double d = 1.0 / v[P.dmap[i]];
+    P.dinv[i] = d;
+    P.dinvr[P.perm[i]] = d;
+  }
 }
 
 }  // namespace
@@ -115,25 +158,34 @@ cudaError_t launch_ssor(const PrecDev& P, const Layout& L, DevState* st, const d
                         cudaStream_t s) {
   SsorArgs a{};
   a.P = P; a.in = in; a.out = out; a.gate = gate; a.L = L; a.st = st;
-  // forward colours 0 .. nc-1, backward nc-2 .. 0 (the backward sweep of the last colour is the identity)
-  for (int pass = 0; pass < 2 * P.ncolors - 1; ++pass) {
-    const bool bwd = pass >= P.ncolors;
-    const int c = bwd ? 2 * P.ncolors - 2 - pass : pass;
+  // forward colours {0, 1} (one launch), 2 .. nc-1, backward nc-2 .. 0 (the backward sweep of the last
+  // colour is the identity)
+  const int nc = P.ncolors;
+  const int nfwd = nc >= 2 ? nc - 1 : 1, nbwd = nc - 1;
+  a.nsweeps = nfwd + nbwd;
+  for (int pass = 0; pass < nfwd + nbwd; ++pass) {
+    const bool bwd = pass >= nfwd;
+    int clo, chi;  // colours [clo, chi) of this launch
+    if (bwd) { clo = nc - 2 - (pass - nfwd); chi = clo + 1; }
+    else if (pass == 0) { clo = 0; chi = nc >= 2 ? 2 : 1; }
+    else { clo = pass + 1; chi = clo + 1; }
     a.backward = bwd ? 1 : 0;
+    a.fuse0 = (!bwd && pass == 0 && nc >= 2) ? 1 : 0;
     a.first = pass == 0;
-    a.c0 = P.coff[c];
-    a.c1 = P.coff[c + 1];
+    a.last = pass == nfwd + nbwd - 1;
+    a.c0 = P.coff[clo];
+    a.c1 = P.coff[chi];
     const double rows = (double)(a.c1 - a.c0);
-    // algorithmic bytes: this colour's L (or U) entries + perm, row pointer, 1/a_rr, vector in/out
-    a.bytes = 12.0 * (double)(bwd ? P.cU[c] : P.cL[c]) + rows * (4.0 + 4.0 + 8.0 + 16.0);
+    // algorithmic bytes: the colours' L (or U) entries + perm, row pointer, 1/a_rr, vector in/out
+    double ent = 0.0;
+    for (int c = clo; c < chi; ++c) ent += (double)(bwd ? P.cU[c] : P.cL[c]);
+    a.bytes = 12.0 * ent + rows * (4.0 + 4.0 + 8.0 + 16.0);
     const int64_t nrows = a.c1 - a.c0;
     const int g = (int)(nrows > 0 ? (nrows + ST - 1) / ST : 1);
-    k_ssor<<<g, ST, 0, s>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_ex(k_ssor, dim3(g), dim3(ST), 0, s, pass > 0, a);
     if (e != cudaSuccess) return e;
   }
-  k_ssor_done<<<1, 1, 0, s>>>(st, gate, 2 * P.ncolors - 1);
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 }  // namespace rg

@@ -1287,7 +1287,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
     return RG_OK;
   };
   rg_status s;
-  void *d_perm, *d_Lrp, *d_Lci, *d_Lmap, *d_Lv, *d_Urp, *d_Uci, *d_Umap, *d_Uv, *d_dinv, *d_dmap;
+  void *d_perm, *d_Lrp, *d_Lci, *d_Lmap, *d_Lv, *d_Urp, *d_Uci, *d_Umap, *d_Uv, *d_dinv, *d_dinvr, *d_dmap;
   if ((s = up(perm.data(), sizeof(int32_t) * n, "perm", &d_perm)) != RG_OK ||
       (s = up(Lrp.data(), sizeof(int32_t) * (n + 1), "L row pointer", &d_Lrp)) != RG_OK ||
       (s = up(Lci.data(), sizeof(int32_t) * P.nL, "L columns", &d_Lci)) != RG_OK ||
@@ -1298,6 +1298,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
       (s = up(Umap.data(), sizeof(int32_t) * P.nU, "U map", &d_Umap)) != RG_OK ||
       (s = up(nullptr, sizeof(double) * P.nU, "U values", &d_Uv)) != RG_OK ||
       (s = up(nullptr, sizeof(double) * n, "1/diag", &d_dinv)) != RG_OK ||
+      (s = up(nullptr, sizeof(double) * n, "1/diag by row", &d_dinvr)) != RG_OK ||
       (s = up(dmap.data(), sizeof(int32_t) * n, "diag map", &d_dmap)) != RG_OK) {
     cudaStreamSynchronize(c->stream);
     drop_preconditioner(c);
@@ -1306,7 +1307,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
   P.perm = (const int32_t*)d_perm;
   P.Lrp = (const int32_t*)d_Lrp; P.Lci = (const int32_t*)d_Lci; P.Lmap = (const int32_t*)d_Lmap; P.Lv = (double*)d_Lv;
   P.Urp = (const int32_t*)d_Urp; P.Uci = (const int32_t*)d_Uci; P.Umap = (const int32_t*)d_Umap; P.Uv = (double*)d_Uv;
-  P.dinv = (double*)d_dinv; P.dmap = (const int32_t*)d_dmap;
+  P.dinv = (double*)d_dinv; P.dinvr = (double*)d_dinvr; P.dmap = (const int32_t*)d_dmap;
   if (!c->pz) {
     if ((s = dalloc(&c->pz, (size_t)c->npad, "pz")) != RG_OK || (s = dalloc(&c->pt, (size_t)c->npad, "pt")) != RG_OK) {
       drop_preconditioner(c);
