@@ -120,7 +120,9 @@ struct PrecDev {
   double* Uv = nullptr;
   const int32_t* Umap = nullptr;
   double* dinv = nullptr;         // [n] over idx
-  double* dinvr = nullptr;        // [n] over the matrix row (the fused colour-0/1 forward sweep gathers it)
+  double* dinvr = nullptr;        // [n] over the matrix row
+  double* Lv1 = nullptr;          // [nL1] L values of the colour-1 rows times 1/a_jj of their column (fused forward sweep)
+  int64_t l1base = 0, nL1 = 0;    // the colour-1 rows' L entries: [l1base, l1base + nL1)
   const int32_t* dmap = nullptr;  // position of a_rr (over idx)
   int64_t nL = 0, nU = 0;
   int ncolors = 0;

@@ -39,9 +39,10 @@ struct SsorArgs {
 
 // One sweep = one launch, thread per row of the colour(s).  Round 2: (1) the forward sweeps of colours
 // 0 and 1 are ONE launch: a colour-0 row has no lower-coloured coupling, so its forward value is the
-// diagonal scale w_j = w(2-w) z_j / a_jj, which a colour-1 row forms on the fly from z and the row-
-// indexed 1/a_jj (dinvr) instead of reading it back — the same operations in the same order, so the
-// result is bitwise what the two-launch sequence gave; (2) every sweep after the first is launched with
+// diagonal scale w_j = w(2-w) z_j / a_jj, which a colour-1 row forms on the fly from z instead of
+// reading it back; the 1/a_jj factor is folded into the colour-1 rows' coupling values when the values
+// are gathered (Lv1 = a_rj / a_jj: one gather per coupling, not two; rounding-level difference from
+// the two-launch sequence); (2) every sweep after the first is launched with
 // PDL and loads its row's matrix entries (constant data) before griddepcontrol.wait, so the launch ramp
 // and the entry loads overlap the previous sweep's tail; (3) the last sweep closes the profiling
 // interval (there was a 1-thread kernel for that).  2-colour patterns (5- / 7-point): 4 launches -> 2.
@@ -75,7 +76,8 @@ __global__ void __launch_bounds__(ST) k_ssor(SsorArgs a) {
     const int32_t r = __ldg(P.perm + idx);
     const int32_t* __restrict__ rp = a.backward ? P.Urp : P.Lrp;
     const int32_t* __restrict__ ci = a.backward ? P.Uci : P.Lci;
-    const double* __restrict__ vv = a.backward ? P.Uv : P.Lv;
+    // fused launch: the colour-1 rows' couplings pre-multiplied by the column's 1/a_jj (Lv1, offset l1base)
+    const double* __restrict__ vv = a.backward ? P.Uv : (a.fuse0 ? P.Lv1 - P.l1base : P.Lv);
     const int32_t p0 = __ldg(rp + idx), p1 = __ldg(rp + idx + 1);
     RG_CHK(st, r >= 0 && r < a.L.n && p0 <= p1 && p1 <= (a.backward ? P.nU : P.nL));
     const double om = P.omega, di = __ldg(P.dinv + idx);
@@ -92,15 +94,12 @@ __global__ void __launch_bounds__(ST) k_ssor(SsorArgs a) {
     double s = 0.0;
     for (int32_t p = p0;;) {
       if (a.fuse0) {
-        double zz[8], dd[8];
+        double zz[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          zz[u] = in[cc[u]];
-          dd[u] = __ldg(P.dinvr + cc[u]);
-        }
+        for (int u = 0; u < 8; ++u) zz[u] = in[cc[u]];
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-          if (p + u < p1) s += va[u] * ((cf * zz[u]) * dd[u]);
+          if (p + u < p1) s += va[u] * (cf * zz[u]);
       } else {
 #pragma unroll
         for (int u = 0; u < 8; ++u)
@@ -143,6 +142,13 @@ __global__ void k_ssor_values(PrecDev P, const double* __restrict__ v, int64_t n
   }
 }
 
+// Lv1 = (L values of the colour-1 rows) * 1/a_jj of their (colour-0) column; after k_ssor_values
+__global__ void k_ssor_scale(PrecDev P) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.nL1; i += stride)
+    P.Lv1[i] = P.Lv[P.l1base + i] * P.dinvr[P.Lci[P.l1base + i]];
+}
+
 }  // namespace
 
 cudaError_t launch_ssor_values(const PrecDev& P, const double* v, int64_t n, cudaStream_t s) {
@@ -151,6 +157,12 @@ cudaError_t launch_ssor_values(const PrecDev& P, const double* v, int64_t n, cud
   int64_t g = (work + ST - 1) / ST;
   if (g > (int64_t)NSM * 8) g = (int64_t)NSM * 8;
   k_ssor_values<<<(int)(g < 1 ? 1 : g), ST, 0, s>>>(P, v, n);
+  if (P.nL1 > 0) {
+    note_host_launches(1);
+    int64_t g1 = (P.nL1 + ST - 1) / ST;
+    if (g1 > (int64_t)NSM * 8) g1 = (int64_t)NSM * 8;
+    k_ssor_scale<<<(int)g1, ST, 0, s>>>(P);
+  }
   return cudaGetLastError();
 }
 

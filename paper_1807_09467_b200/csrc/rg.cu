@@ -671,6 +671,18 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
     cudaGetLastError();
     return fail(RG_E_CUDA, "no CUDA device available");
   }
+  {  // the library is sm_100a code sized for the B200's 148 SMs (NSM): refuse anything else loudly
+    int dev = 0, major = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(RG_E_CUDA, "cannot query the current CUDA device");
+    }
+    if (major != 10 || sms < NSM)
+      return fail(RG_E_CUDA, "librg is built for sm_100a with " + std::to_string(NSM) + " SMs (B200); the current device has "
+                                 "compute capability " + std::to_string(major) + ".x and " + std::to_string(sms) + " SMs");
+  }
   rg_ctx* c = new rg_ctx();
   CK(cudaGetDevice(&c->dev));
   c->flags = opt->flags;
@@ -1270,6 +1282,10 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
   }
   P.nL = (int64_t)Lci.size();
   P.nU = (int64_t)Uci.size();
+  if (nc >= 2) {
+    P.l1base = Lrp[P.coff[1]];
+    P.nL1 = Lrp[P.coff[2]] - Lrp[P.coff[1]];
+  }
   CK(cudaStreamSynchronize(c->stream));
   clear_graphs(c);
   drop_preconditioner(c);
@@ -1287,7 +1303,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
     return RG_OK;
   };
   rg_status s;
-  void *d_perm, *d_Lrp, *d_Lci, *d_Lmap, *d_Lv, *d_Urp, *d_Uci, *d_Umap, *d_Uv, *d_dinv, *d_dinvr, *d_dmap;
+  void *d_perm, *d_Lrp, *d_Lci, *d_Lmap, *d_Lv, *d_Urp, *d_Uci, *d_Umap, *d_Uv, *d_dinv, *d_dinvr, *d_dmap, *d_Lv1;
   if ((s = up(perm.data(), sizeof(int32_t) * n, "perm", &d_perm)) != RG_OK ||
       (s = up(Lrp.data(), sizeof(int32_t) * (n + 1), "L row pointer", &d_Lrp)) != RG_OK ||
       (s = up(Lci.data(), sizeof(int32_t) * P.nL, "L columns", &d_Lci)) != RG_OK ||
@@ -1299,6 +1315,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
       (s = up(nullptr, sizeof(double) * P.nU, "U values", &d_Uv)) != RG_OK ||
       (s = up(nullptr, sizeof(double) * n, "1/diag", &d_dinv)) != RG_OK ||
       (s = up(nullptr, sizeof(double) * n, "1/diag by row", &d_dinvr)) != RG_OK ||
+      (s = up(nullptr, sizeof(double) * P.nL1, "scaled colour-1 L values", &d_Lv1)) != RG_OK ||
       (s = up(dmap.data(), sizeof(int32_t) * n, "diag map", &d_dmap)) != RG_OK) {
     cudaStreamSynchronize(c->stream);
     drop_preconditioner(c);
@@ -1307,7 +1324,7 @@ RG_API rg_status rg_set_preconditioner(rg_ctx* c, int32_t kind, double omega, co
   P.perm = (const int32_t*)d_perm;
   P.Lrp = (const int32_t*)d_Lrp; P.Lci = (const int32_t*)d_Lci; P.Lmap = (const int32_t*)d_Lmap; P.Lv = (double*)d_Lv;
   P.Urp = (const int32_t*)d_Urp; P.Uci = (const int32_t*)d_Uci; P.Umap = (const int32_t*)d_Umap; P.Uv = (double*)d_Uv;
-  P.dinv = (double*)d_dinv; P.dinvr = (double*)d_dinvr; P.dmap = (const int32_t*)d_dmap;
+  P.dinv = (double*)d_dinv; P.dinvr = (double*)d_dinvr; P.Lv1 = (double*)d_Lv1; P.dmap = (const int32_t*)d_dmap;
   if (!c->pz) {
     if ((s = dalloc(&c->pz, (size_t)c->npad, "pz")) != RG_OK || (s = dalloc(&c->pt, (size_t)c->npad, "pt")) != RG_OK) {
       drop_preconditioner(c);
