@@ -495,16 +495,21 @@ __device__ __forceinline__ uint64_t ts_policy(bool keep) {
   else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-// producer: stage number t (global sequence) of `nc` column segments [col_c + base, +cnt rows)
+// producer WARP: stage number t (global sequence) of `nc` column segments [col_c + base, +cnt rows).  Lane c
+// issues column c's bulk copy (round 2, late: one lane issuing all 8 copies, each with its own index
+// load and 64-bit address arithmetic, took about as long per stage as the stage's 32 KB take to stream
+// — the producer lane, not HBM, set the rate of the dots pass).
 __device__ __forceinline__ void ts_issue(double* ring, uint64_t* full, uint64_t* empty, int t, const double* Z,
                                          int64_t ld, const int* cols, int nc, int64_t base, int cnt, uint64_t pol) {
-  const int s = t % TS_STG;
+  const int s = t % TS_STG, lane = threadIdx.x & 31;
   if (t >= TS_STG) ts_wait(&empty[s], (uint32_t)((t / TS_STG - 1) & 1));
-  const uint32_t bytes = (uint32_t)(nc * cnt * 8);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ts_u32(&full[s])), "r"(bytes) : "memory");
-  for (int c = 0; c < nc; ++c)
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ts_u32(&full[s])),
+                 "r"((uint32_t)(nc * cnt * 8)) : "memory");
+  __syncwarp();
+  if (lane < nc)
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                 ::"r"(ts_u32(ring + (size_t)s * TS_STAGE + c * TS_R)), "l"(Z + (int64_t)cols[c] * ld + base),
+                 ::"r"(ts_u32(ring + (size_t)s * TS_STAGE + lane * TS_R)), "l"(Z + (int64_t)cols[lane] * ld + base),
                  "r"((uint32_t)(cnt * 8)), "r"(ts_u32(&full[s])), "l"(pol) : "memory");
 }
 __device__ __forceinline__ void ts_release(uint64_t* empty, int s) {
@@ -542,15 +547,13 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk1_tma(Layout L, DevState* st, uns
   const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
   const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
   const int nchunk = (ncols + TS_CH - 1) / TS_CH;
-  if (wid == TS_R / 32) {  // ---- producer (lane 0): chunk outer, row tile inner
-    if (lane == 0) {
-      const uint64_t pol = ts_policy(L.keep_l2 != 0);
-      int t = 0;
-      for (int q = 0; q < nchunk; ++q)
-        for (int64_t base = r0; base < r1; base += TS_R, ++t)
-          ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
-                   (int)min((int64_t)TS_R, r1 - base), pol);
-    }
+  if (wid == TS_R / 32) {  // ---- producer warp (lane = column of the stage): chunk outer, row tile inner
+    const uint64_t pol = ts_policy(L.keep_l2 != 0);
+    int t = 0;
+    for (int q = 0; q < nchunk; ++q)
+      for (int64_t base = r0; base < r1; base += TS_R, ++t)
+        ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
+                 (int)min((int64_t)TS_R, r1 - base), pol);
   } else {  // ---- consumers: thread = row of the tile
     pdl_wait();  // u, y: written by the SpMV this launch may overlap (PDL); the basis stream above is not
     double s_uu = 0.0, s_uy = 0.0;
@@ -673,15 +676,13 @@ __global__ void __launch_bounds__(TS_T, 1) k_dk2_tma(Layout L, DevState* st) {
   const int64_t r0 = ((int64_t)blockIdx.x * ng / gridDim.x) << 5;
   const int64_t r1 = ((int64_t)(blockIdx.x + 1) * ng / gridDim.x) << 5;
   const int nchunk = (ncols + TS_CH - 1) / TS_CH;
-  if (wid == TS_R / 32) {  // ---- producer: row tile outer, column chunk inner
-    if ((tid & 31) == 0) {
-      const uint64_t pol = ts_policy(L.keep_l2 != 0);
-      int t = 0;
-      for (int64_t base = r0; base < r1; base += TS_R)
-        for (int q = 0; q < nchunk; ++q, ++t)
-          ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
-                   (int)min((int64_t)TS_R, r1 - base), pol);
-    }
+  if (wid == TS_R / 32) {  // ---- producer warp: row tile outer, column chunk inner
+    const uint64_t pol = ts_policy(L.keep_l2 != 0);
+    int t = 0;
+    for (int64_t base = r0; base < r1; base += TS_R)
+      for (int q = 0; q < nchunk; ++q, ++t)
+        ts_issue(ring, full, empty, t, L.Z, ld, colidx + q * TS_CH, min(TS_CH, ncols - q * TS_CH), base,
+                 (int)min((int64_t)TS_R, r1 - base), pol);
   } else {
     int t = 0;
     for (int64_t base = r0; base < r1; base += TS_R) {
