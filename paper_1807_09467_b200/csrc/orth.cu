@@ -397,26 +397,27 @@ __global__ void __launch_bounds__(544, 1) k_cgs_tma(Layout L, DevState* st, int 
   for (int i = 0; i < CG_CPT; ++i) dacc[i] = 0.0;
   double nrm = 0.0;
   const int r = tid % TR, g = tid / TR;
-  if (wid == 16) {  // ---- producer
-    if (lane == 0) {
-      uint64_t pol, keep;
-      if (L.keep_l2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-      else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
-      for (int t = 0; t < ntile; ++t) {
-        const int s = t % CG_NS;
-        if (t >= CG_NS) cg_wait(&empty[s], (uint32_t)((t / CG_NS - 1) & 1));
-        const int64_t base = r0 + (int64_t)t * TR;
-        const uint32_t cnt = (uint32_t)min((int64_t)TR, r1 - base);
+  if (wid == 16) {  // ---- producer warp: lane c issues the copies of columns c, c + 32, ... of a tile (one lane
+                    // issuing all p + 1 copies serially was slower than the tile streams, cf. dcgs.cu ts_issue)
+    uint64_t pol, keep;
+    if (L.keep_l2) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(keep));
+    for (int t = 0; t < ntile; ++t) {
+      const int s = t % CG_NS;
+      if (t >= CG_NS) cg_wait(&empty[s], (uint32_t)((t / CG_NS - 1) & 1));
+      const int64_t base = r0 + (int64_t)t * TR;
+      const uint32_t cnt = (uint32_t)min((int64_t)TR, r1 - base);
+      if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(cg_u32(&full[s])),
                      "r"((uint32_t)(p + 1) * cnt * 8u) : "memory");
-        double* stg = ring + (size_t)s * SD;
-        for (int c = 0; c <= p; ++c) {
-          const double* src = c < p ? L.Z + (int64_t)(c0 + c) * ld + base : w + base;
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
-                       ::"r"(cg_u32(stg + (size_t)c * TR)), "l"(src), "r"(cnt * 8u), "r"(cg_u32(&full[s])),
-                       "l"(c < p ? pol : keep) : "memory");
-        }
+      __syncwarp();
+      double* stg = ring + (size_t)s * SD;
+      for (int c = lane; c <= p; c += 32) {
+        const double* src = c < p ? L.Z + (int64_t)(c0 + c) * ld + base : w + base;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+                     ::"r"(cg_u32(stg + (size_t)c * TR)), "l"(src), "r"(cnt * 8u), "r"(cg_u32(&full[s])),
+                     "l"(c < p ? pol : keep) : "memory");
       }
     }
   } else {  // ---- consumers
