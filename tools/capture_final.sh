@@ -14,6 +14,7 @@ for v in augment oblique orthogonal; do
   timeout 900 python bench.py --config C2 --variant $v --steps 12 --warmup 3 --no-cpu-baseline --no-e2e --no-vs-plain > $O/bench_C2_$v.json 2> $O/bench_C2_$v.err
 done
 timeout 900 python bench.py --config C4 --precond ssor --steps 8 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C4_ssor.json 2> $O/bench_C4_ssor.err
+timeout 900 python bench.py --config C3 --precond ssor --steps 8 --warmup 3 --no-cpu-baseline --no-e2e > $O/bench_C3_ssor.json 2> $O/bench_C3_ssor.err
 for c in C3 C4 C5; do timeout 600 python tools/trace.py $c deflate 2 > $O/trace_$c.txt 2>&1; done
 B="python bench.py --no-graph --no-cpu-baseline --no-e2e --no-vs-plain"
 N="ncu --set full --clock-control none --import-source on"
@@ -22,6 +23,7 @@ timeout 900 $N -k regex:k_spmv_bsr_tma -s 30 -c 1 -o $O/c5_spmv $B --steps 4 --w
 timeout 900 $N -k regex:k_spmm_bsr_tma -s 8 -c 1 -o $O/c5_spmm $B --steps 10 --warmup 3 > $O/c5_spmm.log 2>&1
 timeout 900 $N -k regex:k_dk1_tma -s 300 -c 1 -o $O/c4_dk1 $B --config C4 --steps 4 --warmup 3 > $O/c4_dk1.log 2>&1
 timeout 900 $N -k regex:k_dk1_tma -s 300 -c 1 -o $O/c3_dk1 $B --config C3 --steps 4 --warmup 3 > $O/c3_dk1.log 2>&1
+timeout 900 $N -k regex:k_ssor -s 200 -c 2 -o $O/c4_ssor $B --config C4 --precond ssor --steps 4 --warmup 3 > $O/c4_ssor.log 2>&1
 timeout 900 $N -k regex:k_dk2_tma -s 300 -c 1 -o $O/c4_dk2 $B --config C4 --steps 4 --warmup 3 > $O/c4_dk2.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_dk -c 600 --csv --log-file $O/c4_dk_launches.csv $B --config C4 --steps 1 --warmup 3 > $O/c4_dk_launch.log 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_dk -c 600 --csv --log-file $O/c3_dk_launches.csv $B --config C3 --steps 1 --warmup 3 > $O/c3_dk_launch.log 2>&1
