@@ -558,11 +558,20 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
       }
       const int64_t J64 = (int64_t)ci_cur * 64;
       const uint32_t pan = su32(wpan + (size_t)s * 64 * WS);
-      for (int e = lane; e < 64 * k; e += 32) {  // W(J64 + kk, n) -> panel[kk][n]; coalesced per column
-        const int kk = e & 63, n = e >> 6;
-        const double* src = n < kw ? W + (int64_t)n * ld + J64 + kk : xe + J64 + kk;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(pan + 8u * (uint32_t)(kk * WS + n)), "l"(src)
-                     : "memory");
+      {  // W(J64 + kk, n) -> panel[kk][n], kk = lane and lane + 32; coalesced per column.  Pointer increments
+         // only: the index / select arithmetic of a flat element loop made this loop (2 k copies per lane,
+         // behind the consumers on the warp's scheduler) the per-block critical path at k >= 9
+        const double* src = W + J64 + lane;
+        uint32_t dst = pan + 8u * (uint32_t)(lane * WS);
+#pragma unroll 4
+        for (int n = 0; n < kw; ++n, src += ld, dst += 8u) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * 32u * (uint32_t)WS), "l"(src + 32) : "memory");
+        }
+        if (xe) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(xe + J64 + lane) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * 32u * (uint32_t)WS), "l"(xe + J64 + lane + 32) : "memory");
+        }
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(&full[s])) : "memory");
       I = I2;
