@@ -21,6 +21,9 @@ the same generator (C5: A_t = A_{t-1} o (1 + 0.01 xi_t), b fixed).  Other config
              cannot bracket single kernels), against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the oracle (plain C, deterministic OpenMP threads on all online cores) on the first
              timed systems of the same workload, bounded to ~--cpu-budget seconds
+  phases_ms_per_step  device time per system of the recycle build (a3), the generation of A_t, b_t (the
+             synthetic source, not a library kernel), the solve (a4-a10) and the snapshot push (a2),
+             from events at the phase boundaries of every timed step; `value` has all four
 
 --impl reference runs the oracle (the reference arm for this tier) on the same config.
 Multi-GPU (torchrun): independent replicas, one sequence per rank, no collective on the data
