@@ -211,3 +211,56 @@ def test_persistent_and_graph_paths_agree_preconditioned(rng, variant):
     assert r0["converged"] and r1["converged"]
     assert abs(r0["iterations"] - r1["iterations"]) <= 1
     assert np.linalg.norm(x0 - x1) <= 1e-9 * np.linalg.norm(x1)
+
+
+def grid5(N, rng):
+    """5-point stencil on an N x N grid with random couplings: exactly 2 colours (red-black)."""
+    n = N * N
+    rp, ci, v = [0], [], []
+    for j in range(N):
+        for i in range(N):
+            r = j * N + i
+            for (di, dj) in ((0, -1), (-1, 0), (0, 0), (1, 0), (0, 1)):
+                ii, jj = i + di, j + dj
+                if 0 <= ii < N and 0 <= jj < N:
+                    ci.append(jj * N + ii)
+                    v.append(4.5 if (di, dj) == (0, 0) else -1.0 + 0.3 * rng.standard_normal())
+            rp.append(len(ci))
+    return synth.HostMatrix("csr", n, np.array(rp, np.int32), np.array(ci, np.int32), np.array(v))
+
+
+@pytest.mark.parametrize("omega", [1.0, 1.3])
+def test_ssor_two_colours_fused_forward_sweep_and_value_update(rng, omega):
+    """2 colours: the forward sweeps of colours 0 and 1 run as ONE launch (colour-0 values formed on the
+    fly, couplings pre-scaled by 1 / a_jj when the values are gathered); n spans many CTAs and a ragged
+    last one.  A values-only update must re-gather the pre-scaled couplings."""
+    hm = grid5(301, rng)
+    col = greedy_colors(hm.n, hm.row_ptr, hm.col_idx)
+    assert col.max() == 1
+    ctx = ctx_for(hm)
+    assert ctx.set_preconditioner("ssor", omega, colors=col) == 2
+    order = oracle.ssor_order(col)
+    for rep in range(2):
+        x = rng.standard_normal(hm.n)
+        y = torch.zeros(hm.n, dtype=torch.float64, device=DEV)
+        ctx.apply_preconditioner(t(x), y)
+        ref = oracle.ssor(oracle.Matrix.from_host(hm), order, omega, x)
+        assert np.linalg.norm(y.cpu().numpy() - ref) <= 1e-13 * np.linalg.norm(ref)
+        assert np.max(np.abs(y.cpu().numpy() - ref)) <= 1e-12 * np.max(np.abs(ref))
+        hm = synth.HostMatrix("csr", hm.n, hm.row_ptr, hm.col_idx, hm.val * (1.0 + 0.2 * rng.random(hm.val.size)))
+        ctx.update_matrix(t(hm.val))   # values only: Lv, Uv, 1 / a_rr and the pre-scaled Lv1 follow
+    ctx.close()
+
+
+def test_ssor_one_colour_diagonal_matrix(rng):
+    """A diagonal matrix has one colour: a single forward launch, no backward sweep; M^{-1} = w(2-w) D^{-1}."""
+    n, omega = 5000, 1.2
+    d = 1.0 + rng.random(n)
+    hm = synth.HostMatrix("csr", n, np.arange(n + 1, dtype=np.int32), np.arange(n, dtype=np.int32), d)
+    ctx = ctx_for(hm)
+    assert ctx.set_preconditioner("ssor", omega) == 1
+    x = rng.standard_normal(n)
+    y = torch.zeros(n, dtype=torch.float64, device=DEV)
+    ctx.apply_preconditioner(t(x), y)
+    np.testing.assert_allclose(y.cpu().numpy(), omega * (2.0 - omega) * x / d, rtol=1e-14, atol=0)
+    ctx.close()
