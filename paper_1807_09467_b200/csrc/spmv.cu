@@ -444,16 +444,17 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // stride WS == 2 mod 16 (the B elements W(kcol(s, j), 8g + i) of a half-warp, i < 4, j < 4, land in 16
 // distinct bank pairs).  ae / ao: this lane's A element of k-steps 0 / 1 (k-step s adds 128 (s / 2));
 // we / wo: its W element of k-steps 0 / 1 (+ 8 WS (s / 2) + 8 g).
+// CH independent accumulator chains per column group hide the DMMA latency when NG is small.  The chains
+// PERSIST over the blocks of a block row (round 2, late): folding them into one accumulator after every block
+// drained the DMMA pipe once per block and warp — a fixed ~0.26 us per block whatever the warp mapping.
+template <int NG>
+struct SpmmChains {
+  static constexpr int CH = NG >= 4 ? 1 : (NG >= 2 ? 2 : 4);
+};
 template <int NG, int WS>
-__device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk, const double* wp, int ae, int ao,
-                                          int we, int wo) {
-  // CH independent accumulator chains per column group hide the DMMA latency when NG is small
-  constexpr int CH = NG >= 4 ? 1 : (NG >= 2 ? 2 : 4);
-  double ch[NG][CH][2];
-#pragma unroll
-  for (int g = 0; g < NG; ++g)
-#pragma unroll
-    for (int c = 0; c < CH; ++c) ch[g][c][0] = ch[g][c][1] = 0.0;
+__device__ __forceinline__ void block_mma(double (&ch)[NG][SpmmChains<NG>::CH][2], const double* blk, const double* wp,
+                                          int ae, int ao, int we, int wo) {
+  constexpr int CH = SpmmChains<NG>::CH;
 #pragma unroll
   for (int s0 = 0; s0 < 16; s0 += CH) {
 #pragma unroll
@@ -465,13 +466,54 @@ __device__ __forceinline__ void block_mma(double (&acc)[8][2], const double* blk
       for (int g = 0; g < NG; ++g) dmma884(ch[g][c][0], ch[g][c][1], av, wp[wb + 8 * g]);  // W(kcol, 8g + lane/4)
     }
   }
+}
+
+// The consumer loop of one CTA for a fixed number NG of 8-column groups: block rows I = blockIdx, +gridDim, ...;
+// the blocks of a row stream through the ring; the chains are folded and the 8 rows stored once per block row.
+template <int NG, int NST, int WS>
+__device__ __forceinline__ void spmm_consume(const MatDev& A, const double* ring, const double* wpan, uint64_t* full,
+                                             uint64_t* empty, double* Y, int64_t ld, int kw, const double* xe,
+                                             double* ye, int wid, int lane) {
+  constexpr int CH = SpmmChains<NG>::CH;
+  const int rrow = wid * 8 + (lane >> 2);                    // A fragment row inside the block
+  const int ae = swz_off(rrow, kcol(0, lane & 3)), ao = swz_off(rrow, kcol(1, lane & 3));
+  const int we = kcol(0, lane & 3) * WS + (lane >> 2), wo = kcol(1, lane & 3) * WS + (lane >> 2);
+  int t = 0;
+  int64_t I = blockIdx.x;
+  int32_t p = I < A.nb ? __ldg(A.rp + I) : 0, pend = I < A.nb ? __ldg(A.rp + I + 1) : 0;
+  for (; I < A.nb; I += gridDim.x) {
+    const int64_t In = I + gridDim.x;  // the next block row's range, loaded early
+    const int32_t pn = In < A.nb ? __ldg(A.rp + In) : 0, pendn = In < A.nb ? __ldg(A.rp + In + 1) : 0;
+    double ch[NG][CH][2];
 #pragma unroll
-  for (int g = 0; g < NG; ++g)
+    for (int g = 0; g < NG; ++g)
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      acc[g][0] += ch[g][c][0];
-      acc[g][1] += ch[g][c][1];
+      for (int c = 0; c < CH; ++c) ch[g][c][0] = ch[g][c][1] = 0.0;
+    for (; p < pend; ++p, ++t) {
+      const int st = t % NST;
+      bar_wait(&full[st], (uint32_t)((t / NST) & 1));
+      block_mma<NG, WS>(ch, ring + (size_t)st * (BSTAGE / 8), wpan + (size_t)st * 64 * WS, ae, ao, we, wo);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
     }
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      double a0 = ch[g][0][0], a1 = ch[g][0][1];
+#pragma unroll
+      for (int c = 1; c < CH; ++c) {
+        a0 += ch[g][c][0];
+        a1 += ch[g][c][1];
+      }
+      const int col = g * 8 + (lane & 3) * 2;
+      const int64_t row = I * 64 + rrow;
+      if (col < kw) Y[(int64_t)col * ld + row] = a0;
+      else if (col == kw && xe) ye[row] = a0;
+      if (col + 1 < kw) Y[(int64_t)(col + 1) * ld + row] = a1;
+      else if (col + 1 == kw && xe) ye[row] = a1;
+    }
+    p = pn;
+    pend = pendn;
+  }
 }
 
 // xe != nullptr: one extra input column (panel column k) whose product goes to ye (y = A x0 of the
@@ -582,50 +624,17 @@ __global__ void __launch_bounds__(BT, 1) k_spmm_bsr_tma(const __grid_constant__ 
     }
     return;
   }
-  // ---- consumers
-  const int rrow = wid * 8 + (lane >> 2);                    // A fragment row inside the block
-  const int ae = swz_off(rrow, kcol(0, lane & 3)), ao = swz_off(rrow, kcol(1, lane & 3));
-  const int we = kcol(0, lane & 3) * WS + (lane >> 2), wo = kcol(1, lane & 3) * WS + (lane >> 2);
-  int t = 0;
-  int64_t I = blockIdx.x;
-  int32_t p = I < A.nb ? __ldg(A.rp + I) : 0, pend = I < A.nb ? __ldg(A.rp + I + 1) : 0;
-  for (; I < A.nb; I += gridDim.x) {
-    const int64_t In = I + gridDim.x;  // the next block row's range, loaded early
-    const int32_t pn = In < A.nb ? __ldg(A.rp + In) : 0, pendn = In < A.nb ? __ldg(A.rp + In + 1) : 0;
-    double acc[8][2];
-#pragma unroll
-    for (int g = 0; g < 8; ++g) acc[g][0] = acc[g][1] = 0.0;
-    for (; p < pend; ++p, ++t) {
-      const int st = t % NST;
-      bar_wait(&full[st], (uint32_t)((t / NST) & 1));
-      const double* blk = ring + (size_t)st * (BSTAGE / 8);
-      const double* wp = wpan + (size_t)st * 64 * WS;
-      switch (ng) {  // exact trip count: predicated-off DMMAs still occupy the tensor pipe
-        case 1: block_mma<1, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        case 2: block_mma<2, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        case 3: block_mma<3, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        case 4: block_mma<4, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        case 5: block_mma<5, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        case 6: block_mma<6, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        case 7: block_mma<7, WS>(acc, blk, wp, ae, ao, we, wo); break;
-        default: block_mma<8, WS>(acc, blk, wp, ae, ao, we, wo); break;
-      }
-      __syncwarp();
-      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&empty[st])) : "memory");
-    }
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      if (g < ng) {
-        const int col = g * 8 + (lane & 3) * 2;
-        const int64_t row = I * 64 + rrow;
-        if (col < kw) Y[(int64_t)col * ld + row] = acc[g][0];
-        else if (col == kw && xe) ye[row] = acc[g][0];
-        if (col + 1 < kw) Y[(int64_t)(col + 1) * ld + row] = acc[g][1];
-        else if (col + 1 == kw && xe) ye[row] = acc[g][1];
-      }
-    }
-    p = pn;
-    pend = pendn;
+  // ---- consumers (the loop is instantiated per number of 8-column groups: exact DMMA trip counts, and the
+  // accumulator chains of a block row stay in registers)
+  switch (ng) {
+    case 1: spmm_consume<1, NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    case 2: spmm_consume<2, NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    case 3: spmm_consume<3, NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    case 4: spmm_consume<(WS > 24 ? 4 : 1), NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    case 5: spmm_consume<(WS > 32 ? 5 : 1), NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    case 6: spmm_consume<(WS > 40 ? 6 : 1), NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    case 7: spmm_consume<(WS > 48 ? 7 : 1), NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
+    default: spmm_consume<(WS > 56 ? 8 : 1), NST, WS>(A, ring, wpan, full, empty, Y, ld, kw, xe, ye, wid, lane); break;
   }
   if (pst && pst->profile) {
     asm volatile("bar.sync 1, %0;" ::"r"(BT_CONS) : "memory");
