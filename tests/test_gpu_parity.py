@@ -285,6 +285,32 @@ def test_recycle_operator_thin_qr(name, N, sell, rng):
     assert np.allclose(np.tril(R, -1), 0.0)
 
 
+@pytest.mark.parametrize("k", [1, 7, 8, 9, 16, 17, 24, 25, 33, 34, 35, 41, 49, 57, 64])
+def test_bsr_spmm_every_column_group_count(k, rng):
+    """a4 on BSR-64: C = A W through the TMA + DMMA SpMM for every number of 8-column groups (1..8) and every
+    panel-stride instantiation (widths <= 18, <= 34, <= 66), incl. widths that are not multiples of 8; the
+    consumer loop is instantiated per group count and keeps its accumulator chains over a block row.
+    A W = Q R_C against the oracle's SpMV on the exported W."""
+    cfg = synth.CONFIGS["C5"].reduced(3)
+    seq = synth.HostSequence(cfg)
+    hm = seq.matrix(1, seq.initial())
+    ctx = make_ctx(hm, s=max(k, 1), k=k, max_m=cfg.m)
+    for i in range(k):
+        ctx.push_snapshot(t(rng.standard_normal(cfg.n)))
+    ke, _ = ctx.build_recycle(k)
+    assert ke == k
+    x = torch.zeros(cfg.n, dtype=torch.float64, device=DEV)
+    ctx.solve(t(rng.standard_normal(cfg.n)), x, m=cfg.m, variant="deflate", max_iters=2)
+    W = np.zeros((ke, cfg.n)); ctx.export(0, W); W = W.T
+    Q = np.zeros((ke, cfg.n)); ctx.export(1, Q); Q = Q.T
+    R = np.zeros((ke, ke)); ctx.export(2, R); R = R.T      # exported column-major
+    M = oracle.Matrix.from_host(hm)
+    AW = np.column_stack([oracle.spmv(M, W[:, i]) for i in range(ke)])
+    assert np.linalg.norm(AW - Q @ R) <= 1e-12 * np.linalg.norm(AW)
+    assert np.linalg.norm(Q.T @ Q - np.eye(ke)) <= 1e-11
+    ctx.close()
+
+
 @pytest.mark.parametrize("variant", ["plain", "augment", "deflate", "oblique", "orthogonal"])
 def test_persistent_and_graph_paths_agree(variant, rng):
     """The single cooperative-kernel solve and the CUDA-graph solve compute the same iterates
