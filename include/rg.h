@@ -149,7 +149,9 @@ typedef struct {
  * matrix A = A_1 (validated and copied into device memory the library owns; the caller keeps its
  * arrays).  *ctx receives the context (NULL on failure).  Errors: RG_E_INVAL (n < 1 or >= 2^31, max_m
  * outside 1..128, max_snapshots outside 1..64, max_k outside 0..min(64, max_snapshots), a malformed
- * descriptor or pattern — no side effects), RG_E_CUDA (no device), RG_E_NOMEM. */
+ * descriptor or pattern — no side effects), RG_E_CUDA (no device, or the current device is not compute
+ * capability 10.x with at least 148 SMs: the kernels are sm_100a code with grids sized for the B200),
+ * RG_E_NOMEM. */
 RG_API rg_status rg_create(rg_ctx** ctx, int64_t n, const rg_matrix* A, const rg_options* opt);
 
 /* Replace A by the next matrix A_t of the sequence ("the sequence of matrices and
