@@ -135,22 +135,29 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
       double t2 = 0.0;
       for (int i = 0; i <= j; ++i) t2 += tv[i] * tv[i];
       const double tau2 = mc[j + 1] - t2;
-      if (!(tau2 > 1e-14)) s_tb = 1;  // v_{j+1} (numerically) in span(Q) + span(V_{j+1}): end the cycle
-      else s_sc[4] = sqrt(tau2);
+      // tau^2 <= 1e-14: v_{j+1} lies (numerically) in span(Q) + span(V_{j+1}) — the search space
+      // span(W) + K_{j+1} already holds everything the next direction could add (k + j + 1 >= n at the
+      // latest).  The column is ACCEPTED with tau = 0: the last row of M = T H-bar vanishes, the projected
+      // least squares has a zero residual, and the cycle ends here (R5).  (Until the soak runs of
+      // round 2 this ended the cycle at the PREVIOUS step, discarding the step that completes the solve:
+      // n = 7, k = 5 took 23 iterations in 11 cycles where the explicit-space oracle takes 2.)
+      s_sc[4] = tau2 > 1e-14 ? sqrt(tau2) : 0.0;
     }
     __syncthreads();
-    if (!s_tb) {
+    {
       const double tau = s_sc[4];
-      for (int l = tid >> 5; l <= j; l += nw) {  // S(l, j+1) = -(sum_{i>=l} S(l,i) t_i)/tau
-        double sacc = 0.0;
-        for (int i = l + lane; i <= j; i += 32) sacc += st->Si[i][l] * tv[i];
-        sacc = warp_sum(sacc);
-        if (lane == 0) st->Si[j + 1][l] = -sacc / tau;
+      if (tau > 0.0) {  // S = T^{-1} is only needed by later columns of this cycle
+        for (int l = tid >> 5; l <= j; l += nw) {  // S(l, j+1) = -(sum_{i>=l} S(l,i) t_i)/tau
+          double sacc = 0.0;
+          for (int i = l + lane; i <= j; i += 32) sacc += st->Si[i][l] * tv[i];
+          sacc = warp_sum(sacc);
+          if (lane == 0) st->Si[j + 1][l] = -sacc / tau;
+        }
       }
       for (int i = tid; i <= j; i += bd) st->T[j + 1][i] = tv[i];
       if (tid == 0) {
         st->T[j + 1][j + 1] = tau;
-        st->Si[j + 1][j + 1] = 1.0 / tau;
+        if (tau > 0.0) st->Si[j + 1][j + 1] = 1.0 / tau;
       }
       __syncthreads();
       for (int i = tid >> 5; i <= j + 1; i += nw) {  // column j of M = T H: sum_{l>=i} T(i,l) h_l
@@ -203,7 +210,8 @@ __device__ __noinline__ static void epi_ls(DevState* st, const Layout& L, const 
         stop = 1;
         jf = -1;
       } else {
-        stop = (res <= tol) || (nrm <= 1e-14 * beta) || (j + 1 >= s_ic[0]) || (iters >= s_ic[2]);
+        stop = (res <= tol) || (nrm <= 1e-14 * beta) || (j + 1 >= s_ic[0]) || (iters >= s_ic[2]) ||
+               (var == RG_AUGMENT && k > 0 && !(s_sc[4] > 0.0));  // tau = 0: nothing left to add this cycle
       }
     }
     st->iters = iters;

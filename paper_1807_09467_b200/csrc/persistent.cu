@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
         if (tid == 0) Hs[col * (m + 2) + j] = nu;
         __syncthreads();
         const int M2 = m + 2;
-        int aug_tb = 0;  // augment: v_j (numerically) in span(Q) + span(V_j): end the cycle at col - 1
+        int aug_tb = 0;  // (kept for the Givens step below: no augment-specific breakdown any more, see tau = 0)
         if (aug) {
           // G row j = Q^T v_j = (Q^T u - G_j^T a) / nu; then the new column of T (Cholesky factor of
           // M = I - G^T G) and of S = T^{-1}; the least squares runs on M H-bar column col = T h.
@@ -754,19 +754,24 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
             s_sc[2] = tau2 > 1e-14 ? sqrt(tau2) : 0.0;
           }
           __syncthreads();
-          aug_tb = !(s_sc[2] > 0.0);
-          if (!aug_tb) {
+          // tau = 0 (tau^2 <= 1e-14): v_j adds nothing outside span(Q) + span(V_j); the column is accepted
+          // with a vanishing last row of M = T H-bar (zero projected residual) and ends the cycle — see
+          // epi_ls (epilogue.cuh); S = T^{-1} is only needed by later columns
+          aug_tb = 0;
+          {
             const double tau = s_sc[2];
-            for (int l = wid; l < j; l += PT / 32) {  // S(l, j) = -(sum_{i >= l} S(l, i) t_i) / tau
-              double sacc = 0.0;
-              for (int i = l + lane; i < j; i += 32) sacc += Ss[i * M2 + l] * cn[i];
-              sacc = warp_sum(sacc);
-              if (lane == 0) Ss[j * M2 + l] = -sacc / tau;
+            if (tau > 0.0) {
+              for (int l = wid; l < j; l += PT / 32) {  // S(l, j) = -(sum_{i >= l} S(l, i) t_i) / tau
+                double sacc = 0.0;
+                for (int i = l + lane; i < j; i += 32) sacc += Ss[i * M2 + l] * cn[i];
+                sacc = warp_sum(sacc);
+                if (lane == 0) Ss[j * M2 + l] = -sacc / tau;
+              }
             }
             for (int i = tid; i < j; i += PT) Ts[j * M2 + i] = cn[i];
             if (tid == 0) {
               Ts[j * M2 + j] = tau;
-              Ss[j * M2 + j] = 1.0 / tau;
+              if (tau > 0.0) Ss[j * M2 + j] = 1.0 / tau;
             }
             __syncthreads();
             for (int i = wid; i <= j; i += PT / 32) {  // column col of M = T H: sum_{l >= i} T(i, l) h_l -> ys[i]
@@ -806,7 +811,9 @@ __global__ void __launch_bounds__(PTT, 1024 / PTT) k_solve_persistent(PArgs pa) 
             const double res = fabs(s * gj) / bnorm;
             if (cta0 && hist_len < hist_cap) L.hist[hist_len] = res;
             if (!isfinite(res)) stop = 3;
-            else if (res <= tol || nu <= 1e-14 * beta || col + 1 >= m || iters + 1 >= max_iters) stop = 1;
+            else if (res <= tol || nu <= 1e-14 * beta || col + 1 >= m || iters + 1 >= max_iters ||
+                     (aug && !(s_sc[2] > 0.0)))
+              stop = 1;
           }
           s_stop = stop;
         } else if (wid > 0) {

@@ -285,6 +285,31 @@ def test_recycle_operator_thin_qr(name, N, sell, rng):
     assert np.allclose(np.tril(R, -1), 0.0)
 
 
+@pytest.mark.parametrize("flags", [0, 8, 4])   # persistent, graph (RG_FLAG_NO_PERSIST), classical CGS2
+@pytest.mark.parametrize("n,k", [(7, 5), (7, 1), (12, 4), (40, 8)])
+def test_augment_search_space_exhaustion(n, k, flags, rng):
+    """Augment with k + m > n: at Krylov step j = n - k the space span(W) + K_j is all of R^n, the Cholesky
+    factor T of I - G^T G gets a zero diagonal (tau = 0) and that step COMPLETES the solve.  The GPU must
+    accept the column (zero projected residual) as the explicit-space oracle does — found by the soak runs of
+    the fuzz (tools/soak.sh): ending the cycle at the previous step took 23 iterations where the oracle
+    takes 2 (R5)."""
+    hm = random_csr(n, rng, per_row=(1, 5), diag=2.5)
+    ctx = make_ctx(hm, s=k, k=k, max_m=64, flags=flags)
+    W = np.linalg.qr(rng.standard_normal((n, k)))[0]
+    for i in range(k):
+        ctx.push_snapshot(t(W[:, i] * (k - i)))
+    assert ctx.build_recycle(k)[0] == k
+    b = rng.standard_normal(n)
+    x = torch.zeros(n, dtype=torch.float64, device=DEV)
+    rep = ctx.solve(t(b), x, m=min(2 * n, 64), variant="augment", tol=1e-9, max_iters=500)
+    ref = oracle.solve(oracle.Matrix.from_host(hm), b, m=min(2 * n, 64), variant="augment", W=W, tol=1e-9, max_iters=500)
+    assert rep["converged"] and ref["converged"]
+    assert ref["iterations"] <= n - k and rep["restarts"] == 0
+    assert abs(rep["iterations"] - ref["iterations"]) <= 1, (rep["iterations"], ref["iterations"])
+    assert np.linalg.norm(x.cpu().numpy() - ref["x"]) <= 1e-9 * np.linalg.norm(ref["x"])
+    ctx.close()
+
+
 @pytest.mark.parametrize("k", [1, 7, 8, 9, 16, 17, 24, 25, 33, 34, 35, 41, 49, 57, 64])
 def test_bsr_spmm_every_column_group_count(k, rng):
     """a4 on BSR-64: C = A W through the TMA + DMMA SpMM for every number of 8-column groups (1..8) and every
