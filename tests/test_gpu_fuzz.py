@@ -45,7 +45,8 @@ def test_fuzz_case(case):
     n = int(rng.choice(sizes))
     m = int(rng.integers(1, 41))
     variant = VARIANTS[case % len(VARIANTS)] if n > 1 else "plain"
-    k = int(rng.integers(1, min(8, max(n - 1, 1)) + 1)) if variant != "plain" else 0
+    kmax = 8 if base == 9000 else 24   # soak runs also reach the k > 16 operator-build paths
+    k = int(rng.integers(1, min(kmax, max(n - 1, 1)) + 1)) if variant != "plain" else 0
     sell = bool(rng.integers(0, 2))
     pc = bool(rng.integers(0, 3) == 0)
     omega = float(rng.choice([1.0, 1.3]))
