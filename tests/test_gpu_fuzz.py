@@ -43,7 +43,7 @@ def test_fuzz_case(case):
     rng = np.random.default_rng(base + case)
     sizes = [1, 7, 63, 64, 65, 500, 4096, 4097, 20000] + ([150001] if base != 9000 else [])
     n = int(rng.choice(sizes))
-    m = int(rng.integers(1, 41))
+    m = int(rng.integers(1, 41 if base == 9000 else 101))   # soak runs: m > 64 forces the graph path
     variant = VARIANTS[case % len(VARIANTS)] if n > 1 else "plain"
     kmax = 8 if base == 9000 else 24   # soak runs also reach the k > 16 operator-build paths
     k = int(rng.integers(1, min(kmax, max(n - 1, 1)) + 1)) if variant != "plain" else 0
