@@ -3,6 +3,6 @@
 O=$1; shift
 for b in "$@"; do
   echo "== RG_FUZZ_SEED_BASE=$b" >> $O
-  RG_FUZZ_SEED_BASE=$b timeout 1500 python -m pytest tests/test_gpu_fuzz.py tests/test_gpu_fuzz_bsr.py -q 2>&1 | tail -4 >> $O
+  RG_FUZZ_SEED_BASE=$b timeout 1500 python -m pytest tests/test_gpu_fuzz.py tests/test_gpu_fuzz_bsr.py tests/test_gpu_fuzz_seq.py -q 2>&1 | tail -4 >> $O
 done
 cat $O
