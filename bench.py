@@ -519,8 +519,9 @@ def run_ours(args, cfg):
         if roof["frac"] > 1.0:
             # MEASURED_PEAKS.json's hbm_gbs is a COPY (read + write) rate; a read-dominated stream runs a
             # few percent above it (flat 16-byte read probe on the B200: 6.96 TB/s, profiles/r02/)
-            roof["note"] = ("peak is the measured read+write copy rate; this kernel is a read-only stream "
-                            "(DRAM traffic 1.005x algorithmic), which exceeds a copy by a few percent")
+            ratio = f" (DRAM traffic {traffic / bytes_per:.3f}x algorithmic)" if traffic else ""
+            roof["note"] = ("peak is the measured read+write copy rate; this kernel is a read-dominated stream"
+                            + ratio + ", which exceeds a copy by a few percent")
     # kernel launches in the timed region: device-counted executions (incl. launches that found nothing
     # to do), the library's host-launched kernels, and the input generator's kernels.  Not summed:
     # the p_* phase timers inside the persistent solve and "ssor" (per application; its kernels are
