@@ -89,6 +89,7 @@ struct rg_ctx {
   bool own_stream = false;
   cudaStream_t side = nullptr;     // DCGS2 split epilogue: k_dcgs_ls runs here, concurrently with DK2
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t cap = nullptr;  // non-blocking stream the solve graphs are CAPTURED on (see run_solve)
   int flags = 0;
   int64_t n = 0, npad = 0;
   int max_m = 0, max_s = 0, max_k = 0;
@@ -607,8 +608,16 @@ rg_status run_solve(rg_ctx* c, int variant, int m) {
   GraphKey key{variant, c->dcgs_now ? 1 : 0, c->L.prec};
   auto it = c->graphs.find(key);
   if (it == c->graphs.end()) {
+    // The graph is captured on a stream of its own: a library-created c->stream is a BLOCKING stream, and
+    // while it captures, any work another host thread puts on the legacy default stream (another context's
+    // caller, torch) would fail with "operation would make the legacy stream depend on a capturing blocking
+    // stream" (tests/test_gpu_contexts.py).  Nodes do not keep the capture stream; the graph is launched on
+    // c->stream.
     cudaGraphExec_t ge;
+    cudaStream_t user = c->stream;
+    c->stream = c->cap;
     rg_status s = build_solve_graph(c, variant, &ge);
+    c->stream = user;
     if (s != RG_OK) return s;
     it = c->graphs.emplace(key, ge).first;
   }
@@ -651,6 +660,7 @@ RG_API void rg_destroy(rg_ctx* c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->cap) cudaStreamDestroy(c->cap);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -758,6 +768,7 @@ RG_API rg_status rg_create(rg_ctx** out, int64_t n, const rg_matrix* A, const rg
   ok(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   ok(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
   ok(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  ok(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
   ok(cudaStreamSynchronize(c->stream));
   if (e != cudaSuccess) {
     rg_destroy(c);
