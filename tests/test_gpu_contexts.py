@@ -120,3 +120,62 @@ def test_concurrent_host_threads_match_solo_runs_bitwise():
     assert not err, err
     for a, b in zip(ref, res):
         same(a, b)
+
+
+def test_create_solve_destroy_does_not_leak_device_memory():
+    """60 create -> push -> build -> solve -> close cycles (graph path, persistent path, SSOR on every third):
+    the free device memory returns to where it was (rg_destroy frees every buffer, graph and stream)."""
+    from paper_1807_09467_b200 import Context
+    rng = np.random.default_rng(5)
+    hm = random_csr(4000, rng, 1, 6, diag=2.6)
+    rp, ci, v = t(hm.row_ptr), t(hm.col_idx), t(hm.val)
+    b = t(rng.standard_normal(hm.n))
+    snap = t(rng.standard_normal(hm.n))
+    x = torch.zeros(hm.n, dtype=torch.float64, device=DEV)
+
+    def cycle(i):
+        ctx = Context(hm.n, rp, ci, v, max_m=20, max_snapshots=4, max_k=2, flags=8 if i % 2 else 0)
+        if i % 3 == 0:
+            ctx.set_preconditioner("ssor", 1.0)
+        ctx.push_snapshot(snap)
+        ctx.build_recycle(2)
+        assert ctx.solve(b, x, m=20, variant="deflate", tol=1e-8)["converged"]
+        ctx.close()
+
+    for i in range(6):     # warm-up: module loading, per-process caches
+        cycle(i)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    for i in range(60):
+        cycle(i)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 <= 8 << 20, (free0, free1)   # (allocator granularity slack: 8 MiB)
+
+
+def test_context_stays_usable_after_errors(rng):
+    """Every error return leaves the context usable (include/rg.h: nothing aborts, throws or exits)."""
+    from paper_1807_09467_b200 import Context, rg as rgb
+    hm = random_csr(3000, rng, 1, 6, diag=2.6)
+    ctx = Context(hm.n, t(hm.row_ptr), t(hm.col_idx), t(hm.val), max_m=20, max_snapshots=4, max_k=3)
+    b = t(rng.standard_normal(hm.n))
+    x = torch.zeros(hm.n, dtype=torch.float64, device=DEV)
+    with pytest.raises(rgb.RgError) as e:
+        ctx.build_recycle(2)                          # no snapshots yet
+    assert e.value.status == rgb.RG_E_STATE
+    with pytest.raises(rgb.RgError) as e:
+        ctx.solve(b, x, m=21, variant="plain")        # m > max_m
+    assert e.value.status == rgb.RG_E_INVAL
+    with pytest.raises(rgb.RgError) as e:
+        ctx.solve(b, x, m=10, variant="plain", tol=-1.0)
+    assert e.value.status == rgb.RG_E_INVAL
+    v = rng.standard_normal(hm.n)
+    for s in (v, 2.0 * v, -v):                        # rank-1 window: k_eff = 1
+        ctx.push_snapshot(t(s))
+    assert ctx.build_recycle(3)[0] == 1
+    r1 = ctx.solve(b, x, m=20, variant="deflate", tol=1e-9)
+    assert r1["converged"]
+    x1 = x.clone()
+    r2 = ctx.solve(b, x, m=20, variant="deflate", tol=1e-9)   # and the same call again: bitwise the same
+    assert r2["iterations"] == r1["iterations"] and torch.equal(x, x1)
+    ctx.close()
