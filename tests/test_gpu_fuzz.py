@@ -55,6 +55,10 @@ def test_fuzz_case(case):
     x0 = rng.standard_normal(n) * 0.1 if rng.integers(0, 2) else None
     from paper_1807_09467_b200 import rg as rgb
     flags = int(rng.choice([0, 0, rgb.RG_FLAG_NO_PERSIST, rgb.RG_FLAG_CGS2]))  # persistent / graph / classical CGS2
+    if base != 9000:  # soak runs: also the host-driven loop, profiling and basis-keeping builds of each path
+        flags |= int(np.random.default_rng(base + 31337 + case).choice(
+            [0, 0, rgb.RG_FLAG_NO_GRAPH, rgb.RG_FLAG_PROFILE, rgb.RG_FLAG_KEEP_BASIS,
+             rgb.RG_FLAG_NO_GRAPH | rgb.RG_FLAG_NO_PERSIST, rgb.RG_FLAG_PROFILE | rgb.RG_FLAG_KEEP_BASIS]))
     # SELL-32-sigma row sorting (own generator: the main draw sequence of the cases stays as it was)
     sigma = int(np.random.default_rng(base - 1300 + case).choice([1, 32, 256])) if sell else 1
     ctx = Context(n, t(hm.row_ptr), t(hm.col_idx), t(hm.val), sell_C=32 if sell else 0, max_m=max(m, 2),
